@@ -1,0 +1,199 @@
+/*
+ * hep.h — C-ABI boundary of the B200-native HybridEP MoE-layer hot path.
+ *
+ * Plain pointers and sizes only (no C++ or torch types); device pointers are
+ * CUDA device addresses, `stream` is a cudaStream_t passed as void*.  Every call
+ * returns a hep_status; on failure hep_last_error() (thread-local) describes it.
+ * Error classes mirror the exceptions the reference throws at the same points
+ * (SURVEY.md §8(b)): DOMAIN ~ std::domain_error, INVALID_ARGUMENT ~
+ * std::invalid_argument, RUNTIME ~ std::runtime_error.
+ *
+ * Each entry point names the reference interface it replaces (file:line under
+ * /root/reference/proj).  The C++ API (include/hybridep/ headers) is layered on the
+ * same library; INTEGRATION.md shows the ctypes / C++ bindings.
+ */
+#ifndef HEP_H_
+#define HEP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HEP_OK = 0,
+  HEP_ERR_DOMAIN = 1,
+  HEP_ERR_INVALID_ARGUMENT = 2,
+  HEP_ERR_RUNTIME = 3,
+  HEP_ERR_CUDA = 4,
+  HEP_ERR_NCCL = 5,
+  HEP_ERR_UNSUPPORTED = 6
+} hep_status;
+
+typedef enum { HEP_F32 = 0, HEP_BF16 = 1 } hep_dtype;
+
+/* One level of the multilevel description, outermost first
+ * (replaces topo::LevelSpec, topology.hpp:19-23). */
+typedef struct {
+  int64_t scaling_factor; /* SF */
+  int64_t domain_size;    /* S_ED */
+  double bandwidth;       /* bytes/s */
+} hep_level;
+
+const char* hep_last_error(void);
+const char* hep_version(void);
+
+/* ------------------------------------------------------------- topology (host) */
+/* G = prod SF; validates like ClusterSpec::validate (topology.cpp:35-61). */
+int hep_topology_gpus(const hep_level* levels, int num_levels, int64_t* gpus);
+/* Dense G x G pair table, row-major m*G+n: pair_level (-1 = none) and pair_type
+ * (0 none, 1 AG, 2 A2A).  Replaces CommTopology::CommTopology (topology.cpp:142-177). */
+int hep_topology_build(const hep_level* levels, int num_levels, int8_t* pair_level,
+                       uint8_t* pair_type);
+/* f(m): coords[num_levels].  Replaces topo::renumber (topology.cpp:74-83). */
+int hep_renumber(const hep_level* levels, int num_levels, int64_t m, int64_t* coords);
+/* Inverse of f.  Replaces topo::global_index (topology.cpp:85-97). */
+int hep_global_index(const hep_level* levels, int num_levels, const int64_t* coords, int64_t* m);
+/* Algorithm 1 for one (m, n, level).  Replaces topo::comm_type (topology.cpp:117-131). */
+int hep_comm_type(const hep_level* levels, int num_levels, int64_t m, int64_t n, int level,
+                  int* type);
+/* Closed-form directed pair counts per level.  Replaces level_frequency_closed_form
+ * via CommTopology::frequencies (topology.cpp:133-153). */
+int hep_level_frequency(const hep_level* levels, int num_levels, int64_t* a2a, int64_t* ag);
+/* Per-level bytes of one pass (stripe model).  Replaces topo::traffic_report
+ * (topology.cpp:249-281).  Outputs are arrays of num_levels. */
+int hep_traffic_report(const hep_level* levels, int num_levels, double data_size_D,
+                       double expert_size_PE, double token_multiplier, double* a2a_pair_bytes,
+                       double* ag_pair_bytes, double* a2a_bytes, double* ag_bytes);
+/* Ring-ordered peer lists of GPU m (simcore.cpp:30-74), flattened over levels
+ * (outermost first); *_level[i] is the level of peer i.  Arrays hold >= G entries. */
+int hep_peer_lists(const hep_level* levels, int num_levels, int64_t m, int64_t* ag_peers,
+                   int* ag_level, int* n_ag, int64_t* a2a_peers, int* a2a_level, int* n_a2a);
+/* route[m*G+o] = GPU computing, for tokens on m, the experts owned by o (S2 rule). */
+int hep_route_table(const hep_level* levels, int num_levels, int32_t* route);
+/* Innermost-first gcd split (plan.cpp:41-58). */
+int hep_factor_domain_sizes(int64_t domain_size, const hep_level* levels, int num_levels,
+                            int64_t* out);
+
+/* ------------------------------------------------------------- planner (host) */
+typedef struct {
+  double data_size_D, expert_size_PE;
+  int64_t experts_per_gpu_n, pre_blocks_m;
+  double attn_latency, ffn_latency, expert_latency, backward_allreduce_const;
+} hep_workload;
+/* Divisor-grid solver (perfmodel.cpp:200-217): returns p, S_ED and the modelled
+ * latency terms {comp, pre_expert, comm_a2a, comm_ag, overlap, total}. */
+int hep_solve_optimal_p(const hep_workload* w, double throughput_C, double bandwidth_B,
+                        int64_t gpus, double* p, int64_t* domain_size, double* latency6);
+
+/* ------------------------------------------------------------- SR migration codec */
+typedef struct {
+  double ratio_CR;           /* used when k < 0 */
+  int64_t k;                 /* explicit budget (>= 0 wins), clamped to P */
+  uint32_t index_width_bits; /* 32 or 64 */
+  uint32_t value_width_bits; /* 32 or 64 */
+  int per_matrix_budget;
+} hep_sr_config;
+
+/* CompressionConfig::resolve_k (sparsecomp.cpp:133-145). */
+int hep_sr_resolve_k(const hep_sr_config* cfg, int64_t total_elements, int64_t elem_bytes,
+                     int64_t* k);
+/* Exact SRC1 wire size of one expert of shape (h, m) under cfg (header + k entries). */
+int hep_sr_wire_bytes(int64_t h, int64_t m, const hep_sr_config* cfg, size_t* bytes);
+int hep_sr_workspace_bytes(size_t* bytes);
+/* Device encode = sr_encode + serialize (sparsecomp.cpp:175-224, :71-97).
+ * expert: flat P = 2hm elements (w_up h x m then w_down m x h, row-major), fp32 or
+ * bf16 (upcast exactly); shared: fp32 flat P.  wire: device buffer of
+ * hep_sr_wire_bytes bytes.  Asynchronous; no host synchronisation. */
+int hep_sr_encode(const void* expert, hep_dtype expert_dtype, const float* shared, int64_t h,
+                  int64_t m, const hep_sr_config* cfg, void* wire, size_t wire_capacity,
+                  void* workspace, size_t workspace_bytes, void* stream);
+/* Device decode = deserialize + sr_decode (sparsecomp.cpp:99-131, :226-246).
+ * out: fp32 flat P.  status: device int32[4] (16 bytes); status[0] after the stream
+ * reaches this point: 0 ok, 1 bad magic, 2 truncated, 3 bad widths, 4 shape tag
+ * mismatch, 5 index out of bounds, 6 indices not increasing (status[1] = entry). */
+int hep_sr_decode(const void* wire, size_t wire_bytes, const float* shared, int64_t h, int64_t m,
+                  float* out, int32_t* status, void* stream);
+/* Synchronises `stream` and maps a decode status to a hep_status + message
+ * (RUNTIME for corrupt wires, INVALID_ARGUMENT for a shape mismatch). */
+int hep_sr_check_status(const int32_t* status, void* stream);
+/* init_shared / update_shared (sparsecomp.cpp:147-173): experts = host array of n
+ * device pointers to flat P elements. */
+int hep_shared_mean(const void* const* experts, int n, hep_dtype dtype, int64_t P, float* out,
+                    void* stream);
+
+/* ------------------------------------------------------------- communicator */
+typedef struct hep_comm_s* hep_comm_t;
+/* 128-byte NCCL unique id, to be broadcast by the caller (e.g. torch.distributed). */
+int hep_comm_unique_id(void* id128);
+int hep_comm_init(const void* id128, int rank, int nranks, hep_comm_t* comm);
+int hep_comm_destroy(hep_comm_t comm);
+
+/* ------------------------------------------------------------- MoE layer step */
+typedef struct {
+  int64_t hidden;      /* H */
+  int64_t ffn;         /* F (the reference's inner_m) */
+  int64_t experts;     /* E, global */
+  int64_t top_k;       /* k */
+  int64_t max_tokens;  /* T capacity per GPU */
+  hep_dtype dtype;     /* activations and expert weights */
+  const hep_level* levels;
+  int num_levels;
+  int rank;            /* this GPU's global index m */
+  int use_sr;          /* migrate gathered experts as SR wires instead of dense */
+  hep_sr_config sr;
+} hep_layer_params;
+
+typedef struct hep_layer_s* hep_layer_t;
+
+/* comm may be NULL when G == 1.  Selects the current CUDA device's resources. */
+int hep_layer_create(const hep_layer_params* params, hep_comm_t comm, hep_layer_t* layer);
+int hep_layer_destroy(hep_layer_t layer);
+/* Gate matrix W_g, H x E row-major (logits = x . W_g), device pointer, dtype F32 or BF16. */
+int hep_layer_set_gate(hep_layer_t layer, const void* w_gate, hep_dtype dtype, void* stream);
+/* One owned expert (global id e, owner(e) == rank): w_up H x F, w_down F x H row-major
+ * (reference layout, sparsecomp.hpp:29-36), device pointers. */
+int hep_layer_set_expert(hep_layer_t layer, int64_t expert, const void* w_up, const void* w_down,
+                         hep_dtype dtype, void* stream);
+/* SR mode: the shared expert (fp32 flat P, device) that residuals are coded against. */
+int hep_layer_set_shared(hep_layer_t layer, const float* shared, void* stream);
+/* Expert-domain All-Gather of the owned experts (dense or SR-migrated), so that every
+ * held expert is resident.  Issued on `stream`. */
+int hep_layer_gather_experts(hep_layer_t layer, void* stream);
+/* The step: gate -> permute -> dispatch -> expert FFN -> combine.  x, y: device
+ * [tokens, H] in the layer dtype. */
+int hep_layer_forward(hep_layer_t layer, const void* x, int64_t tokens, void* y, void* stream);
+/* Same step with host buffers (pinned recommended): H2D copy, forward, D2H copy. */
+int hep_layer_forward_host(hep_layer_t layer, const void* host_x, int64_t tokens, void* host_y,
+                           void* stream);
+/* Introspection of the last forward (device pointers owned by the layer):
+ * topk_idx int32[T*k], topk_w f32[T*k], pos int32[T*k] (row of (t,j) in the packed
+ * buffer), packed [rows, H] send buffer grouped by (dest, expert); counts int32[G*E]
+ * rows per (dest, expert) key. */
+int hep_layer_debug(hep_layer_t layer, const int32_t** topk_idx, const float** topk_w,
+                    const int32_t** pos, const void** packed, const int32_t** key_counts);
+/* Per-kernel device times (ms) of the last `profile`d forward; names is a
+ * ';'-separated list.  Enable with hep_layer_set_profiling(layer, 1). */
+int hep_layer_set_profiling(hep_layer_t layer, int on);
+int hep_layer_timings(hep_layer_t layer, char* names, size_t names_cap, float* ms, int cap,
+                      int* count);
+/* Number of kernels the last forward launched (this library's own kernels). */
+int hep_layer_launch_count(hep_layer_t layer, int* count);
+
+/* ------------------------------------------------------------- kernel-level entry points */
+/* Exposed for parity tests and for frameworks that own their buffers. */
+int hep_grouped_gemm(hep_dtype dtype, const void* A, int64_t a_rows, const void* B,
+                     int64_t b_slots, void* C, int64_t N, int64_t K, const int32_t* g_row_start,
+                     const int32_t* g_rows, const int32_t* g_slot, int num_groups, int relu,
+                     void* stream);
+/* Reference layout [rows, cols] -> compute layout [cols, rows] (K-major weight copy). */
+int hep_transpose_convert(hep_dtype in_dtype, const void* in, int64_t rows, int64_t cols,
+                          hep_dtype out_dtype, void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HEP_H_ */

@@ -1,0 +1,422 @@
+// MoE-layer step executor: the B200 realisation of the step the reference only
+// simulates (sim::build_schedule, simcore.cpp:96-266):
+//   AgTransfer   -> gather_experts(): dense expert All-Gather, or SR wires encoded
+//                   on the owner, gathered, decoded on the holder (migration)
+//   PreExpert/gate, dispatch -> gate + counting-sort permute + NCCL grouped
+//                   send/recv with the A2A peers in build_peer_lists ring order
+//   ExpertChunk  -> one grouped GEMM pair over local + received rows
+//   A2aCombine   -> NCCL send/recv back + gate-weighted combine
+// Peer sets and routing come from the topology table (hybridep::moe::route_table).
+
+#include "layer.h"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+
+#include "hybridep/moe.hpp"
+#include "hybridep/simcore.hpp"
+
+namespace hep {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw std::runtime_error(std::string("NCCL error in ") + what + ": " + ncclGetErrorString(r));
+}
+
+ncclDataType_t nccl_type(DType dt) { return dt == DType::BF16 ? ncclBfloat16 : ncclFloat32; }
+
+}  // namespace
+
+void DevBuf::alloc(size_t n) {
+  release();
+  if (n == 0) n = 16;
+  ck(cudaMalloc(&p, n), "cudaMalloc");
+  bytes = n;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
+  H_ = prm.hidden;
+  F_ = prm.ffn;
+  E_ = prm.experts;
+  k_ = prm.top_k;
+  Tmax_ = prm.max_tokens;
+  dt_ = prm.dtype == HEP_BF16 ? DType::BF16 : DType::F32;
+  rank_ = prm.rank;
+  use_sr_ = prm.use_sr != 0;
+  if (H_ <= 0 || F_ <= 0 || E_ <= 0 || k_ <= 0 || Tmax_ <= 0)
+    throw std::invalid_argument("layer shape must be positive");
+  if (k_ > 8 || k_ > E_ || E_ > 64) throw std::invalid_argument("need top_k <= 8, top_k <= experts <= 64");
+  if (H_ % 64 || F_ % 64) throw std::invalid_argument("hidden and ffn must be multiples of 64");
+  if (!prm.levels || prm.num_levels <= 0) throw std::invalid_argument("layer needs a cluster description");
+  for (int i = 0; i < prm.num_levels; ++i) {
+    const hep_level& l = prm.levels[i];
+    // Bandwidth is a planner input; the executor only needs SF and S_ED.
+    cluster_.levels.push_back({l.scaling_factor, l.domain_size, l.bandwidth > 0 ? l.bandwidth : 1.0});
+  }
+  cluster_.validate();
+  G_ = cluster_.total_gpus();
+  if (E_ % G_) throw std::invalid_argument("experts must be divisible by the GPU count");
+  if (rank_ < 0 || rank_ >= G_) throw std::domain_error("rank out of range");
+  if (G_ > 1 && (!comm_ || comm_->nranks != G_ || comm_->rank != rank_))
+    throw std::invalid_argument("a communicator of G ranks matching this rank is required when G > 1");
+  n_ = E_ / G_;
+  NK_ = G_ * E_;
+  if (use_sr_) {
+    sr_cfg_.ratio_CR = prm.sr.k >= 0 ? std::optional<double>() : std::optional<double>(prm.sr.ratio_CR);
+    if (prm.sr.k >= 0) sr_cfg_.k = prm.sr.k;
+    sr_cfg_.index_width_bits = prm.sr.index_width_bits;
+    sr_cfg_.value_width_bits = prm.sr.value_width_bits;
+    sr_cfg_.per_matrix_budget = prm.sr.per_matrix_budget != 0;
+  }
+
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  ck(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, dev), "sm count");
+
+  // Placement and routing from the topology table.
+  const std::vector<int32_t> route = hybridep::moe::route_table(cluster_);
+  route_row_.assign(route.begin() + rank_ * G_, route.begin() + (rank_ + 1) * G_);
+  held_owners_ = hybridep::moe::held_owners(cluster_)[static_cast<size_t>(rank_)];
+  slot_of_expert_.assign(static_cast<size_t>(E_), -1);
+  slots_ = 0;
+  for (int64_t o : held_owners_)
+    for (int64_t i = 0; i < n_; ++i) slot_of_expert_[static_cast<size_t>(o * n_ + i)] = static_cast<int32_t>(slots_++);
+  const std::vector<hybridep::sim::PeerLists> peers = hybridep::sim::peer_lists(cluster_);
+  for (const auto& l : peers[static_cast<size_t>(rank_)].ag) ag_peers_.insert(ag_peers_.end(), l.begin(), l.end());
+  for (const auto& l : peers[static_cast<size_t>(rank_)].a2a) a2a_peers_.insert(a2a_peers_.end(), l.begin(), l.end());
+
+  const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
+  d_route_.alloc(sizeof(int32_t) * G_);
+  ck(cudaMemcpy(d_route_.p, route_row_.data(), sizeof(int32_t) * G_, cudaMemcpyHostToDevice), "route");
+  d_slot_of_expert_.alloc(sizeof(int32_t) * E_);
+  ck(cudaMemcpy(d_slot_of_expert_.p, slot_of_expert_.data(), sizeof(int32_t) * E_, cudaMemcpyHostToDevice), "slots");
+  wg_t_.alloc(sizeof(float) * E_ * H_);
+  w_up_c_.alloc(eb * slots_ * F_ * H_);
+  w_down_c_.alloc(eb * slots_ * H_ * F_);
+
+  const int64_t TK = Tmax_ * k_;
+  const int64_t nchunks = (Tmax_ + 31) / 32;
+  topk_idx_.alloc(sizeof(int) * TK);
+  topk_w_.alloc(sizeof(float) * TK);
+  keys_.alloc(sizeof(int) * TK);
+  ranks_.alloc(sizeof(int) * TK);
+  pos_.alloc(sizeof(int) * TK);
+  chunk_counts_.alloc(sizeof(int) * nchunks * NK_);
+  chunk_off_.alloc(sizeof(int) * nchunks * NK_);
+  key_total_.alloc(sizeof(int) * NK_);
+  key_off_.alloc(sizeof(int) * NK_);
+  dest_rows_.alloc(sizeof(int) * G_);
+  dest_off_.alloc(sizeof(int) * G_);
+  const int64_t max_groups = slots_ * (1 + static_cast<int64_t>(a2a_peers_.size()));
+  g_row_start_.alloc(sizeof(int) * max_groups);
+  g_rows_.alloc(sizeof(int) * max_groups);
+  g_slot_.alloc(sizeof(int) * max_groups);
+  all_counts_.alloc(sizeof(int) * G_ * NK_);
+
+  rows_cap_ = TK * (1 + static_cast<int64_t>(a2a_peers_.size()));
+  xall_.alloc(eb * rows_cap_ * H_);
+  hbuf_.alloc(eb * rows_cap_ * F_);
+  oall_.alloc(eb * rows_cap_ * H_);
+
+  if (dt_ == DType::BF16) {
+    ck(make_tmap_bf16_2d(&map_a1_, xall_.p, rows_cap_, H_, 128, 64), "tmap a1");
+    ck(make_tmap_bf16_2d(&map_b1_, w_up_c_.p, slots_ * F_, H_, 256, 64), "tmap b1");
+    ck(make_tmap_bf16_2d(&map_a2_, hbuf_.p, rows_cap_, F_, 128, 64), "tmap a2");
+    ck(make_tmap_bf16_2d(&map_b2_, w_down_c_.p, slots_ * H_, F_, 256, 64), "tmap b2");
+  }
+
+  if (use_sr_) {
+    const int64_t P = 2 * H_ * F_;
+    shared_.alloc(sizeof(float) * P);
+    master_.alloc(sizeof(float) * n_ * P);
+    size_t wb = 0;
+    hep_sr_config c{sr_cfg_.ratio_CR.value_or(1.0), sr_cfg_.k.value_or(-1), sr_cfg_.index_width_bits,
+                    sr_cfg_.value_width_bits, sr_cfg_.per_matrix_budget ? 1 : 0};
+    if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
+    wires_.alloc(((wb + 15) / 16 * 16) * slots_);
+    sr_ws_.alloc(sr_workspace_bytes());
+    sr_tmp_.alloc(sizeof(float) * P);
+    sr_status_.alloc(16);
+  }
+  x_dev_.alloc(eb * Tmax_ * H_);
+  y_dev_.alloc(eb * Tmax_ * H_);
+  send_off_.resize(a2a_peers_.size());
+  send_rows_.resize(a2a_peers_.size());
+  recv_off_.resize(a2a_peers_.size());
+  recv_rows_.resize(a2a_peers_.size());
+  num_groups_ = static_cast<int>(slots_);
+}
+
+Layer::~Layer() {
+  for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+}
+
+void Layer::set_gate(const void* w_gate, DType dt, cudaStream_t s) {
+  // W_g is H x E; the gate kernel wants it expert-major fp32.
+  ck(launch_transpose_convert(dt, w_gate, H_, E_, DType::F32, wg_t_.p, s), "gate layout");
+}
+
+void Layer::set_expert(int64_t e, const void* w_up, const void* w_down, DType dt, cudaStream_t s) {
+  if (e < 0 || e >= E_) throw std::domain_error("expert id out of range");
+  if (e / n_ != rank_) throw std::invalid_argument("expert is not owned by this rank");
+  const int64_t slot = slot_of_expert_[static_cast<size_t>(e)];
+  const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
+  uint8_t* up = w_up_c_.as<uint8_t>() + eb * slot * F_ * H_;
+  uint8_t* down = w_down_c_.as<uint8_t>() + eb * slot * H_ * F_;
+  ck(launch_transpose_convert(dt, w_up, H_, F_, dt_, up, s), "w_up layout");
+  ck(launch_transpose_convert(dt, w_down, F_, H_, dt_, down, s), "w_down layout");
+  if (use_sr_) {
+    // fp32 master copy in the reference flat layout (w_up then w_down) for encode.
+    const int64_t P = 2 * H_ * F_;
+    float* m = master_.as<float>() + (e - rank_ * n_) * P;
+    if (dt == DType::F32) {
+      ck(cudaMemcpyAsync(m, w_up, sizeof(float) * H_ * F_, cudaMemcpyDeviceToDevice, s), "master up");
+      ck(cudaMemcpyAsync(m + H_ * F_, w_down, sizeof(float) * H_ * F_, cudaMemcpyDeviceToDevice, s), "master down");
+    } else {
+      // bf16 -> fp32 is exact: two transposes reproduce the row-major layout.
+      ck(launch_transpose_convert(DType::BF16, w_up, H_, F_, DType::F32, sr_tmp_.p, s), "up32");
+      ck(launch_transpose_convert(DType::F32, sr_tmp_.p, F_, H_, DType::F32, m, s), "up32b");
+      ck(launch_transpose_convert(DType::BF16, w_down, F_, H_, DType::F32, sr_tmp_.p, s), "down32");
+      ck(launch_transpose_convert(DType::F32, sr_tmp_.p, H_, F_, DType::F32, m + H_ * F_, s), "down32b");
+    }
+  }
+}
+
+void Layer::set_shared(const float* shared, cudaStream_t s) {
+  if (!use_sr_) throw std::invalid_argument("shared expert is only used with SR migration");
+  ck(cudaMemcpyAsync(shared_.p, shared, sizeof(float) * 2 * H_ * F_, cudaMemcpyDeviceToDevice, s), "shared");
+}
+
+void Layer::gather_experts(cudaStream_t s) {
+  if (G_ == 1 || ag_peers_.empty()) return;
+  const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
+  const size_t per_slot_up = static_cast<size_t>(F_ * H_), per_slot_down = static_cast<size_t>(H_ * F_);
+  auto first_slot_of = [&](int64_t owner) { return slot_of_expert_[static_cast<size_t>(owner * n_)]; };
+  if (!use_sr_) {
+    nck(ncclGroupStart(), "group start");
+    for (int64_t p : ag_peers_) {
+      const int64_t mine = first_slot_of(rank_), theirs = first_slot_of(p);
+      nck(ncclSend(w_up_c_.as<uint8_t>() + eb * mine * per_slot_up, n_ * per_slot_up, nccl_type(dt_), static_cast<int>(p), comm_->nccl, s), "send up");
+      nck(ncclRecv(w_up_c_.as<uint8_t>() + eb * theirs * per_slot_up, n_ * per_slot_up, nccl_type(dt_), static_cast<int>(p), comm_->nccl, s), "recv up");
+      nck(ncclSend(w_down_c_.as<uint8_t>() + eb * mine * per_slot_down, n_ * per_slot_down, nccl_type(dt_), static_cast<int>(p), comm_->nccl, s), "send down");
+      nck(ncclRecv(w_down_c_.as<uint8_t>() + eb * theirs * per_slot_down, n_ * per_slot_down, nccl_type(dt_), static_cast<int>(p), comm_->nccl, s), "recv down");
+    }
+    nck(ncclGroupEnd(), "group end");
+    return;
+  }
+  // SR migration: encode own experts against the shared expert, gather the wires,
+  // decode each gathered wire straight into its compute slot.
+  const int64_t P = 2 * H_ * F_;
+  size_t wb = 0;
+  hep_sr_config c{sr_cfg_.ratio_CR.value_or(1.0), sr_cfg_.k.value_or(-1), sr_cfg_.index_width_bits,
+                  sr_cfg_.value_width_bits, sr_cfg_.per_matrix_budget ? 1 : 0};
+  if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
+  const size_t stride = (wb + 15) / 16 * 16;
+  uint8_t* wires = wires_.as<uint8_t>();
+  for (int64_t i = 0; i < n_; ++i) {
+    if (hep_sr_encode(master_.as<float>() + i * P, HEP_F32, shared_.as<float>(), H_, F_, &c,
+                      wires + stride * (first_slot_of(rank_) + i), wb, sr_ws_.p, sr_ws_.bytes, s) != HEP_OK)
+      throw std::runtime_error(hep_last_error());
+  }
+  nck(ncclGroupStart(), "group start");
+  for (int64_t p : ag_peers_) {
+    nck(ncclSend(wires + stride * first_slot_of(rank_), stride * n_, ncclUint8, static_cast<int>(p), comm_->nccl, s), "send wire");
+    nck(ncclRecv(wires + stride * first_slot_of(p), stride * n_, ncclUint8, static_cast<int>(p), comm_->nccl, s), "recv wire");
+  }
+  nck(ncclGroupEnd(), "group end");
+  for (int64_t p : ag_peers_)
+    for (int64_t i = 0; i < n_; ++i) {
+      const int64_t slot = first_slot_of(p) + i;
+      ck(launch_sr_decode(wires + stride * slot, wb, shared_.as<float>(), H_, F_, sr_tmp_.as<float>(), sr_status_.as<int32_t>(), s), "decode");
+      ck(launch_transpose_convert(DType::F32, sr_tmp_.p, H_, F_, dt_, w_up_c_.as<uint8_t>() + eb * slot * per_slot_up, s), "dec up");
+      ck(launch_transpose_convert(DType::F32, sr_tmp_.as<float>() + H_ * F_, F_, H_, dt_, w_down_c_.as<uint8_t>() + eb * slot * per_slot_down, s), "dec down");
+    }
+}
+
+void Layer::mark(const char* name, cudaStream_t s) {
+  if (!profiling_) return;
+  cudaEvent_t ev;
+  if (marks_.size() < event_pool_.size()) {
+    ev = event_pool_[marks_.size()];
+  } else {
+    ck(cudaEventCreate(&ev), "event");
+    event_pool_.push_back(ev);
+  }
+  ck(cudaEventRecord(ev, s), "event record");
+  marks_.emplace_back(name, ev);
+}
+
+void Layer::build_comm_plan_and_groups(int T, cudaStream_t s) {
+  // Counts exchange: every rank learns every rank's (dest, expert) row counts.
+  nck(ncclAllGather(key_total_.p, all_counts_.p, static_cast<size_t>(NK_), ncclInt32, comm_->nccl, s), "count allgather");
+  h_counts_.resize(static_cast<size_t>(G_ * NK_));
+  ck(cudaMemcpyAsync(h_counts_.data(), all_counts_.p, sizeof(int32_t) * G_ * NK_, cudaMemcpyDeviceToHost, s), "counts d2h");
+  ck(cudaStreamSynchronize(s), "counts sync");
+  auto cnt = [&](int64_t src, int64_t dest, int64_t e) {
+    return static_cast<int64_t>(h_counts_[static_cast<size_t>(src * NK_ + dest * E_ + e)]);
+  };
+  // Send side: my packed buffer is grouped by (dest, expert).
+  std::vector<int64_t> key_off(static_cast<size_t>(NK_));
+  int64_t acc = 0;
+  for (int64_t key = 0; key < NK_; ++key) {
+    key_off[static_cast<size_t>(key)] = acc;
+    acc += cnt(rank_, key / E_, key % E_);
+  }
+  (void)T;
+  std::vector<int32_t> grs, grows, gslot;
+  for (int64_t e = 0; e < E_; ++e) {
+    const int32_t sl = slot_of_expert_[static_cast<size_t>(e)];
+    if (sl < 0) continue;
+    grs.push_back(static_cast<int32_t>(key_off[static_cast<size_t>(rank_ * E_ + e)]));
+    grows.push_back(static_cast<int32_t>(cnt(rank_, rank_, e)));
+    gslot.push_back(sl);
+  }
+  int64_t recv_at = Tmax_ * k_;
+  for (size_t i = 0; i < a2a_peers_.size(); ++i) {
+    const int64_t p = a2a_peers_[i];
+    send_off_[i] = key_off[static_cast<size_t>(p * E_)];
+    int64_t sr = 0;
+    for (int64_t e = 0; e < E_; ++e) sr += cnt(rank_, p, e);
+    send_rows_[i] = sr;
+    recv_off_[i] = recv_at;
+    int64_t rr = 0;
+    for (int64_t e = 0; e < E_; ++e) {
+      const int64_t c = cnt(p, rank_, e);
+      if (c == 0) { continue; }
+      const int32_t sl = slot_of_expert_[static_cast<size_t>(e)];
+      if (sl < 0) throw std::runtime_error("received rows for an expert this GPU does not hold");
+      grs.push_back(static_cast<int32_t>(recv_at + rr));
+      grows.push_back(static_cast<int32_t>(c));
+      gslot.push_back(sl);
+      rr += c;
+    }
+    recv_rows_[i] = rr;
+    recv_at += rr;
+  }
+  num_groups_ = static_cast<int>(grs.size());
+  ck(cudaMemcpyAsync(g_row_start_.p, grs.data(), sizeof(int32_t) * grs.size(), cudaMemcpyHostToDevice, s), "groups");
+  ck(cudaMemcpyAsync(g_rows_.p, grows.data(), sizeof(int32_t) * grows.size(), cudaMemcpyHostToDevice, s), "groups");
+  ck(cudaMemcpyAsync(g_slot_.p, gslot.data(), sizeof(int32_t) * gslot.size(), cudaMemcpyHostToDevice, s), "groups");
+}
+
+void Layer::exchange(bool dispatch, cudaStream_t s) {
+  if (a2a_peers_.empty()) return;
+  const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
+  uint8_t* buf = (dispatch ? xall_ : oall_).as<uint8_t>();
+  nck(ncclGroupStart(), "group start");
+  for (size_t i = 0; i < a2a_peers_.size(); ++i) {
+    const int p = static_cast<int>(a2a_peers_[i]);
+    // dispatch: my rows for p go out, p's rows for me come in; combine reverses it.
+    const int64_t out_off = dispatch ? send_off_[i] : recv_off_[i];
+    const int64_t out_rows = dispatch ? send_rows_[i] : recv_rows_[i];
+    const int64_t in_off = dispatch ? recv_off_[i] : send_off_[i];
+    const int64_t in_rows = dispatch ? recv_rows_[i] : send_rows_[i];
+    if (out_rows) nck(ncclSend(buf + eb * out_off * H_, out_rows * H_, nccl_type(dt_), p, comm_->nccl, s), "a2a send");
+    if (in_rows) nck(ncclRecv(buf + eb * in_off * H_, in_rows * H_, nccl_type(dt_), p, comm_->nccl, s), "a2a recv");
+  }
+  nck(ncclGroupEnd(), "group end");
+}
+
+void Layer::run_expert_gemms(cudaStream_t s) {
+  GroupTable gt{g_row_start_.as<int>(), g_rows_.as<int>(), g_slot_.as<int>(), num_groups_};
+  if (dt_ == DType::BF16) {
+    mark("gemm_up", s);
+    ck(launch_grouped_gemm_bf16(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s), "gemm up");
+    mark("gemm_down", s);
+    ck(launch_grouped_gemm_bf16(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s), "gemm down");
+  } else {
+    mark("gemm_up", s);
+    ck(launch_grouped_gemm_f32(xall_.as<float>(), static_cast<int>(H_), w_up_c_.as<float>(), hbuf_.as<float>(), static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_ * 2, s), "gemm up");
+    mark("gemm_down", s);
+    ck(launch_grouped_gemm_f32(hbuf_.as<float>(), static_cast<int>(F_), w_down_c_.as<float>(), oall_.as<float>(), static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_ * 2, s), "gemm down");
+  }
+  launches_ += 2;
+}
+
+void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
+  if (T <= 0 || T > Tmax_) throw std::invalid_argument("token count must be in [1, max_tokens]");
+  launches_ = 0;
+  const int Ti = static_cast<int>(T);
+  const int nchunks = (Ti + 31) / 32;
+  mark("gate", s);
+  ck(launch_gate(dt_, x, wg_t_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(E_), static_cast<int>(k_),
+                 d_route_.as<int>(), static_cast<int>(n_), static_cast<int>(NK_), topk_idx_.as<int>(),
+                 topk_w_.as<float>(), keys_.as<int>(), ranks_.as<int>(), chunk_counts_.as<int>(), s), "gate");
+  mark("scan", s);
+  ck(launch_chunk_scan(chunk_counts_.as<int>(), nchunks, static_cast<int>(NK_), chunk_off_.as<int>(), key_total_.as<int>(), s), "chunk scan");
+  ck(launch_key_scan(key_total_.as<int>(), static_cast<int>(G_), static_cast<int>(E_), rank_, d_slot_of_expert_.as<int>(),
+                     key_off_.as<int>(), dest_rows_.as<int>(), dest_off_.as<int>(), g_row_start_.as<int>(),
+                     g_rows_.as<int>(), g_slot_.as<int>(), s), "key scan");
+  mark("permute", s);
+  ck(launch_permute(dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), static_cast<int>(NK_), keys_.as<int>(),
+                    ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), pos_.as<int>(), xall_.p, s), "permute");
+  launches_ += 4;
+  num_groups_ = static_cast<int>(slots_);
+  if (G_ > 1) {
+    mark("dispatch", s);
+    build_comm_plan_and_groups(Ti, s);
+    exchange(true, s);
+  }
+  run_expert_gemms(s);
+  if (G_ > 1) {
+    mark("combine_a2a", s);
+    exchange(false, s);
+  }
+  mark("combine", s);
+  ck(launch_combine(dt_, oall_.p, pos_.as<int>(), topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine");
+  launches_ += 1;
+  mark("end", s);
+}
+
+void Layer::collect_timings(char* names, size_t names_cap, float* ms, int cap, int* count) {
+  std::vector<std::string> order;
+  std::vector<double> total;
+  std::vector<int> hits;
+  if (!marks_.empty()) ck(cudaEventSynchronize(marks_.back().second), "event sync");
+  for (size_t i = 0; i + 1 < marks_.size(); ++i) {
+    if (marks_[i].first == "end") continue;  // forward boundary
+    float t = 0.f;
+    ck(cudaEventElapsedTime(&t, marks_[i].second, marks_[i + 1].second), "elapsed");
+    size_t j = 0;
+    while (j < order.size() && order[j] != marks_[i].first) ++j;
+    if (j == order.size()) { order.push_back(marks_[i].first); total.push_back(0); hits.push_back(0); }
+    total[j] += t;
+    hits[j] += 1;
+  }
+  marks_.clear();
+  std::string joined;
+  int c = 0;
+  for (size_t j = 0; j < order.size() && c < cap; ++j, ++c) {
+    ms[c] = static_cast<float>(total[j] / hits[j]);
+    if (!joined.empty()) joined += ';';
+    joined += order[j];
+  }
+  *count = c;
+  if (names && names_cap) {
+    std::strncpy(names, joined.c_str(), names_cap - 1);
+    names[names_cap - 1] = 0;
+  }
+}
+
+void Layer::forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s) {
+  const size_t bytes = static_cast<size_t>(T * H_ * dtype_bytes(dt_));
+  if (T <= 0 || T > Tmax_) throw std::invalid_argument("token count must be in [1, max_tokens]");
+  ck(cudaMemcpyAsync(x_dev_.p, hx, bytes, cudaMemcpyHostToDevice, s), "h2d");
+  forward(x_dev_.p, T, y_dev_.p, s);
+  ck(cudaMemcpyAsync(hy, y_dev_.p, bytes, cudaMemcpyDeviceToHost, s), "d2h");
+}
+
+}  // namespace hep

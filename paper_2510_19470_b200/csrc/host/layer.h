@@ -1,0 +1,108 @@
+// MoE-layer step executor (C++ host side of the B200 path).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.h"
+#include "hep.h"
+#include "hybridep/sparsecomp.hpp"
+#include "hybridep/topology.hpp"
+
+namespace hep {
+
+struct Comm {
+  ncclComm_t nccl = nullptr;
+  int rank = 0;
+  int nranks = 1;
+};
+
+// Device buffer with RAII.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(size_t n);
+  void release();
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+class Layer {
+ public:
+  Layer(const hep_layer_params& prm, Comm* comm);
+  ~Layer();
+
+  void set_gate(const void* w_gate, DType dt, cudaStream_t s);
+  void set_expert(int64_t e, const void* w_up, const void* w_down, DType dt, cudaStream_t s);
+  void set_shared(const float* shared, cudaStream_t s);  // SR mode: fp32 flat P
+  void gather_experts(cudaStream_t s);
+  void forward(const void* x, int64_t T, void* y, cudaStream_t s);
+  void forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s);
+
+  // introspection
+  const int* topk_idx() const { return topk_idx_.as<int>(); }
+  const float* topk_w() const { return topk_w_.as<float>(); }
+  const int* pos() const { return pos_.as<int>(); }
+  const void* packed() const { return xall_.p; }
+  const int* key_counts() const { return key_total_.as<int>(); }
+  void set_profiling(bool on) { profiling_ = on; }
+  // Mean device time per named phase over every profiled forward since the last call.
+  void collect_timings(char* names, size_t names_cap, float* ms, int cap, int* count);
+  int launch_count() const { return launches_; }
+
+ private:
+  void mark(const char* name, cudaStream_t s);
+  void build_comm_plan_and_groups(int T, cudaStream_t s);
+  void exchange(bool dispatch, cudaStream_t s);
+  void run_expert_gemms(cudaStream_t s);
+
+  // shape
+  int64_t H_, F_, E_, k_, Tmax_, G_, n_, NK_;
+  DType dt_;
+  int rank_;
+  bool use_sr_;
+  hybridep::sr::CompressionConfig sr_cfg_;
+  hybridep::topo::ClusterSpec cluster_;
+  Comm* comm_;
+  int num_sms_;
+
+  // routing / placement
+  std::vector<int32_t> route_row_;         // dest GPU for each owner
+  std::vector<int64_t> held_owners_;       // owners whose experts this GPU holds
+  std::vector<int32_t> slot_of_expert_;    // -1 if not held
+  std::vector<int64_t> ag_peers_, a2a_peers_;
+  int64_t slots_;
+
+  // device state
+  DevBuf d_route_, d_slot_of_expert_, wg_t_, w_up_c_, w_down_c_;
+  DevBuf shared_, master_, wires_, sr_ws_, sr_tmp_, sr_status_;
+  DevBuf topk_idx_, topk_w_, keys_, ranks_, chunk_counts_, chunk_off_, key_total_, key_off_;
+  DevBuf dest_rows_, dest_off_, g_row_start_, g_rows_, g_slot_, all_counts_;
+  DevBuf pos_, xall_, hbuf_, oall_;
+  int64_t rows_cap_;
+  CUtensorMap map_a1_, map_b1_, map_a2_, map_b2_;
+
+  // per-forward plan
+  int num_groups_;
+  std::vector<int64_t> send_off_, send_rows_, recv_off_, recv_rows_;  // per a2a peer
+  std::vector<int32_t> h_counts_;
+
+  // host staging for forward_host
+  DevBuf x_dev_, y_dev_;
+
+  bool profiling_ = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks_;
+  std::vector<cudaEvent_t> event_pool_;
+  int launches_ = 0;
+};
+
+}  // namespace hep

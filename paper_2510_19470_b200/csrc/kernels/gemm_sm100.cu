@@ -1,0 +1,280 @@
+// K8: expert FFN grouped GEMM on the 5th-gen tensor cores (sm_100a).
+//
+//   C[r, n] = act( sum_k A[r, k] * B[slot(g) * N + n, k] )   for rows r of group g
+//
+// A (tokens, bf16, K-major) and B (expert weights, bf16, stored K-major i.e. the
+// compute copy w^T) are streamed by TMA into 128-byte-swizzled shared-memory
+// stages; one elected thread issues tcgen05.mma (M=128, N=256, K=16) into a
+// double-buffered fp32 accumulator in TMEM (2 x 256 columns); four epilogue warps
+// drain TMEM with tcgen05.ld, apply ReLU, round to bf16 and store.  The kernel is
+// persistent (one CTA per SM) and walks a device-side group table, so token
+// counts per expert never have to reach the host.
+//
+// Warp roles (192 threads): w0 TMA producer, w1 TMEM owner + MMA issuer,
+// w2..w5 epilogue (warp w drains TMEM lanes 32*(w%4) .. +31).
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hep {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int STAGES = 4;
+constexpr int ACC = 2;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = ACC * BN;  // 512
+constexpr int kMaxGroups = 512;
+constexpr int kThreads = 192;
+
+struct SmemCtl {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[ACC];
+  uint64_t tempty[ACC];
+  uint32_t tmem_base;
+  int num_tiles;
+  int tile_start[kMaxGroups + 1];
+  int row_start[kMaxGroups];
+  int rows[kMaxGroups];
+  int slot[kMaxGroups];
+};
+
+constexpr size_t kSmemBytes = 1024 + STAGES * STAGE_BYTES + sizeof(SmemCtl);
+
+__device__ __forceinline__ int find_group(const SmemCtl& s, int ng, int tile) {
+  int lo = 0, hi = ng - 1;  // largest g with tile_start[g] <= tile
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s.tile_start[mid] <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
+                         const __grid_constant__ CUtensorMap map_b, __nv_bfloat16* __restrict__ C,
+                         int ldc, int N, int K, const int* __restrict__ g_row_start,
+                         const int* __restrict__ g_rows, const int* __restrict__ g_slot, int ng,
+                         int relu) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* stage_a = smem;
+  uint8_t* stage_b = smem + STAGES * A_BYTES;
+  SmemCtl& s = *reinterpret_cast<SmemCtl*>(smem + STAGES * STAGE_BYTES);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_kb = K / BK;
+
+  // ---- group table -> tile prefix (warp 2), barriers (warp 0), TMEM (warp 1)
+  if (warp == 2) {
+    int carry = 0;
+    for (int base = 0; base < ng; base += 32) {
+      const int g = base + lane;
+      int tiles = 0;
+      if (g < ng) {
+        const int r = g_rows[g];
+        s.row_start[g] = g_row_start[g];
+        s.rows[g] = r;
+        s.slot[g] = g_slot[g];
+        tiles = ((r + BM - 1) / BM) * n_tiles;
+      }
+      int incl = tiles;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+      }
+      if (g < ng) s.tile_start[g] = carry + incl - tiles;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      s.tile_start[ng] = carry;
+      s.num_tiles = carry;
+    }
+  } else if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < ACC; ++i) {
+      mbar_init(&s.tfull[i], 1);
+      mbar_init(&s.tempty[i], 4);
+    }
+    fence_barrier_init();
+  } else if (warp == 1) {
+    tmem_alloc(&s.tmem_base, TMEM_COLS);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  const int total = s.num_tiles;
+  const uint32_t tmem_base = s.tmem_base;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const uint64_t pol_a = l2_policy_evict_first();
+      const uint64_t pol_b = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int g = find_group(s, ng, tile);
+        const int local = tile - s.tile_start[g];
+        const int m_tiles = (s.rows[g] + BM - 1) / BM;
+        const int mt = local % m_tiles, nt = local / m_tiles;
+        const int a_row = s.row_start[g] + mt * BM;
+        const int b_row = s.slot[g] * N + nt * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&s.empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&s.full[stage], STAGE_BYTES);
+          tma_load_2d(stage_a + stage * A_BYTES, &map_a, &s.full[stage], kb * BK, a_row, pol_a);
+          tma_load_2d(stage_b + stage * B_BYTES, &map_b, &s.full[stage], kb * BK, b_row, pol_b);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&s.full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_addr(stage_a + stage * A_BYTES);
+          const uint32_t b_addr = smem_addr(stage_b + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            umma_bf16(d_tmem, umma_desc_k_sw128(a_addr + 32 * k), umma_desc_k_sw128(b_addr + 32 * k),
+                      idesc, (kb | k) != 0);
+          }
+          umma_commit(&s.empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&s.tfull[acc]);
+        if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ================= epilogue (warps 2..5) =================
+    const uint32_t quarter = warp & 3u;  // TMEM lane quarter this warp may access
+    const int row_in_tile = static_cast<int>(quarter * 32 + lane);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int g = find_group(s, ng, tile);
+      const int local = tile - s.tile_start[g];
+      const int m_tiles = (s.rows[g] + BM - 1) / BM;
+      const int mt = local % m_tiles, nt = local / m_tiles;
+      const int r_local = mt * BM + row_in_tile;
+      const bool row_ok = r_local < s.rows[g];
+      __nv_bfloat16* crow = C + static_cast<size_t>(s.row_start[g] + r_local) * ldc + nt * BN;
+
+      mbar_wait(&s.tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_base = tmem_base + static_cast<uint32_t>(acc * BN) + ((quarter * 32u) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        if (nt * BN + c >= N) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_base + static_cast<uint32_t>(c), v);
+        tmem_ld_wait();
+        if (row_ok) {
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = __uint_as_float(v[i]);
+            f[i] = relu ? fmaxf(x, 0.f) : x;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) st_v4(crow + c + 8 * q, pack8(f + 8 * q));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.tempty[acc]);
+      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  __syncwarp();  // reconverge the single-lane roles before the CTA barrier
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+}  // namespace
+
+cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                              uint32_t box_rows, uint32_t box_cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C,
+                                     int ldc, int N, int K, const GroupTable& groups, int relu,
+                                     int num_sms, cudaStream_t stream) {
+  if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
+    return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        grouped_gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  grouped_gemm_bf16_kernel<<<num_sms, kThreads, kSmemBytes, stream>>>(
+      map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
+      groups.slot, groups.num_groups, relu);
+  return cudaGetLastError();
+}
+
+}  // namespace hep

@@ -1,0 +1,92 @@
+// Launchers for the sm_100a kernels (internal C++ interface; the public boundary is
+// the C-ABI in include/hep.h).  All launchers are asynchronous on `stream` and
+// return the launch status.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hep {
+
+enum class DType : int { F32 = 0, BF16 = 1 };
+
+inline int dtype_bytes(DType t) { return t == DType::F32 ? 4 : 2; }
+
+// ----------------------------------------------------------------- routing (route.cu)
+// Gate + top-k + per-32-token-chunk stable ranking.  x:[T,H] (dtype), wg_t:[E,H] fp32
+// (the gate matrix stored expert-major).  Outputs per (t, j): expert, weight, key =
+// dest*E + e, rank of (t, j) among earlier tokens of its 32-token chunk with the same
+// key; chunk_counts:[ceil(T/32), NK] with NK = G*E.
+cudaError_t launch_gate(DType dt, const void* x, const float* wg_t, int T, int H, int E, int k,
+                        const int* dest_of_owner, int experts_per_gpu, int NK, int* topk_idx,
+                        float* topk_w, int* keys, int* ranks, int* chunk_counts,
+                        cudaStream_t stream);
+
+// Column-wise exclusive scan of chunk_counts -> chunk_off, and key_total[NK].
+cudaError_t launch_chunk_scan(const int* chunk_counts, int nchunks, int NK, int* chunk_off,
+                              int* key_total, cudaStream_t stream);
+
+// Exclusive scan of key_total -> key_off; per-destination row counts/offsets
+// (dest_rows[G], dest_off[G]); and the local GEMM group table for destination
+// `self`: groups are the experts e with slot_of_expert[e] >= 0, in expert order.
+cudaError_t launch_key_scan(const int* key_total, int G, int E, int self,
+                            const int* slot_of_expert, int* key_off, int* dest_rows,
+                            int* dest_off, int* g_row_start, int* g_rows, int* g_slot,
+                            cudaStream_t stream);
+
+// pos[t*k+j] = key_off[key] + chunk_off[chunk, key] + rank; packed[pos] = x[t].
+cudaError_t launch_permute(DType dt, const void* x, int T, int H, int k, int NK, const int* keys,
+                           const int* ranks, const int* chunk_off, const int* key_off, int* pos,
+                           void* packed, cudaStream_t stream);
+
+// y[t] = sum_j w[t,j] * out[pos[t,j]]  (slot order, fp32 accumulate).
+cudaError_t launch_combine(DType dt, const void* out, const int* pos, const float* topk_w, int T,
+                           int H, int k, void* y, cudaStream_t stream);
+
+// ----------------------------------------------------------------- expert GEMM
+struct GroupTable {
+  const int* row_start;  // first row of the group in A (and in C)
+  const int* rows;       // rows in the group
+  const int* slot;       // weight slot: B rows [slot*N, slot*N + N)
+  int num_groups;
+};
+
+// bf16 tcgen05 grouped GEMM (gemm_sm100.cu): C[r, n] = act(sum_k A[r,k] B[slot*N+n, k]).
+// A:[*, K] bf16 row-major, B:[slots*N, K] bf16 (K-major), C:[*, ldc] bf16.
+cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                              uint32_t box_rows, uint32_t box_cols);
+cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C,
+                                     int ldc, int N, int K, const GroupTable& groups, int relu,
+                                     int num_sms, cudaStream_t stream);
+
+// fp32 SIMT grouped GEMM (gemm_f32.cu), same contract with fp32 operands.
+cudaError_t launch_grouped_gemm_f32(const float* A, int lda, const float* B, float* C, int ldc,
+                                    int N, int K, const GroupTable& groups, int relu,
+                                    int num_blocks, cudaStream_t stream);
+
+// ----------------------------------------------------------------- SR codec (sr_codec.cu)
+struct SrPlan {
+  int64_t h, m;           // w_up is h x m, w_down is m x h
+  int64_t total;          // P = 2 h m
+  int64_t k, k_up, k_down;
+  int per_matrix;
+  uint32_t index_bits, value_bits;
+  size_t wire_bytes;
+};
+
+size_t sr_workspace_bytes();
+cudaError_t launch_sr_encode(DType expert_dt, const void* expert, const float* shared,
+                             const SrPlan& plan, void* wire, void* workspace, cudaStream_t stream);
+// Validates the wire (status[0] = code, 0 ok) and writes out = shared + residual (fp32).
+cudaError_t launch_sr_decode(const void* wire, size_t wire_bytes, const float* shared, int64_t h,
+                             int64_t m, float* out, int32_t* status, cudaStream_t stream);
+// out = mean over experts (fp64 accumulate in list order, times 1/n, round to fp32).
+cudaError_t launch_shared_mean(DType dt, const void* const* experts, int n, int64_t P, float* out,
+                               cudaStream_t stream);
+
+// Reference-layout matrix [rows, cols] (fp32 or bf16) -> compute layout [cols, rows] in `out_dt`.
+cudaError_t launch_transpose_convert(DType in_dt, const void* in, int64_t rows, int64_t cols,
+                                     DType out_dt, void* out, cudaStream_t stream);
+
+}  // namespace hep

@@ -1,0 +1,407 @@
+// K1 gate/top-k, K2 permute/pack and K9 unpermute+combine for sm_100a.
+//
+// Semantics are the pinned S3/S5/S7 of SURVEY.md §8(c) (no reference code exists
+// for them; oracle/moe_oracle.c is the CPU restatement they are tested against):
+//   gate:    logits = x . W_g; top-k by (logit desc, expert id asc); weights =
+//            softmax over the k selected logits (fp32).
+//   permute: rows grouped by key = (destination GPU, expert), stable by (token,
+//            slot): a counting sort done as per-32-token-chunk ranks + two scans.
+//   combine: y_t = sum_j w_tj * out[pos_tj], slot order, fp32 accumulate.
+// All three are HBM-bound; they move rows with 16-byte vector accesses, one warp
+// per token row.
+
+#include <float.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hep {
+
+namespace {
+
+constexpr int kChunk = 32;      // tokens per gate block == ranking chunk
+constexpr int kHc = 64;         // hidden columns staged per step
+constexpr int kMaxE = 64;       // experts supported by the gate kernel
+constexpr int kMaxK = 8;
+
+template <typename T>
+__device__ __forceinline__ float to_f32(T v);
+template <>
+__device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// One block = one chunk of 32 tokens, 256 threads.
+template <typename T>
+__global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ x,
+                                                   const float* __restrict__ wg_t, int T_tok,
+                                                   int H, int E, int k,
+                                                   const int* __restrict__ dest_of_owner,
+                                                   int n_per_gpu, int NK, int* __restrict__ topk_idx,
+                                                   float* __restrict__ topk_w,
+                                                   int* __restrict__ keys, int* __restrict__ ranks,
+                                                   int* __restrict__ chunk_counts) {
+  __shared__ float xs[kChunk][kHc + 1];
+  __shared__ float ws[kMaxE][kHc + 1];
+  __shared__ float logits[kChunk][kMaxE + 1];
+  __shared__ int skey[kChunk][kMaxK];
+
+  const int tid = threadIdx.x;
+  const int chunk = blockIdx.x;
+  const int t0 = chunk * kChunk;
+  const int tok = tid >> 3;   // 0..31
+  const int eg = tid & 7;     // expert group: experts eg, eg+8, ...
+
+  float acc[kMaxE / 8];
+#pragma unroll
+  for (int i = 0; i < kMaxE / 8; ++i) acc[i] = 0.f;
+
+  for (int hc = 0; hc < H; hc += kHc) {
+    const int width = min(kHc, H - hc);
+    for (int i = tid; i < kChunk * kHc; i += blockDim.x) {
+      const int r = i / kHc, c = i % kHc;
+      const int t = t0 + r;
+      xs[r][c] = (t < T_tok && c < width) ? to_f32<T>(x[static_cast<size_t>(t) * H + hc + c]) : 0.f;
+    }
+    for (int i = tid; i < E * kHc; i += blockDim.x) {
+      const int e = i / kHc, c = i % kHc;
+      ws[e][c] = c < width ? wg_t[static_cast<size_t>(e) * H + hc + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int c = 0; c < kHc; ++c) {
+      const float xv = xs[tok][c];
+#pragma unroll
+      for (int i = 0; i < kMaxE / 8; ++i)
+        if (eg + 8 * i < E) acc[i] = fmaf(xv, ws[eg + 8 * i][c], acc[i]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxE / 8; ++i)
+    if (eg + 8 * i < E) logits[tok][eg + 8 * i] = acc[i];
+  __syncthreads();
+
+  // Top-k per token: warp w handles tokens 4w..4w+3.
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int q = 0; q < 4; ++q) {
+    const int r = warp * 4 + q;
+    const int t = t0 + r;
+    if (t >= T_tok) break;  // warp-uniform
+    float v0 = lane < E ? logits[r][lane] : -FLT_MAX;
+    float v1 = lane + 32 < E ? logits[r][lane + 32] : -FLT_MAX;
+    bool used0 = lane >= E, used1 = lane + 32 >= E;
+    float sel_v[kMaxK];
+    int sel_e[kMaxK];
+    for (int j = 0; j < k; ++j) {
+      // Candidate of this lane: the better of its two experts (lower id wins ties).
+      float bv = -FLT_MAX;
+      int be = 0x7fffffff;
+      if (!used0) { bv = v0; be = lane; }
+      if (!used1 && (be == 0x7fffffff || v1 > bv)) { bv = v1; be = lane + 32; }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (oe != 0x7fffffff && (be == 0x7fffffff || ov > bv || (ov == bv && oe < be))) {
+          bv = ov;
+          be = oe;
+        }
+      }
+      sel_v[j] = bv;
+      sel_e[j] = be;
+      if (be == lane) used0 = true;
+      if (be == lane + 32) used1 = true;
+    }
+    if (lane == 0) {
+      float ex[kMaxK], s = 0.f;
+      for (int j = 0; j < k; ++j) {
+        ex[j] = expf(sel_v[j] - sel_v[0]);
+        s += ex[j];
+      }
+      for (int j = 0; j < k; ++j) {
+        const size_t o = static_cast<size_t>(t) * k + j;
+        const int e = sel_e[j];
+        const int key = dest_of_owner[e / n_per_gpu] * E + e;
+        topk_idx[o] = e;
+        topk_w[o] = ex[j] / s;
+        keys[o] = key;
+        skey[r][j] = key;
+      }
+    }
+  }
+  __syncthreads();
+
+  // Stable rank of (t, j) among earlier tokens of the chunk with the same key.
+  int* counts = chunk_counts + static_cast<size_t>(chunk) * NK;
+  for (int i = tid; i < NK; i += blockDim.x) counts[i] = 0;
+  __syncthreads();
+  const int valid = min(kChunk, T_tok - t0);
+  for (int i = tid; i < valid * k; i += blockDim.x) {
+    const int r = i / k, j = i % k;
+    const int key = skey[r][j];
+    int before = 0, after = 0;
+    for (int r2 = 0; r2 < valid; ++r2) {
+      if (r2 == r) continue;
+      for (int j2 = 0; j2 < k; ++j2)
+        if (skey[r2][j2] == key) {
+          if (r2 < r) ++before; else ++after;
+        }
+    }
+    ranks[static_cast<size_t>(t0 + r) * k + j] = before;
+    if (after == 0) counts[key] = before + 1;
+  }
+}
+
+// One block per key: exclusive scan of chunk_counts[:, key] over chunks.
+__global__ void __launch_bounds__(1024) chunk_scan_kernel(const int* __restrict__ chunk_counts,
+                                                          int nchunks, int NK,
+                                                          int* __restrict__ chunk_off,
+                                                          int* __restrict__ key_total) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry_s;
+  const int key = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = 0; base < nchunks; base += blockDim.x) {
+    const int c = base + threadIdx.x;
+    const int v = c < nchunks ? chunk_counts[static_cast<size_t>(c) * NK + key] : 0;
+    int incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += o;
+      }
+      warp_sums[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int carry = carry_s;
+    const int warp_base = warp ? warp_sums[warp - 1] : 0;
+    if (c < nchunks) chunk_off[static_cast<size_t>(c) * NK + key] = carry + warp_base + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) key_total[key] = carry_s;
+}
+
+// Single block: key offsets, per-destination totals and the local group table.
+__global__ void __launch_bounds__(1024) key_scan_kernel(const int* __restrict__ key_total, int G,
+                                                        int E, int self,
+                                                        const int* __restrict__ slot_of_expert,
+                                                        int* __restrict__ key_off,
+                                                        int* __restrict__ dest_rows,
+                                                        int* __restrict__ dest_off,
+                                                        int* __restrict__ g_row_start,
+                                                        int* __restrict__ g_rows,
+                                                        int* __restrict__ g_slot) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry_s;
+  const int NK = G * E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = 0; base < NK; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int v = i < NK ? key_total[i] : 0;
+    int incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += o;
+      }
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const int carry = carry_s;
+    if (i < NK) key_off[i] = carry + (warp ? warp_sums[warp - 1] : 0) + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  // key_off is complete (same block, synced above).
+  for (int d = threadIdx.x; d < G; d += blockDim.x) {
+    int rows = 0;
+    for (int e = 0; e < E; ++e) rows += key_total[d * E + e];
+    dest_rows[d] = rows;
+    dest_off[d] = key_off[d * E];
+  }
+  if (threadIdx.x == 0) {
+    int g = 0;
+    for (int e = 0; e < E; ++e) {
+      const int s = slot_of_expert[e];
+      if (s < 0) continue;
+      g_row_start[g] = key_off[self * E + e];
+      g_rows[g] = key_total[self * E + e];
+      g_slot[g] = s;
+      ++g;
+    }
+  }
+}
+
+// One warp per token: compute the k destinations and copy the row there.
+__global__ void __launch_bounds__(256) permute_kernel(const uint8_t* __restrict__ x, int T_tok,
+                                                      int row_bytes, int k, int NK,
+                                                      const int* __restrict__ keys,
+                                                      const int* __restrict__ ranks,
+                                                      const int* __restrict__ chunk_off,
+                                                      const int* __restrict__ key_off,
+                                                      int* __restrict__ pos,
+                                                      uint8_t* __restrict__ packed) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T_tok) return;
+  const int chunk = t / kChunk;
+  int dst[kMaxK];
+  for (int j = 0; j < k; ++j) {
+    const size_t o = static_cast<size_t>(t) * k + j;
+    const int key = keys[o];
+    dst[j] = key_off[key] + chunk_off[static_cast<size_t>(chunk) * NK + key] + ranks[o];
+    if (lane == 0) pos[o] = dst[j];
+  }
+  const uint8_t* src = x + static_cast<size_t>(t) * row_bytes;
+  const int vecs = row_bytes >> 4;
+  for (int v = lane; v < vecs; v += 32) {
+    const uint4 val = ld_nc_v4(src + 16 * v);
+    for (int j = 0; j < k; ++j) st_v4(packed + static_cast<size_t>(dst[j]) * row_bytes + 16 * v, val);
+  }
+}
+
+// One warp per token.  bf16 rows: 8 elements per 16-byte vector.
+__global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* __restrict__ out,
+                                                           const int* __restrict__ pos,
+                                                           const float* __restrict__ w, int T_tok,
+                                                           int H, int k,
+                                                           __nv_bfloat16* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T_tok) return;
+  int p[kMaxK];
+  float wt[kMaxK];
+  for (int j = 0; j < k; ++j) {
+    p[j] = pos[static_cast<size_t>(t) * k + j];
+    wt[j] = w[static_cast<size_t>(t) * k + j];
+  }
+  const int vecs = H >> 3;
+  for (int v = lane; v < vecs; v += 32) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < k; ++j) {
+      float f[8];
+      unpack8(ld_nc_v4(out + static_cast<size_t>(p[j]) * H + 8 * v), f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fmaf(wt[j], f[i], acc[i]);
+    }
+    st_v4(y + static_cast<size_t>(t) * H + 8 * v, pack8(acc));
+  }
+}
+
+__global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restrict__ out,
+                                                          const int* __restrict__ pos,
+                                                          const float* __restrict__ w, int T_tok,
+                                                          int H, int k, float* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T_tok) return;
+  int p[kMaxK];
+  float wt[kMaxK];
+  for (int j = 0; j < k; ++j) {
+    p[j] = pos[static_cast<size_t>(t) * k + j];
+    wt[j] = w[static_cast<size_t>(t) * k + j];
+  }
+  const int vecs = H >> 2;
+  for (int v = lane; v < vecs; v += 32) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      const uint4 r = ld_nc_v4(out + static_cast<size_t>(p[j]) * H + 4 * v);
+      acc.x = fmaf(wt[j], __uint_as_float(r.x), acc.x);
+      acc.y = fmaf(wt[j], __uint_as_float(r.y), acc.y);
+      acc.z = fmaf(wt[j], __uint_as_float(r.z), acc.z);
+      acc.w = fmaf(wt[j], __uint_as_float(r.w), acc.w);
+    }
+    reinterpret_cast<float4*>(y + static_cast<size_t>(t) * H)[v] = acc;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_gate(DType dt, const void* x, const float* wg_t, int T, int H, int E, int k,
+                        const int* dest_of_owner, int experts_per_gpu, int NK, int* topk_idx,
+                        float* topk_w, int* keys, int* ranks, int* chunk_counts,
+                        cudaStream_t stream) {
+  if (E > kMaxE || k > kMaxK || k > E || T <= 0) return cudaErrorInvalidValue;
+  const int nchunks = (T + kChunk - 1) / kChunk;
+  if (dt == DType::BF16)
+    gate_kernel<__nv_bfloat16><<<nchunks, 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(x), wg_t, T, H, E, k, dest_of_owner, experts_per_gpu, NK,
+        topk_idx, topk_w, keys, ranks, chunk_counts);
+  else
+    gate_kernel<float><<<nchunks, 256, 0, stream>>>(static_cast<const float*>(x), wg_t, T, H, E, k,
+                                                    dest_of_owner, experts_per_gpu, NK, topk_idx,
+                                                    topk_w, keys, ranks, chunk_counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_scan(const int* chunk_counts, int nchunks, int NK, int* chunk_off,
+                              int* key_total, cudaStream_t stream) {
+  const int threads = nchunks >= 1024 ? 1024 : ((nchunks + 31) / 32) * 32;
+  chunk_scan_kernel<<<NK, threads, 0, stream>>>(chunk_counts, nchunks, NK, chunk_off, key_total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_key_scan(const int* key_total, int G, int E, int self,
+                            const int* slot_of_expert, int* key_off, int* dest_rows,
+                            int* dest_off, int* g_row_start, int* g_rows, int* g_slot,
+                            cudaStream_t stream) {
+  key_scan_kernel<<<1, 1024, 0, stream>>>(key_total, G, E, self, slot_of_expert, key_off,
+                                          dest_rows, dest_off, g_row_start, g_rows, g_slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute(DType dt, const void* x, int T, int H, int k, int NK, const int* keys,
+                           const int* ranks, const int* chunk_off, const int* key_off, int* pos,
+                           void* packed, cudaStream_t stream) {
+  const int row_bytes = H * dtype_bytes(dt);
+  if (row_bytes % 16) return cudaErrorInvalidValue;
+  const int blocks = (T + 7) / 8;
+  permute_kernel<<<blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(x), T, row_bytes, k, NK,
+                                             keys, ranks, chunk_off, key_off, pos,
+                                             static_cast<uint8_t*>(packed));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(DType dt, const void* out, const int* pos, const float* topk_w, int T,
+                           int H, int k, void* y, cudaStream_t stream) {
+  const int blocks = (T + 7) / 8;
+  if (dt == DType::BF16) {
+    if (H % 8) return cudaErrorInvalidValue;
+    combine_bf16_kernel<<<blocks, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(out), pos,
+                                                    topk_w, T, H, k,
+                                                    static_cast<__nv_bfloat16*>(y));
+  } else {
+    if (H % 4) return cudaErrorInvalidValue;
+    combine_f32_kernel<<<blocks, 256, 0, stream>>>(static_cast<const float*>(out), pos, topk_w, T,
+                                                   H, k, static_cast<float*>(y));
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hep

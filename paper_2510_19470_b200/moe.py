@@ -1,0 +1,153 @@
+"""MoE-layer step (hybridep::moe) over the C-ABI: the drop-in for the step the
+reference simulates (sim::build_schedule, simcore.cpp:96-266).
+
+    layer = MoELayer(hidden=4096, ffn=14336, experts=8, top_k=2, max_tokens=16384,
+                     dtype=torch.bfloat16, sf=[2, 4], sed=[1, 4], rank=r, comm=comm)
+    layer.set_gate(w_gate)                    # H x E
+    layer.set_expert(e, w_up, w_down)         # owned experts, reference layout
+    layer.gather_experts()                    # expert-domain All-Gather (dense or SR)
+    y = layer.forward(x)                      # [T, H] -> [T, H]
+
+Communication is NCCL inside libhep.so; `Communicator.from_torch()` only uses
+torch.distributed to broadcast the NCCL unique id.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from ._lib import HEP_BF16, HEP_F32, LayerParams, Level, SrConfig, check, lib
+from .sr import CompressionConfig
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dt(dtype) -> int:
+    return {torch.float32: HEP_F32, torch.bfloat16: HEP_BF16}[dtype]
+
+
+class Communicator:
+    def __init__(self, handle, rank: int, nranks: int):
+        self.handle, self.rank, self.nranks = handle, rank, nranks
+
+    @staticmethod
+    def from_torch(group=None) -> "Communicator":
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            check(lib.hep_comm_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        check(lib.hep_comm_init(uid, rank, world, C.byref(h)))
+        return Communicator(h, rank, world)
+
+    def close(self):
+        if self.handle:
+            check(lib.hep_comm_destroy(self.handle))
+            self.handle = None
+
+
+class MoELayer:
+    def __init__(self, *, hidden, ffn, experts, top_k, max_tokens, dtype=torch.bfloat16, sf=(1,), sed=None,
+                 rank=0, comm: Optional[Communicator] = None, sr: Optional[CompressionConfig] = None):
+        sed = list(sed) if sed is not None else [1] * len(sf)
+        self.H, self.F, self.E, self.k, self.Tmax = hidden, ffn, experts, top_k, max_tokens
+        self.dtype, self.sf, self.sed, self.rank = dtype, list(sf), sed, rank
+        self.G = 1
+        for s in sf:
+            self.G *= s
+        self.n = experts // self.G
+        self._levels = (Level * len(sf))(*[Level(a, b, 1e9) for a, b in zip(sf, sed)])
+        srcfg = sr._c() if sr is not None else SrConfig(1.0, -1, 32, 32, 0)
+        prm = LayerParams(hidden, ffn, experts, top_k, max_tokens, _dt(dtype), self._levels, len(sf), rank,
+                          1 if sr is not None else 0, srcfg)
+        self.handle = C.c_void_p()
+        check(lib.hep_layer_create(C.byref(prm), comm.handle if comm else None, C.byref(self.handle)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.hep_layer_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    def owned_experts(self):
+        return range(self.rank * self.n, (self.rank + 1) * self.n)
+
+    def set_gate(self, w_gate: torch.Tensor, stream=None):
+        w_gate = w_gate.contiguous()
+        check(lib.hep_layer_set_gate(self.handle, w_gate.data_ptr(), _dt(w_gate.dtype), _stream(stream)))
+
+    def set_expert(self, e: int, w_up: torch.Tensor, w_down: torch.Tensor, stream=None):
+        w_up, w_down = w_up.contiguous(), w_down.contiguous()
+        check(lib.hep_layer_set_expert(self.handle, e, w_up.data_ptr(), w_down.data_ptr(), _dt(w_up.dtype),
+                                       _stream(stream)))
+
+    def set_shared(self, shared_flat_f32: torch.Tensor, stream=None):
+        check(lib.hep_layer_set_shared(self.handle, shared_flat_f32.data_ptr(), _stream(stream)))
+
+    def gather_experts(self, stream=None):
+        check(lib.hep_layer_gather_experts(self.handle, _stream(stream)))
+
+    def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        assert x.is_cuda and x.dtype == self.dtype and x.shape[-1] == self.H and x.is_contiguous()
+        T = x.shape[0]
+        y = out if out is not None else torch.empty_like(x)
+        check(lib.hep_layer_forward(self.handle, x.data_ptr(), T, y.data_ptr(), _stream(stream)))
+        return y
+
+    __call__ = forward
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor, stream=None):
+        """End-to-end call with host buffers (pinned recommended)."""
+        check(lib.hep_layer_forward_host(self.handle, x_host.data_ptr(), x_host.shape[0], y_host.data_ptr(),
+                                         _stream(stream)))
+
+    def debug(self, T: int):
+        """Device views of the last forward's routing: topk_idx, topk_w, pos, key_counts."""
+        ti, tw, pos, packed, kc = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib.hep_layer_debug(self.handle, C.byref(ti), C.byref(tw), C.byref(pos), C.byref(packed), C.byref(kc)))
+        dev = torch.cuda.current_device()
+
+        def view(ptr, n, dtype):
+            class _Dev:  # zero-copy view of layer-owned device memory, then an owned copy
+                __cuda_array_interface__ = {"shape": (n,), "version": 3, "data": (ptr.value, True),
+                                            "typestr": {torch.int32: "<i4", torch.float32: "<f4",
+                                                        torch.bfloat16: "<u2"}[dtype]}
+            t = torch.as_tensor(_Dev(), device=dev).clone()
+            return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
+
+        kT = T * self.k
+        rows = kT  # packed send rows of this GPU
+        return {
+            "topk_idx": view(ti, kT, torch.int32).view(T, self.k),
+            "topk_w": view(tw, kT, torch.float32).view(T, self.k),
+            "pos": view(pos, kT, torch.int32).view(T, self.k),
+            "packed": view(packed, rows * self.H, self.dtype).view(rows, self.H),
+            "key_counts": view(kc, self.G * self.E, torch.int32),
+        }
+
+    def set_profiling(self, on: bool):
+        check(lib.hep_layer_set_profiling(self.handle, int(on)))
+
+    def timings(self) -> dict:
+        names = C.create_string_buffer(1024)
+        ms = (C.c_float * 32)()
+        cnt = C.c_int()
+        check(lib.hep_layer_timings(self.handle, names, 1024, ms, 32, C.byref(cnt)))
+        keys = names.value.decode().split(";") if cnt.value else []
+        return dict(zip(keys, list(ms)[: cnt.value]))
+
+    def launch_count(self) -> int:
+        c = C.c_int()
+        check(lib.hep_layer_launch_count(self.handle, C.byref(c)))
+        return c.value

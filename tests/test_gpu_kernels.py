@@ -1,0 +1,179 @@
+"""Device kernels through the C-ABI vs the oracle / an fp32 reference (GPU only)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2510_19470_b200 import sr as srmod
+from paper_2510_19470_b200._lib import HEP_BF16, HEP_F32, check, lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _groups(rows, slots):
+    starts = np.concatenate([[0], np.cumsum(rows)[:-1]]).astype(np.int32)
+    return (torch.tensor(starts, dtype=torch.int32, device="cuda"),
+            torch.tensor(np.asarray(rows, np.int32), device="cuda"),
+            torch.tensor(np.asarray(slots, np.int32), device="cuda"))
+
+
+def _gemm(dtype, A, B, n_slots, N, K, rows, slots, relu):
+    R = A.shape[0]
+    Cout = torch.full((R, N), float("nan"), dtype=A.dtype, device="cuda")
+    gs, gr, gl = _groups(rows, slots)
+    check(lib.hep_grouped_gemm(dtype, A.data_ptr(), R, B.data_ptr(), n_slots, Cout.data_ptr(), N, K,
+                               gs.data_ptr(), gr.data_ptr(), gl.data_ptr(), len(rows), relu, _stream()))
+    torch.cuda.synchronize()
+    return Cout
+
+
+def _reference(A, B, N, rows, slots, relu):
+    out = []
+    start = 0
+    for r, s in zip(rows, slots):
+        a = A[start:start + r].double()
+        b = B[s * N:(s + 1) * N].double()
+        y = a @ b.T
+        out.append(torch.relu(y) if relu else y)
+        start += r
+    return torch.cat(out) if out else None
+
+
+@pytest.mark.parametrize("K,N,rows,relu", [
+    (256, 512, [300, 0, 128, 1, 77], 1),
+    (1408, 2048, [129, 256], 0),      # cfg4 down-projection K, N multiple of 256
+    (2048, 1408, [200, 513], 1),      # cfg4 up-projection: N tail (1408 = 5.5 x 256)
+    (4096, 768, [1000], 0),
+])
+def test_grouped_gemm_bf16(K, N, rows, relu):
+    g = torch.Generator(device="cuda").manual_seed(1)
+    n_slots = 3
+    R = sum(rows)
+    A = (torch.randn(R, K, generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+    B = (torch.randn(n_slots * N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    slots = [i % n_slots for i in range(len(rows))]
+    got = _gemm(HEP_BF16, A, B, n_slots, N, K, rows, slots, relu).double()
+    ref = _reference(A, B, N, rows, slots, relu)
+    # tolerance: bf16 output rounding (2^-8 relative) + fp32 accumulation
+    err = (got - ref).abs()
+    tol = 2 ** -8 * ref.abs() + 1e-3 * ref.abs().max()
+    assert torch.isfinite(got).all()
+    assert (err <= tol).all(), f"max err {err.max().item()}"
+
+
+@pytest.mark.parametrize("K,N,rows", [(1024, 4096, [130, 0, 512]), (4096, 1024, [257, 31])])
+def test_grouped_gemm_f32(K, N, rows):
+    g = torch.Generator(device="cuda").manual_seed(2)
+    n_slots = 2
+    R = sum(rows)
+    A = torch.randn(R, K, generator=g, device="cuda")
+    B = torch.randn(n_slots * N, K, generator=g, device="cuda") * 0.03
+    slots = [i % n_slots for i in range(len(rows))]
+    got = _gemm(HEP_F32, A, B, n_slots, N, K, rows, slots, 1).double()
+    ref = _reference(A, B, N, rows, slots, 1)
+    rel = (got - ref).abs().max() / ref.abs().max()
+    assert rel < 1e-5, rel
+
+
+def _demo_expert_pair(h, m, seed, quantize=False):
+    rng = np.random.default_rng(seed)
+    P = 2 * h * m
+    base = (0.05 + 0.95 * rng.random(P)) * np.where(rng.random(P) < 0.5, -1, 1)
+    e = (base + rng.uniform(-0.05, 0.05, P)).astype(np.float32)
+    s = base.astype(np.float32)
+    if quantize:  # heavy ties in |r|
+        e = (s + np.round(rng.uniform(-4, 4, P)) / 64).astype(np.float32)
+    return e, s
+
+
+@pytest.mark.parametrize("h,m,ratio,k,iw,vw,per_matrix,quant", [
+    (16, 24, None, 40, 32, 32, False, False),
+    (16, 24, None, 40, 64, 64, False, True),
+    (32, 8, None, 100, 32, 64, True, True),
+    (64, 96, 50.0, None, 32, 32, False, False),
+    (64, 96, 50.0, None, 32, 32, True, False),
+    (8, 8, None, 0, 32, 32, False, False),
+    (8, 8, None, 10 ** 9, 32, 32, False, False),
+    (333, 77, 7.0, None, 64, 32, False, True),
+])
+def test_sr_encode_decode_bitexact(h, m, ratio, k, iw, vw, per_matrix, quant):
+    e, s = _demo_expert_pair(h, m, seed=h * 1000 + m, quantize=quant)
+    want = oracle.sr_encode(e, s, h, m, ratio=ratio, k=k, iw=iw, vw=vw, per_matrix=per_matrix,
+                            use_ref=oracle.ref is not None)
+    cfg = srmod.CompressionConfig(ratio_CR=ratio, k=k, index_width_bits=iw, value_width_bits=vw,
+                                  per_matrix_budget=per_matrix)
+    et, st = torch.from_numpy(e).cuda(), torch.from_numpy(s).cuda()
+    wire = srmod.sr_encode(et, st, h, m, cfg)
+    torch.cuda.synchronize()
+    got = wire.cpu().numpy()
+    assert got.tobytes() == want.tobytes(), "SRC1 wire differs from the reference"
+    dec = srmod.sr_decode(wire, st, h, m).cpu().numpy()
+    rc, want_dec = oracle.sr_decode(want, s, h, m, use_ref=oracle.ref is not None)
+    assert rc == 0
+    assert dec.tobytes() == want_dec.tobytes(), "decoded expert differs from the reference"
+
+
+def test_sr_bf16_expert_upcast():
+    h, m = 48, 40
+    e, s = _demo_expert_pair(h, m, seed=5)
+    e_bf = torch.from_numpy(e).to(torch.bfloat16)
+    want = oracle.sr_encode(e_bf.float().numpy(), s, h, m, k=200)
+    wire = srmod.sr_encode(e_bf.cuda(), torch.from_numpy(s).cuda(), h, m, srmod.CompressionConfig(k=200))
+    assert wire.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_sr_cfg4_expert_bitexact():
+    """Full cfg4 expert (H=2048, F=1408, P=5,767,168) at CR=50 against the reference."""
+    h, m = 2048, 1408
+    e, s = _demo_expert_pair(h, m, seed=11)
+    want = oracle.sr_encode(e, s, h, m, ratio=50.0, use_ref=oracle.ref is not None)
+    assert want.size == 461396
+    cfg = srmod.CompressionConfig(ratio_CR=50.0)
+    wire = srmod.sr_encode(torch.from_numpy(e).cuda(), torch.from_numpy(s).cuda(), h, m, cfg)
+    assert wire.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_sr_decode_rejects_corrupt_wires():
+    from paper_2510_19470_b200._lib import InvalidArgument, RuntimeFailure
+
+    h, m = 4, 4
+    e, s = _demo_expert_pair(h, m, seed=3)
+    st = torch.from_numpy(s).cuda()
+    good = oracle.sr_encode(e, s, h, m, k=4)
+    cases = []
+    bad = good.copy(); bad[3] = ord("2"); cases.append((bad, RuntimeFailure, 1))           # magic
+    cases.append((good[:20].copy(), RuntimeFailure, 2))                                     # truncated header
+    bad = good.copy(); bad[20] = 16; cases.append((bad, RuntimeFailure, 3))                # widths
+    cases.append((good[:28 + 8 * 3].copy(), RuntimeFailure, 2))                             # truncated entries
+    bad = good.copy(); bad[28:32] = np.frombuffer(np.uint32(1000).tobytes(), np.uint8); cases.append((bad, RuntimeFailure, 5))
+    bad = good.copy(); bad[36:40] = bad[28:32]; cases.append((bad, RuntimeFailure, 6))      # repeated index
+    for wire, exc, code in cases:
+        rc, _ = oracle.sr_decode(wire, s, h, m)
+        assert rc == code
+        with pytest.raises(exc):
+            srmod.sr_decode(torch.from_numpy(wire).cuda(), st, h, m)
+    with pytest.raises(InvalidArgument):
+        srmod.sr_decode(torch.from_numpy(good).cuda(), torch.zeros(2 * 5 * 4, device="cuda"), 5, 4)
+
+
+def test_shared_mean_bitexact():
+    rng = np.random.default_rng(7)
+    h, m, n = 64, 48, 8
+    experts = [rng.standard_normal(2 * h * m).astype(np.float32) for _ in range(n)]
+    want = oracle.shared_mean(experts, use_ref=oracle.ref is not None, h=h, m=m)
+    got = srmod.shared_mean([torch.from_numpy(x).cuda() for x in experts]).cpu().numpy()
+    assert got.tobytes() == want.tobytes()
+
+
+def test_transpose_convert():
+    x = torch.randn(100, 260, device="cuda")
+    out = torch.empty(260, 100, dtype=torch.bfloat16, device="cuda")
+    check(lib.hep_transpose_convert(HEP_F32, x.data_ptr(), 100, 260, HEP_BF16, out.data_ptr(), _stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(out, x.T.contiguous().to(torch.bfloat16))

@@ -1,0 +1,117 @@
+"""Full MoE-layer step through the C-ABI vs the CPU oracle (GPU only).
+
+Routing (top-k indices), the permutation (pos) and per-(dest, expert) counts must be
+bit-exact; outputs within the stated tolerance:
+  * fp32 layers: max |y - y_ref| <= 1e-4 * max |y_ref|   (north_star: 1e-4 relative)
+  * bf16 layers: max |y - y_ref| <= 2e-2 * max |y_ref| and mean abs err <= 2e-3 * max |y_ref|
+    (the oracle mirrors the bf16 rounding points of h, y_expert and y; the remaining
+    difference is fp32-vs-fp64 accumulation flipping bf16 roundings)
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2510_19470_b200 import synthetic
+from paper_2510_19470_b200.moe import MoELayer
+
+pytestmark = pytest.mark.gpu
+
+
+def run_layer(H, F, E, k, T, dtype, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    x = synthetic.dyadic((T, H), g, dtype=dtype)
+    wg = synthetic.dyadic((H, E), g)
+    w_up, w_down = synthetic.experts(E, H, F, g, dtype=dtype)
+    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype)
+    layer.set_gate(wg.cuda())
+    for e in range(E):
+        layer.set_expert(e, w_up[e].cuda(), w_down[e].cuda())
+    y = layer.forward(x.cuda())
+    dbg = layer.debug(T)
+    torch.cuda.synchronize()
+    ref = oracle.moe_layer(x.float().numpy()[None], wg.numpy(), w_up.float().numpy(), w_down.float().numpy(), k,
+                           [1], [1], bf16=dtype == torch.bfloat16)
+    layer.close()
+    return x, y.float().cpu().numpy(), dbg, ref
+
+
+def check_routing(dbg, ref):
+    assert np.array_equal(dbg["topk_idx"].cpu().numpy(), ref["topk_idx"][0])
+    np.testing.assert_allclose(dbg["topk_w"].cpu().numpy(), ref["topk_w"][0], rtol=2e-6, atol=1e-7)
+    assert np.array_equal(dbg["pos"].cpu().numpy(), ref["pos"][0])
+    assert np.array_equal(dbg["key_counts"].cpu().numpy(), ref["key_counts"][0])
+
+
+def check_packed(x, dbg, k):
+    # packed[pos[t, j]] == x[t]
+    packed = dbg["packed"].float().cpu()
+    pos = dbg["pos"].cpu().long()
+    for j in range(k):
+        assert torch.equal(packed[pos[:, j]], x.float())
+
+
+def test_layer_fp32_cfg1_shape():
+    """cfg1 per-GPU shape (H=1024, F=4096, E=8, k=2, T=512, fp32)."""
+    x, y, dbg, ref = run_layer(1024, 4096, 8, 2, 512, torch.float32)
+    check_routing(dbg, ref)
+    check_packed(x, dbg, 2)
+    err = np.abs(y - ref["y"][0]).max() / np.abs(ref["y"][0]).max()
+    assert err <= 1e-4, err
+
+
+def test_layer_bf16_small_ragged():
+    x, y, dbg, ref = run_layer(512, 1024, 8, 2, 1000, torch.bfloat16, seed=3)
+    check_routing(dbg, ref)
+    check_packed(x, dbg, 2)
+    scale = np.abs(ref["y"][0]).max()
+    d = np.abs(y - ref["y"][0])
+    assert d.max() <= 2e-2 * scale and d.mean() <= 2e-3 * scale, (d.max() / scale, d.mean() / scale)
+
+
+def test_layer_bf16_cfg4_shape():
+    """cfg4 expert shape (H=2048, F=1408, E=64, k=6) at G=1, T=256."""
+    x, y, dbg, ref = run_layer(2048, 1408, 64, 6, 256, torch.bfloat16, seed=4)
+    check_routing(dbg, ref)
+    scale = np.abs(ref["y"][0]).max()
+    d = np.abs(y - ref["y"][0])
+    assert d.max() <= 2e-2 * scale and d.mean() <= 2e-3 * scale, (d.max() / scale, d.mean() / scale)
+
+
+def test_layer_single_token_and_repeat():
+    """Edge cases: T=1, and a second forward on the same layer reuses buffers."""
+    H, F, E, k = 256, 512, 8, 2
+    g = torch.Generator().manual_seed(9)
+    wg = synthetic.dyadic((H, E), g)
+    w_up, w_down = synthetic.experts(E, H, F, g, dtype=torch.bfloat16)
+    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=64, dtype=torch.bfloat16)
+    layer.set_gate(wg.cuda())
+    for e in range(E):
+        layer.set_expert(e, w_up[e].cuda(), w_down[e].cuda())
+    for T in (1, 64, 33):
+        x = synthetic.dyadic((T, H), g, dtype=torch.bfloat16)
+        y = layer.forward(x.cuda()).float().cpu().numpy()
+        ref = oracle.moe_layer(x.float().numpy()[None], wg.numpy(), w_up.float().numpy(), w_down.float().numpy(),
+                               k, [1], [1], bf16=True)
+        scale = np.abs(ref["y"][0]).max()
+        assert np.abs(y - ref["y"][0]).max() <= 2e-2 * scale
+    layer.close()
+
+
+def test_layer_forward_host_matches_device():
+    H, F, E, k, T = 256, 512, 8, 2, 100
+    g = torch.Generator().manual_seed(10)
+    x = synthetic.dyadic((T, H), g, dtype=torch.bfloat16)
+    wg = synthetic.dyadic((H, E), g)
+    w_up, w_down = synthetic.experts(E, H, F, g, dtype=torch.bfloat16)
+    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=torch.bfloat16)
+    layer.set_gate(wg.cuda())
+    for e in range(E):
+        layer.set_expert(e, w_up[e].cuda(), w_down[e].cuda())
+    y_dev = layer.forward(x.cuda()).cpu()
+    xh = x.pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    layer.forward_host(xh, yh)
+    torch.cuda.synchronize()
+    assert torch.equal(y_dev, yh)
+    layer.close()

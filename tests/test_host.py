@@ -1,0 +1,155 @@
+"""Host-side logic of libhep.so (no GPU needed): the reference-compatible topology /
+plan / schedule / solver API against the reference itself (oracle/_ref) and against
+the committed golden fixtures, plus the C-ABI export check."""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2510_19470_b200 import DomainError, InvalidArgument, declared_symbols, lib
+from paper_2510_19470_b200 import topology as topo
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+needs_ref = pytest.mark.skipif(oracle.ref is None, reason="reference library not built here")
+
+
+def hierarchies(G=8):
+    """Every (SF, S_ED) with prod SF = G, SF_i >= 2, S_ED_i | SF_i."""
+    def factorizations(n, start=2):
+        if n == 1:
+            yield []
+        for f in range(start, n + 1):
+            if n % f == 0:
+                for rest in factorizations(n // f, 2):
+                    yield [f] + rest
+    for sf in factorizations(G):
+        divs = [[d for d in range(1, s + 1) if s % d == 0] for s in sf]
+        for sed in itertools.product(*divs):
+            yield sf, list(sed)
+
+
+def test_exports_every_declared_symbol():
+    names = declared_symbols()
+    assert len(names) >= 35
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_renumber_goldens_and_errors():
+    c = topo.ClusterSpec.of([4, 4])
+    assert topo.renumber(9, c) == [2, 1]          # test_topology.cpp:44
+    assert topo.renumber(15, c) == [3, 3]
+    assert topo.global_index([2, 1], c) == 9
+    with pytest.raises(DomainError):
+        topo.renumber(16, c)
+    with pytest.raises(DomainError):
+        topo.renumber(-1, c)
+    with pytest.raises(DomainError):
+        topo.global_index([4, 0], c)
+    with pytest.raises(DomainError):
+        topo.global_index([0], c)
+    c2 = topo.ClusterSpec.of([2, 4])
+    assert topo.renumber(5, c2) == [1, 1] and topo.renumber(6, c2) == [1, 2]
+    assert topo.renumber(5, topo.ClusterSpec.of([2, 2, 2])) == [1, 0, 1]
+
+
+def test_flat_classification():
+    c = topo.ClusterSpec.of([8], [2])
+    assert topo.comm_type(0, 1, 0, c) == topo.AG
+    assert topo.comm_type(0, 2, 0, c) == topo.A2A
+    assert topo.comm_type(0, 3, 0, c) == topo.NONE
+    with pytest.raises(DomainError):
+        topo.comm_type(3, 3, 0, c)
+
+
+def test_invalid_clusters():
+    with pytest.raises(InvalidArgument):
+        topo.build_topology(topo.ClusterSpec.of([4], [3]))
+    with pytest.raises(InvalidArgument):
+        topo.build_topology(topo.ClusterSpec.of([2], [4]))
+
+
+def test_topology_tables_match_golden_all_8gpu_hierarchies():
+    gold = json.load(open(os.path.join(GOLDEN, "topology_g8.json")))
+    assert len(gold) == len(list(hierarchies()))
+    for case in gold:
+        t = topo.build_topology(topo.ClusterSpec.of(case["sf"], case["sed"]))
+        assert t.level.tolist() == case["level"], case["sf"]
+        assert t.type.tolist() == case["type"], case["sf"]
+        assert t.freq_a2a == case["freq_a2a"] and t.freq_ag == case["freq_ag"]
+        for m in range(8):
+            ag, a2a = topo.peer_lists(topo.ClusterSpec.of(case["sf"], case["sed"]), m)
+            assert [p for p, _ in ag] == case["ag_peers"][m]
+            assert [p for p, _ in a2a] == case["a2a_peers"][m]
+        tr = topo.traffic_report(topo.ClusterSpec.of(case["sf"], case["sed"]), 4194304.0, 33554432.0)
+        np.testing.assert_array_equal(tr["a2a_bytes"], case["a2a_bytes"])
+        np.testing.assert_array_equal(tr["ag_bytes"], case["ag_bytes"])
+
+
+@needs_ref
+def test_topology_matches_reference_random():
+    rng = np.random.default_rng(23)
+    for _ in range(40):
+        L = int(rng.integers(1, 4))
+        sf = [int(rng.integers(1, 7)) for _ in range(L)]
+        sed = [int(rng.choice([d for d in range(1, s + 1) if s % d == 0])) for s in sf]
+        lvl_r, typ_r = oracle.topology(sf, sed, lib=oracle.ref)
+        t = topo.build_topology(topo.ClusterSpec.of(sf, sed))
+        assert np.array_equal(t.level, lvl_r) and np.array_equal(t.type, typ_r), (sf, sed)
+
+
+def test_route_table_matches_oracle_restatement():
+    for sf, sed in hierarchies():
+        ours = topo.route_table(topo.ClusterSpec.of(sf, sed))
+        assert np.array_equal(ours, oracle.route_table(sf, sed)), (sf, sed)
+
+
+def test_route_table_semantics_cfg1():
+    # SF=[2,4], S_ED=[1,4]: Algorithm 1 classifies every pair whose level-1 digits
+    # differ as AG (m=0 row ". G1 G1 G1 A0 G1 G1 G1"), so after the
+    # All-Gather GPU 0 holds every expert except GPU 4's, which it reaches by A2A.
+    r = topo.route_table(topo.ClusterSpec.of([2, 4], [1, 4]))
+    assert r[0].tolist() == [0, 0, 0, 0, 4, 0, 0, 0]
+    assert r[5].tolist() == [5, 1, 5, 5, 5, 5, 5, 5]
+    # Ambiguous hierarchy SF=[2,4], S_ED=[1,2]: owner 3 from GPU 0 relays via 2 (first in ring order).
+    r = topo.route_table(topo.ClusterSpec.of([2, 4], [1, 2]))
+    assert r[0, 3] == 2
+
+
+def test_factor_domain_sizes():
+    assert topo.factor_domain_sizes(4, topo.ClusterSpec.of([2, 4])) == [1, 4]
+    assert topo.factor_domain_sizes(8, topo.ClusterSpec.of([4, 4])) == [2, 4]
+    with pytest.raises(InvalidArgument):
+        topo.factor_domain_sizes(3, topo.ClusterSpec.of([2, 4]))
+
+
+@needs_ref
+def test_solver_matches_reference():
+    import ctypes as C
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        G = int(rng.choice([2, 4, 8, 16, 32]))
+        kw = dict(data_size_D=float(rng.uniform(1e6, 5e8)), expert_size_PE=float(rng.uniform(1e6, 5e8)),
+                  experts_per_gpu_n=int(rng.integers(1, 9)), pre_blocks_m=int(rng.integers(0, 4)),
+                  attn_latency=float(rng.uniform(1e-4, 1e-2)), ffn_latency=float(rng.uniform(1e-4, 1e-2)),
+                  expert_latency=float(rng.uniform(1e-4, 1e-2)))
+        C_, B_ = 1e15, float(rng.uniform(1e9, 9e11))
+        p, s, lat = topo.solve_optimal_p(**kw, throughput_C=C_, bandwidth_B=B_, gpus=G)
+        rp, rs, rt = C.c_double(), C.c_int64(), C.c_double()
+        oracle.ref.ref_solve_optimal_p(kw["data_size_D"], kw["expert_size_PE"], kw["experts_per_gpu_n"],
+                                       kw["pre_blocks_m"], kw["attn_latency"], kw["ffn_latency"],
+                                       kw["expert_latency"], 0.0, C_, B_, G, C.byref(rp), C.byref(rs), C.byref(rt))
+        assert (p, s, lat["total"]) == (rp.value, rs.value, rt.value)
+
+
+def test_sr_resolve_k_goldens():
+    from paper_2510_19470_b200.sr import CompressionConfig
+    assert CompressionConfig(ratio_CR=50.0).resolve_k(32768, 4) == 327      # test_sparsecomp.cpp:325
+    assert CompressionConfig(ratio_CR=1.0).resolve_k(100, 4) == 50
+    assert CompressionConfig(ratio_CR=50.0).resolve_k(8388608, 4) == 83886  # cfg1 expert
+    assert CompressionConfig(ratio_CR=50.0).resolve_k(5767168, 4) == 57671  # cfg4 expert
+    with pytest.raises(InvalidArgument):
+        CompressionConfig(ratio_CR=0.5).resolve_k(100, 4)
