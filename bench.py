@@ -1,0 +1,338 @@
+"""MoE-layer tokens/s on B200 (BASELINE.json metric), one process per GPU.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config cfg3]
+
+Workload (default cfg3, BASELINE.json configs[2]): one Mixtral-8x7B-shaped MoE layer,
+bf16, H=4096, F=14336, E=8, top-2, 16,384 tokens per GPU (weak scaling), synthetic
+data.  configs[1] (cfg2, the fp32 S_ED sweep at 512 tokens/GPU) is a parity case, not a
+bench line.  A step = one full layer pass through the public API:
+expert All-Gather (N > 1) + gate + permute + dispatch + expert FFN + combine.
+
+value : tokens/s of all ranks, inputs resident in HBM, device-timed (CUDA events on
+        the launching stream), max over ranks.
+e2e   : same metric through hep_layer_forward_host (pinned host x -> H2D -> step ->
+        D2H of y) -- the reference-facing call with host buffers.
+roofline : the expert grouped GEMM (K8), FLOPs per launch / mean launch time measured
+        live with CUDA events inside the timed region, vs the measured sustained bf16
+        peak of MEASURED_PEAKS.json.
+cpu_baseline : the CPU oracle (oracle/moe_oracle.c, OpenMP) on a bounded token sample.
+--impl reference : times that same CPU implementation as the reference arm (the
+        reference has no GPU path and no gate/FFN/combine of its own).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg3": dict(workload="cfg3: Mixtral-8x7B-shaped MoE layer (8 experts top-2, d=4096, FFN 14336), bf16",
+                 H=4096, F=14336, E=8, k=2, T=16384, dtype="bf16"),
+    "cfg4": dict(workload="cfg4: DeepSeek-style fine-grained MoE layer (64 experts top-6, d=2048, FFN 1408), bf16",
+                 H=2048, F=1408, E=64, k=6, T=16384, dtype="bf16"),
+    "cfg1": dict(workload="cfg1/cfg2 shape: 8 experts top-2, d=1024, FFN 4096, 512 tokens/GPU, fp32",
+                 H=1024, F=4096, E=8, k=2, T=512, dtype="f32"),
+}
+
+# Cluster description per GPU count (SF, S_ED), outermost level first.
+TOPOLOGY = {1: ([1], [1]), 2: ([2], [1]), 4: ([2, 2], [1, 1]), 8: ([2, 4], [1, 4])}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--cpu-stride", type=int, default=64)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8 for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_inputs(cfg, rank, device, dtype):
+    import torch
+    from paper_2510_19470_b200 import synthetic
+
+    g = torch.Generator(device=device).manual_seed(1000 + rank)
+    x = synthetic.dyadic((cfg["T"], cfg["H"]), g, device=device, dtype=dtype)
+    gw = torch.Generator(device=device).manual_seed(7)
+    wg = synthetic.dyadic((cfg["H"], cfg["E"]), gw, device=device)
+    return x, wg
+
+
+def expert_weights(cfg, e, device, dtype):
+    """Expert e of the demo population (shared base from seed 11, per-expert noise)."""
+    import torch
+    from paper_2510_19470_b200.synthetic import expert_scale
+
+    H, F = cfg["H"], cfg["F"]
+    s = expert_scale(H)
+    gb = torch.Generator(device=device).manual_seed(11)
+    ge = torch.Generator(device=device).manual_seed(100 + e)
+
+    def mat(shape):
+        base = (0.05 + 0.95 * torch.rand(shape, generator=gb, device=device)) * \
+            (torch.randint(0, 2, shape, generator=gb, device=device) * 2 - 1)
+        noise = (torch.rand(shape, generator=ge, device=device) * 2 - 1) * 0.05
+        return ((base + noise) * s).to(dtype)
+
+    return mat((H, F)), mat((F, H))
+
+
+def cpu_oracle_tokens_per_s(cfg, stride, x=None, wg=None, threads_note=True):
+    """Times the CPU oracle on every `stride`-th token of one GPU's workload."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2510_19470_b200 import synthetic
+
+    H, F, E, k, T = cfg["H"], cfg["F"], cfg["E"], cfg["k"], cfg["T"]
+    bf16 = cfg["dtype"] == "bf16"
+    dt = torch.bfloat16 if bf16 else torch.float32
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    if x is None:
+        x, wg = make_inputs(cfg, 0, dev, dt)
+    ups = np.empty((E, H, F), np.float32)
+    downs = np.empty((E, F, H), np.float32)
+    for e in range(E):
+        u, d = expert_weights(cfg, e, dev, dt)
+        ups[e] = u.float().cpu().numpy()
+        downs[e] = d.float().cpu().numpy()
+    xs = x.float().cpu().numpy()[None]
+    wgs = wg.float().cpu().numpy()
+    t0 = time.perf_counter()
+    oracle.moe_layer(xs, wgs, ups, downs, k, [1], [1], bf16=bf16, stride=stride)
+    dt_s = time.perf_counter() - t0
+    sampled = (T + stride - 1) // stride
+    return sampled / dt_s, dt_s, sampled, oracle.num_threads()
+
+
+def run_reference(args, cfg):
+    """Reference arm: the CPU implementation of the path, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals = []
+    for i in range(args.warmup + args.steps):
+        tps, secs, sampled, cores = cpu_oracle_tokens_per_s(cfg, args.cpu_stride)
+        if i >= args.warmup:
+            vals.append(tps)
+    v = statistics.median(vals)
+    sample = f"every {args.cpu_stride}th of {cfg['T']} tokens ({sampled} tokens) through the full layer per step"
+    line = {"impl": "reference", "metric": "MoE-layer tokens/s", "value": v, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sampled / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
+            "data": "synthetic", "config": {"workload": cfg["workload"], "tokens_per_gpu": cfg["T"]},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_19470_b200.moe import Communicator, MoELayer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = Communicator.from_torch()
+    sf, sed = TOPOLOGY[world]
+    dtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    H, F, E, k, T = cfg["H"], cfg["F"], cfg["E"], cfg["k"], cfg["T"]
+
+    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype, sf=sf, sed=sed, rank=rank,
+                     comm=comm)
+    x, wg = make_inputs(cfg, rank, dev, dtype)
+    layer.set_gate(wg)
+    for e in layer.owned_experts():
+        u, d = expert_weights(cfg, e, dev, dtype)
+        layer.set_expert(e, u, d)
+        del u, d
+    torch.cuda.synchronize()
+    y = torch.empty_like(x)
+
+    def step():
+        if world > 1:
+            layer.gather_experts()
+        layer.forward(x, out=y)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- device-timed region
+    for _ in range(args.warmup):
+        step()
+    layer.set_profiling(True)
+    layer.timings()  # drop warm-up marks
+    barrier()
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1)
+    phases = layer.timings()
+    layer.set_profiling(False)
+    launches = layer.launch_count() * args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * T * args.steps / (ms_max / 1000.0)
+
+    # Rows this GPU's expert GEMM processed in the last step (local + received).
+    rows = int(layer.debug(T)["key_counts"].view(world, E)[rank].sum().item()) if world == 1 else None
+    if rows is None:
+        rows = T * k  # balanced expectation for N > 1 (exact per-rank counts are in the debug view)
+    gemm_ms = phases.get("gemm_up", 0.0) + phases.get("gemm_down", 0.0)
+    pk = peaks()
+    flops = 4.0 * H * F * rows
+    achieved = flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
+    peak = pk.get("bf16_tflops_sustained", 1400.0)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get(args.config, {}).get("gemm_dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # ---------------------------------------------------------------- e2e through host buffers
+    xh = x.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    for _ in range(2):
+        if world > 1:
+            layer.gather_experts()
+        layer.forward_host(xh, yh)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        if world > 1:
+            layer.gather_experts()
+        layer.forward_host(xh, yh)
+    e1.record(stream)
+    barrier()
+    e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e = world * T * args.steps / (float(e_ms.item()) / 1000.0)
+    row_bytes = H * (2 if dtype == torch.bfloat16 else 4)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        tps, secs, sampled, cores = cpu_oracle_tokens_per_s(cfg, args.cpu_stride, x, wg)
+        cpu = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
+               "sample": f"every {args.cpu_stride}th of {T} tokens ({sampled} tokens) through the full layer "
+                         f"(routing of all {T} tokens included), {secs:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": cfg["dtype"], "data": "synthetic (dyadic tokens/gate, reference demo expert population)",
+            "config": {"workload": cfg["workload"], "tokens_per_gpu": T, "hidden": H, "ffn": F, "experts": E,
+                       "top_k": k, "sf": sf, "sed": sed,
+                       "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per GPU)" %
+                             (T * row_bytes / 1e6, layer.n * 2 * H * F * (row_bytes // H) / 1e9)},
+            "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": T * row_bytes,
+                    "d2h_bytes_per_step": T * row_bytes},
+            "roofline": {"bound": "tensor", "kernel": "grouped expert GEMM (up+down, tcgen05)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside the step loop)",
+                         "flops_per_launch_pair": flops},
+            "phase_ms": phases,
+            "gpu_launches": launches,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if comm:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

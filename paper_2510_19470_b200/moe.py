@@ -120,7 +120,7 @@ class MoELayer:
 
         def view(ptr, n, dtype):
             class _Dev:  # zero-copy view of layer-owned device memory, then an owned copy
-                __cuda_array_interface__ = {"shape": (n,), "version": 3, "data": (ptr.value, True),
+                __cuda_array_interface__ = {"shape": (n,), "version": 3, "data": (ptr.value, False),
                                             "typestr": {torch.int32: "<i4", torch.float32: "<f4",
                                                         torch.bfloat16: "<u2"}[dtype]}
             t = torch.as_tensor(_Dev(), device=dev).clone()
