@@ -49,7 +49,7 @@ TOPOLOGY = {1: ([1], [1]), 2: ([2], [1]), 4: ([2, 2], [1, 1]), 8: ([2, 4], [1, 4
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
@@ -78,7 +78,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -137,17 +137,13 @@ def expert_weights(cfg, e, device, dtype):
     return mat((H, F)), mat((F, H))
 
 
-def cpu_oracle_tokens_per_s(cfg, stride, x=None, wg=None, threads_note=True):
-    """Times the CPU oracle on every `stride`-th token of one GPU's workload."""
+def cpu_oracle_inputs(cfg, x=None, wg=None):
+    """The same synthetic workload as the GPU arm, as fp32 host arrays for the oracle."""
     import numpy as np
     import torch
 
-    import oracle
-    from paper_2510_19470_b200 import synthetic
-
-    H, F, E, k, T = cfg["H"], cfg["F"], cfg["E"], cfg["k"], cfg["T"]
-    bf16 = cfg["dtype"] == "bf16"
-    dt = torch.bfloat16 if bf16 else torch.float32
+    H, F, E = cfg["H"], cfg["F"], cfg["E"]
+    dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     if x is None:
         x, wg = make_inputs(cfg, 0, dev, dt)
@@ -157,13 +153,20 @@ def cpu_oracle_tokens_per_s(cfg, stride, x=None, wg=None, threads_note=True):
         u, d = expert_weights(cfg, e, dev, dt)
         ups[e] = u.float().cpu().numpy()
         downs[e] = d.float().cpu().numpy()
-    xs = x.float().cpu().numpy()[None]
-    wgs = wg.float().cpu().numpy()
+    return x.float().cpu().numpy()[None], wg.float().cpu().numpy(), ups, downs
+
+
+def cpu_oracle_time(cfg, inputs, stride):
+    """Times the CPU oracle (all host threads) on every `stride`-th token of one GPU's
+    workload; routing covers every token.  Returns (tokens/s, seconds, sampled, threads)."""
+    import oracle
+
+    xs, wgs, ups, downs = inputs
     t0 = time.perf_counter()
-    oracle.moe_layer(xs, wgs, ups, downs, k, [1], [1], bf16=bf16, stride=stride)
-    dt_s = time.perf_counter() - t0
-    sampled = (T + stride - 1) // stride
-    return sampled / dt_s, dt_s, sampled, oracle.num_threads()
+    oracle.moe_layer(xs, wgs, ups, downs, cfg["k"], [1], [1], bf16=cfg["dtype"] == "bf16", stride=stride)
+    secs = time.perf_counter() - t0
+    sampled = (cfg["T"] + stride - 1) // stride
+    return sampled / secs, secs, sampled, oracle.num_threads()
 
 
 def run_reference(args, cfg):
@@ -171,9 +174,10 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    inputs = cpu_oracle_inputs(cfg)
     vals = []
     for i in range(args.warmup + args.steps):
-        tps, secs, sampled, cores = cpu_oracle_tokens_per_s(cfg, args.cpu_stride)
+        tps, secs, sampled, cores = cpu_oracle_time(cfg, inputs, args.cpu_stride)
         if i >= args.warmup:
             vals.append(tps)
     v = statistics.median(vals)
@@ -243,12 +247,12 @@ def main():
     barrier()
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        t0.record(stream)
-        for _ in range(args.steps):
-            step()
-        t1.record(stream)
-        barrier()
+    clocks = ClockSampler(local).__enter__()
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    barrier()
     ms = t0.elapsed_time(t1)
     phases = layer.timings()
     layer.set_profiling(False)
@@ -282,6 +286,7 @@ def main():
         if world > 1:
             layer.gather_experts()
         layer.forward_host(xh, yh)
+    layer.host_fence()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -289,8 +294,10 @@ def main():
         if world > 1:
             layer.gather_experts()
         layer.forward_host(xh, yh)
+    layer.host_fence()
     e1.record(stream)
     barrier()
+    clocks.__exit__()
     e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     if world > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
@@ -299,7 +306,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        tps, secs, sampled, cores = cpu_oracle_tokens_per_s(cfg, args.cpu_stride, x, wg)
+        tps, secs, sampled, cores = cpu_oracle_time(cfg, cpu_oracle_inputs(cfg, x, wg), args.cpu_stride)
         cpu = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
                "sample": f"every {args.cpu_stride}th of {T} tokens ({sampled} tokens) through the full layer "
                          f"(routing of all {T} tokens included), {secs:.1f} s"}

@@ -165,9 +165,13 @@ int hep_layer_gather_experts(hep_layer_t layer, void* stream);
 /* The step: gate -> permute -> dispatch -> expert FFN -> combine.  x, y: device
  * [tokens, H] in the layer dtype. */
 int hep_layer_forward(hep_layer_t layer, const void* x, int64_t tokens, void* y, void* stream);
-/* Same step with host buffers (pinned recommended): H2D copy, forward, D2H copy. */
+/* Same step with host buffers (pinned recommended): H2D copy, forward, D2H copy.
+ * Asynchronous and double-buffered: the H2D of the next call and the D2H of the
+ * previous one run on the copy engines while this step computes on `stream`.
+ * host_y is complete once `stream` passes hep_layer_host_fence (or the device syncs). */
 int hep_layer_forward_host(hep_layer_t layer, const void* host_x, int64_t tokens, void* host_y,
                            void* stream);
+int hep_layer_host_fence(hep_layer_t layer, void* stream);
 /* Introspection of the last forward (device pointers owned by the layer):
  * topk_idx int32[T*k], topk_w f32[T*k], pos int32[T*k] (row of (t,j) in the packed
  * buffer), packed [rows, H] send buffer grouped by (dest, expert); counts int32[G*E]

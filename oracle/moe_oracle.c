@@ -375,8 +375,12 @@ int orc_moe_layer(int bf16, const float* x, const float* wg, const float* w_up, 
   const int64_t n = E / G, NK = G * E;
   int32_t* route = (int32_t*)malloc(sizeof(int32_t) * G * G);
   if (orc_route_table(sf, sed, L, route)) { free(route); return -1; }
+  /* bf16 layers route with bf16 gate weights (the device keeps W_g in the layer dtype). */
+  float* wgr = (float*)malloc(sizeof(float) * H * E);
+  for (int64_t i = 0; i < H * E; ++i) wgr[i] = bf16 ? bf16_round(wg[i]) : wg[i];
   for (int64_t g = 0; g < G; ++g)
-    orc_gate(x + g * T * H, wg, T, H, E, k, topk_idx + g * T * k, topk_w + g * T * k);
+    orc_gate(x + g * T * H, wgr, T, H, E, k, topk_idx + g * T * k, topk_w + g * T * k);
+  free(wgr);
   /* S7: stable counting sort by key = dest*E + e over (t, j). */
   for (int64_t g = 0; g < G; ++g) {
     int32_t* cnt = key_counts + g * NK;

@@ -366,6 +366,10 @@ int hep_layer_forward_host(hep_layer_t layer, const void* host_x, int64_t tokens
   return guarded([&] { layer->impl->forward_host(host_x, tokens, host_y, st(stream)); });
 }
 
+int hep_layer_host_fence(hep_layer_t layer, void* stream) {
+  return guarded([&] { layer->impl->host_fence(st(stream)); });
+}
+
 int hep_layer_debug(hep_layer_t layer, const int32_t** topk_idx, const float** topk_w, const int32_t** pos,
                     const void** packed, const int32_t** key_counts) {
   return guarded([&] {

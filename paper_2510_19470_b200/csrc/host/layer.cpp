@@ -103,7 +103,7 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
   ck(cudaMemcpy(d_route_.p, route_row_.data(), sizeof(int32_t) * G_, cudaMemcpyHostToDevice), "route");
   d_slot_of_expert_.alloc(sizeof(int32_t) * E_);
   ck(cudaMemcpy(d_slot_of_expert_.p, slot_of_expert_.data(), sizeof(int32_t) * E_, cudaMemcpyHostToDevice), "slots");
-  wg_t_.alloc(sizeof(float) * E_ * H_);
+  wg_t_.alloc(eb * E_ * H_);
   w_up_c_.alloc(eb * slots_ * F_ * H_);
   w_down_c_.alloc(eb * slots_ * H_ * F_);
 
@@ -151,22 +151,41 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
     sr_tmp_.alloc(sizeof(float) * P);
     sr_status_.alloc(16);
   }
-  x_dev_.alloc(eb * Tmax_ * H_);
-  y_dev_.alloc(eb * Tmax_ * H_);
+  for (int b = 0; b < 2; ++b) {
+    x_dev_[b].alloc(eb * Tmax_ * H_);
+    y_dev_[b].alloc(eb * Tmax_ * H_);
+    ck(cudaEventCreateWithFlags(&ev_h2d_[b], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_comp_[b], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_d2h_[b], cudaEventDisableTiming), "event");
+  }
+  ck(cudaStreamCreateWithFlags(&h2d_s_, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&d2h_s_, cudaStreamNonBlocking), "stream");
   send_off_.resize(a2a_peers_.size());
   send_rows_.resize(a2a_peers_.size());
   recv_off_.resize(a2a_peers_.size());
   recv_rows_.resize(a2a_peers_.size());
   num_groups_ = static_cast<int>(slots_);
+  const int rows_per_expert = static_cast<int>(Tmax_ * k_ / E_);
+  sched_up_ = gemm_schedule(rows_per_expert, static_cast<int>(F_), static_cast<int>(H_), true);
+  sched_down_ = gemm_schedule(rows_per_expert, static_cast<int>(H_), static_cast<int>(F_), false);
 }
 
 Layer::~Layer() {
+  if (h2d_s_) cudaStreamSynchronize(h2d_s_);
+  if (d2h_s_) cudaStreamSynchronize(d2h_s_);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+  for (int b = 0; b < 2; ++b) {
+    if (ev_h2d_[b]) cudaEventDestroy(ev_h2d_[b]);
+    if (ev_comp_[b]) cudaEventDestroy(ev_comp_[b]);
+    if (ev_d2h_[b]) cudaEventDestroy(ev_d2h_[b]);
+  }
+  if (h2d_s_) cudaStreamDestroy(h2d_s_);
+  if (d2h_s_) cudaStreamDestroy(d2h_s_);
 }
 
 void Layer::set_gate(const void* w_gate, DType dt, cudaStream_t s) {
-  // W_g is H x E; the gate kernel wants it expert-major fp32.
-  ck(launch_transpose_convert(dt, w_gate, H_, E_, DType::F32, wg_t_.p, s), "gate layout");
+  // W_g is H x E; the gate kernel wants it expert-major in the layer dtype.
+  ck(launch_transpose_convert(dt, w_gate, H_, E_, dt_, wg_t_.p, s), "gate layout");
 }
 
 void Layer::set_expert(int64_t e, const void* w_up, const void* w_down, DType dt, cudaStream_t s) {
@@ -334,9 +353,9 @@ void Layer::run_expert_gemms(cudaStream_t s) {
   GroupTable gt{g_row_start_.as<int>(), g_rows_.as<int>(), g_slot_.as<int>(), num_groups_};
   if (dt_ == DType::BF16) {
     mark("gemm_up", s);
-    ck(launch_grouped_gemm_bf16(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s), "gemm up");
+    ck(launch_grouped_gemm_bf16(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_), "gemm up");
     mark("gemm_down", s);
-    ck(launch_grouped_gemm_bf16(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s), "gemm down");
+    ck(launch_grouped_gemm_bf16(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, sched_down_), "gemm down");
   } else {
     mark("gemm_up", s);
     ck(launch_grouped_gemm_f32(xall_.as<float>(), static_cast<int>(H_), w_up_c_.as<float>(), hbuf_.as<float>(), static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_ * 2, s), "gemm up");
@@ -352,7 +371,7 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
   const int Ti = static_cast<int>(T);
   const int nchunks = (Ti + 31) / 32;
   mark("gate", s);
-  ck(launch_gate(dt_, x, wg_t_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(E_), static_cast<int>(k_),
+  ck(launch_gate(dt_, x, wg_t_.p, Ti, static_cast<int>(H_), static_cast<int>(E_), static_cast<int>(k_),
                  d_route_.as<int>(), static_cast<int>(n_), static_cast<int>(NK_), topk_idx_.as<int>(),
                  topk_w_.as<float>(), keys_.as<int>(), ranks_.as<int>(), chunk_counts_.as<int>(), s), "gate");
   mark("scan", s);
@@ -414,9 +433,26 @@ void Layer::collect_timings(char* names, size_t names_cap, float* ms, int cap, i
 void Layer::forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s) {
   const size_t bytes = static_cast<size_t>(T * H_ * dtype_bytes(dt_));
   if (T <= 0 || T > Tmax_) throw std::invalid_argument("token count must be in [1, max_tokens]");
-  ck(cudaMemcpyAsync(x_dev_.p, hx, bytes, cudaMemcpyHostToDevice, s), "h2d");
-  forward(x_dev_.p, T, y_dev_.p, s);
-  ck(cudaMemcpyAsync(hy, y_dev_.p, bytes, cudaMemcpyDeviceToHost, s), "d2h");
+  const int b = hslot_;
+  hslot_ ^= 1;
+  // H2D on its own stream once the step that last used this slot stopped reading it.
+  ck(cudaStreamWaitEvent(h2d_s_, ev_comp_[b], 0), "wait");
+  ck(cudaMemcpyAsync(x_dev_[b].p, hx, bytes, cudaMemcpyHostToDevice, h2d_s_), "h2d");
+  ck(cudaEventRecord(ev_h2d_[b], h2d_s_), "record");
+  // The step itself on the caller's stream.
+  ck(cudaStreamWaitEvent(s, ev_h2d_[b], 0), "wait");
+  ck(cudaStreamWaitEvent(s, ev_d2h_[b], 0), "wait");
+  forward(x_dev_[b].p, T, y_dev_[b].p, s);
+  ck(cudaEventRecord(ev_comp_[b], s), "record");
+  // D2H of the result on the other copy engine.
+  ck(cudaStreamWaitEvent(d2h_s_, ev_comp_[b], 0), "wait");
+  ck(cudaMemcpyAsync(hy, y_dev_[b].p, bytes, cudaMemcpyDeviceToHost, d2h_s_), "d2h");
+  ck(cudaEventRecord(ev_d2h_[b], d2h_s_), "record");
+}
+
+void Layer::host_fence(cudaStream_t s) {
+  ck(cudaStreamWaitEvent(s, ev_d2h_[0], 0), "wait");
+  ck(cudaStreamWaitEvent(s, ev_d2h_[1], 0), "wait");
 }
 
 }  // namespace hep

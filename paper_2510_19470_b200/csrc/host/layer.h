@@ -47,6 +47,7 @@ class Layer {
   void gather_experts(cudaStream_t s);
   void forward(const void* x, int64_t T, void* y, cudaStream_t s);
   void forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s);
+  void host_fence(cudaStream_t s);
 
   // introspection
   const int* topk_idx() const { return topk_idx_.as<int>(); }
@@ -90,14 +91,19 @@ class Layer {
   DevBuf pos_, xall_, hbuf_, oall_;
   int64_t rows_cap_;
   CUtensorMap map_a1_, map_b1_, map_a2_, map_b2_;
+  uint32_t sched_up_ = 0, sched_down_ = 0;
 
   // per-forward plan
   int num_groups_;
   std::vector<int64_t> send_off_, send_rows_, recv_off_, recv_rows_;  // per a2a peer
   std::vector<int32_t> h_counts_;
 
-  // host staging for forward_host
-  DevBuf x_dev_, y_dev_;
+  // host staging for forward_host: double-buffered so the H2D of step i+1 and the
+  // D2H of step i-1 run on the copy engines while step i computes.
+  DevBuf x_dev_[2], y_dev_[2];
+  cudaStream_t h2d_s_ = nullptr, d2h_s_ = nullptr;
+  cudaEvent_t ev_h2d_[2] = {}, ev_comp_[2] = {}, ev_d2h_[2] = {};
+  int hslot_ = 0;
 
   bool profiling_ = false;
   std::vector<std::pair<std::string, cudaEvent_t>> marks_;

@@ -13,6 +13,9 @@
 // Warp roles (192 threads): w0 TMA producer, w1 TMEM owner + MMA issuer,
 // w2..w5 epilogue (warp w drains TMEM lanes 32*(w%4) .. +31).
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -47,6 +50,35 @@ struct SmemCtl {
 
 constexpr size_t kSmemBytes = 1024 + STAGES * STAGE_BYTES + sizeof(SmemCtl);
 
+__device__ __forceinline__ uint64_t make_policy(uint32_t p) {
+  uint64_t pol;
+  if (p == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else if (p == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// Raster of a group's tiles (sched bits 4-5): 0 = m fastest, 1 = n fastest,
+// 2 = super-rows of GM m-tiles (bits 8-15) with n fastest inside.
+__device__ __forceinline__ void decode_tile(int local, int m_tiles, int n_tiles, uint32_t sched, int& mt,
+                                            int& nt) {
+  const uint32_t raster = (sched >> 4) & 3u;
+  if (raster == 0) {
+    mt = local % m_tiles;
+    nt = local / m_tiles;
+  } else if (raster == 1) {
+    nt = local % n_tiles;
+    mt = local / n_tiles;
+  } else {
+    const int gm = max(1, static_cast<int>((sched >> 8) & 0xffu));
+    const int super = local / (gm * n_tiles);
+    const int within = local - super * gm * n_tiles;
+    const int rows = min(gm, m_tiles - super * gm);
+    mt = super * gm + within % rows;
+    nt = within / rows;
+  }
+}
+
 __device__ __forceinline__ int find_group(const SmemCtl& s, int ng, int tile) {
   int lo = 0, hi = ng - 1;  // largest g with tile_start[g] <= tile
   while (lo < hi) {
@@ -61,7 +93,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_b, __nv_bfloat16* __restrict__ C,
                          int ldc, int N, int K, const int* __restrict__ g_row_start,
                          const int* __restrict__ g_rows, const int* __restrict__ g_slot, int ng,
-                         int relu) {
+                         int relu, uint32_t sched) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -125,15 +157,16 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
   if (warp == 0) {
     // ================= TMA producer =================
     if (lane == 0) {
-      const uint64_t pol_a = l2_policy_evict_first();
-      const uint64_t pol_b = l2_policy_evict_last();
+      const uint64_t pol_a = make_policy(sched & 3u);
+      const uint64_t pol_b = make_policy((sched >> 2) & 3u);
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
         const int g = find_group(s, ng, tile);
         const int local = tile - s.tile_start[g];
         const int m_tiles = (s.rows[g] + BM - 1) / BM;
-        const int mt = local % m_tiles, nt = local / m_tiles;
+        int mt, nt;
+        decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
         const int a_row = s.row_start[g] + mt * BM;
         const int b_row = s.slot[g] * N + nt * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -184,7 +217,8 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
       const int g = find_group(s, ng, tile);
       const int local = tile - s.tile_start[g];
       const int m_tiles = (s.rows[g] + BM - 1) / BM;
-      const int mt = local % m_tiles, nt = local / m_tiles;
+      int mt, nt;
+      decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
       const int r_local = mt * BM + row_in_tile;
       const bool row_ok = r_local < s.rows[g];
       __nv_bfloat16* crow = C + static_cast<size_t>(s.row_start[g] + r_local) * ldc + nt * BN;
@@ -244,6 +278,21 @@ EncodeTiledFn encode_fn() {
 
 }  // namespace
 
+uint32_t gemm_schedule(int rows_per_expert, int N, int K, bool up) {
+  const char* env = std::getenv(up ? "HEP_GEMM_SCHED_UP" : "HEP_GEMM_SCHED_DOWN");
+  if (env && *env) return static_cast<uint32_t>(std::strtoul(env, nullptr, 16));
+  (void)N;
+  // Measured on B200 (tools/gemm_sched_sweep.sh, profiles/README): keep the operand
+  // that is re-used across a wave in L2 (evict_last) and stream the other
+  // (evict_first).  When one expert's A rows fit comfortably in L2, rasterise m-fastest
+  // so A stays resident across all n-tiles; otherwise walk super-rows of gm m-tiles
+  // (A stripe of ~32 MB resident, B streamed once per stripe).
+  const double a_bytes = static_cast<double>(rows_per_expert) * K * 2.0;
+  if (a_bytes <= 48e6) return 0x2u | (0x1u << 2);
+  const int gm = std::max(1, std::min(255, static_cast<int>(32e6 / (128.0 * K * 2.0))));
+  return 0x2u | (0x1u << 2) | (0x2u << 4) | (static_cast<uint32_t>(gm) << 8);
+}
+
 cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                               uint32_t box_rows, uint32_t box_cols) {
   EncodeTiledFn fn = encode_fn();
@@ -261,7 +310,7 @@ cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows,
 
 cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C,
                                      int ldc, int N, int K, const GroupTable& groups, int relu,
-                                     int num_sms, cudaStream_t stream) {
+                                     int num_sms, cudaStream_t stream, uint32_t sched) {
   if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
     return cudaErrorInvalidValue;
   static bool attr_set = false;
@@ -273,7 +322,7 @@ cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap
   }
   grouped_gemm_bf16_kernel<<<num_sms, kThreads, kSmemBytes, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
-      groups.slot, groups.num_groups, relu);
+      groups.slot, groups.num_groups, relu, sched);
   return cudaGetLastError();
 }
 

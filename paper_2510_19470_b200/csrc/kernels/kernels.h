@@ -14,11 +14,11 @@ enum class DType : int { F32 = 0, BF16 = 1 };
 inline int dtype_bytes(DType t) { return t == DType::F32 ? 4 : 2; }
 
 // ----------------------------------------------------------------- routing (route.cu)
-// Gate + top-k + per-32-token-chunk stable ranking.  x:[T,H] (dtype), wg_t:[E,H] fp32
-// (the gate matrix stored expert-major).  Outputs per (t, j): expert, weight, key =
+// Gate + top-k + per-32-token-chunk stable ranking.  x:[T,H] (dtype).  Outputs per (t, j): expert, weight, key =
 // dest*E + e, rank of (t, j) among earlier tokens of its 32-token chunk with the same
-// key; chunk_counts:[ceil(T/32), NK] with NK = G*E.
-cudaError_t launch_gate(DType dt, const void* x, const float* wg_t, int T, int H, int E, int k,
+// key; chunk_counts:[ceil(T/32), NK] with NK = G*E.  wg_t: [E, H] in the layer dtype (bf16
+// layers route with bf16 gate weights on the tensor cores, fp32 layers with FFMA).
+cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H, int E, int k,
                         const int* dest_of_owner, int experts_per_gpu, int NK, int* topk_idx,
                         float* topk_w, int* keys, int* ranks, int* chunk_counts,
                         cudaStream_t stream);
@@ -56,9 +56,15 @@ struct GroupTable {
 // A:[*, K] bf16 row-major, B:[slots*N, K] bf16 (K-major), C:[*, ldc] bf16.
 cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                               uint32_t box_rows, uint32_t box_cols);
+// sched: bits 0-1 L2 policy of A, 2-3 of B (0 normal, 1 evict_first, 2 evict_last),
+// bits 4-5 raster (0 m-fastest, 1 n-fastest, 2 super-rows of bits 8-15 m-tiles).
 cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C,
                                      int ldc, int N, int K, const GroupTable& groups, int relu,
-                                     int num_sms, cudaStream_t stream);
+                                     int num_sms, cudaStream_t stream, uint32_t sched = 0x8u);
+// Schedule for one expert GEMM shape: A operand reused across n-tiles is kept in L2
+// (evict_last) when one expert's A fits, otherwise super-row rasterisation.  The
+// HEP_GEMM_SCHED_UP / HEP_GEMM_SCHED_DOWN environment variables override (hex).
+uint32_t gemm_schedule(int rows_per_expert, int N, int K, bool up);
 
 // fp32 SIMT grouped GEMM (gemm_f32.cu), same contract with fp32 operands.
 cudaError_t launch_grouped_gemm_f32(const float* A, int lda, const float* B, float* C, int ldc,

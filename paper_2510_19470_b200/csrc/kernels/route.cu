@@ -25,11 +25,7 @@ constexpr int kMaxE = 64;       // experts supported by the gate kernel
 constexpr int kMaxK = 8;
 
 template <typename T>
-__device__ __forceinline__ float to_f32(T v);
-template <>
-__device__ __forceinline__ float to_f32<float>(float v) { return v; }
-template <>
-__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_f32(T v) { return static_cast<float>(v); }
 
 // One block = one chunk of 32 tokens, 256 threads.
 template <typename T>
@@ -150,6 +146,196 @@ __global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ x,
     }
     ranks[static_cast<size_t>(t0 + r) * k + j] = before;
     if (after == 0) counts[key] = before + 1;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// bf16 gate: logits on the tensor cores (mma.sync m16n8k16, fp32 accumulate), x and
+// W_g^T streamed through a 4-stage cp.async pipeline.  One block = 64 tokens (two
+// ranking chunks), 4 warps x 16 tokens.  The gate is HBM-bound on reading x; the old
+// CUDA-core kernel above was latency-bound (one global round trip per 64 columns).
+// Exactness: bf16 x bf16 products are exact in fp32 and, for the dyadic parity inputs,
+// every partial sum is exactly representable, so the logits do not depend on the
+// tensor core's summation order.
+constexpr int kGT = 64;          // tokens per block
+constexpr int kGC = 64;          // hidden columns per stage
+constexpr int kGStages = 4;
+constexpr int kGPitch = kGC + 8; // bf16 elements per smem row (16-byte pad: no ldmatrix conflicts)
+constexpr size_t kGateSmem = static_cast<size_t>(kGStages) * 2 * kGT * kGPitch * 2;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(const void* p, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(smem_addr(p)));
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __restrict__ x,
+                                                      const __nv_bfloat16* __restrict__ wg_t, int T_tok,
+                                                      int H, int E, int k,
+                                                      const int* __restrict__ dest_of_owner, int n_per_gpu,
+                                                      int NK, int* __restrict__ topk_idx,
+                                                      float* __restrict__ topk_w, int* __restrict__ keys,
+                                                      int* __restrict__ ranks,
+                                                      int* __restrict__ chunk_counts) {
+  extern __shared__ __align__(128) uint8_t gsm[];
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(gsm);                      // [S][64][pitch]
+  __nv_bfloat16* ws = xs + static_cast<size_t>(kGStages) * kGT * kGPitch;         // [S][64][pitch]
+  __shared__ float logits[kGT][kMaxE + 1];
+  __shared__ int skey[kGT][kMaxK];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t0 = blockIdx.x * kGT;
+  const int nkc = H / kGC;
+  const int ntiles = E / 8;
+
+  auto load_stage = [&](int s, int kc) {
+    const int hc = kc * kGC;
+    __nv_bfloat16* xd = xs + static_cast<size_t>(s) * kGT * kGPitch;
+    __nv_bfloat16* wd = ws + static_cast<size_t>(s) * kGT * kGPitch;
+#pragma unroll
+    for (int i = tid; i < kGT * (kGC / 8); i += 128) {
+      const int r = i >> 3, c8 = (i & 7) * 8;
+      const int t = t0 + r;
+      cp_async16(xd + r * kGPitch + c8, x + static_cast<size_t>(t < T_tok ? t : 0) * H + hc + c8, t < T_tok);
+    }
+    for (int i = tid; i < E * (kGC / 8); i += 128) {
+      const int r = i >> 3, c8 = (i & 7) * 8;
+      cp_async16(wd + r * kGPitch + c8, wg_t + static_cast<size_t>(r) * H + hc + c8, true);
+    }
+  };
+
+  float acc[kMaxE / 8][4];
+#pragma unroll
+  for (int i = 0; i < kMaxE / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+
+#pragma unroll
+  for (int s = 0; s < kGStages - 1; ++s) {
+    if (s < nkc) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kc = 0; kc < nkc; ++kc) {
+    cp_async_wait<kGStages - 2>();
+    __syncthreads();
+    const int pre = kc + kGStages - 1;
+    if (pre < nkc) load_stage(pre % kGStages, pre);
+    cp_async_commit();
+    const int s = kc % kGStages;
+    const __nv_bfloat16* xa = xs + static_cast<size_t>(s) * kGT * kGPitch + (warp * 16) * kGPitch;
+    const __nv_bfloat16* wb = ws + static_cast<size_t>(s) * kGT * kGPitch;
+#pragma unroll
+    for (int ks = 0; ks < kGC / 16; ++ks) {
+      uint32_t a[4];
+      ldsm_x4(xa + (lane & 15) * kGPitch + ks * 16 + (lane >> 4) * 8, a[0], a[1], a[2], a[3]);
+#pragma unroll
+      for (int nt = 0; nt < kMaxE / 8; nt += 2) {
+        if (nt >= ntiles) break;
+        uint32_t b0, b1, b2, b3;
+        const int n = nt * 8 + (lane >> 4) * 8 + (lane & 7);
+        ldsm_x4(wb + (n < E ? n : 0) * kGPitch + ks * 16 + ((lane >> 3) & 1) * 8, b0, b1, b2, b3);
+        mma_bf16_16816(acc[nt], a, b0, b1);
+        if (nt + 1 < ntiles) mma_bf16_16816(acc[nt + 1], a, b2, b3);
+      }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int nt = 0; nt < kMaxE / 8; ++nt) {
+    if (nt >= ntiles) break;
+    const int r = warp * 16 + (lane >> 2), c = nt * 8 + (lane & 3) * 2;
+    logits[r][c] = acc[nt][0];
+    logits[r][c + 1] = acc[nt][1];
+    logits[r + 8][c] = acc[nt][2];
+    logits[r + 8][c + 1] = acc[nt][3];
+  }
+  __syncthreads();
+
+  for (int q = 0; q < 16; ++q) {
+    const int r = warp * 16 + q;
+    const int t = t0 + r;
+    if (t >= T_tok) break;  // warp-uniform
+    float v0 = lane < E ? logits[r][lane] : -FLT_MAX;
+    float v1 = lane + 32 < E ? logits[r][lane + 32] : -FLT_MAX;
+    bool used0 = lane >= E, used1 = lane + 32 >= E;
+    float sel_v[kMaxK];
+    int sel_e[kMaxK];
+    for (int j = 0; j < k; ++j) {
+      float bv = -FLT_MAX;
+      int be = 0x7fffffff;
+      if (!used0) { bv = v0; be = lane; }
+      if (!used1 && (be == 0x7fffffff || v1 > bv)) { bv = v1; be = lane + 32; }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (oe != 0x7fffffff && (be == 0x7fffffff || ov > bv || (ov == bv && oe < be))) {
+          bv = ov;
+          be = oe;
+        }
+      }
+      sel_v[j] = bv;
+      sel_e[j] = be;
+      if (be == lane) used0 = true;
+      if (be == lane + 32) used1 = true;
+    }
+    if (lane < k) {
+      float s = 0.f, mine = 0.f;
+      for (int j = 0; j < k; ++j) {
+        const float ex = expf(sel_v[j] - sel_v[0]);
+        s += ex;
+        if (j == lane) mine = ex;
+      }
+      const size_t o = static_cast<size_t>(t) * k + lane;
+      const int e = sel_e[lane];
+      const int key = dest_of_owner[e / n_per_gpu] * E + e;
+      topk_idx[o] = e;
+      topk_w[o] = mine / s;
+      keys[o] = key;
+      skey[r][lane] = key;
+    }
+  }
+  __syncthreads();
+
+  // Ranking per 32-token chunk (two chunks per block).
+  for (int sub = 0; sub < kGT / kChunk; ++sub) {
+    const int chunk = blockIdx.x * (kGT / kChunk) + sub;
+    const int c0 = sub * kChunk;
+    const int valid = min(kChunk, T_tok - (t0 + c0));
+    if (valid <= 0) break;
+    int* counts = chunk_counts + static_cast<size_t>(chunk) * NK;
+    for (int i = tid; i < NK; i += blockDim.x) counts[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < valid * k; i += blockDim.x) {
+      const int r = i / k, j = i % k;
+      const int key = skey[c0 + r][j];
+      int before = 0, after = 0;
+      for (int r2 = 0; r2 < valid; ++r2) {
+        if (r2 == r) continue;
+        for (int j2 = 0; j2 < k; ++j2)
+          if (skey[c0 + r2][j2] == key) {
+            if (r2 < r) ++before; else ++after;
+          }
+      }
+      ranks[static_cast<size_t>(t0 + c0 + r) * k + j] = before;
+      if (after == 0) counts[key] = before + 1;
+    }
+    __syncthreads();
   }
 }
 
@@ -343,20 +529,31 @@ __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restric
 
 }  // namespace
 
-cudaError_t launch_gate(DType dt, const void* x, const float* wg_t, int T, int H, int E, int k,
+cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H, int E, int k,
                         const int* dest_of_owner, int experts_per_gpu, int NK, int* topk_idx,
                         float* topk_w, int* keys, int* ranks, int* chunk_counts,
                         cudaStream_t stream) {
   if (E > kMaxE || k > kMaxK || k > E || T <= 0) return cudaErrorInvalidValue;
-  const int nchunks = (T + kChunk - 1) / kChunk;
-  if (dt == DType::BF16)
-    gate_kernel<__nv_bfloat16><<<nchunks, 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(x), wg_t, T, H, E, k, dest_of_owner, experts_per_gpu, NK,
-        topk_idx, topk_w, keys, ranks, chunk_counts);
-  else
-    gate_kernel<float><<<nchunks, 256, 0, stream>>>(static_cast<const float*>(x), wg_t, T, H, E, k,
-                                                    dest_of_owner, experts_per_gpu, NK, topk_idx,
+  if (dt == DType::BF16) {
+    // wg_t is bf16 [E, H] for bf16 layers.
+    if (H % kGC || E % 8) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+      const cudaError_t e = cudaFuncSetAttribute(gate_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kGateSmem));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    const int blocks = (T + kGT - 1) / kGT;
+    gate_mma_kernel<<<blocks, 128, kGateSmem, stream>>>(
+        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg_t), T, H, E, k, dest_of_owner,
+        experts_per_gpu, NK, topk_idx, topk_w, keys, ranks, chunk_counts);
+  } else {
+    const int nchunks = (T + kChunk - 1) / kChunk;
+    gate_kernel<float><<<nchunks, 256, 0, stream>>>(static_cast<const float*>(x), static_cast<const float*>(wg_t),
+                                                    T, H, E, k, dest_of_owner, experts_per_gpu, NK, topk_idx,
                                                     topk_w, keys, ranks, chunk_counts);
+  }
   return cudaGetLastError();
 }
 

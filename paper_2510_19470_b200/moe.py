@@ -108,9 +108,13 @@ class MoELayer:
     __call__ = forward
 
     def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor, stream=None):
-        """End-to-end call with host buffers (pinned recommended)."""
+        """End-to-end call with host buffers (pinned recommended).  Asynchronous and
+        double-buffered; y_host is complete after host_fence() + stream sync."""
         check(lib.hep_layer_forward_host(self.handle, x_host.data_ptr(), x_host.shape[0], y_host.data_ptr(),
                                          _stream(stream)))
+
+    def host_fence(self, stream=None):
+        check(lib.hep_layer_host_fence(self.handle, _stream(stream)))
 
     def debug(self, T: int):
         """Device views of the last forward's routing: topk_idx, topk_w, pos, key_counts."""
