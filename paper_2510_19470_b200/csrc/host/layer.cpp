@@ -165,12 +165,66 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
   recv_off_.resize(a2a_peers_.size());
   recv_rows_.resize(a2a_peers_.size());
   num_groups_ = static_cast<int>(slots_);
+  if (G_ > 1) {
+    const char* mode = std::getenv("HEP_COMM");
+    p2p_ = !(mode && std::string(mode) == "nccl");
+    if (p2p_) setup_p2p();
+  }
   const int rows_per_expert = static_cast<int>(Tmax_ * k_ / E_);
   sched_up_ = gemm_schedule(rows_per_expert, static_cast<int>(F_), static_cast<int>(H_), true);
   sched_down_ = gemm_schedule(rows_per_expert, static_cast<int>(H_), static_cast<int>(F_), false);
 }
 
+void Layer::setup_p2p() {
+  if (G_ > kMaxG || E_ > kMaxE) throw std::invalid_argument("peer-memory path supports G <= 8, E <= 64");
+  sync_.alloc(p2p_sync_bytes(static_cast<int>(G_), static_cast<int>(E_)));
+  ck(cudaMemset(sync_.p, 0, sync_.bytes), "sync memset");
+  send_base_.alloc(sizeof(int) * NK_);
+  // Exchange CUDA IPC handles of xall / oall / sync through NCCL.
+  cudaIpcMemHandle_t mine[3];
+  ck(cudaIpcGetMemHandle(&mine[0], xall_.p), "ipc handle");
+  ck(cudaIpcGetMemHandle(&mine[1], oall_.p), "ipc handle");
+  ck(cudaIpcGetMemHandle(&mine[2], sync_.p), "ipc handle");
+  DevBuf dmine, dall;
+  dmine.alloc(sizeof(mine));
+  dall.alloc(sizeof(mine) * G_);
+  ck(cudaMemcpy(dmine.p, mine, sizeof(mine), cudaMemcpyHostToDevice), "ipc h2d");
+  nck(ncclAllGather(dmine.p, dall.p, sizeof(mine), ncclUint8, comm_->nccl, 0), "ipc allgather");
+  ck(cudaStreamSynchronize(0), "ipc sync");
+  std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(3 * G_));
+  ck(cudaMemcpy(all.data(), dall.p, sizeof(mine) * G_, cudaMemcpyDeviceToHost), "ipc d2h");
+  P2PArgs& a = p2p_args_;
+  a.G = static_cast<int>(G_);
+  a.E = static_cast<int>(E_);
+  a.rank = rank_;
+  a.recv_start = static_cast<int>(Tmax_ * k_);
+  for (int r = 0; r < G_; ++r) {
+    if (r == rank_) {
+      a.xall[r] = xall_.p;
+      a.oall[r] = oall_.p;
+      a.sync[r] = sync_.p;
+      continue;
+    }
+    void* ptrs[3];
+    for (int b = 0; b < 3; ++b) {
+      ck(cudaIpcOpenMemHandle(&ptrs[b], all[static_cast<size_t>(3 * r + b)], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+      ipc_opened_.push_back(ptrs[b]);
+    }
+    a.xall[r] = ptrs[0];
+    a.oall[r] = ptrs[1];
+    a.sync[r] = ptrs[2];
+  }
+  const std::vector<hybridep::sim::PeerLists> peers = hybridep::sim::peer_lists(cluster_);
+  for (int d = 0; d < G_; ++d) {
+    int n = 0;
+    for (const auto& level : peers[static_cast<size_t>(d)].a2a)
+      for (int64_t p : level) a.src_list[d * kMaxG + n++] = static_cast<int>(p);
+    a.n_src[d] = n;
+  }
+}
+
 Layer::~Layer() {
+  for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   if (h2d_s_) cudaStreamSynchronize(h2d_s_);
   if (d2h_s_) cudaStreamSynchronize(d2h_s_);
   for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
@@ -379,11 +433,34 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
   ck(launch_key_scan(key_total_.as<int>(), static_cast<int>(G_), static_cast<int>(E_), rank_, d_slot_of_expert_.as<int>(),
                      key_off_.as<int>(), dest_rows_.as<int>(), dest_off_.as<int>(), g_row_start_.as<int>(),
                      g_rows_.as<int>(), g_slot_.as<int>(), s), "key scan");
+  launches_ += 3;
+  num_groups_ = static_cast<int>(slots_);
+  if (p2p_) {
+    // Device-side count exchange, then rows go straight into peers' receive areas.
+    p2p_args_.epoch = ++epoch_;
+    mark("dispatch", s);
+    ck(launch_count_exchange(p2p_args_, key_total_.as<int>(), key_off_.as<int>(), d_slot_of_expert_.as<int>(),
+                             send_base_.as<int>(), g_row_start_.as<int>(), g_rows_.as<int>(), g_slot_.as<int>(),
+                             all_counts_.as<int>(), s), "count exchange");
+    ck(launch_permute_p2p(p2p_args_, dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), keys_.as<int>(),
+                          ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
+                          pos_.as<int>(), s), "permute p2p");
+    ck(launch_signal_wait(p2p_args_, 1, s), "dispatch flags");
+    launches_ += 3;
+    num_groups_ = static_cast<int>(slots_ * (1 + p2p_args_.n_src[rank_]));
+    run_expert_gemms(s);
+    mark("combine", s);
+    ck(launch_signal_wait(p2p_args_, 2, s), "combine flags");
+    ck(launch_combine_p2p(p2p_args_, dt_, keys_.as<int>(), pos_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
+                          topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine p2p");
+    launches_ += 2;
+    mark("end", s);
+    return;
+  }
   mark("permute", s);
   ck(launch_permute(dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), static_cast<int>(NK_), keys_.as<int>(),
                     ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), pos_.as<int>(), xall_.p, s), "permute");
-  launches_ += 4;
-  num_groups_ = static_cast<int>(slots_);
+  launches_ += 1;
   if (G_ > 1) {
     mark("dispatch", s);
     build_comm_plan_and_groups(Ti, s);

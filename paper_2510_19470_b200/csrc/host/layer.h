@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "../kernels/comm_p2p.h"
 #include "../kernels/kernels.h"
 #include "hep.h"
 #include "hybridep/sparsecomp.hpp"
@@ -59,6 +60,7 @@ class Layer {
   // Mean device time per named phase over every profiled forward since the last call.
   void collect_timings(char* names, size_t names_cap, float* ms, int cap, int* count);
   int launch_count() const { return launches_; }
+  bool p2p() const { return p2p_; }
 
  private:
   void mark(const char* name, cudaStream_t s);
@@ -92,6 +94,14 @@ class Layer {
   int64_t rows_cap_;
   CUtensorMap map_a1_, map_b1_, map_a2_, map_b2_;
   uint32_t sched_up_ = 0, sched_down_ = 0;
+
+  // NVLink peer-memory path (default for G > 1; HEP_COMM=nccl selects the NCCL baseline)
+  bool p2p_ = false;
+  P2PArgs p2p_args_{};
+  DevBuf sync_, send_base_;
+  std::vector<void*> ipc_opened_;
+  uint32_t epoch_ = 0;
+  void setup_p2p();
 
   // per-forward plan
   int num_groups_;

@@ -1,0 +1,265 @@
+// K2/K3/K9 fused with NVLink peer memory: the domain-based token A2A without NCCL and
+// without a host round trip.
+//
+//   count exchange  every rank stores its (dest, expert) row counts straight into every
+//                   peer's inbox (NVLink stores), raises a flag, waits for all flags;
+//                   then derives on device where its rows land in each destination's
+//                   receive area and the GEMM group table for rows it will receive.
+//   dispatch        permute_p2p writes each (token, slot) row either into the local
+//                   packed buffer or directly into the destination GPU's receive area.
+//   combine         after the outputs-ready flags, combine_p2p gathers every expert
+//                   output row from local HBM or from the computing peer's HBM.
+//
+// Receive area of GPU d: rows [Tmax*k, ...) of its xall/oall, ordered by source in
+// d's A2A peer-list order (simcore.cpp:53-72), then by expert, then (token, slot):
+// the same layout the NCCL path produces, so both paths feed the same GEMM groups.
+// Flags carry a per-forward epoch; spins time out (trap) instead of hanging.
+
+#include "common.cuh"
+#include "comm_p2p.h"
+
+namespace hep {
+
+namespace {
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ void wait_flag(const uint32_t* f, uint32_t epoch) {
+  const uint64_t t0 = globaltimer();
+  // Epochs only grow; a peer that already moved on to a later epoch also satisfies us.
+  while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
+    if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();  // peer never arrived
+    __nanosleep(64);
+  }
+}
+
+// Sync buffer of one rank (in its HBM, written by peers).
+struct SyncView {
+  uint32_t* flags;  // [3][kMaxG]: 0 counts, 1 dispatched, 2 outputs ready; index = source rank
+  int* inbox;       // [2][kMaxG][NK]: counts of every source, double-buffered by epoch parity
+};
+
+__device__ __forceinline__ SyncView view(void* base, int NK) {
+  SyncView v;
+  v.flags = static_cast<uint32_t*>(base);
+  v.inbox = reinterpret_cast<int*>(static_cast<uint8_t*>(base) + 3 * kMaxG * sizeof(uint32_t));
+  (void)NK;
+  return v;
+}
+
+__global__ void __launch_bounds__(256) count_exchange_kernel(P2PArgs a, const int* __restrict__ key_total,
+                                                             const int* __restrict__ key_off,
+                                                             const int* __restrict__ slot_of_expert,
+                                                             int* __restrict__ send_base, int* __restrict__ g_row_start,
+                                                             int* __restrict__ g_rows, int* __restrict__ g_slot,
+                                                             int* __restrict__ counts_out) {
+  const int G = a.G, E = a.E, NK = G * E, me = a.rank;
+  const int par = a.epoch & 1;
+  __shared__ int cnt[kMaxG * kMaxG * kMaxE];  // cnt[s][d*E+e]
+  // 1) broadcast my counts into every rank's inbox (including mine).
+  for (int d = 0; d < G; ++d) {
+    const SyncView v = view(a.sync[d], NK);
+    int* dst = v.inbox + (par * kMaxG + me) * NK;
+    for (int i = threadIdx.x; i < NK; i += blockDim.x) dst[i] = key_total[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < G && static_cast<int>(threadIdx.x) != me)
+    st_release_sys(view(a.sync[threadIdx.x], NK).flags + 0 * kMaxG + me, a.epoch);
+  // 2) wait for everyone's counts.
+  const SyncView mine = view(a.sync[me], NK);
+  if (threadIdx.x < G && static_cast<int>(threadIdx.x) != me) wait_flag(mine.flags + 0 * kMaxG + threadIdx.x, a.epoch);
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * NK; i += blockDim.x) {
+    const int s = i / NK, key = i % NK;
+    const int v = s == me ? key_total[key] : ld_acquire_sys(reinterpret_cast<const uint32_t*>(mine.inbox + (par * kMaxG + s) * NK + key));
+    cnt[i] = v;
+    counts_out[i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  // 3) where my rows for (d, e) land in d's receive area.
+  for (int d = 0; d < G; ++d) {
+    if (d == me) {
+      for (int e = 0; e < E; ++e) send_base[d * E + e] = key_off[d * E + e];
+      continue;
+    }
+    int base = a.recv_start;
+    for (int i = 0; i < a.n_src[d]; ++i) {
+      const int s = a.src_list[d * kMaxG + i];
+      if (s == me) break;
+      for (int e = 0; e < E; ++e) base += cnt[s * NK + d * E + e];
+    }
+    for (int e = 0; e < E; ++e) {
+      send_base[d * E + e] = base;
+      base += cnt[me * NK + d * E + e];
+    }
+  }
+  // 4) GEMM groups: local rows per held expert, then received rows per (source, expert).
+  int g = 0;
+  for (int e = 0; e < E; ++e) {
+    const int sl = slot_of_expert[e];
+    if (sl < 0) continue;
+    g_row_start[g] = key_off[me * E + e];
+    g_rows[g] = cnt[me * NK + me * E + e];
+    g_slot[g++] = sl;
+  }
+  int at = a.recv_start;
+  for (int i = 0; i < a.n_src[me]; ++i) {
+    const int s = a.src_list[me * kMaxG + i];
+    for (int e = 0; e < E; ++e) {
+      const int sl = slot_of_expert[e];
+      if (sl < 0) continue;  // never receives rows for an expert it does not hold (S2)
+      const int c = cnt[s * NK + me * E + e];
+      g_row_start[g] = at;
+      g_rows[g] = c;
+      g_slot[g++] = sl;
+      at += c;
+    }
+  }
+}
+
+// One warp per token: local rows into the packed buffer, remote rows straight into the
+// destination's receive area over NVLink.
+__global__ void __launch_bounds__(256) permute_p2p_kernel(P2PArgs a, const uint8_t* __restrict__ x, int T_tok,
+                                                          int row_bytes, int k, const int* __restrict__ keys,
+                                                          const int* __restrict__ ranks,
+                                                          const int* __restrict__ chunk_off,
+                                                          const int* __restrict__ key_off,
+                                                          const int* __restrict__ send_base, int* __restrict__ pos) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T_tok) return;
+  const int NK = a.G * a.E;
+  const int chunk = t / 32;
+  uint8_t* dst[8];
+  for (int j = 0; j < k; ++j) {
+    const size_t o = static_cast<size_t>(t) * k + j;
+    const int key = keys[o];
+    const int p = key_off[key] + chunk_off[static_cast<size_t>(chunk) * NK + key] + ranks[o];
+    if (lane == 0) pos[o] = p;
+    const int d = key / a.E;
+    const int row = d == a.rank ? p : send_base[key] + (p - key_off[key]);
+    dst[j] = static_cast<uint8_t*>(a.xall[d]) + static_cast<size_t>(row) * row_bytes;
+  }
+  const uint8_t* src = x + static_cast<size_t>(t) * row_bytes;
+  for (int v = lane; v < (row_bytes >> 4); v += 32) {
+    const uint4 val = ld_nc_v4(src + 16 * v);
+    for (int j = 0; j < k; ++j) st_v4(dst[j] + 16 * v, val);
+  }
+}
+
+// Raise flag `slot` on every A2A peer, then wait for theirs.
+__global__ void signal_wait_kernel(P2PArgs a, int slot) {
+  __threadfence_system();
+  const int NK = a.G * a.E;
+  const int i = threadIdx.x;
+  if (i < a.n_src[a.rank]) {
+    const int p = a.src_list[a.rank * kMaxG + i];
+    st_release_sys(view(a.sync[p], NK).flags + slot * kMaxG + a.rank, a.epoch);
+  }
+  __syncthreads();
+  if (i < a.n_src[a.rank]) {
+    const int p = a.src_list[a.rank * kMaxG + i];
+    wait_flag(view(a.sync[a.rank], NK).flags + slot * kMaxG + p, a.epoch);
+  }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(256) combine_p2p_kernel(P2PArgs a, const int* __restrict__ keys,
+                                                          const int* __restrict__ pos,
+                                                          const int* __restrict__ key_off,
+                                                          const int* __restrict__ send_base,
+                                                          const float* __restrict__ w, int T_tok, int H, int k,
+                                                          void* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T_tok) return;
+  const int eb = BF16 ? 2 : 4;
+  const uint8_t* row[8];
+  float wt[8];
+  for (int j = 0; j < k; ++j) {
+    const size_t o = static_cast<size_t>(t) * k + j;
+    const int key = keys[o], p = pos[o], d = key / a.E;
+    const int r = d == a.rank ? p : send_base[key] + (p - key_off[key]);
+    row[j] = static_cast<const uint8_t*>(a.oall[d]) + static_cast<size_t>(r) * H * eb;
+    wt[j] = w[o];
+  }
+  const int per = 16 / eb;
+  for (int v = lane; v < H / per; v += 32) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < k; ++j) {
+      const uint4 r = *reinterpret_cast<const uint4*>(row[j] + 16 * v);
+      if (BF16) {
+        float f[8];
+        unpack8(r, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(wt[j], f[i], acc[i]);
+      } else {
+        acc[0] = fmaf(wt[j], __uint_as_float(r.x), acc[0]);
+        acc[1] = fmaf(wt[j], __uint_as_float(r.y), acc[1]);
+        acc[2] = fmaf(wt[j], __uint_as_float(r.z), acc[2]);
+        acc[3] = fmaf(wt[j], __uint_as_float(r.w), acc[3]);
+      }
+    }
+    uint8_t* out = static_cast<uint8_t*>(y) + (static_cast<size_t>(t) * H) * eb + 16 * v;
+    if (BF16) st_v4(out, pack8(acc));
+    else st_v4(out, make_uint4(__float_as_uint(acc[0]), __float_as_uint(acc[1]), __float_as_uint(acc[2]),
+                               __float_as_uint(acc[3])));
+  }
+}
+
+}  // namespace
+
+size_t p2p_sync_bytes(int G, int E) {
+  return 3 * kMaxG * sizeof(uint32_t) + 2 * kMaxG * static_cast<size_t>(G) * E * sizeof(int) + 256;
+}
+
+cudaError_t launch_count_exchange(const P2PArgs& a, const int* key_total, const int* key_off,
+                                  const int* slot_of_expert, int* send_base, int* g_row_start, int* g_rows,
+                                  int* g_slot, int* counts_out, cudaStream_t s) {
+  if (a.G > kMaxG || a.E > kMaxE) return cudaErrorInvalidValue;
+  count_exchange_kernel<<<1, 256, 0, s>>>(a, key_total, key_off, slot_of_expert, send_base, g_row_start, g_rows,
+                                          g_slot, counts_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T, int H, int k, const int* keys,
+                               const int* ranks, const int* chunk_off, const int* key_off, const int* send_base,
+                               int* pos, cudaStream_t s) {
+  const int row_bytes = H * dtype_bytes(dt);
+  if (row_bytes % 16 || k > 8) return cudaErrorInvalidValue;
+  permute_p2p_kernel<<<(T + 7) / 8, 256, 0, s>>>(a, static_cast<const uint8_t*>(x), T, row_bytes, k, keys, ranks,
+                                                 chunk_off, key_off, send_base, pos);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s) {
+  signal_wait_kernel<<<1, 32, 0, s>>>(a, slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, const int* pos, const int* key_off,
+                               const int* send_base, const float* w, int T, int H, int k, void* y,
+                               cudaStream_t s) {
+  if (k > 8) return cudaErrorInvalidValue;
+  if (dt == DType::BF16)
+    combine_p2p_kernel<true><<<(T + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y);
+  else
+    combine_p2p_kernel<false><<<(T + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y);
+  return cudaGetLastError();
+}
+
+}  // namespace hep

@@ -37,8 +37,11 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("comm", ["p2p", "nccl"])
 @pytest.mark.parametrize("sf,sed,extra", CASES, ids=lambda v: str(v))
-def test_multi_gpu_layer(sf, sed, extra):
+def test_multi_gpu_layer(sf, sed, extra, comm):
+    """comm=p2p: fused NVLink peer-memory dispatch/combine (default product path);
+    comm=nccl: the NCCL grouped send/recv baseline (HEP_COMM=nccl)."""
     G = 1
     for s in sf:
         G *= s
@@ -47,5 +50,6 @@ def test_multi_gpu_layer(sf, sed, extra):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(HERE, "mgpu_worker.py"),
            "--sf", *map(str, sf), "--sed", *map(str, sed), *extra]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, HEP_COMM=comm)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
