@@ -35,15 +35,39 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     "cfg3": dict(workload="cfg3: Mixtral-8x7B-shaped MoE layer (8 experts top-2, d=4096, FFN 14336), bf16",
-                 H=4096, F=14336, E=8, k=2, T=16384, dtype="bf16"),
-    "cfg4": dict(workload="cfg4: DeepSeek-style fine-grained MoE layer (64 experts top-6, d=2048, FFN 1408), bf16",
-                 H=2048, F=1408, E=64, k=6, T=16384, dtype="bf16"),
+                 H=4096, F=14336, E=8, k=2, T=16384, dtype="bf16", layers=1, sr=False,
+                 topo={1: ([1], [1]), 2: ([2], [1]), 4: ([2, 2], [1, 1]), 8: ([2, 4], [1, 4])}),
+    "cfg4": dict(workload="cfg4: DeepSeek-style fine-grained MoE layer (64 experts top-6, d=2048, FFN 1408), bf16, "
+                          "SR-migrated experts (CR=50)",
+                 H=2048, F=1408, E=64, k=6, T=16384, dtype="bf16", layers=1, sr=True,
+                 topo={1: ([1], [1]), 2: ([2], [2]), 4: ([2, 2], [1, 2]), 8: ([2, 2, 2], [1, 2, 2])}),
+    "cfg5": dict(workload="cfg5: 8-layer stack of Mixtral-shaped MoE layers, bf16, S_ED from perf::solve_optimal_p "
+                          "on measured B200 numbers",
+                 H=4096, F=14336, E=8, k=2, T=16384, dtype="bf16", layers=8, sr=False,
+                 topo={1: ([1], [1]), 2: ([2], None), 4: ([2, 2], None), 8: ([2, 4], None)}),
     "cfg1": dict(workload="cfg1/cfg2 shape: 8 experts top-2, d=1024, FFN 4096, 512 tokens/GPU, fp32",
-                 H=1024, F=4096, E=8, k=2, T=512, dtype="f32"),
+                 H=1024, F=4096, E=8, k=2, T=512, dtype="f32", layers=1, sr=False,
+                 topo={1: ([1], [1]), 2: ([2], [1]), 4: ([2, 2], [1, 1]), 8: ([2, 4], [1, 4])}),
 }
 
-# Cluster description per GPU count (SF, S_ED), outermost level first.
-TOPOLOGY = {1: ([1], [1]), 2: ([2], [1]), 4: ([2, 2], [1, 1]), 8: ([2, 4], [1, 4])}
+# Measured on B200 (profiles/): used only to let the reference planner pick S_ED (cfg5).
+PLANNER_INPUTS = dict(pre_expert_s=0.17e-3,        # gate + scans + permute, cfg3 shape (profiles/r1_bench_*)
+                      expert_s_per_token_row=6.0e-3 / 32768,  # up+down GEMM time per routed row
+                      nvlink_Bps=770e9)             # peer-copy bandwidth (B200_PROFILING.md)
+
+
+def planned_sed(cfg, sf, world):
+    """cfg5: the reference solver (hep_solve_optimal_p, perfmodel.cpp:200-217) on measured
+    numbers, then the innermost-first split (plan.cpp:41-58)."""
+    from paper_2510_19470_b200 import topology as topo
+    n = cfg["E"] // world
+    rows = cfg["T"] * cfg["k"]
+    p, s, _ = topo.solve_optimal_p(
+        data_size_D=float(rows * cfg["H"] * 2), expert_size_PE=float(n * 2 * cfg["H"] * cfg["F"] * 2),
+        experts_per_gpu_n=n, pre_blocks_m=0, attn_latency=PLANNER_INPUTS["pre_expert_s"], ffn_latency=1e-9,
+        expert_latency=PLANNER_INPUTS["expert_s_per_token_row"] * rows / n, throughput_C=1.3e15,
+        bandwidth_B=PLANNER_INPUTS["nvlink_Bps"], gpus=world)
+    return topo.factor_domain_sizes(s, topo.ClusterSpec.of(sf)), p
 
 
 def parse():
@@ -55,6 +79,7 @@ def parse():
     p.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--cpu-stride", type=int, default=64)
+    p.add_argument("--sed", default="", help="override S_ED per level, e.g. 1,4")
     return p.parse_args()
 
 
@@ -166,7 +191,8 @@ def cpu_oracle_time(cfg, inputs, stride):
     oracle.moe_layer(xs, wgs, ups, downs, cfg["k"], [1], [1], bf16=cfg["dtype"] == "bf16", stride=stride)
     secs = time.perf_counter() - t0
     sampled = (cfg["T"] + stride - 1) // stride
-    return sampled / secs, secs, sampled, oracle.num_threads()
+    # a step of an L-layer stack is L layer passes (cfg5); the sample times one of them
+    return sampled / (secs * cfg.get("layers", 1)), secs, sampled, oracle.num_threads()
 
 
 def run_reference(args, cfg):
@@ -213,25 +239,50 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         comm = Communicator.from_torch()
-    sf, sed = TOPOLOGY[world]
+    sf, sed = cfg["topo"][world]
+    p_plan = None
+    if args.sed:
+        sed = [int(v) for v in args.sed.split(",")]
+    elif sed is None:
+        sed, p_plan = planned_sed(cfg, sf, world)
     dtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     H, F, E, k, T = cfg["H"], cfg["F"], cfg["E"], cfg["k"], cfg["T"]
+    use_sr = cfg["sr"] and world > 1
+    srcfg = None
+    if use_sr:
+        from paper_2510_19470_b200.sr import CompressionConfig
+        srcfg = CompressionConfig(ratio_CR=50.0)
 
-    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype, sf=sf, sed=sed, rank=rank,
-                     comm=comm)
+    layers = []
     x, wg = make_inputs(cfg, rank, dev, dtype)
-    layer.set_gate(wg)
-    for e in layer.owned_experts():
-        u, d = expert_weights(cfg, e, dev, dtype)
-        layer.set_expert(e, u, d)
-        del u, d
+    for li in range(cfg["layers"]):
+        layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype, sf=sf, sed=sed, rank=rank,
+                         comm=comm, sr=srcfg)
+        layer.set_gate(wg)
+        if use_sr:
+            # shared expert = mean of the population (the reference's init_shared); the demo
+            # population shares one base, so every rank computes the same mean locally.
+            from paper_2510_19470_b200 import sr as srmod
+            acc = None
+            for e in range(E):
+                u, d = expert_weights(cfg, e, dev, dtype)
+                flat = torch.cat([u.float().reshape(-1), d.float().reshape(-1)])
+                acc = flat.double() if acc is None else acc + flat.double()
+            layer.set_shared((acc / E).float().contiguous())
+            del acc
+        for e in layer.owned_experts():
+            u, d = expert_weights(cfg, e + 1000 * li, dev, dtype)
+            layer.set_expert(e, u, d)
+            del u, d
+        layers.append(layer)
     torch.cuda.synchronize()
-    y = torch.empty_like(x)
+    acts = [x] + [torch.empty_like(x) for _ in range(cfg["layers"])]
 
     def step():
-        if world > 1:
-            layer.gather_experts()
-        layer.forward(x, out=y)
+        for li, layer in enumerate(layers):
+            if world > 1:
+                layer.gather_experts()
+            layer.forward(acts[li], out=acts[li + 1])
 
     def barrier():
         torch.cuda.synchronize()
@@ -242,8 +293,9 @@ def main():
     # ---------------------------------------------------------------- device-timed region
     for _ in range(args.warmup):
         step()
-    layer.set_profiling(True)
-    layer.timings()  # drop warm-up marks
+    for layer in layers:
+        layer.set_profiling(True)
+        layer.timings()  # drop warm-up marks
     barrier()
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -254,19 +306,23 @@ def main():
     t1.record(stream)
     barrier()
     ms = t0.elapsed_time(t1)
-    phases = layer.timings()
-    layer.set_profiling(False)
-    launches = layer.launch_count() * args.steps
+    phases = {}
+    for layer in layers:
+        for kname, v in layer.timings().items():
+            phases[kname] = phases.get(kname, 0.0) + v
+        layer.set_profiling(False)
+    launches = sum(layer.launch_count() for layer in layers) * args.steps
     ms_t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
     value = world * T * args.steps / (ms_max / 1000.0)
 
-    # Rows this GPU's expert GEMM processed in the last step (local + received).
-    rows = int(layer.debug(T)["key_counts"].view(world, E)[rank].sum().item()) if world == 1 else None
-    if rows is None:
-        rows = T * k  # balanced expectation for N > 1 (exact per-rank counts are in the debug view)
+    # Rows this GPU's expert GEMMs processed in one step (local + received), all layers.
+    rows = 0
+    for layer in layers:
+        kc = layer.debug(T)["key_counts"]
+        rows += int(kc.sum().item()) if world == 1 else T * k
     gemm_ms = phases.get("gemm_up", 0.0) + phases.get("gemm_down", 0.0)
     pk = peaks()
     flops = 4.0 * H * F * rows
@@ -282,19 +338,30 @@ def main():
     # ---------------------------------------------------------------- e2e through host buffers
     xh = x.cpu().pin_memory()
     yh = torch.empty_like(xh).pin_memory()
+
+    def e2e_step():
+        if len(layers) == 1:
+            if world > 1:
+                layers[0].gather_experts()
+            layers[0].forward_host(xh, yh)
+        else:
+            acts[0].copy_(xh, non_blocking=True)
+            step()
+            yh.copy_(acts[-1], non_blocking=True)
+
+    def e2e_fence():
+        if len(layers) == 1:
+            layers[0].host_fence()
+
     for _ in range(2):
-        if world > 1:
-            layer.gather_experts()
-        layer.forward_host(xh, yh)
-    layer.host_fence()
+        e2e_step()
+    e2e_fence()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        if world > 1:
-            layer.gather_experts()
-        layer.forward_host(xh, yh)
-    layer.host_fence()
+        e2e_step()
+    e2e_fence()
     e1.record(stream)
     barrier()
     clocks.__exit__()
@@ -303,6 +370,7 @@ def main():
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     e2e = world * T * args.steps / (float(e_ms.item()) / 1000.0)
     row_bytes = H * (2 if dtype == torch.bfloat16 else 4)
+    layer = layers[0]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -318,9 +386,10 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": cfg["dtype"], "data": "synthetic (dyadic tokens/gate, reference demo expert population)",
             "config": {"workload": cfg["workload"], "tokens_per_gpu": T, "hidden": H, "ffn": F, "experts": E,
-                       "top_k": k, "sf": sf, "sed": sed,
+                       "top_k": k, "sf": sf, "sed": sed, "layers": cfg["layers"], "sr_migration": use_sr,
+                       "planner_p": p_plan, "comm": "nccl" if os.environ.get("HEP_COMM") == "nccl" else "nvlink-p2p",
                        "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per GPU)" %
-                             (T * row_bytes / 1e6, layer.n * 2 * H * F * (row_bytes // H) / 1e9)},
+                             (T * row_bytes / 1e6, cfg["layers"] * len(layer.owned_experts()) * 2 * H * F * (row_bytes // H) / 1e9)},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": T * row_bytes,
                     "d2h_bytes_per_step": T * row_bytes},
             "roofline": {"bound": "tensor", "kernel": "grouped expert GEMM (up+down, tcgen05)",
@@ -334,7 +403,8 @@ def main():
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
-    layer.close()
+    for layer in layers:
+        layer.close()
     if comm:
         comm.close()
     if world > 1:

@@ -102,7 +102,8 @@ int hep_sr_resolve_k(const hep_sr_config* cfg, int64_t total_elements, int64_t e
                      int64_t* k);
 /* Exact SRC1 wire size of one expert of shape (h, m) under cfg (header + k entries). */
 int hep_sr_wire_bytes(int64_t h, int64_t m, const hep_sr_config* cfg, size_t* bytes);
-int hep_sr_workspace_bytes(size_t* bytes);
+/* Device scratch for encoding `batch` experts of shape (h, m) at once. */
+int hep_sr_workspace_bytes(int64_t h, int64_t m, int batch, size_t* bytes);
 /* Device encode = sr_encode + serialize (sparsecomp.cpp:175-224, :71-97).
  * expert: flat P = 2hm elements (w_up h x m then w_down m x h, row-major), fp32 or
  * bf16 (upcast exactly); shared: fp32 flat P.  wire: device buffer of
@@ -110,12 +111,20 @@ int hep_sr_workspace_bytes(size_t* bytes);
 int hep_sr_encode(const void* expert, hep_dtype expert_dtype, const float* shared, int64_t h,
                   int64_t m, const hep_sr_config* cfg, void* wire, size_t wire_capacity,
                   void* workspace, size_t workspace_bytes, void* stream);
+/* Batched encode: n experts (host array of device pointers, same shape, same shared
+ * expert) into n wires (host array of device pointers) in one launch sequence. */
+int hep_sr_encode_batch(const void* const* experts, int n, hep_dtype expert_dtype, const float* shared,
+                        int64_t h, int64_t m, const hep_sr_config* cfg, void* const* wires,
+                        size_t wire_capacity, void* workspace, size_t workspace_bytes, void* stream);
 /* Device decode = deserialize + sr_decode (sparsecomp.cpp:99-131, :226-246).
  * out: fp32 flat P.  status: device int32[4] (16 bytes); status[0] after the stream
  * reaches this point: 0 ok, 1 bad magic, 2 truncated, 3 bad widths, 4 shape tag
  * mismatch, 5 index out of bounds, 6 indices not increasing (status[1] = entry). */
 int hep_sr_decode(const void* wire, size_t wire_bytes, const float* shared, int64_t h, int64_t m,
                   float* out, int32_t* status, void* stream);
+/* Batched decode of n wires of wire_bytes each; status: device int32[4*n]. */
+int hep_sr_decode_batch(const void* const* wires, int n, size_t wire_bytes, const float* shared, int64_t h,
+                        int64_t m, float* const* outs, int32_t* status, void* stream);
 /* Synchronises `stream` and maps a decode status to a hep_status + message
  * (RUNTIME for corrupt wires, INVALID_ARGUMENT for a shape mismatch). */
 int hep_sr_check_status(const int32_t* status, void* stream);
@@ -187,6 +196,15 @@ int hep_layer_timings(hep_layer_t layer, char* names, size_t names_cap, float* m
 int hep_layer_launch_count(hep_layer_t layer, int* count);
 
 /* ------------------------------------------------------------- kernel-level entry points */
+/* Routing of one GPU's tokens without moving them (gate + top-k + S2 destination +
+ * S7 stable counting sort), as the step runs it on GPU `rank` of the cluster:
+ * x [T, H] and w_gate [H, E] on the device in `dtype`; outputs (device):
+ * topk_idx int32[T*k], topk_w f32[T*k], pos int32[T*k] (row in the packed send buffer),
+ * key_counts int32[G*E] (rows per (dest, expert)).  Lets one GPU verify every rank of a
+ * G-GPU hierarchy (cfg2's S_ED sweep). */
+int hep_route_plan(const hep_level* levels, int num_levels, int rank, hep_dtype dtype, const void* x,
+                   int64_t tokens, int64_t hidden, const void* w_gate, int64_t experts, int64_t top_k,
+                   int32_t* topk_idx, float* topk_w, int32_t* pos, int32_t* key_counts, void* stream);
 /* Exposed for parity tests and for frameworks that own their buffers. */
 int hep_grouped_gemm(hep_dtype dtype, const void* A, int64_t a_rows, const void* B,
                      int64_t b_slots, void* C, int64_t N, int64_t K, const int32_t* g_row_start,

@@ -118,9 +118,11 @@ SIGNATURES = {
     "hep_solve_optimal_p": [P(Workload), C.c_double, C.c_double, I64, P(C.c_double), P(I64), P(C.c_double)],
     "hep_sr_resolve_k": [P(SrConfig), I64, I64, P(I64)],
     "hep_sr_wire_bytes": [I64, I64, P(SrConfig), P(SZ)],
-    "hep_sr_workspace_bytes": [P(SZ)],
+    "hep_sr_workspace_bytes": [I64, I64, I32, P(SZ)],
     "hep_sr_encode": [VP, I32, VP, I64, I64, P(SrConfig), VP, SZ, VP, SZ, VP],
+    "hep_sr_encode_batch": [P(VP), I32, I32, VP, I64, I64, P(SrConfig), P(VP), SZ, VP, SZ, VP],
     "hep_sr_decode": [VP, SZ, VP, I64, I64, VP, VP, VP],
+    "hep_sr_decode_batch": [P(VP), I32, SZ, VP, I64, I64, P(VP), VP, VP],
     "hep_sr_check_status": [VP, VP],
     "hep_shared_mean": [P(VP), I32, I32, I64, VP, VP],
     "hep_comm_unique_id": [VP],
@@ -139,6 +141,7 @@ SIGNATURES = {
     "hep_layer_set_profiling": [VP, I32],
     "hep_layer_timings": [VP, C.c_char_p, SZ, P(C.c_float), I32, P(I32)],
     "hep_layer_launch_count": [VP, P(I32)],
+    "hep_route_plan": [P(Level), I32, I32, I32, VP, I64, I64, VP, I64, I64, VP, VP, VP, VP, VP],
     "hep_grouped_gemm": [I32, VP, I64, VP, I64, VP, I64, I64, VP, VP, VP, I32, I32, VP],
     "hep_transpose_convert": [I32, VP, I64, I64, I32, VP, VP],
 }

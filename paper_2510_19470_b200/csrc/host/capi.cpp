@@ -9,6 +9,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../kernels/kernels.h"
 #include "hep.h"
@@ -229,46 +230,80 @@ int hep_sr_wire_bytes(int64_t h, int64_t m, const hep_sr_config* cfg, size_t* by
   });
 }
 
-int hep_sr_workspace_bytes(size_t* bytes) {
-  return guarded([&] { *bytes = hep::sr_workspace_bytes(); });
+int hep_sr_workspace_bytes(int64_t h, int64_t m, int batch, size_t* bytes) {
+  return guarded([&] {
+    if (h <= 0 || m <= 0 || batch <= 0) throw std::invalid_argument("bad workspace query");
+    *bytes = hep::sr_workspace_bytes(h, m, batch);
+  });
+}
+
+namespace {
+
+hep::SrPlan make_sr_plan(int64_t h, int64_t m, const hep_sr_config* cfg) {
+  if (h <= 0 || m <= 0) throw std::invalid_argument("empty expert matrix");
+  const auto c = sr_config_of(cfg);
+  if ((c.index_width_bits != 32 && c.index_width_bits != 64) || (c.value_width_bits != 32 && c.value_width_bits != 64))
+    throw std::invalid_argument("residual widths must be 32 or 64 bits");
+  if (h > 0xffffffffll || m > 0xffffffffll) throw std::invalid_argument("shape does not fit the wire header");
+  hep::SrPlan plan{};
+  plan.h = h;
+  plan.m = m;
+  plan.total = 2 * h * m;
+  plan.k = c.resolve_k(plan.total, 4);
+  const int64_t up = h * m;
+  plan.per_matrix = c.per_matrix_budget ? 1 : 0;
+  plan.k_up = plan.per_matrix ? std::min(up, plan.k * up / plan.total) : plan.k;
+  plan.k_down = plan.per_matrix ? std::min(plan.total - up, plan.k - plan.k_up) : 0;
+  if (plan.per_matrix) plan.k = plan.k_up + plan.k_down;
+  plan.index_bits = c.index_width_bits;
+  plan.value_bits = c.value_width_bits;
+  if (c.index_width_bits == 32 && plan.total > 0xffffffffll)
+    throw std::invalid_argument("32-bit indices cannot address this expert");
+  plan.wire_bytes = static_cast<size_t>(28 + plan.k * (plan.index_bits + plan.value_bits) / 8);
+  return plan;
+}
+
+}  // namespace
+
+int hep_sr_encode_batch(const void* const* experts, int n, hep_dtype expert_dtype, const float* shared, int64_t h,
+                        int64_t m, const hep_sr_config* cfg, void* const* wires, size_t wire_capacity, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    if (n <= 0 || n > hep::kMaxSrBatch) throw std::invalid_argument("batch must be in [1, 64]");
+    const hep::SrPlan plan = make_sr_plan(h, m, cfg);
+    if (wire_capacity < plan.wire_bytes) throw std::invalid_argument("wire buffer too small");
+    if (workspace_bytes < hep::sr_workspace_bytes(h, m, n)) throw std::invalid_argument("workspace too small");
+    cuda_ok(hep::launch_sr_encode_batch(dt_of(expert_dtype), experts, n, shared, plan,
+                                        reinterpret_cast<uint8_t* const*>(wires), workspace, st(stream)),
+            "sr encode");
+  });
 }
 
 int hep_sr_encode(const void* expert, hep_dtype expert_dtype, const float* shared, int64_t h, int64_t m,
                   const hep_sr_config* cfg, void* wire, size_t wire_capacity, void* workspace,
                   size_t workspace_bytes, void* stream) {
+  const void* e[1] = {expert};
+  void* w[1] = {wire};
+  return hep_sr_encode_batch(e, 1, expert_dtype, shared, h, m, cfg, w, wire_capacity, workspace, workspace_bytes,
+                             stream);
+}
+
+int hep_sr_decode_batch(const void* const* wires, int n, size_t wire_bytes, const float* shared, int64_t h, int64_t m,
+                        float* const* outs, int32_t* status, void* stream) {
   return guarded([&] {
     if (h <= 0 || m <= 0) throw std::invalid_argument("empty expert matrix");
-    const auto c = sr_config_of(cfg);
-    if ((c.index_width_bits != 32 && c.index_width_bits != 64) || (c.value_width_bits != 32 && c.value_width_bits != 64))
-      throw std::invalid_argument("residual widths must be 32 or 64 bits");
-    if (h > 0xffffffffll || m > 0xffffffffll) throw std::invalid_argument("shape does not fit the wire header");
-    hep::SrPlan plan{};
-    plan.h = h;
-    plan.m = m;
-    plan.total = 2 * h * m;
-    plan.k = c.resolve_k(plan.total, 4);
-    const int64_t up = h * m;
-    plan.per_matrix = c.per_matrix_budget ? 1 : 0;
-    plan.k_up = plan.per_matrix ? std::min(up, plan.k * up / plan.total) : plan.k;
-    plan.k_down = plan.per_matrix ? std::min(plan.total - up, plan.k - plan.k_up) : 0;
-    if (plan.per_matrix) plan.k = plan.k_up + plan.k_down;
-    plan.index_bits = c.index_width_bits;
-    plan.value_bits = c.value_width_bits;
-    if (c.index_width_bits == 32 && plan.total > 0xffffffffll)
-      throw std::invalid_argument("32-bit indices cannot address this expert");
-    plan.wire_bytes = static_cast<size_t>(28 + plan.k * (plan.index_bits + plan.value_bits) / 8);
-    if (wire_capacity < plan.wire_bytes) throw std::invalid_argument("wire buffer too small");
-    if (workspace_bytes < hep::sr_workspace_bytes()) throw std::invalid_argument("workspace too small");
-    cuda_ok(hep::launch_sr_encode(dt_of(expert_dtype), expert, shared, plan, wire, workspace, st(stream)), "sr encode");
+    if (n <= 0 || n > hep::kMaxSrBatch) throw std::invalid_argument("batch must be in [1, 64]");
+    cuda_ok(hep::launch_sr_decode_batch(reinterpret_cast<const uint8_t* const*>(wires), n, wire_bytes, shared, h, m,
+                                        outs, status, st(stream)),
+            "sr decode");
   });
 }
 
 int hep_sr_decode(const void* wire, size_t wire_bytes, const float* shared, int64_t h, int64_t m, float* out,
                   int32_t* status, void* stream) {
-  return guarded([&] {
-    if (h <= 0 || m <= 0) throw std::invalid_argument("empty expert matrix");
-    cuda_ok(hep::launch_sr_decode(wire, wire_bytes, shared, h, m, out, status, st(stream)), "sr decode");
-  });
+  const void* w[1] = {wire};
+  float* o[1] = {out};
+  return hep_sr_decode_batch(w, 1, wire_bytes, shared, h, m, o, status, stream);
 }
 
 int hep_sr_check_status(const int32_t* status, void* stream) {
@@ -392,6 +427,52 @@ int hep_layer_timings(hep_layer_t layer, char* names, size_t names_cap, float* m
 
 int hep_layer_launch_count(hep_layer_t layer, int* count) {
   return guarded([&] { *count = layer->impl->launch_count(); });
+}
+
+int hep_route_plan(const hep_level* levels, int num_levels, int rank, hep_dtype dtype, const void* x,
+                   int64_t tokens, int64_t hidden, const void* w_gate, int64_t experts, int64_t top_k,
+                   int32_t* topk_idx, float* topk_w, int32_t* pos, int32_t* key_counts, void* stream) {
+  return guarded([&] {
+    const auto c = cluster_of(levels, num_levels);
+    c.validate();
+    const int64_t G = c.total_gpus();
+    if (rank < 0 || rank >= G) throw std::domain_error("rank out of range");
+    if (experts % G) throw std::invalid_argument("experts must be divisible by the GPU count");
+    if (tokens <= 0 || hidden <= 0 || top_k <= 0 || top_k > 8 || top_k > experts || experts > 64)
+      throw std::invalid_argument("bad routing shape");
+    const auto route = hybridep::moe::route_table(c);
+    const int T = static_cast<int>(tokens), H = static_cast<int>(hidden), E = static_cast<int>(experts);
+    const int k = static_cast<int>(top_k), NK = static_cast<int>(G * experts);
+    const int nchunks = (T + 31) / 32;
+    const hep::DType dt = dt_of(dtype);
+    cudaStream_t s = st(stream);
+    hep::DevBuf wg, dest, keys, ranks, cc, coff, koff, dr, doff, gs, grs, gsl, slots;
+    wg.alloc(static_cast<size_t>(experts * hidden * hep::dtype_bytes(dt)));
+    cuda_ok(hep::launch_transpose_convert(dt, w_gate, hidden, experts, dt, wg.p, s), "gate layout");
+    dest.alloc(sizeof(int) * G);
+    cuda_ok(cudaMemcpyAsync(dest.p, route.data() + rank * G, sizeof(int) * G, cudaMemcpyHostToDevice, s), "route");
+    keys.alloc(sizeof(int) * T * k);
+    ranks.alloc(sizeof(int) * T * k);
+    cc.alloc(sizeof(int) * nchunks * NK);
+    coff.alloc(sizeof(int) * nchunks * NK);
+    koff.alloc(sizeof(int) * NK);
+    dr.alloc(sizeof(int) * G);
+    doff.alloc(sizeof(int) * G);
+    gs.alloc(sizeof(int) * E);
+    grs.alloc(sizeof(int) * E);
+    gsl.alloc(sizeof(int) * E);
+    std::vector<int32_t> none(static_cast<size_t>(E), -1);
+    slots.alloc(sizeof(int) * E);
+    cuda_ok(cudaMemcpyAsync(slots.p, none.data(), sizeof(int) * E, cudaMemcpyHostToDevice, s), "slots");
+    cuda_ok(hep::launch_gate(dt, x, wg.p, T, H, E, k, dest.as<int>(), static_cast<int>(experts / G), NK, topk_idx,
+                             topk_w, keys.as<int>(), ranks.as<int>(), cc.as<int>(), s), "gate");
+    cuda_ok(hep::launch_chunk_scan(cc.as<int>(), nchunks, NK, coff.as<int>(), key_counts, s), "chunk scan");
+    cuda_ok(hep::launch_key_scan(key_counts, static_cast<int>(G), E, rank, slots.as<int>(), koff.as<int>(), dr.as<int>(),
+                                 doff.as<int>(), gs.as<int>(), grs.as<int>(), gsl.as<int>(), s), "key scan");
+    cuda_ok(hep::launch_positions(T, k, NK, keys.as<int>(), ranks.as<int>(), coff.as<int>(), koff.as<int>(), pos, s),
+            "positions");
+    cuda_ok(cudaStreamSynchronize(s), "route sync");  // scratch buffers are freed on return
+  });
 }
 
 int hep_grouped_gemm(hep_dtype dtype, const void* A, int64_t a_rows, const void* B, int64_t b_slots, void* C,

@@ -147,9 +147,10 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
                     sr_cfg_.value_width_bits, sr_cfg_.per_matrix_budget ? 1 : 0};
     if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
     wires_.alloc(((wb + 15) / 16 * 16) * slots_);
-    sr_ws_.alloc(sr_workspace_bytes());
+    sr_ws_.alloc(sr_workspace_bytes(H_, F_, static_cast<int>(n_)));
+    sr_dec_.alloc(sizeof(float) * P * std::max<int64_t>(1, std::min<int64_t>(slots_ - n_, kMaxSrBatch)));
     sr_tmp_.alloc(sizeof(float) * P);
-    sr_status_.alloc(16);
+    sr_status_.alloc(16 * kMaxSrBatch);
   }
   for (int b = 0; b < 2; ++b) {
     x_dev_[b].alloc(eb * Tmax_ * H_);
@@ -299,9 +300,15 @@ void Layer::gather_experts(cudaStream_t s) {
   if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
   const size_t stride = (wb + 15) / 16 * 16;
   uint8_t* wires = wires_.as<uint8_t>();
-  for (int64_t i = 0; i < n_; ++i) {
-    if (hep_sr_encode(master_.as<float>() + i * P, HEP_F32, shared_.as<float>(), H_, F_, &c,
-                      wires + stride * (first_slot_of(rank_) + i), wb, sr_ws_.p, sr_ws_.bytes, s) != HEP_OK)
+  {
+    std::vector<const void*> ex;
+    std::vector<void*> wo;
+    for (int64_t i = 0; i < n_; ++i) {
+      ex.push_back(master_.as<float>() + i * P);
+      wo.push_back(wires + stride * (first_slot_of(rank_) + i));
+    }
+    if (hep_sr_encode_batch(ex.data(), static_cast<int>(n_), HEP_F32, shared_.as<float>(), H_, F_, &c, wo.data(), wb,
+                            sr_ws_.p, sr_ws_.bytes, s) != HEP_OK)
       throw std::runtime_error(hep_last_error());
   }
   nck(ncclGroupStart(), "group start");
@@ -310,13 +317,27 @@ void Layer::gather_experts(cudaStream_t s) {
     nck(ncclRecv(wires + stride * first_slot_of(p), stride * n_, ncclUint8, static_cast<int>(p), comm_->nccl, s), "recv wire");
   }
   nck(ncclGroupEnd(), "group end");
+  // Decode gathered wires in batches, then lay each decoded expert out as a compute slot.
+  std::vector<int64_t> gathered;
   for (int64_t p : ag_peers_)
-    for (int64_t i = 0; i < n_; ++i) {
-      const int64_t slot = first_slot_of(p) + i;
-      ck(launch_sr_decode(wires + stride * slot, wb, shared_.as<float>(), H_, F_, sr_tmp_.as<float>(), sr_status_.as<int32_t>(), s), "decode");
-      ck(launch_transpose_convert(DType::F32, sr_tmp_.p, H_, F_, dt_, w_up_c_.as<uint8_t>() + eb * slot * per_slot_up, s), "dec up");
-      ck(launch_transpose_convert(DType::F32, sr_tmp_.as<float>() + H_ * F_, F_, H_, dt_, w_down_c_.as<uint8_t>() + eb * slot * per_slot_down, s), "dec down");
+    for (int64_t i = 0; i < n_; ++i) gathered.push_back(first_slot_of(p) + i);
+  const int64_t cap = static_cast<int64_t>(sr_dec_.bytes / (sizeof(float) * P));
+  for (size_t b0 = 0; b0 < gathered.size(); b0 += static_cast<size_t>(cap)) {
+    const size_t nb = std::min(gathered.size() - b0, static_cast<size_t>(cap));
+    std::vector<const void*> wi;
+    std::vector<float*> outs;
+    for (size_t i = 0; i < nb; ++i) {
+      wi.push_back(wires + stride * gathered[b0 + i]);
+      outs.push_back(sr_dec_.as<float>() + static_cast<int64_t>(i) * P);
     }
+    ck(launch_sr_decode_batch(reinterpret_cast<const uint8_t* const*>(wi.data()), static_cast<int>(nb), wb,
+                              shared_.as<float>(), H_, F_, outs.data(), sr_status_.as<int32_t>(), s), "decode");
+    for (size_t i = 0; i < nb; ++i) {
+      const int64_t slot = gathered[b0 + i];
+      ck(launch_transpose_convert(DType::F32, outs[i], H_, F_, dt_, w_up_c_.as<uint8_t>() + eb * slot * per_slot_up, s), "dec up");
+      ck(launch_transpose_convert(DType::F32, outs[i] + H_ * F_, F_, H_, dt_, w_down_c_.as<uint8_t>() + eb * slot * per_slot_down, s), "dec down");
+    }
+  }
 }
 
 void Layer::mark(const char* name, cudaStream_t s) {

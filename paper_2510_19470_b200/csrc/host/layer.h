@@ -87,7 +87,7 @@ class Layer {
 
   // device state
   DevBuf d_route_, d_slot_of_expert_, wg_t_, w_up_c_, w_down_c_;
-  DevBuf shared_, master_, wires_, sr_ws_, sr_tmp_, sr_status_;
+  DevBuf shared_, master_, wires_, sr_ws_, sr_tmp_, sr_dec_, sr_status_;
   DevBuf topk_idx_, topk_w_, keys_, ranks_, chunk_counts_, chunk_off_, key_total_, key_off_;
   DevBuf dest_rows_, dest_off_, g_row_start_, g_rows_, g_slot_, all_counts_;
   DevBuf pos_, xall_, hbuf_, oall_;

@@ -40,6 +40,10 @@ cudaError_t launch_permute(DType dt, const void* x, int T, int H, int k, int NK,
                            const int* ranks, const int* chunk_off, const int* key_off, int* pos,
                            void* packed, cudaStream_t stream);
 
+// pos only (no row movement): the routing-plan entry point.
+cudaError_t launch_positions(int T, int k, int NK, const int* keys, const int* ranks, const int* chunk_off,
+                             const int* key_off, int* pos, cudaStream_t stream);
+
 // y[t] = sum_j w[t,j] * out[pos[t,j]]  (slot order, fp32 accumulate).
 cudaError_t launch_combine(DType dt, const void* out, const int* pos, const float* topk_w, int T,
                            int H, int k, void* y, cudaStream_t stream);
@@ -81,12 +85,16 @@ struct SrPlan {
   size_t wire_bytes;
 };
 
-size_t sr_workspace_bytes();
-cudaError_t launch_sr_encode(DType expert_dt, const void* expert, const float* shared,
-                             const SrPlan& plan, void* wire, void* workspace, cudaStream_t stream);
-// Validates the wire (status[0] = code, 0 ok) and writes out = shared + residual (fp32).
-cudaError_t launch_sr_decode(const void* wire, size_t wire_bytes, const float* shared, int64_t h,
-                             int64_t m, float* out, int32_t* status, cudaStream_t stream);
+constexpr int kMaxSrBatch = 64;
+size_t sr_workspace_bytes(int64_t h, int64_t m, int batch);
+// Encodes `batch` experts (same shape, same shared expert) in one launch sequence.
+cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, int batch, const float* shared,
+                                   const SrPlan& plan, uint8_t* const* wires, void* workspace,
+                                   cudaStream_t stream);
+// Validates each wire (status int32[4] per wire: code, failing entry, scratch) and writes
+// out_b = shared + residual_b (fp32).
+cudaError_t launch_sr_decode_batch(const uint8_t* const* wires, int batch, size_t wire_bytes, const float* shared,
+                                   int64_t h, int64_t m, float* const* outs, int32_t* status, cudaStream_t stream);
 // out = mean over experts (fp64 accumulate in list order, times 1/n, round to fp32).
 cudaError_t launch_shared_mean(DType dt, const void* const* experts, int n, int64_t P, float* out,
                                cudaStream_t stream);

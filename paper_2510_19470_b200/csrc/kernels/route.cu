@@ -472,6 +472,15 @@ __global__ void __launch_bounds__(256) permute_kernel(const uint8_t* __restrict_
   }
 }
 
+__global__ void positions_kernel(int T_tok, int k, int NK, const int* __restrict__ keys,
+                                 const int* __restrict__ ranks, const int* __restrict__ chunk_off,
+                                 const int* __restrict__ key_off, int* __restrict__ pos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= T_tok * k) return;
+  const int t = i / k, key = keys[i];
+  pos[i] = key_off[key] + chunk_off[static_cast<size_t>(t / kChunk) * NK + key] + ranks[i];
+}
+
 // One warp per token.  bf16 rows: 8 elements per 16-byte vector.
 __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* __restrict__ out,
                                                            const int* __restrict__ pos,
@@ -582,6 +591,12 @@ cudaError_t launch_permute(DType dt, const void* x, int T, int H, int k, int NK,
   permute_kernel<<<blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(x), T, row_bytes, k, NK,
                                              keys, ranks, chunk_off, key_off, pos,
                                              static_cast<uint8_t*>(packed));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_positions(int T, int k, int NK, const int* keys, const int* ranks, const int* chunk_off,
+                             const int* key_off, int* pos, cudaStream_t stream) {
+  positions_kernel<<<(T * k + 255) / 256, 256, 0, stream>>>(T, k, NK, keys, ranks, chunk_off, key_off, pos);
   return cudaGetLastError();
 }
 

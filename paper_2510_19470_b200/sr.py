@@ -59,11 +59,11 @@ def wire_bytes(h: int, m: int, cfg: CompressionConfig) -> int:
 _ws_cache: dict = {}
 
 
-def _workspace(device) -> torch.Tensor:
+def _workspace(device, h: int, m: int, batch: int = 1) -> torch.Tensor:
+    n = C.c_size_t()
+    check(lib.hep_sr_workspace_bytes(h, m, batch, C.byref(n)))
     key = str(device)
-    if key not in _ws_cache:
-        n = C.c_size_t()
-        check(lib.hep_sr_workspace_bytes(C.byref(n)))
+    if key not in _ws_cache or _ws_cache[key].numel() < n.value:
         _ws_cache[key] = torch.empty(n.value, dtype=torch.uint8, device=device)
     return _ws_cache[key]
 
@@ -73,10 +73,36 @@ def sr_encode(expert: torch.Tensor, shared: torch.Tensor, h: int, m: int, cfg: C
     assert expert.is_cuda and expert.is_contiguous() and shared.dtype == torch.float32
     nbytes = wire_bytes(h, m, cfg)
     wire = torch.empty(nbytes, dtype=torch.uint8, device=expert.device)
-    ws = _workspace(expert.device)
+    ws = _workspace(expert.device, h, m)
     check(lib.hep_sr_encode(expert.data_ptr(), _dt(expert), shared.data_ptr(), h, m, C.byref(cfg._c()),
                             wire.data_ptr(), nbytes, ws.data_ptr(), ws.numel(), _stream()))
     return wire
+
+
+def sr_encode_batch(experts: list, shared: torch.Tensor, h: int, m: int, cfg: CompressionConfig) -> list:
+    """Encodes several experts (same shape, same shared expert) in one launch sequence."""
+    n = len(experts)
+    nbytes = wire_bytes(h, m, cfg)
+    wires = [torch.empty(nbytes, dtype=torch.uint8, device=shared.device) for _ in range(n)]
+    ws = _workspace(shared.device, h, m, n)
+    eps = (C.c_void_p * n)(*[e.data_ptr() for e in experts])
+    wps = (C.c_void_p * n)(*[w.data_ptr() for w in wires])
+    check(lib.hep_sr_encode_batch(eps, n, _dt(experts[0]), shared.data_ptr(), h, m, C.byref(cfg._c()), wps, nbytes,
+                                  ws.data_ptr(), ws.numel(), _stream()))
+    return wires
+
+
+def sr_decode_batch(wires: list, shared: torch.Tensor, h: int, m: int) -> list:
+    n = len(wires)
+    outs = [torch.empty(2 * h * m, dtype=torch.float32, device=shared.device) for _ in range(n)]
+    status = torch.zeros(4 * n, dtype=torch.int32, device=shared.device)
+    wps = (C.c_void_p * n)(*[w.data_ptr() for w in wires])
+    ops = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    check(lib.hep_sr_decode_batch(wps, n, wires[0].numel(), shared.data_ptr(), h, m, ops, status.data_ptr(),
+                                  _stream()))
+    for i in range(n):
+        check(lib.hep_sr_check_status(status[4 * i:].data_ptr(), _stream()))
+    return outs
 
 
 def sr_decode(wire: torch.Tensor, shared: torch.Tensor, h: int, m: int, check_status: bool = True) -> torch.Tensor:

@@ -177,3 +177,20 @@ def test_transpose_convert():
     check(lib.hep_transpose_convert(HEP_F32, x.data_ptr(), 100, 260, HEP_BF16, out.data_ptr(), _stream()))
     torch.cuda.synchronize()
     assert torch.equal(out, x.T.contiguous().to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("per_matrix", [False, True])
+def test_sr_batched_encode_decode_bitexact(per_matrix):
+    """One launch sequence for several experts (the layer encodes all owned experts at once)."""
+    h, m, n = 40, 56, 5
+    s = _demo_expert_pair(h, m, seed=99)[1]
+    experts = [_demo_expert_pair(h, m, seed=100 + i, quantize=bool(i % 2))[0] for i in range(n)]
+    cfg = srmod.CompressionConfig(ratio_CR=9.0, per_matrix_budget=per_matrix)
+    st = torch.from_numpy(s).cuda()
+    wires = srmod.sr_encode_batch([torch.from_numpy(e).cuda() for e in experts], st, h, m, cfg)
+    outs = srmod.sr_decode_batch(wires, st, h, m)
+    for e, w, o in zip(experts, wires, outs):
+        want = oracle.sr_encode(e, s, h, m, ratio=9.0, per_matrix=per_matrix)
+        assert w.cpu().numpy().tobytes() == want.tobytes()
+        rc, dec = oracle.sr_decode(want, s, h, m)
+        assert rc == 0 and o.cpu().numpy().tobytes() == dec.tobytes()
