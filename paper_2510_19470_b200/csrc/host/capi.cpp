@@ -485,9 +485,13 @@ int hep_grouped_gemm(hep_dtype dtype, const void* A, int64_t a_rows, const void*
     hep::GroupTable gt{g_row_start, g_rows, g_slot, num_groups};
     if (dt_of(dtype) == hep::DType::BF16) {
       CUtensorMap ma, mb;
+      const bool pair = hep::gemm_use_cta_pair();
       cuda_ok(hep::make_tmap_bf16_2d(&ma, A, static_cast<uint64_t>(a_rows), static_cast<uint64_t>(K), 128, 64), "tmap A");
-      cuda_ok(hep::make_tmap_bf16_2d(&mb, B, static_cast<uint64_t>(b_slots * N), static_cast<uint64_t>(K), 256, 64), "tmap B");
-      cuda_ok(hep::launch_grouped_gemm_bf16(ma, mb, C, static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt, relu, sms, st(stream)), "gemm bf16");
+      cuda_ok(hep::make_tmap_bf16_2d(&mb, B, static_cast<uint64_t>(b_slots * N), static_cast<uint64_t>(K), pair ? 128 : 256, 64), "tmap B");
+      if (pair)
+        cuda_ok(hep::launch_grouped_gemm_bf16_2cta(ma, mb, C, static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt, relu, sms, st(stream)), "gemm bf16 2cta");
+      else
+        cuda_ok(hep::launch_grouped_gemm_bf16(ma, mb, C, static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt, relu, sms, st(stream)), "gemm bf16");
     } else {
       cuda_ok(hep::launch_grouped_gemm_f32(static_cast<const float*>(A), static_cast<int>(K), static_cast<const float*>(B),
                                            static_cast<float*>(C), static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt,

@@ -133,9 +133,11 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
 
   if (dt_ == DType::BF16) {
     ck(make_tmap_bf16_2d(&map_a1_, xall_.p, rows_cap_, H_, 128, 64), "tmap a1");
-    ck(make_tmap_bf16_2d(&map_b1_, w_up_c_.p, slots_ * F_, H_, 256, 64), "tmap b1");
+    cta_pair_ = gemm_use_cta_pair();
+    const uint32_t b_box = cta_pair_ ? 128 : 256;
+    ck(make_tmap_bf16_2d(&map_b1_, w_up_c_.p, slots_ * F_, H_, b_box, 64), "tmap b1");
     ck(make_tmap_bf16_2d(&map_a2_, hbuf_.p, rows_cap_, F_, 128, 64), "tmap a2");
-    ck(make_tmap_bf16_2d(&map_b2_, w_down_c_.p, slots_ * H_, F_, 256, 64), "tmap b2");
+    ck(make_tmap_bf16_2d(&map_b2_, w_down_c_.p, slots_ * H_, F_, b_box, 64), "tmap b2");
   }
 
   if (use_sr_) {
@@ -428,9 +430,10 @@ void Layer::run_expert_gemms(cudaStream_t s) {
   GroupTable gt{g_row_start_.as<int>(), g_rows_.as<int>(), g_slot_.as<int>(), num_groups_};
   if (dt_ == DType::BF16) {
     mark("gemm_up", s);
-    ck(launch_grouped_gemm_bf16(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_), "gemm up");
+    auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta : launch_grouped_gemm_bf16;
+    ck(gemm(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_), "gemm up");
     mark("gemm_down", s);
-    ck(launch_grouped_gemm_bf16(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, sched_down_), "gemm down");
+    ck(gemm(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, sched_down_), "gemm down");
   } else {
     mark("gemm_up", s);
     ck(launch_grouped_gemm_f32(xall_.as<float>(), static_cast<int>(H_), w_up_c_.as<float>(), hbuf_.as<float>(), static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_ * 2, s), "gemm up");

@@ -94,6 +94,7 @@ class Layer {
   int64_t rows_cap_;
   CUtensorMap map_a1_, map_b1_, map_a2_, map_b2_;
   uint32_t sched_up_ = 0, sched_down_ = 0;
+  bool cta_pair_ = true;
 
   // NVLink peer-memory path (default for G > 1; HEP_COMM=nccl selects the NCCL baseline)
   bool p2p_ = false;

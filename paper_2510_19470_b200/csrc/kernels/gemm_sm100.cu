@@ -259,6 +259,217 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
   }
 }
 
+// ============================================================================
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x 256 tile.  CTA r stages rows [128r, 128r+128) of the A tile and of the B tile
+// (N half) in its own shared memory; the leader (rank 0) issues one
+// tcgen05.mma.cta_group::2 M=256 N=256 K=16 that reads both CTAs' halves and writes
+// each CTA's 128 accumulator rows into that CTA's TMEM.  Per SM this halves the B
+// bytes staged and read per FLOP (32 KB per 64-deep k-step instead of 48 KB), which is
+// what lets the tensor pipe stay fed; both CTAs' TMA loads complete on the leader's
+// full barrier, the leader's commits multicast to both CTAs' empty/tfull barriers,
+// and both epilogues release the accumulator on the leader's tempty barrier.
+constexpr int P_BM = 256;          // rows per cluster tile (128 per CTA)
+constexpr int P_BN = 256;
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * BK * 2;
+constexpr int P_B_BYTES = 128 * BK * 2;
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+
+struct SmemCtl2 {
+  uint64_t full[P_STAGES];
+  uint64_t empty[P_STAGES];
+  uint64_t tfull[ACC];
+  uint64_t tempty[ACC];
+  uint32_t tmem_base;
+  int num_tiles;
+  int tile_start[kMaxGroups + 1];
+  int row_start[kMaxGroups];
+  int rows[kMaxGroups];
+  int slot[kMaxGroups];
+};
+
+constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + sizeof(SmemCtl2);
+
+__device__ __forceinline__ int find_group2(const SmemCtl2& s, int ng, int tile) {
+  int lo = 0, hi = ng - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s.tile_start[mid] <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                              __nv_bfloat16* __restrict__ C, int ldc, int N, int K,
+                              const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
+                              const int* __restrict__ g_slot, int ng, int relu, uint32_t sched) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* stage_a = smem;
+  uint8_t* stage_b = smem + P_STAGES * P_A_BYTES;
+  SmemCtl2& s = *reinterpret_cast<SmemCtl2*>(smem + P_STAGES * P_STAGE_BYTES);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t cta = cluster_ctarank();
+  const int cluster = static_cast<int>(blockIdx.x >> 1), nclusters = static_cast<int>(gridDim.x >> 1);
+  const int n_tiles = (N + P_BN - 1) / P_BN;
+  const int num_kb = K / BK;
+
+  if (warp == 2) {
+    int carry = 0;
+    for (int base = 0; base < ng; base += 32) {
+      const int g = base + lane;
+      int tiles = 0;
+      if (g < ng) {
+        const int r = g_rows[g];
+        s.row_start[g] = g_row_start[g];
+        s.rows[g] = r;
+        s.slot[g] = g_slot[g];
+        tiles = ((r + P_BM - 1) / P_BM) * n_tiles;
+      }
+      int incl = tiles;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+      }
+      if (g < ng) s.tile_start[g] = carry + incl - tiles;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      s.tile_start[ng] = carry;
+      s.num_tiles = carry;
+    }
+  } else if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int i = 0; i < P_STAGES; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < ACC; ++i) {
+      mbar_init(&s.tfull[i], 1);
+      mbar_init(&s.tempty[i], 8);  // 4 epilogue warps x 2 CTAs (used in the leader)
+    }
+    fence_barrier_init();
+  } else if (warp == 1) {
+    tmem_alloc_2sm(&s.tmem_base, TMEM_COLS);
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+
+  const int total = s.num_tiles;
+  const uint32_t tmem_base = s.tmem_base;
+
+  if (warp == 0) {
+    // ================= TMA producer (both CTAs) =================
+    if (lane == 0) {
+      const uint64_t pol_a = make_policy(sched & 3u);
+      const uint64_t pol_b = make_policy((sched >> 2) & 3u);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < total; tile += nclusters) {
+        const int g = find_group2(s, ng, tile);
+        const int local = tile - s.tile_start[g];
+        const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
+        int mt, nt;
+        decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
+        const int a_row = s.row_start[g] + mt * P_BM + 128 * static_cast<int>(cta);
+        const int b_row = s.slot[g] * N + nt * P_BN + 128 * static_cast<int>(cta);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&s.empty[stage], phase ^ 1);
+          if (cta == 0) mbar_arrive_expect_tx(&s.full[stage], 2 * P_STAGE_BYTES);
+          tma_load_2d_2sm(stage_a + stage * P_A_BYTES, &map_a, &s.full[stage], kb * BK, a_row, pol_a);
+          tma_load_2d_2sm(stage_b + stage * P_B_BYTES, &map_b, &s.full[stage], kb * BK, b_row, pol_b);
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (leader CTA only) =================
+    if (cta == 0 && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(P_BM, P_BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster; tile < total; tile += nclusters) {
+        mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * P_BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&s.full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_addr(stage_a + stage * P_A_BYTES);
+          const uint32_t b_addr = smem_addr(stage_b + stage * P_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_2sm(d_tmem, umma_desc_k_sw128(a_addr + 32 * k), umma_desc_k_sw128(b_addr + 32 * k), idesc,
+                          (kb | k) != 0);
+          umma_commit_2sm_mc(&s.empty[stage], 0x3);
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_2sm_mc(&s.tfull[acc], 0x3);
+        if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ================= epilogue (warps 2..5, both CTAs) =================
+    const uint32_t quarter = warp & 3u;
+    const int row_in_tile = static_cast<int>(128 * cta + quarter * 32 + lane);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cluster; tile < total; tile += nclusters) {
+      const int g = find_group2(s, ng, tile);
+      const int local = tile - s.tile_start[g];
+      const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
+      int mt, nt;
+      decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
+      const int r_local = mt * P_BM + row_in_tile;
+      const bool row_ok = r_local < s.rows[g];
+      __nv_bfloat16* crow = C + static_cast<size_t>(s.row_start[g] + r_local) * ldc + nt * P_BN;
+
+      mbar_wait(&s.tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_base = tmem_base + static_cast<uint32_t>(acc * P_BN) + ((quarter * 32u) << 16);
+#pragma unroll 1
+      for (int c = 0; c < P_BN; c += 32) {
+        if (nt * P_BN + c >= N) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_base + static_cast<uint32_t>(c), v);
+        tmem_ld_wait();
+        if (row_ok) {
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = __uint_as_float(v[i]);
+            f[i] = relu ? fmaxf(x, 0.f) : x;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) st_v4(crow + c + 8 * q, pack8(f + 8 * q));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&s.tempty[acc]);
+      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+  }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -277,6 +488,11 @@ EncodeTiledFn encode_fn() {
 }
 
 }  // namespace
+
+bool gemm_use_cta_pair() {
+  const char* env = std::getenv("HEP_GEMM_2CTA");
+  return !(env && env[0] == '0');
+}
 
 uint32_t gemm_schedule(int rows_per_expert, int N, int K, bool up) {
   const char* env = std::getenv(up ? "HEP_GEMM_SCHED_UP" : "HEP_GEMM_SCHED_DOWN");
@@ -323,6 +539,25 @@ cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap
   grouped_gemm_bf16_kernel<<<num_sms, kThreads, kSmemBytes, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
       groups.slot, groups.num_groups, relu, sched);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C, int ldc,
+                                          int N, int K, const GroupTable& groups, int relu, int num_sms,
+                                          cudaStream_t stream, uint32_t sched) {
+  if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(kSmemBytes2));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int grid = (num_sms / 2) * 2;
+  grouped_gemm_bf16_2cta_kernel<<<grid, kThreads, kSmemBytes2, stream>>>(
+      map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
+      groups.num_groups, relu, sched);
   return cudaGetLastError();
 }
 

@@ -65,6 +65,12 @@ cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows,
 cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C,
                                      int ldc, int N, int K, const GroupTable& groups, int relu,
                                      int num_sms, cudaStream_t stream, uint32_t sched = 0x8u);
+// CTA-pair variant (cta_group::2, 256x256 cluster tiles); B's tensor map box is 128 rows.
+cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C, int ldc,
+                                          int N, int K, const GroupTable& groups, int relu, int num_sms,
+                                          cudaStream_t stream, uint32_t sched = 0x6u);
+// CTA-pair GEMM unless HEP_GEMM_2CTA=0 (the 1-CTA kernel stays for A/B comparisons).
+bool gemm_use_cta_pair();
 // Schedule for one expert GEMM shape: A operand reused across n-tiles is kept in L2
 // (evict_last) when one expert's A fits, otherwise super-row rasterisation.  The
 // HEP_GEMM_SCHED_UP / HEP_GEMM_SCHED_DOWN environment variables override (hex).

@@ -92,7 +92,7 @@ def sr_encode_batch(experts: list, shared: torch.Tensor, h: int, m: int, cfg: Co
     return wires
 
 
-def sr_decode_batch(wires: list, shared: torch.Tensor, h: int, m: int) -> list:
+def sr_decode_batch(wires: list, shared: torch.Tensor, h: int, m: int, check_status: bool = True) -> list:
     n = len(wires)
     outs = [torch.empty(2 * h * m, dtype=torch.float32, device=shared.device) for _ in range(n)]
     status = torch.zeros(4 * n, dtype=torch.int32, device=shared.device)
@@ -100,8 +100,9 @@ def sr_decode_batch(wires: list, shared: torch.Tensor, h: int, m: int) -> list:
     ops = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
     check(lib.hep_sr_decode_batch(wps, n, wires[0].numel(), shared.data_ptr(), h, m, ops, status.data_ptr(),
                                   _stream()))
-    for i in range(n):
-        check(lib.hep_sr_check_status(status[4 * i:].data_ptr(), _stream()))
+    if check_status:
+        for i in range(n):
+            check(lib.hep_sr_check_status(status[4 * i:].data_ptr(), _stream()))
     return outs
 
 

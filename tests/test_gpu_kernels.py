@@ -45,13 +45,15 @@ def _reference(A, B, N, rows, slots, relu):
     return torch.cat(out) if out else None
 
 
+@pytest.mark.parametrize("pair", ["1", "0"], ids=["cta_pair", "single_cta"])
 @pytest.mark.parametrize("K,N,rows,relu", [
     (256, 512, [300, 0, 128, 1, 77], 1),
     (1408, 2048, [129, 256], 0),      # cfg4 down-projection K, N multiple of 256
     (2048, 1408, [200, 513], 1),      # cfg4 up-projection: N tail (1408 = 5.5 x 256)
     (4096, 768, [1000], 0),
 ])
-def test_grouped_gemm_bf16(K, N, rows, relu):
+def test_grouped_gemm_bf16(K, N, rows, relu, pair, monkeypatch):
+    monkeypatch.setenv("HEP_GEMM_2CTA", pair)
     g = torch.Generator(device="cuda").manual_seed(1)
     n_slots = 3
     R = sum(rows)

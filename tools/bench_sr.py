@@ -25,12 +25,21 @@ SHAPES = {"cfg1": (1024, 4096, 8), "cfg4": (2048, 1408, 64), "cfg3": (4096, 1433
 
 
 def timed(fn, reps):
+    """Device time per call: the call is captured once in a CUDA graph and replayed, so
+    host-side Python/ctypes overhead (tens of us) does not leak into small-expert timings."""
     fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(reps):
-        fn()
+        g.replay()
     e.record()
     torch.cuda.synchronize()
     return s.elapsed_time(e) / reps
@@ -63,7 +72,7 @@ def main():
         batch = [expert + float(i) * 2 ** -12 for i in range(nb)]
         t_enc_b = timed(lambda: sr.sr_encode_batch(batch, shared, h, m, cfg), max(2, a.reps // 4))
         wires_b = sr.sr_encode_batch(batch, shared, h, m, cfg)
-        t_dec_b = timed(lambda: sr.sr_decode_batch(wires_b, shared, h, m), max(2, a.reps // 4))
+        t_dec_b = timed(lambda: sr.sr_decode_batch(wires_b, shared, h, m, check_status=False), max(2, a.reps // 4))
         n_mean = min(E, 8)
         experts = [expert + float(i) * 2 ** -10 for i in range(n_mean)]  # distinct buffers (no L2 reuse)
         t_mean = timed(lambda: sr.shared_mean(experts), a.reps)
