@@ -201,6 +201,8 @@ void Layer::setup_p2p() {
   a.E = static_cast<int>(E_);
   a.rank = rank_;
   a.recv_start = static_cast<int>(Tmax_ * k_);
+  a.row_bytes = static_cast<int>(H_ * dtype_bytes(dt_));
+  g_out_down_.alloc(sizeof(unsigned long long) * slots_ * (1 + static_cast<int64_t>(a2a_peers_.size())));
   for (int r = 0; r < G_; ++r) {
     if (r == rank_) {
       a.xall[r] = xall_.p;
@@ -426,14 +428,16 @@ void Layer::exchange(bool dispatch, cudaStream_t s) {
   nck(ncclGroupEnd(), "group end");
 }
 
-void Layer::run_expert_gemms(cudaStream_t s) {
+void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down) {
   GroupTable gt{g_row_start_.as<int>(), g_rows_.as<int>(), g_slot_.as<int>(), num_groups_};
+  GroupTable gt_down = gt;
+  gt_down.out = out_down;
   if (dt_ == DType::BF16) {
     mark("gemm_up", s);
     auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta : launch_grouped_gemm_bf16;
     ck(gemm(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_), "gemm up");
     mark("gemm_down", s);
-    ck(gemm(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, sched_down_), "gemm down");
+    ck(gemm(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_), "gemm down");
   } else {
     mark("gemm_up", s);
     ck(launch_grouped_gemm_f32(xall_.as<float>(), static_cast<int>(H_), w_up_c_.as<float>(), hbuf_.as<float>(), static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_ * 2, s), "gemm up");
@@ -465,18 +469,23 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
     mark("dispatch", s);
     ck(launch_count_exchange(p2p_args_, key_total_.as<int>(), key_off_.as<int>(), d_slot_of_expert_.as<int>(),
                              send_base_.as<int>(), g_row_start_.as<int>(), g_rows_.as<int>(), g_slot_.as<int>(),
-                             all_counts_.as<int>(), s), "count exchange");
+                             g_out_down_.as<unsigned long long>(), all_counts_.as<int>(), s), "count exchange");
     ck(launch_permute_p2p(p2p_args_, dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), keys_.as<int>(),
                           ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
                           pos_.as<int>(), s), "permute p2p");
     ck(launch_signal_wait(p2p_args_, 1, s), "dispatch flags");
     launches_ += 3;
     num_groups_ = static_cast<int>(slots_ * (1 + p2p_args_.n_src[rank_]));
-    run_expert_gemms(s);
+    // The down-projection writes received rows' outputs straight into their source GPU's
+    // oall (fused GEMM + combine exchange), so the combine below only reads local HBM.
+    run_expert_gemms(s, p2p_ && dt_ == DType::BF16 ? g_out_down_.as<unsigned long long>() : nullptr);
     mark("combine", s);
     ck(launch_signal_wait(p2p_args_, 2, s), "combine flags");
-    ck(launch_combine_p2p(p2p_args_, dt_, keys_.as<int>(), pos_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
-                          topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine p2p");
+    if (dt_ == DType::BF16)
+      ck(launch_combine(dt_, oall_.p, pos_.as<int>(), topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine");
+    else
+      ck(launch_combine_p2p(p2p_args_, dt_, keys_.as<int>(), pos_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
+                            topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine p2p");
     launches_ += 2;
     mark("end", s);
     return;

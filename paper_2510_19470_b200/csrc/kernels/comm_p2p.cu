@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(256) count_exchange_kernel(P2PArgs a, const in
                                                              const int* __restrict__ slot_of_expert,
                                                              int* __restrict__ send_base, int* __restrict__ g_row_start,
                                                              int* __restrict__ g_rows, int* __restrict__ g_slot,
+                                                             unsigned long long* __restrict__ g_out_down,
                                                              int* __restrict__ counts_out) {
   const int G = a.G, E = a.E, NK = G * E, me = a.rank;
   const int par = a.epoch & 1;
@@ -108,25 +109,36 @@ __global__ void __launch_bounds__(256) count_exchange_kernel(P2PArgs a, const in
     }
   }
   // 4) GEMM groups: local rows per held expert, then received rows per (source, expert).
+  //    Down-projection outputs of received rows go straight back to the source's oall at
+  //    key_off_s(me, e), the rows its combine reads.
+  auto row_addr = [&](int rank, long long row) {
+    return reinterpret_cast<unsigned long long>(static_cast<uint8_t*>(a.oall[rank]) + row * a.row_bytes);
+  };
   int g = 0;
   for (int e = 0; e < E; ++e) {
     const int sl = slot_of_expert[e];
     if (sl < 0) continue;
     g_row_start[g] = key_off[me * E + e];
     g_rows[g] = cnt[me * NK + me * E + e];
+    g_out_down[g] = row_addr(me, key_off[me * E + e]);
     g_slot[g++] = sl;
   }
   int at = a.recv_start;
   for (int i = 0; i < a.n_src[me]; ++i) {
     const int s = a.src_list[me * kMaxG + i];
+    long long src_off = 0;  // key_off of source s for key (me, 0)
+    for (int key = 0; key < me * E; ++key) src_off += cnt[s * NK + key];
     for (int e = 0; e < E; ++e) {
       const int sl = slot_of_expert[e];
-      if (sl < 0) continue;  // never receives rows for an expert it does not hold (S2)
       const int c = cnt[s * NK + me * E + e];
-      g_row_start[g] = at;
-      g_rows[g] = c;
-      g_slot[g++] = sl;
-      at += c;
+      if (sl >= 0) {  // a source only routes to this GPU experts it holds (S2)
+        g_row_start[g] = at;
+        g_rows[g] = c;
+        g_out_down[g] = row_addr(s, src_off);
+        g_slot[g++] = sl;
+        at += c;
+      }
+      src_off += c;
     }
   }
 }
@@ -229,10 +241,10 @@ size_t p2p_sync_bytes(int G, int E) {
 
 cudaError_t launch_count_exchange(const P2PArgs& a, const int* key_total, const int* key_off,
                                   const int* slot_of_expert, int* send_base, int* g_row_start, int* g_rows,
-                                  int* g_slot, int* counts_out, cudaStream_t s) {
+                                  int* g_slot, unsigned long long* g_out_down, int* counts_out, cudaStream_t s) {
   if (a.G > kMaxG || a.E > kMaxE) return cudaErrorInvalidValue;
   count_exchange_kernel<<<1, 256, 0, s>>>(a, key_total, key_off, slot_of_expert, send_base, g_row_start, g_rows,
-                                          g_slot, counts_out);
+                                          g_slot, g_out_down, counts_out);
   return cudaGetLastError();
 }
 

@@ -21,13 +21,17 @@ struct P2PArgs {
   int n_src[kMaxG];
   int G, E, rank;
   int recv_start;               // first receive row (Tmax * k), same on every rank
+  int row_bytes;                // H * element bytes of xall / oall rows
   uint32_t epoch;
 };
 
 size_t p2p_sync_bytes(int G, int E);
+// Also writes g_out_down: where the down-projection stores each group's rows -- local
+// rows into this GPU's oall, received rows straight back into the source GPU's oall at
+// the rows that source's combine reads (its packed positions).
 cudaError_t launch_count_exchange(const P2PArgs& a, const int* key_total, const int* key_off,
                                   const int* slot_of_expert, int* send_base, int* g_row_start, int* g_rows,
-                                  int* g_slot, int* counts_out, cudaStream_t s);
+                                  int* g_slot, unsigned long long* g_out_down, int* counts_out, cudaStream_t s);
 cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T, int H, int k, const int* keys,
                                const int* ranks, const int* chunk_off, const int* key_off, const int* send_base,
                                int* pos, cudaStream_t s);

@@ -46,6 +46,7 @@ struct SmemCtl {
   int row_start[kMaxGroups];
   int rows[kMaxGroups];
   int slot[kMaxGroups];
+  __nv_bfloat16* out[kMaxGroups];  // output row 0 of the group (local or a peer GPU's HBM)
 };
 
 constexpr size_t kSmemBytes = 1024 + STAGES * STAGE_BYTES + sizeof(SmemCtl);
@@ -92,8 +93,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_b, __nv_bfloat16* __restrict__ C,
                          int ldc, int N, int K, const int* __restrict__ g_row_start,
-                         const int* __restrict__ g_rows, const int* __restrict__ g_slot, int ng,
-                         int relu, uint32_t sched) {
+                         const int* __restrict__ g_rows, const int* __restrict__ g_slot,
+                         const unsigned long long* __restrict__ g_out, int ng, int relu, uint32_t sched) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -117,6 +118,8 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         s.row_start[g] = g_row_start[g];
         s.rows[g] = r;
         s.slot[g] = g_slot[g];
+        s.out[g] = g_out ? reinterpret_cast<__nv_bfloat16*>(g_out[g])
+                         : C + static_cast<size_t>(g_row_start[g]) * ldc;
         tiles = ((r + BM - 1) / BM) * n_tiles;
       }
       int incl = tiles;
@@ -221,7 +224,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
       decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
       const int r_local = mt * BM + row_in_tile;
       const bool row_ok = r_local < s.rows[g];
-      __nv_bfloat16* crow = C + static_cast<size_t>(s.row_start[g] + r_local) * ldc + nt * BN;
+      __nv_bfloat16* crow = s.out[g] + static_cast<size_t>(r_local) * ldc + nt * BN;
 
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
@@ -248,6 +251,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
       if (lane == 0) mbar_arrive(&s.tempty[acc]);
       if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
     }
+    if (g_out) __threadfence_system();  // outputs may live in a peer GPU's HBM
   }
 
   __syncwarp();  // reconverge the single-lane roles before the CTA barrier
@@ -287,6 +291,7 @@ struct SmemCtl2 {
   int row_start[kMaxGroups];
   int rows[kMaxGroups];
   int slot[kMaxGroups];
+  __nv_bfloat16* out[kMaxGroups];
 };
 
 constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + sizeof(SmemCtl2);
@@ -304,7 +309,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                               __nv_bfloat16* __restrict__ C, int ldc, int N, int K,
                               const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
-                              const int* __restrict__ g_slot, int ng, int relu, uint32_t sched) {
+                              const int* __restrict__ g_slot, const unsigned long long* __restrict__ g_out, int ng,
+                              int relu, uint32_t sched) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -329,6 +335,8 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
         s.row_start[g] = g_row_start[g];
         s.rows[g] = r;
         s.slot[g] = g_slot[g];
+        s.out[g] = g_out ? reinterpret_cast<__nv_bfloat16*>(g_out[g])
+                         : C + static_cast<size_t>(g_row_start[g]) * ldc;
         tiles = ((r + P_BM - 1) / P_BM) * n_tiles;
       }
       int incl = tiles;
@@ -432,7 +440,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
       decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
       const int r_local = mt * P_BM + row_in_tile;
       const bool row_ok = r_local < s.rows[g];
-      __nv_bfloat16* crow = C + static_cast<size_t>(s.row_start[g] + r_local) * ldc + nt * P_BN;
+      __nv_bfloat16* crow = s.out[g] + static_cast<size_t>(r_local) * ldc + nt * P_BN;
 
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
@@ -459,6 +467,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
       if (lane == 0) mbar_arrive_leader(&s.tempty[acc]);
       if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
     }
+    if (g_out) __threadfence_system();  // outputs may live in a peer GPU's HBM
   }
 
   __syncwarp();
@@ -538,7 +547,7 @@ cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap
   }
   grouped_gemm_bf16_kernel<<<num_sms, kThreads, kSmemBytes, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
-      groups.slot, groups.num_groups, relu, sched);
+      groups.slot, groups.out, groups.num_groups, relu, sched);
   return cudaGetLastError();
 }
 
@@ -557,7 +566,7 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
   const int grid = (num_sms / 2) * 2;
   grouped_gemm_bf16_2cta_kernel<<<grid, kThreads, kSmemBytes2, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
-      groups.num_groups, relu, sched);
+      groups.out, groups.num_groups, relu, sched);
   return cudaGetLastError();
 }
 

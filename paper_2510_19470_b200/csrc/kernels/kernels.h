@@ -54,6 +54,10 @@ struct GroupTable {
   const int* rows;       // rows in the group
   const int* slot;       // weight slot: B rows [slot*N, slot*N + N)
   int num_groups;
+  // Optional per-group output address (bf16 row 0 of the group, row stride ldc): lets the
+  // down-projection write rows that came from another GPU straight back into that
+  // GPU's output buffer over NVLink.  nullptr: C + row_start*ldc.
+  const unsigned long long* out = nullptr;
 };
 
 // bf16 tcgen05 grouped GEMM (gemm_sm100.cu): C[r, n] = act(sum_k A[r,k] B[slot*N+n, k]).
