@@ -36,7 +36,10 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "cfg3": dict(workload="cfg3: Mixtral-8x7B-shaped MoE layer (8 experts top-2, d=4096, FFN 14336), bf16",
                  H=4096, F=14336, E=8, k=2, T=16384, dtype="bf16", layers=1, sr=False,
-                 topo={1: ([1], [1]), 2: ([2], [1]), 4: ([2, 2], [1, 1]), 8: ([2, 4], [1, 4])}),
+                 # SF per N; S_ED = the reference planner's pick on measured B200 numbers
+                 # (cfg3: "S_ED pinned [1,4] plus the solver's pick"; the pinned [1,4] at N=8
+                 # is `--sed 1,4`).
+                 topo={1: ([1], [1]), 2: ([2], None), 4: ([2, 2], None), 8: ([2, 4], None)}),
     "cfg4": dict(workload="cfg4: DeepSeek-style fine-grained MoE layer (64 experts top-6, d=2048, FFN 1408), bf16, "
                           "SR-migrated experts (CR=50)",
                  H=2048, F=1408, E=64, k=6, T=16384, dtype="bf16", layers=1, sr=True,
@@ -245,6 +248,7 @@ def main():
         sed = [int(v) for v in args.sed.split(",")]
     elif sed is None:
         sed, p_plan = planned_sed(cfg, sf, world)
+    sed_source = "override" if args.sed else ("planner" if p_plan is not None else "pinned")
     dtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     H, F, E, k, T = cfg["H"], cfg["F"], cfg["E"], cfg["k"], cfg["T"]
     use_sr = cfg["sr"] and world > 1
@@ -387,7 +391,7 @@ def main():
             "dtype": cfg["dtype"], "data": "synthetic (dyadic tokens/gate, reference demo expert population)",
             "config": {"workload": cfg["workload"], "tokens_per_gpu": T, "hidden": H, "ffn": F, "experts": E,
                        "top_k": k, "sf": sf, "sed": sed, "layers": cfg["layers"], "sr_migration": use_sr,
-                       "planner_p": p_plan, "comm": "nccl" if os.environ.get("HEP_COMM") == "nccl" else "nvlink-p2p",
+                       "planner_p": p_plan, "sed_source": sed_source, "comm": "nccl" if os.environ.get("HEP_COMM") == "nccl" else "nvlink-p2p",
                        "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per GPU)" %
                              (T * row_bytes / 1e6, cfg["layers"] * len(layer.owned_experts()) * 2 * H * F * (row_bytes // H) / 1e9)},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": T * row_bytes,
