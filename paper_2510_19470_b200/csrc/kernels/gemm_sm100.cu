@@ -507,11 +507,16 @@ uint32_t gemm_schedule(int rows_per_expert, int N, int K, bool up) {
   const char* env = std::getenv(up ? "HEP_GEMM_SCHED_UP" : "HEP_GEMM_SCHED_DOWN");
   if (env && *env) return static_cast<uint32_t>(std::strtoul(env, nullptr, 16));
   (void)N;
-  // Measured on B200 (tools/gemm_sched_sweep.sh, profiles/README): keep the operand
-  // that is re-used across a wave in L2 (evict_last) and stream the other
-  // (evict_first).  When one expert's A rows fit comfortably in L2, rasterise m-fastest
-  // so A stays resident across all n-tiles; otherwise walk super-rows of gm m-tiles
-  // (A stripe of ~32 MB resident, B streamed once per stripe).
+  // Measured on B200 (tools/gemm_sched_sweep.sh, profiles/r1_gemm_sched_sweep*.log).
+  // CTA pair (256-row tiles): A evict_last, B default policy, m-fastest.  evict_first on
+  // B hurt here: a B half-tile is re-read by the other clusters of its n-column after
+  // it would have been evicted (DRAM reads 4.9 -> 2.2 GB up, 13.8 -> 8.4 GB down;
+  // 1.25 -> 1.44-1.48 PFLOP/s).
+  if (gemm_use_cta_pair()) return 0x2u;
+  // Single CTA (128-row tiles): keep the operand re-used across a wave in L2
+  // (evict_last) and stream the other (evict_first).  When one expert's A rows fit in
+  // L2, rasterise m-fastest so A stays resident across all n-tiles; otherwise walk
+  // super-rows of gm m-tiles (A stripe of ~32 MB resident, B streamed once per stripe).
   const double a_bytes = static_cast<double>(rows_per_expert) * K * 2.0;
   if (a_bytes <= 48e6) return 0x2u | (0x1u << 2);
   const int gm = std::max(1, std::min(255, static_cast<int>(32e6 / (128.0 * K * 2.0))));
