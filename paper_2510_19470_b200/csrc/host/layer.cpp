@@ -203,6 +203,10 @@ void Layer::setup_p2p() {
   a.recv_start = static_cast<int>(Tmax_ * k_);
   a.row_bytes = static_cast<int>(H_ * dtype_bytes(dt_));
   g_out_down_.alloc(sizeof(unsigned long long) * slots_ * (1 + static_cast<int64_t>(a2a_peers_.size())));
+  g_wait_.alloc(sizeof(int) * slots_ * (1 + static_cast<int64_t>(a2a_peers_.size())));
+  ck(cudaStreamCreateWithFlags(&side_s_, cudaStreamNonBlocking), "side stream");
+  ck(cudaEventCreateWithFlags(&ev_counts_, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&ev_remote_, cudaEventDisableTiming), "event");
   for (int r = 0; r < G_; ++r) {
     if (r == rank_) {
       a.xall[r] = xall_.p;
@@ -229,6 +233,12 @@ void Layer::setup_p2p() {
 }
 
 Layer::~Layer() {
+  if (side_s_) {
+    cudaStreamSynchronize(side_s_);
+    cudaStreamDestroy(side_s_);
+  }
+  if (ev_counts_) cudaEventDestroy(ev_counts_);
+  if (ev_remote_) cudaEventDestroy(ev_remote_);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   if (h2d_s_) cudaStreamSynchronize(h2d_s_);
   if (d2h_s_) cudaStreamSynchronize(d2h_s_);
@@ -428,10 +438,15 @@ void Layer::exchange(bool dispatch, cudaStream_t s) {
   nck(ncclGroupEnd(), "group end");
 }
 
-void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down) {
+void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down, const int* wait_src) {
   GroupTable gt{g_row_start_.as<int>(), g_rows_.as<int>(), g_slot_.as<int>(), num_groups_};
   GroupTable gt_down = gt;
   gt_down.out = out_down;
+  if (wait_src) {
+    gt.wait_src = wait_src;
+    gt.wait_flags = p2p_dispatch_flags(p2p_args_);
+    gt.epoch = p2p_args_.epoch;
+  }
   if (dt_ == DType::BF16) {
     mark("gemm_up", s);
     auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta : launch_grouped_gemm_bf16;
@@ -469,23 +484,43 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
     mark("dispatch", s);
     ck(launch_count_exchange(p2p_args_, key_total_.as<int>(), key_off_.as<int>(), d_slot_of_expert_.as<int>(),
                              send_base_.as<int>(), g_row_start_.as<int>(), g_rows_.as<int>(), g_slot_.as<int>(),
-                             g_out_down_.as<unsigned long long>(), all_counts_.as<int>(), s), "count exchange");
-    ck(launch_permute_p2p(p2p_args_, dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), keys_.as<int>(),
-                          ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
-                          pos_.as<int>(), s), "permute p2p");
-    ck(launch_signal_wait(p2p_args_, 1, s), "dispatch flags");
-    launches_ += 3;
+                             g_out_down_.as<unsigned long long>(), g_wait_.as<int>(), all_counts_.as<int>(), s),
+       "count exchange");
     num_groups_ = static_cast<int>(slots_ * (1 + p2p_args_.n_src[rank_]));
-    // The down-projection writes received rows' outputs straight into their source GPU's
-    // oall (fused GEMM + combine exchange), so the combine below only reads local HBM.
-    run_expert_gemms(s, p2p_ && dt_ == DType::BF16 ? g_out_down_.as<unsigned long long>() : nullptr);
-    mark("combine", s);
-    ck(launch_signal_wait(p2p_args_, 2, s), "combine flags");
-    if (dt_ == DType::BF16)
+    if (dt_ == DType::BF16) {
+      // Overlapped dispatch: remote rows go out over NVLink on a side stream while the
+      // up-projection starts on local rows; its TMA producer waits per source group
+      // for that source's dispatch flag.
+      ck(cudaEventRecord(ev_counts_, s), "record");
+      ck(cudaStreamWaitEvent(side_s_, ev_counts_, 0), "wait");
+      ck(launch_permute_p2p(p2p_args_, dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), keys_.as<int>(),
+                            ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
+                            pos_.as<int>(), side_s_, 2), "permute remote");
+      ck(launch_signal_wait(p2p_args_, 1, side_s_, false), "dispatch flags");
+      ck(cudaEventRecord(ev_remote_, side_s_), "record");
+      ck(launch_permute_p2p(p2p_args_, dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), keys_.as<int>(),
+                            ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
+                            pos_.as<int>(), s, 1), "permute local");
+      launches_ += 4;
+      // The down-projection writes received rows' outputs straight into their source
+      // GPU's oall (fused GEMM + combine exchange); the combine reads local HBM only.
+      run_expert_gemms(s, g_out_down_.as<unsigned long long>(), g_wait_.as<int>());
+      ck(cudaStreamWaitEvent(s, ev_remote_, 0), "wait");
+      mark("combine", s);
+      ck(launch_signal_wait(p2p_args_, 2, s), "combine flags");
       ck(launch_combine(dt_, oall_.p, pos_.as<int>(), topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine");
-    else
+    } else {
+      ck(launch_permute_p2p(p2p_args_, dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), keys_.as<int>(),
+                            ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
+                            pos_.as<int>(), s), "permute p2p");
+      ck(launch_signal_wait(p2p_args_, 1, s), "dispatch flags");
+      launches_ += 3;
+      run_expert_gemms(s);
+      mark("combine", s);
+      ck(launch_signal_wait(p2p_args_, 2, s), "combine flags");
       ck(launch_combine_p2p(p2p_args_, dt_, keys_.as<int>(), pos_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
                             topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine p2p");
+    }
     launches_ += 2;
     mark("end", s);
     return;

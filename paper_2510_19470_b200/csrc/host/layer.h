@@ -66,7 +66,7 @@ class Layer {
   void mark(const char* name, cudaStream_t s);
   void build_comm_plan_and_groups(int T, cudaStream_t s);
   void exchange(bool dispatch, cudaStream_t s);
-  void run_expert_gemms(cudaStream_t s, const unsigned long long* out_down = nullptr);
+  void run_expert_gemms(cudaStream_t s, const unsigned long long* out_down = nullptr, const int* wait_src = nullptr);
 
   // shape
   int64_t H_, F_, E_, k_, Tmax_, G_, n_, NK_;
@@ -99,7 +99,9 @@ class Layer {
   // NVLink peer-memory path (default for G > 1; HEP_COMM=nccl selects the NCCL baseline)
   bool p2p_ = false;
   P2PArgs p2p_args_{};
-  DevBuf sync_, send_base_, g_out_down_;
+  DevBuf sync_, send_base_, g_out_down_, g_wait_;
+  cudaStream_t side_s_ = nullptr;
+  cudaEvent_t ev_counts_ = nullptr, ev_remote_ = nullptr;
   std::vector<void*> ipc_opened_;
   uint32_t epoch_ = 0;
   void setup_p2p();

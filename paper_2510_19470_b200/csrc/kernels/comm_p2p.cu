@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) count_exchange_kernel(P2PArgs a, const in
                                                              int* __restrict__ send_base, int* __restrict__ g_row_start,
                                                              int* __restrict__ g_rows, int* __restrict__ g_slot,
                                                              unsigned long long* __restrict__ g_out_down,
-                                                             int* __restrict__ counts_out) {
+                                                             int* __restrict__ g_wait, int* __restrict__ counts_out) {
   const int G = a.G, E = a.E, NK = G * E, me = a.rank;
   const int par = a.epoch & 1;
   __shared__ int cnt[kMaxG * kMaxG * kMaxE];  // cnt[s][d*E+e]
@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(256) count_exchange_kernel(P2PArgs a, const in
     g_row_start[g] = key_off[me * E + e];
     g_rows[g] = cnt[me * NK + me * E + e];
     g_out_down[g] = row_addr(me, key_off[me * E + e]);
+    g_wait[g] = -1;
     g_slot[g++] = sl;
   }
   int at = a.recv_start;
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(256) count_exchange_kernel(P2PArgs a, const in
         g_row_start[g] = at;
         g_rows[g] = c;
         g_out_down[g] = row_addr(s, src_off);
+        g_wait[g] = s;
         g_slot[g++] = sl;
         at += c;
       }
@@ -150,7 +152,9 @@ __global__ void __launch_bounds__(256) permute_p2p_kernel(P2PArgs a, const uint8
                                                           const int* __restrict__ ranks,
                                                           const int* __restrict__ chunk_off,
                                                           const int* __restrict__ key_off,
-                                                          const int* __restrict__ send_base, int* __restrict__ pos) {
+                                                          const int* __restrict__ send_base, int* __restrict__ pos,
+                                                          int mode) {
+  // mode 0: every row; 1: rows staying on this GPU (and all of pos); 2: remote rows only.
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= T_tok) return;
@@ -161,20 +165,25 @@ __global__ void __launch_bounds__(256) permute_p2p_kernel(P2PArgs a, const uint8
     const size_t o = static_cast<size_t>(t) * k + j;
     const int key = keys[o];
     const int p = key_off[key] + chunk_off[static_cast<size_t>(chunk) * NK + key] + ranks[o];
-    if (lane == 0) pos[o] = p;
+    if (lane == 0 && mode != 2) pos[o] = p;
     const int d = key / a.E;
+    const bool skip = (mode == 1 && d != a.rank) || (mode == 2 && d == a.rank);
     const int row = d == a.rank ? p : send_base[key] + (p - key_off[key]);
-    dst[j] = static_cast<uint8_t*>(a.xall[d]) + static_cast<size_t>(row) * row_bytes;
+    dst[j] = skip ? nullptr : static_cast<uint8_t*>(a.xall[d]) + static_cast<size_t>(row) * row_bytes;
   }
   const uint8_t* src = x + static_cast<size_t>(t) * row_bytes;
+  bool any = false;
+  for (int j = 0; j < k; ++j) any |= dst[j] != nullptr;
+  if (!any) return;
   for (int v = lane; v < (row_bytes >> 4); v += 32) {
     const uint4 val = ld_nc_v4(src + 16 * v);
-    for (int j = 0; j < k; ++j) st_v4(dst[j] + 16 * v, val);
+    for (int j = 0; j < k; ++j)
+      if (dst[j]) st_v4(dst[j] + 16 * v, val);
   }
 }
 
-// Raise flag `slot` on every A2A peer, then wait for theirs.
-__global__ void signal_wait_kernel(P2PArgs a, int slot) {
+// Raise flag `slot` on every A2A peer, then (if `wait`) wait for theirs.
+__global__ void signal_wait_kernel(P2PArgs a, int slot, int wait) {
   __threadfence_system();
   const int NK = a.G * a.E;
   const int i = threadIdx.x;
@@ -182,6 +191,7 @@ __global__ void signal_wait_kernel(P2PArgs a, int slot) {
     const int p = a.src_list[a.rank * kMaxG + i];
     st_release_sys(view(a.sync[p], NK).flags + slot * kMaxG + a.rank, a.epoch);
   }
+  if (!wait) return;
   __syncthreads();
   if (i < a.n_src[a.rank]) {
     const int p = a.src_list[a.rank * kMaxG + i];
@@ -235,31 +245,45 @@ __global__ void __launch_bounds__(256) combine_p2p_kernel(P2PArgs a, const int* 
 
 }  // namespace
 
+const uint32_t* p2p_dispatch_flags(const P2PArgs& a) {
+  return static_cast<const uint32_t*>(a.sync[a.rank]) + 1 * kMaxG;
+}
+
 size_t p2p_sync_bytes(int G, int E) {
   return 3 * kMaxG * sizeof(uint32_t) + 2 * kMaxG * static_cast<size_t>(G) * E * sizeof(int) + 256;
 }
 
 cudaError_t launch_count_exchange(const P2PArgs& a, const int* key_total, const int* key_off,
                                   const int* slot_of_expert, int* send_base, int* g_row_start, int* g_rows,
-                                  int* g_slot, unsigned long long* g_out_down, int* counts_out, cudaStream_t s) {
+                                  int* g_slot, unsigned long long* g_out_down, int* g_wait, int* counts_out,
+                                  cudaStream_t s) {
   if (a.G > kMaxG || a.E > kMaxE) return cudaErrorInvalidValue;
   count_exchange_kernel<<<1, 256, 0, s>>>(a, key_total, key_off, slot_of_expert, send_base, g_row_start, g_rows,
-                                          g_slot, g_out_down, counts_out);
+                                          g_slot, g_out_down, g_wait, counts_out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T, int H, int k, const int* keys,
                                const int* ranks, const int* chunk_off, const int* key_off, const int* send_base,
-                               int* pos, cudaStream_t s) {
+                               int* pos, cudaStream_t s, int mode) {
   const int row_bytes = H * dtype_bytes(dt);
   if (row_bytes % 16 || k > 8) return cudaErrorInvalidValue;
+  static bool carveout = false;
+  if (!carveout) {
+    // Same L1/shared split as the persistent GEMM, so remote-row blocks can run on SMs
+    // next to GEMM CTAs that wait for peers' rows (overlapped dispatch).
+    const cudaError_t e = cudaFuncSetAttribute(permute_p2p_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    carveout = true;
+  }
   permute_p2p_kernel<<<(T + 7) / 8, 256, 0, s>>>(a, static_cast<const uint8_t*>(x), T, row_bytes, k, keys, ranks,
-                                                 chunk_off, key_off, send_base, pos);
+                                                 chunk_off, key_off, send_base, pos, mode);
   return cudaGetLastError();
 }
 
-cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s) {
-  signal_wait_kernel<<<1, 32, 0, s>>>(a, slot);
+cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait) {
+  signal_wait_kernel<<<1, 32, 0, s>>>(a, slot, wait ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -31,12 +31,15 @@ size_t p2p_sync_bytes(int G, int E);
 // the rows that source's combine reads (its packed positions).
 cudaError_t launch_count_exchange(const P2PArgs& a, const int* key_total, const int* key_off,
                                   const int* slot_of_expert, int* send_base, int* g_row_start, int* g_rows,
-                                  int* g_slot, unsigned long long* g_out_down, int* counts_out, cudaStream_t s);
+                                  int* g_slot, unsigned long long* g_out_down, int* g_wait, int* counts_out,
+                                  cudaStream_t s);
 cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T, int H, int k, const int* keys,
                                const int* ranks, const int* chunk_off, const int* key_off, const int* send_base,
-                               int* pos, cudaStream_t s);
+                               int* pos, cudaStream_t s, int mode = 0);
 // slot 1: "my rows are in your receive area"; slot 2: "your outputs are ready".
-cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s);
+cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait = true);
+// This rank's dispatch flags (indexed by source rank), for GEMM-side gating.
+const uint32_t* p2p_dispatch_flags(const P2PArgs& a);
 cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, const int* pos, const int* key_off,
                                const int* send_base, const float* w, int T, int H, int k, void* y,
                                cudaStream_t s);

@@ -47,6 +47,7 @@ struct SmemCtl {
   int rows[kMaxGroups];
   int slot[kMaxGroups];
   __nv_bfloat16* out[kMaxGroups];  // output row 0 of the group (local or a peer GPU's HBM)
+  int wait[kMaxGroups];            // source rank whose dispatch flag gates the group, or -1
 };
 
 constexpr size_t kSmemBytes = 1024 + STAGES * STAGE_BYTES + sizeof(SmemCtl);
@@ -80,6 +81,23 @@ __device__ __forceinline__ void decode_tile(int local, int m_tiles, int n_tiles,
   }
 }
 
+// Spin (producer thread) until a peer's dispatch flag reaches `epoch`, then order the
+// TMA (async proxy) reads of the rows that peer stored after its release.
+__device__ __forceinline__ void wait_dispatch(const uint32_t* flag, uint32_t epoch) {
+  uint32_t v;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (static_cast<int32_t>(v - epoch) >= 0) break;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 60ull * 1000000000ull) __trap();
+    __nanosleep(100);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ int find_group(const SmemCtl& s, int ng, int tile) {
   int lo = 0, hi = ng - 1;  // largest g with tile_start[g] <= tile
   while (lo < hi) {
@@ -94,7 +112,9 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_b, __nv_bfloat16* __restrict__ C,
                          int ldc, int N, int K, const int* __restrict__ g_row_start,
                          const int* __restrict__ g_rows, const int* __restrict__ g_slot,
-                         const unsigned long long* __restrict__ g_out, int ng, int relu, uint32_t sched) {
+                         const unsigned long long* __restrict__ g_out, const int* __restrict__ g_wait,
+                         const uint32_t* __restrict__ wait_flags, uint32_t epoch, int ng, int relu,
+                         uint32_t sched) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -120,6 +140,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         s.slot[g] = g_slot[g];
         s.out[g] = g_out ? reinterpret_cast<__nv_bfloat16*>(g_out[g])
                          : C + static_cast<size_t>(g_row_start[g]) * ldc;
+        s.wait[g] = g_wait ? g_wait[g] : -1;
         tiles = ((r + BM - 1) / BM) * n_tiles;
       }
       int incl = tiles;
@@ -172,6 +193,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
         const int a_row = s.row_start[g] + mt * BM;
         const int b_row = s.slot[g] * N + nt * BN;
+        if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&s.full[stage], STAGE_BYTES);
@@ -292,6 +314,7 @@ struct SmemCtl2 {
   int rows[kMaxGroups];
   int slot[kMaxGroups];
   __nv_bfloat16* out[kMaxGroups];
+  int wait[kMaxGroups];
 };
 
 constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + sizeof(SmemCtl2);
@@ -309,8 +332,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                               __nv_bfloat16* __restrict__ C, int ldc, int N, int K,
                               const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
-                              const int* __restrict__ g_slot, const unsigned long long* __restrict__ g_out, int ng,
-                              int relu, uint32_t sched) {
+                              const int* __restrict__ g_slot, const unsigned long long* __restrict__ g_out,
+                              const int* __restrict__ g_wait, const uint32_t* __restrict__ wait_flags,
+                              uint32_t epoch, int ng, int relu, uint32_t sched) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -337,6 +361,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
         s.slot[g] = g_slot[g];
         s.out[g] = g_out ? reinterpret_cast<__nv_bfloat16*>(g_out[g])
                          : C + static_cast<size_t>(g_row_start[g]) * ldc;
+        s.wait[g] = g_wait ? g_wait[g] : -1;
         tiles = ((r + P_BM - 1) / P_BM) * n_tiles;
       }
       int incl = tiles;
@@ -389,6 +414,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
         decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
         const int a_row = s.row_start[g] + mt * P_BM + 128 * static_cast<int>(cta);
         const int b_row = s.slot[g] * N + nt * P_BN + 128 * static_cast<int>(cta);
+        if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
           if (cta == 0) mbar_arrive_expect_tx(&s.full[stage], 2 * P_STAGE_BYTES);
@@ -552,7 +578,7 @@ cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap
   }
   grouped_gemm_bf16_kernel<<<num_sms, kThreads, kSmemBytes, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
-      groups.slot, groups.out, groups.num_groups, relu, sched);
+      groups.slot, groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched);
   return cudaGetLastError();
 }
 
@@ -571,7 +597,7 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
   const int grid = (num_sms / 2) * 2;
   grouped_gemm_bf16_2cta_kernel<<<grid, kThreads, kSmemBytes2, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
-      groups.out, groups.num_groups, relu, sched);
+      groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched);
   return cudaGetLastError();
 }
 

@@ -58,6 +58,13 @@ struct GroupTable {
   // down-projection write rows that came from another GPU straight back into that
   // GPU's output buffer over NVLink.  nullptr: C + row_start*ldc.
   const unsigned long long* out = nullptr;
+  // Optional dispatch gating (NVLink path): before loading a tile of group g with
+  // wait_src[g] >= 0, the TMA producer waits until wait_flags[wait_src[g]] reaches
+  // `epoch` (that source's rows have landed in this GPU's receive area), so the GEMM
+  // starts on local rows while remote rows are still in flight.
+  const int* wait_src = nullptr;
+  const uint32_t* wait_flags = nullptr;
+  uint32_t epoch = 0;
 };
 
 // bf16 tcgen05 grouped GEMM (gemm_sm100.cu): C[r, n] = act(sum_k A[r,k] B[slot*N+n, k]).
