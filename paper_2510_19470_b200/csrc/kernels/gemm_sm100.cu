@@ -297,7 +297,12 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
 // and both epilogues release the accumulator on the leader's tempty barrier.
 constexpr int P_BM = 256;          // rows per cluster tile (128 per CTA)
 constexpr int P_BN = 256;
-constexpr int P_STAGES = 6;
+constexpr int P_STAGES = 4;
+// Epilogue staging: each epilogue warp assembles its 32 rows x 256 bf16 columns in shared
+// memory so global (and NVLink peer) stores go out as whole 512-byte row segments
+// instead of 32 scattered 16-byte pieces per instruction.
+constexpr int P_STG_PITCH = P_BN * 2 + 16;              // bytes per staged row (+16 B pad)
+constexpr int P_STG_BYTES = 4 * 32 * P_STG_PITCH;       // 4 epilogue warps
 constexpr int P_A_BYTES = 128 * BK * 2;
 constexpr int P_B_BYTES = 128 * BK * 2;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
@@ -317,7 +322,7 @@ struct SmemCtl2 {
   int wait[kMaxGroups];
 };
 
-constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + sizeof(SmemCtl2);
+constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + P_STG_BYTES + sizeof(SmemCtl2);
 
 __device__ __forceinline__ int find_group2(const SmemCtl2& s, int ng, int tile) {
   int lo = 0, hi = ng - 1;
@@ -340,7 +345,8 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* stage_a = smem;
   uint8_t* stage_b = smem + P_STAGES * P_A_BYTES;
-  SmemCtl2& s = *reinterpret_cast<SmemCtl2*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint8_t* stage_out = smem + P_STAGES * P_STAGE_BYTES;
+  SmemCtl2& s = *reinterpret_cast<SmemCtl2*>(smem + P_STAGES * P_STAGE_BYTES + P_STG_BYTES);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -455,7 +461,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
   } else {
     // ================= epilogue (warps 2..5, both CTAs) =================
     const uint32_t quarter = warp & 3u;
-    const int row_in_tile = static_cast<int>(128 * cta + quarter * 32 + lane);
+    uint8_t* stg = stage_out + quarter * 32 * P_STG_PITCH;  // this warp's 32 staged rows
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = cluster; tile < total; tile += nclusters) {
@@ -464,34 +470,44 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
       const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
       int mt, nt;
       decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
-      const int r_local = mt * P_BM + row_in_tile;
-      const bool row_ok = r_local < s.rows[g];
-      __nv_bfloat16* crow = s.out[g] + static_cast<size_t>(r_local) * ldc + nt * P_BN;
+      const int row0 = mt * P_BM + static_cast<int>(128 * cta + quarter * 32);  // first row of this warp
+      const int ncols = min(P_BN, N - nt * P_BN);
 
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_base = tmem_base + static_cast<uint32_t>(acc * P_BN) + ((quarter * 32u) << 16);
+      // TMEM -> registers -> (relu, bf16) -> staged row `lane`
 #pragma unroll 1
-      for (int c = 0; c < P_BN; c += 32) {
-        if (nt * P_BN + c >= N) break;  // warp-uniform
+      for (int c = 0; c < ncols; c += 32) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_base + static_cast<uint32_t>(c), v);
         tmem_ld_wait();
-        if (row_ok) {
-          float f[32];
+        float f[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float x = __uint_as_float(v[i]);
-            f[i] = relu ? fmaxf(x, 0.f) : x;
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) st_v4(crow + c + 8 * q, pack8(f + 8 * q));
+        for (int i = 0; i < 32; ++i) {
+          const float x = __uint_as_float(v[i]);
+          f[i] = relu ? fmaxf(x, 0.f) : x;
         }
+        uint4* dst = reinterpret_cast<uint4*>(stg + lane * P_STG_PITCH + c * 2);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = pack8(f + 8 * q);
       }
+      // The accumulator is free as soon as it has been read.
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&s.tempty[acc]);
       if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+      // Staged rows -> global, one row per instruction: lane l writes bytes [16l, 16l+16).
+      const int row_bytes = ncols * 2;
+      const int rows_here = min(32, s.rows[g] - row0);
+      __nv_bfloat16* out0 = s.out[g] + static_cast<size_t>(row0) * ldc + nt * P_BN;
+      for (int r = 0; r < rows_here; ++r) {
+        if (lane * 16 < row_bytes) {
+          const uint4 val = *reinterpret_cast<const uint4*>(stg + r * P_STG_PITCH + lane * 16);
+          st_v4(reinterpret_cast<uint8_t*>(out0 + static_cast<size_t>(r) * ldc) + lane * 16, val);
+        }
+      }
+      __syncwarp();  // staging buffer is rewritten by the next tile
     }
     if (g_out) __threadfence_system();  // outputs may live in a peer GPU's HBM
   }
