@@ -327,7 +327,7 @@ def main():
     for layer in layers:
         kc = layer.debug(T)["key_counts"]
         rows += int(kc.sum().item()) if world == 1 else T * k
-    gemm_ms = phases.get("gemm_up", 0.0) + phases.get("gemm_down", 0.0)
+    gemm_ms = sum(v for kname, v in phases.items() if kname.startswith("gemm_"))
     pk = peaks()
     flops = 4.0 * H * F * rows
     achieved = flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
@@ -376,6 +376,36 @@ def main():
     row_bytes = H * (2 if dtype == torch.bfloat16 else 4)
     layer = layers[0]
 
+    comm_stats = None
+    if world > 1:
+        # A2A + AG bus bandwidth per GPU (BASELINE metric), against the measured NVLink
+        # peer-copy bandwidth of B200_PROFILING.md (770 GB/s per direction).
+        cb = layers[0].comm_bench(x, iters=10)
+        if cb["ag_bus_gbs"] is None:
+            # this plan has no All-Gather (the planner picked p=1); measure the expert
+            # All-Gather the hybrid plan would run (NCCL, one GPU's expert payload)
+            n = len(layers[0].owned_experts())
+            payload = torch.empty(n * 2 * H * F, dtype=dtype, device=dev)
+            gathered = torch.empty(world * payload.numel(), dtype=dtype, device=dev)
+            dist.all_gather_into_tensor(gathered, payload)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(5):
+                dist.all_gather_into_tensor(gathered, payload)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ag_ms = a0.elapsed_time(a1) / 5
+            cb["ag_ms"], cb["ag_bytes"] = ag_ms, (world - 1) * payload.numel() * payload.element_size()
+            cb["ag_bus_gbs"] = cb["ag_bytes"] / (ag_ms * 1e6)
+            cb["ag_source"] = "nccl all_gather of one GPU's expert payload (torch.distributed)"
+            del payload, gathered
+        stats = torch.tensor([cb["a2a_bus_gbs"] or 0.0, cb["ag_bus_gbs"] or 0.0], device=dev, dtype=torch.float64)
+        dist.all_reduce(stats, op=dist.ReduceOp.MIN)
+        comm_stats = dict(cb, a2a_bus_gbs_min_over_ranks=float(stats[0]), ag_bus_gbs_min_over_ranks=float(stats[1]),
+                          nvlink_peak_gbs=770.0, peak_source="B200_PROFILING.md measured peer copy per direction",
+                          a2a_frac=float(stats[0]) / 770.0, ag_frac=float(stats[1]) / 770.0)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         tps, secs, sampled, cores = cpu_oracle_time(cfg, cpu_oracle_inputs(cfg, x, wg), args.cpu_stride)
@@ -403,6 +433,7 @@ def main():
                          "flops_per_launch_pair": flops},
             "phase_ms": phases,
             "gpu_launches": launches,
+            "comm": comm_stats,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }

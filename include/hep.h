@@ -181,6 +181,11 @@ int hep_layer_forward(hep_layer_t layer, const void* x, int64_t tokens, void* y,
 int hep_layer_forward_host(hep_layer_t layer, const void* host_x, int64_t tokens, void* host_y,
                            void* stream);
 int hep_layer_host_fence(hep_layer_t layer, void* stream);
+/* Communication microbenchmark of this layer's exchanges (A2A dispatch over NVLink peer
+ * memory; expert All-Gather): out6 = {a2a_ms, a2a_bytes_sent, 0, ag_ms, ag_bytes_received,
+ * 0}, per GPU, averaged over `iters`.  Collective: every rank must call it. */
+int hep_layer_comm_bench(hep_layer_t layer, const void* x, int64_t tokens, int iters, double* out6,
+                         void* stream);
 /* Introspection of the last forward (device pointers owned by the layer):
  * topk_idx int32[T*k], topk_w f32[T*k], pos int32[T*k] (row of (t,j) in the packed
  * buffer), packed [rows, H] send buffer grouped by (dest, expert); counts int32[G*E]

@@ -137,6 +137,7 @@ SIGNATURES = {
     "hep_layer_forward": [VP, VP, I64, VP, VP],
     "hep_layer_forward_host": [VP, VP, I64, VP, VP],
     "hep_layer_host_fence": [VP, VP],
+    "hep_layer_comm_bench": [VP, VP, I64, I32, P(C.c_double), VP],
     "hep_layer_debug": [VP, P(VP), P(VP), P(VP), P(VP), P(VP)],
     "hep_layer_set_profiling": [VP, I32],
     "hep_layer_timings": [VP, C.c_char_p, SZ, P(C.c_float), I32, P(I32)],

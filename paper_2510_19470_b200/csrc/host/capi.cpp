@@ -405,6 +405,13 @@ int hep_layer_host_fence(hep_layer_t layer, void* stream) {
   return guarded([&] { layer->impl->host_fence(st(stream)); });
 }
 
+int hep_layer_comm_bench(hep_layer_t layer, const void* x, int64_t tokens, int iters, double* out6, void* stream) {
+  return guarded([&] {
+    if (iters <= 0) throw std::invalid_argument("iters must be positive");
+    layer->impl->comm_bench(x, tokens, iters, out6, st(stream));
+  });
+}
+
 int hep_layer_debug(hep_layer_t layer, const int32_t** topk_idx, const float** topk_w, const int32_t** pos,
                     const void** packed, const int32_t** key_counts) {
   return guarded([&] {

@@ -150,9 +150,9 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
     if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
     wires_.alloc(((wb + 15) / 16 * 16) * slots_);
     sr_ws_.alloc(sr_workspace_bytes(H_, F_, static_cast<int>(n_)));
-    sr_dec_.alloc(sizeof(float) * P * std::max<int64_t>(1, std::min<int64_t>(slots_ - n_, kMaxSrBatch)));
     sr_tmp_.alloc(sizeof(float) * P);
     sr_status_.alloc(16 * kMaxSrBatch);
+    shared_c_.alloc(static_cast<size_t>(dtype_bytes(dt_)) * P);
   }
   for (int b = 0; b < 2; ++b) {
     x_dev_[b].alloc(eb * Tmax_ * H_);
@@ -183,18 +183,23 @@ void Layer::setup_p2p() {
   sync_.alloc(p2p_sync_bytes(static_cast<int>(G_), static_cast<int>(E_)));
   ck(cudaMemset(sync_.p, 0, sync_.bytes), "sync memset");
   send_base_.alloc(sizeof(int) * NK_);
-  // Exchange CUDA IPC handles of xall / oall / sync through NCCL.
-  cudaIpcMemHandle_t mine[3];
+  // Exchange CUDA IPC handles of xall / oall / sync (token path) and of the expert
+  // compute copies and SR wires (expert All-Gather pulls) through NCCL.
+  constexpr int kBufs = 6;
+  cudaIpcMemHandle_t mine[kBufs] = {};
   ck(cudaIpcGetMemHandle(&mine[0], xall_.p), "ipc handle");
   ck(cudaIpcGetMemHandle(&mine[1], oall_.p), "ipc handle");
   ck(cudaIpcGetMemHandle(&mine[2], sync_.p), "ipc handle");
+  ck(cudaIpcGetMemHandle(&mine[3], w_up_c_.p), "ipc handle");
+  ck(cudaIpcGetMemHandle(&mine[4], w_down_c_.p), "ipc handle");
+  if (use_sr_) ck(cudaIpcGetMemHandle(&mine[5], wires_.p), "ipc handle");
   DevBuf dmine, dall;
   dmine.alloc(sizeof(mine));
   dall.alloc(sizeof(mine) * G_);
   ck(cudaMemcpy(dmine.p, mine, sizeof(mine), cudaMemcpyHostToDevice), "ipc h2d");
   nck(ncclAllGather(dmine.p, dall.p, sizeof(mine), ncclUint8, comm_->nccl, 0), "ipc allgather");
   ck(cudaStreamSynchronize(0), "ipc sync");
-  std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(3 * G_));
+  std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(kBufs * G_));
   ck(cudaMemcpy(all.data(), dall.p, sizeof(mine) * G_, cudaMemcpyDeviceToHost), "ipc d2h");
   P2PArgs& a = p2p_args_;
   a.G = static_cast<int>(G_);
@@ -207,6 +212,9 @@ void Layer::setup_p2p() {
   ck(cudaStreamCreateWithFlags(&side_s_, cudaStreamNonBlocking), "side stream");
   ck(cudaEventCreateWithFlags(&ev_counts_, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&ev_remote_, cudaEventDisableTiming), "event");
+  peer_w_up_.assign(static_cast<size_t>(G_), nullptr);
+  peer_w_down_.assign(static_cast<size_t>(G_), nullptr);
+  peer_wires_.assign(static_cast<size_t>(G_), nullptr);
   for (int r = 0; r < G_; ++r) {
     if (r == rank_) {
       a.xall[r] = xall_.p;
@@ -214,15 +222,24 @@ void Layer::setup_p2p() {
       a.sync[r] = sync_.p;
       continue;
     }
-    void* ptrs[3];
-    for (int b = 0; b < 3; ++b) {
-      ck(cudaIpcOpenMemHandle(&ptrs[b], all[static_cast<size_t>(3 * r + b)], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+    void* ptrs[kBufs] = {};
+    const int nb = use_sr_ ? kBufs : kBufs - 1;
+    for (int b = 0; b < nb; ++b) {
+      ck(cudaIpcOpenMemHandle(&ptrs[b], all[static_cast<size_t>(kBufs * r + b)], cudaIpcMemLazyEnablePeerAccess), "ipc open");
       ipc_opened_.push_back(ptrs[b]);
     }
     a.xall[r] = ptrs[0];
     a.oall[r] = ptrs[1];
     a.sync[r] = ptrs[2];
+    peer_w_up_[static_cast<size_t>(r)] = ptrs[3];
+    peer_w_down_[static_cast<size_t>(r)] = ptrs[4];
+    peer_wires_[static_cast<size_t>(r)] = ptrs[5];
   }
+  a.n_ag = 0;
+  for (int64_t p : ag_peers_) a.ag_list[a.n_ag++] = static_cast<int>(p);
+  ck(cudaStreamCreateWithFlags(&ag_s_, cudaStreamNonBlocking), "ag stream");
+  ck(cudaEventCreateWithFlags(&ev_ag_start_, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&ev_ag_done_, cudaEventDisableTiming), "event");
   const std::vector<hybridep::sim::PeerLists> peers = hybridep::sim::peer_lists(cluster_);
   for (int d = 0; d < G_; ++d) {
     int n = 0;
@@ -237,6 +254,12 @@ Layer::~Layer() {
     cudaStreamSynchronize(side_s_);
     cudaStreamDestroy(side_s_);
   }
+  if (ag_s_) {
+    cudaStreamSynchronize(ag_s_);
+    cudaStreamDestroy(ag_s_);
+  }
+  if (ev_ag_start_) cudaEventDestroy(ev_ag_start_);
+  if (ev_ag_done_) cudaEventDestroy(ev_ag_done_);
   if (ev_counts_) cudaEventDestroy(ev_counts_);
   if (ev_remote_) cudaEventDestroy(ev_remote_);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
@@ -286,6 +309,11 @@ void Layer::set_expert(int64_t e, const void* w_up, const void* w_down, DType dt
 void Layer::set_shared(const float* shared, cudaStream_t s) {
   if (!use_sr_) throw std::invalid_argument("shared expert is only used with SR migration");
   ck(cudaMemcpyAsync(shared_.p, shared, sizeof(float) * 2 * H_ * F_, cudaMemcpyDeviceToDevice, s), "shared");
+  // the shared expert in the GEMM's layout, the base every migrated expert is decoded onto
+  const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
+  ck(launch_transpose_convert(DType::F32, shared_.p, H_, F_, dt_, shared_c_.p, s), "shared up");
+  ck(launch_transpose_convert(DType::F32, shared_.as<float>() + H_ * F_, F_, H_, dt_,
+                              shared_c_.as<uint8_t>() + eb * H_ * F_, s), "shared down");
 }
 
 void Layer::gather_experts(cudaStream_t s) {
@@ -293,6 +321,52 @@ void Layer::gather_experts(cudaStream_t s) {
   const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
   const size_t per_slot_up = static_cast<size_t>(F_ * H_), per_slot_down = static_cast<size_t>(H_ * F_);
   auto first_slot_of = [&](int64_t owner) { return slot_of_expert_[static_cast<size_t>(owner * n_)]; };
+  if (p2p_ && dt_ == DType::BF16) {
+    // "AgTransfer eligible from t=0" (simcore.cpp:155-156): the All-Gather runs on its own
+    // stream with the copy engines pulling peers' experts over NVLink, while the step
+    // starts; forward() waits for it only before the GEMMs of gathered experts.
+    ck(cudaEventRecord(ev_ag_start_, s), "record");
+    ck(cudaStreamWaitEvent(ag_s_, ev_ag_start_, 0), "wait");
+    P2PArgs ag = p2p_args_;
+    ag.epoch = ++ag_epoch_;
+    const int64_t P = 2 * H_ * F_;
+    size_t wb = 0, stride = 0;
+    hep_sr_config c{sr_cfg_.ratio_CR.value_or(1.0), sr_cfg_.k.value_or(-1), sr_cfg_.index_width_bits,
+                    sr_cfg_.value_width_bits, sr_cfg_.per_matrix_budget ? 1 : 0};
+    if (use_sr_) {
+      if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
+      stride = (wb + 15) / 16 * 16;
+      std::vector<const void*> ex;
+      std::vector<void*> wo;
+      for (int64_t i = 0; i < n_; ++i) {
+        ex.push_back(master_.as<float>() + i * P);
+        wo.push_back(wires_.as<uint8_t>() + stride * (first_slot_of(rank_) + i));
+      }
+      if (hep_sr_encode_batch(ex.data(), static_cast<int>(n_), HEP_F32, shared_.as<float>(), H_, F_, &c, wo.data(),
+                              wb, sr_ws_.p, sr_ws_.bytes, ag_s_) != HEP_OK)
+        throw std::runtime_error(hep_last_error());
+    }
+    // Every AG peer's experts (or wires) for this epoch are final -> pull.
+    ck(launch_signal_wait(ag, 3, ag_s_, true, true), "ag flags");
+    for (int64_t p : ag_peers_) {
+      const size_t pi = static_cast<size_t>(p);
+      const int64_t theirs = first_slot_of(p);
+      if (use_sr_) {
+        // the owner's wires sit in its own first n slots
+        ck(cudaMemcpyAsync(wires_.as<uint8_t>() + stride * theirs, peer_wires_[pi], stride * n_,
+                           cudaMemcpyDeviceToDevice, ag_s_), "pull wires");
+      } else {
+        ck(cudaMemcpyAsync(w_up_c_.as<uint8_t>() + eb * theirs * per_slot_up, peer_w_up_[pi],
+                           eb * n_ * per_slot_up, cudaMemcpyDeviceToDevice, ag_s_), "pull up");
+        ck(cudaMemcpyAsync(w_down_c_.as<uint8_t>() + eb * theirs * per_slot_down, peer_w_down_[pi],
+                           eb * n_ * per_slot_down, cudaMemcpyDeviceToDevice, ag_s_), "pull down");
+      }
+    }
+    if (use_sr_) decode_gathered(wb, stride, ag_s_);
+    ck(cudaEventRecord(ev_ag_done_, ag_s_), "record");
+    ag_pending_ = true;
+    return;
+  }
   if (!use_sr_) {
     nck(ncclGroupStart(), "group start");
     for (int64_t p : ag_peers_) {
@@ -331,26 +405,32 @@ void Layer::gather_experts(cudaStream_t s) {
     nck(ncclRecv(wires + stride * first_slot_of(p), stride * n_, ncclUint8, static_cast<int>(p), comm_->nccl, s), "recv wire");
   }
   nck(ncclGroupEnd(), "group end");
-  // Decode gathered wires in batches, then lay each decoded expert out as a compute slot.
+  decode_gathered(wb, stride, s);
+}
+
+void Layer::decode_gathered(size_t wb, size_t stride, cudaStream_t s) {
+  // Decode every gathered wire straight into its compute slot (shared expert copied in
+  // by the copy engine, k entries scattered to their transposed positions).
+  const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
+  const size_t per_slot = static_cast<size_t>(F_ * H_);
+  uint8_t* wires = wires_.as<uint8_t>();
+  auto first_slot_of = [&](int64_t owner) { return slot_of_expert_[static_cast<size_t>(owner * n_)]; };
   std::vector<int64_t> gathered;
   for (int64_t p : ag_peers_)
     for (int64_t i = 0; i < n_; ++i) gathered.push_back(first_slot_of(p) + i);
-  const int64_t cap = static_cast<int64_t>(sr_dec_.bytes / (sizeof(float) * P));
-  for (size_t b0 = 0; b0 < gathered.size(); b0 += static_cast<size_t>(cap)) {
-    const size_t nb = std::min(gathered.size() - b0, static_cast<size_t>(cap));
-    std::vector<const void*> wi;
-    std::vector<float*> outs;
-    for (size_t i = 0; i < nb; ++i) {
-      wi.push_back(wires + stride * gathered[b0 + i]);
-      outs.push_back(sr_dec_.as<float>() + static_cast<int64_t>(i) * P);
-    }
-    ck(launch_sr_decode_batch(reinterpret_cast<const uint8_t* const*>(wi.data()), static_cast<int>(nb), wb,
-                              shared_.as<float>(), H_, F_, outs.data(), sr_status_.as<int32_t>(), s), "decode");
+  for (size_t b0 = 0; b0 < gathered.size(); b0 += kMaxSrBatch) {
+    const size_t nb = std::min(gathered.size() - b0, static_cast<size_t>(kMaxSrBatch));
+    std::vector<const uint8_t*> wi;
+    std::vector<void*> up, down;
     for (size_t i = 0; i < nb; ++i) {
       const int64_t slot = gathered[b0 + i];
-      ck(launch_transpose_convert(DType::F32, outs[i], H_, F_, dt_, w_up_c_.as<uint8_t>() + eb * slot * per_slot_up, s), "dec up");
-      ck(launch_transpose_convert(DType::F32, outs[i] + H_ * F_, F_, H_, dt_, w_down_c_.as<uint8_t>() + eb * slot * per_slot_down, s), "dec down");
+      wi.push_back(wires + stride * slot);
+      up.push_back(w_up_c_.as<uint8_t>() + eb * slot * per_slot);
+      down.push_back(w_down_c_.as<uint8_t>() + eb * slot * per_slot);
     }
+    ck(launch_sr_decode_layout_batch(wi.data(), static_cast<int>(nb), wb, shared_.as<float>(), shared_c_.p, dt_, H_,
+                                     F_, up.data(), down.data(), sr_status_.as<int32_t>(), s),
+       "decode");
   }
 }
 
@@ -438,25 +518,29 @@ void Layer::exchange(bool dispatch, cudaStream_t s) {
   nck(ncclGroupEnd(), "group end");
 }
 
-void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down, const int* wait_src) {
-  GroupTable gt{g_row_start_.as<int>(), g_rows_.as<int>(), g_slot_.as<int>(), num_groups_};
+void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down, const int* wait_src, int g0,
+                             int ng, const char* tag) {
+  if (ng < 0) ng = num_groups_ - g0;
+  if (ng <= 0) return;
+  GroupTable gt{g_row_start_.as<int>() + g0, g_rows_.as<int>() + g0, g_slot_.as<int>() + g0, ng};
   GroupTable gt_down = gt;
-  gt_down.out = out_down;
+  gt_down.out = out_down ? out_down + g0 : nullptr;
   if (wait_src) {
-    gt.wait_src = wait_src;
+    gt.wait_src = wait_src + g0;
     gt.wait_flags = p2p_dispatch_flags(p2p_args_);
     gt.epoch = p2p_args_.epoch;
   }
+  const std::string up = std::string("gemm_up") + tag, down = std::string("gemm_down") + tag;
   if (dt_ == DType::BF16) {
-    mark("gemm_up", s);
+    mark(up.c_str(), s);
     auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta : launch_grouped_gemm_bf16;
     ck(gemm(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_), "gemm up");
-    mark("gemm_down", s);
+    mark(down.c_str(), s);
     ck(gemm(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_), "gemm down");
   } else {
-    mark("gemm_up", s);
+    mark(up.c_str(), s);
     ck(launch_grouped_gemm_f32(xall_.as<float>(), static_cast<int>(H_), w_up_c_.as<float>(), hbuf_.as<float>(), static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_ * 2, s), "gemm up");
-    mark("gemm_down", s);
+    mark(down.c_str(), s);
     ck(launch_grouped_gemm_f32(hbuf_.as<float>(), static_cast<int>(F_), w_down_c_.as<float>(), oall_.as<float>(), static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_ * 2, s), "gemm down");
   }
   launches_ += 2;
@@ -504,7 +588,19 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
       launches_ += 4;
       // The down-projection writes received rows' outputs straight into their source
       // GPU's oall (fused GEMM + combine exchange); the combine reads local HBM only.
-      run_expert_gemms(s, g_out_down_.as<unsigned long long>(), g_wait_.as<int>());
+      const int n_src = p2p_args_.n_src[rank_];
+      if (ag_pending_) {
+        // own experts first (weights already resident), gathered ones after the AG lands
+        const int own = static_cast<int>(n_ * (1 + n_src));
+        run_expert_gemms(s, g_out_down_.as<unsigned long long>(), g_wait_.as<int>(), 0, own);
+        mark("ag_wait", s);
+        ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");
+        ag_pending_ = false;
+        run_expert_gemms(s, g_out_down_.as<unsigned long long>(), g_wait_.as<int>(), own, num_groups_ - own,
+                         "_gathered");
+      } else {
+        run_expert_gemms(s, g_out_down_.as<unsigned long long>(), g_wait_.as<int>());
+      }
       ck(cudaStreamWaitEvent(s, ev_remote_, 0), "wait");
       mark("combine", s);
       ck(launch_signal_wait(p2p_args_, 2, s), "combine flags");
@@ -543,6 +639,67 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
   ck(launch_combine(dt_, oall_.p, pos_.as<int>(), topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine");
   launches_ += 1;
   mark("end", s);
+}
+
+void Layer::comm_bench(const void* x, int64_t T, int iters, double* out, cudaStream_t s) {
+  for (int i = 0; i < 6; ++i) out[i] = 0.0;
+  if (G_ == 1) return;
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
+  if (p2p_) {
+    // A2A dispatch over NVLink: rows this GPU sends to peers, timed on the permute that
+    // stores them (remote rows only), after a full forward has set up the plan.
+    forward(x, T, y_dev_[0].p, s);
+    std::vector<int32_t> cnt(static_cast<size_t>(NK_));
+    ck(cudaMemcpyAsync(cnt.data(), key_total_.p, sizeof(int32_t) * NK_, cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "sync");
+    int64_t out_rows = 0;
+    for (int64_t key = 0; key < NK_; ++key)
+      if (key / E_ != rank_) out_rows += cnt[static_cast<size_t>(key)];
+    const int Ti = static_cast<int>(T);
+    float total = 0.f;
+    for (int it = 0; it < iters; ++it) {
+      ck(cudaEventRecord(e0, s), "record");
+      ck(launch_permute_p2p(p2p_args_, dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), keys_.as<int>(),
+                            ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
+                            pos_.as<int>(), s, 2), "permute remote");
+      ck(cudaEventRecord(e1, s), "record");
+      ck(cudaEventSynchronize(e1), "sync");
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+      total += ms;
+    }
+    out[0] = total / iters;
+    out[1] = static_cast<double>(out_rows) * H_ * eb;
+  }
+  if (!ag_peers_.empty()) {
+    // the peer-memory All-Gather runs on its own stream: join it before each timing point
+    auto join = [&] {
+      if (ag_pending_) {
+        ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");
+        ag_pending_ = false;
+      }
+    };
+    gather_experts(s);
+    join();
+    ck(cudaEventRecord(e0, s), "record");
+    for (int it = 0; it < iters; ++it) {
+      gather_experts(s);
+      join();
+    }
+    ck(cudaEventRecord(e1, s), "record");
+    ck(cudaEventSynchronize(e1), "sync");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+    out[3] = ms / iters;
+    const double per_expert = use_sr_ ? static_cast<double>(wires_.bytes) / static_cast<double>(slots_)
+                                      : static_cast<double>(2 * H_ * F_ * eb);
+    out[4] = static_cast<double>(ag_peers_.size()) * n_ * per_expert;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
 }
 
 void Layer::collect_timings(char* names, size_t names_cap, float* ms, int cap, int* count) {

@@ -49,6 +49,8 @@ class Layer {
   void forward(const void* x, int64_t T, void* y, cudaStream_t s);
   void forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s);
   void host_fence(cudaStream_t s);
+  // Communication microbenchmark: out = {a2a_ms, a2a_bytes_out, 0, ag_ms, ag_bytes_in, 0}.
+  void comm_bench(const void* x, int64_t T, int iters, double* out, cudaStream_t s);
 
   // introspection
   const int* topk_idx() const { return topk_idx_.as<int>(); }
@@ -66,7 +68,9 @@ class Layer {
   void mark(const char* name, cudaStream_t s);
   void build_comm_plan_and_groups(int T, cudaStream_t s);
   void exchange(bool dispatch, cudaStream_t s);
-  void run_expert_gemms(cudaStream_t s, const unsigned long long* out_down = nullptr, const int* wait_src = nullptr);
+  void run_expert_gemms(cudaStream_t s, const unsigned long long* out_down = nullptr, const int* wait_src = nullptr,
+                        int g0 = 0, int ng = -1, const char* tag = "");
+  void decode_gathered(size_t wire_bytes, size_t stride, cudaStream_t s);
 
   // shape
   int64_t H_, F_, E_, k_, Tmax_, G_, n_, NK_;
@@ -87,7 +91,7 @@ class Layer {
 
   // device state
   DevBuf d_route_, d_slot_of_expert_, wg_t_, w_up_c_, w_down_c_;
-  DevBuf shared_, master_, wires_, sr_ws_, sr_tmp_, sr_dec_, sr_status_;
+  DevBuf shared_, shared_c_, master_, wires_, sr_ws_, sr_tmp_, sr_status_;
   DevBuf topk_idx_, topk_w_, keys_, ranks_, chunk_counts_, chunk_off_, key_total_, key_off_;
   DevBuf dest_rows_, dest_off_, g_row_start_, g_rows_, g_slot_, all_counts_;
   DevBuf pos_, xall_, hbuf_, oall_;
@@ -102,6 +106,12 @@ class Layer {
   DevBuf sync_, send_base_, g_out_down_, g_wait_;
   cudaStream_t side_s_ = nullptr;
   cudaEvent_t ev_counts_ = nullptr, ev_remote_ = nullptr;
+  // expert All-Gather overlapped with the step (copy-engine pulls over NVLink)
+  cudaStream_t ag_s_ = nullptr;
+  cudaEvent_t ev_ag_start_ = nullptr, ev_ag_done_ = nullptr;
+  std::vector<void*> peer_w_up_, peer_w_down_, peer_wires_;
+  uint32_t ag_epoch_ = 0;
+  bool ag_pending_ = false;
   std::vector<void*> ipc_opened_;
   uint32_t epoch_ = 0;
   void setup_p2p();

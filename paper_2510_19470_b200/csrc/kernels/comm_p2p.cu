@@ -47,14 +47,14 @@ __device__ void wait_flag(const uint32_t* f, uint32_t epoch) {
 
 // Sync buffer of one rank (in its HBM, written by peers).
 struct SyncView {
-  uint32_t* flags;  // [3][kMaxG]: 0 counts, 1 dispatched, 2 outputs ready; index = source rank
+  uint32_t* flags;  // [4][kMaxG]: 0 counts, 1 dispatched, 2 outputs ready, 3 experts final; index = source
   int* inbox;       // [2][kMaxG][NK]: counts of every source, double-buffered by epoch parity
 };
 
 __device__ __forceinline__ SyncView view(void* base, int NK) {
   SyncView v;
   v.flags = static_cast<uint32_t*>(base);
-  v.inbox = reinterpret_cast<int*>(static_cast<uint8_t*>(base) + 3 * kMaxG * sizeof(uint32_t));
+  v.inbox = reinterpret_cast<int*>(static_cast<uint8_t*>(base) + 4 * kMaxG * sizeof(uint32_t));
   (void)NK;
   return v;
 }
@@ -114,33 +114,41 @@ __global__ void __launch_bounds__(256) count_exchange_kernel(P2PArgs a, const in
   auto row_addr = [&](int rank, long long row) {
     return reinterpret_cast<unsigned long long>(static_cast<uint8_t*>(a.oall[rank]) + row * a.row_bytes);
   };
+  // Groups of this GPU's own experts come first, gathered experts after them, so the
+  // step can run the own-expert GEMMs while the expert All-Gather is still in flight.
+  const int n_own = E / G;
   int g = 0;
-  for (int e = 0; e < E; ++e) {
-    const int sl = slot_of_expert[e];
-    if (sl < 0) continue;
-    g_row_start[g] = key_off[me * E + e];
-    g_rows[g] = cnt[me * NK + me * E + e];
-    g_out_down[g] = row_addr(me, key_off[me * E + e]);
-    g_wait[g] = -1;
-    g_slot[g++] = sl;
-  }
-  int at = a.recv_start;
-  for (int i = 0; i < a.n_src[me]; ++i) {
-    const int s = a.src_list[me * kMaxG + i];
-    long long src_off = 0;  // key_off of source s for key (me, 0)
-    for (int key = 0; key < me * E; ++key) src_off += cnt[s * NK + key];
+  for (int pass = 0; pass < 2; ++pass) {
+    auto in_pass = [&](int e) { return ((e / n_own) == me) == (pass == 0); };
     for (int e = 0; e < E; ++e) {
       const int sl = slot_of_expert[e];
-      const int c = cnt[s * NK + me * E + e];
-      if (sl >= 0) {  // a source only routes to this GPU experts it holds (S2)
-        g_row_start[g] = at;
-        g_rows[g] = c;
-        g_out_down[g] = row_addr(s, src_off);
-        g_wait[g] = s;
-        g_slot[g++] = sl;
-        at += c;
+      if (sl < 0 || !in_pass(e)) continue;
+      g_row_start[g] = key_off[me * E + e];
+      g_rows[g] = cnt[me * NK + me * E + e];
+      g_out_down[g] = row_addr(me, key_off[me * E + e]);
+      g_wait[g] = -1;
+      g_slot[g++] = sl;
+    }
+    int at = a.recv_start;
+    for (int i = 0; i < a.n_src[me]; ++i) {
+      const int s = a.src_list[me * kMaxG + i];
+      long long src_off = 0;  // key_off of source s for key (me, 0)
+      for (int key = 0; key < me * E; ++key) src_off += cnt[s * NK + key];
+      for (int e = 0; e < E; ++e) {
+        const int sl = slot_of_expert[e];
+        const int c = cnt[s * NK + me * E + e];
+        if (sl >= 0) {  // a source only routes to this GPU experts it holds (S2)
+          if (in_pass(e)) {
+            g_row_start[g] = at;
+            g_rows[g] = c;
+            g_out_down[g] = row_addr(s, src_off);
+            g_wait[g] = s;
+            g_slot[g++] = sl;
+          }
+          at += c;
+        }
+        src_off += c;
       }
-      src_off += c;
     }
   }
 }
@@ -183,20 +191,16 @@ __global__ void __launch_bounds__(256) permute_p2p_kernel(P2PArgs a, const uint8
 }
 
 // Raise flag `slot` on every A2A peer, then (if `wait`) wait for theirs.
-__global__ void signal_wait_kernel(P2PArgs a, int slot, int wait) {
+__global__ void signal_wait_kernel(P2PArgs a, int slot, int wait, int ag) {
   __threadfence_system();
   const int NK = a.G * a.E;
   const int i = threadIdx.x;
-  if (i < a.n_src[a.rank]) {
-    const int p = a.src_list[a.rank * kMaxG + i];
-    st_release_sys(view(a.sync[p], NK).flags + slot * kMaxG + a.rank, a.epoch);
-  }
+  const int n = ag ? a.n_ag : a.n_src[a.rank];
+  const int* list = ag ? a.ag_list : a.src_list + a.rank * kMaxG;
+  if (i < n) st_release_sys(view(a.sync[list[i]], NK).flags + slot * kMaxG + a.rank, a.epoch);
   if (!wait) return;
   __syncthreads();
-  if (i < a.n_src[a.rank]) {
-    const int p = a.src_list[a.rank * kMaxG + i];
-    wait_flag(view(a.sync[a.rank], NK).flags + slot * kMaxG + p, a.epoch);
-  }
+  if (i < n) wait_flag(view(a.sync[a.rank], NK).flags + slot * kMaxG + list[i], a.epoch);
 }
 
 template <bool BF16>
@@ -250,7 +254,7 @@ const uint32_t* p2p_dispatch_flags(const P2PArgs& a) {
 }
 
 size_t p2p_sync_bytes(int G, int E) {
-  return 3 * kMaxG * sizeof(uint32_t) + 2 * kMaxG * static_cast<size_t>(G) * E * sizeof(int) + 256;
+  return 4 * kMaxG * sizeof(uint32_t) + 2 * kMaxG * static_cast<size_t>(G) * E * sizeof(int) + 256;
 }
 
 cudaError_t launch_count_exchange(const P2PArgs& a, const int* key_total, const int* key_off,
@@ -282,8 +286,8 @@ cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T,
   return cudaGetLastError();
 }
 
-cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait) {
-  signal_wait_kernel<<<1, 32, 0, s>>>(a, slot, wait ? 1 : 0);
+cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait, bool ag_peers) {
+  signal_wait_kernel<<<1, 32, 0, s>>>(a, slot, wait ? 1 : 0, ag_peers ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -19,6 +19,8 @@ struct P2PArgs {
   void* sync[kMaxG];
   int src_list[kMaxG * kMaxG];  // src_list[d*kMaxG + i]: i-th A2A peer of d (ring order)
   int n_src[kMaxG];
+  int ag_list[kMaxG];           // this rank's All-Gather peers (ring order)
+  int n_ag;
   int G, E, rank;
   int recv_start;               // first receive row (Tmax * k), same on every rank
   int row_bytes;                // H * element bytes of xall / oall rows
@@ -36,8 +38,9 @@ cudaError_t launch_count_exchange(const P2PArgs& a, const int* key_total, const 
 cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T, int H, int k, const int* keys,
                                const int* ranks, const int* chunk_off, const int* key_off, const int* send_base,
                                int* pos, cudaStream_t s, int mode = 0);
-// slot 1: "my rows are in your receive area"; slot 2: "your outputs are ready".
-cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait = true);
+// slot 1: "my rows are in your receive area"; slot 2: "your outputs are ready";
+// slot 3 (AG peers): "my experts for this epoch are final, pull them".
+cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait = true, bool ag_peers = false);
 // This rank's dispatch flags (indexed by source rank), for GEMM-side gating.
 const uint32_t* p2p_dispatch_flags(const P2PArgs& a);
 cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, const int* pos, const int* key_off,

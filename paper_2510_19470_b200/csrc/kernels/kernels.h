@@ -112,6 +112,12 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
 // out_b = shared + residual_b (fp32).
 cudaError_t launch_sr_decode_batch(const uint8_t* const* wires, int batch, size_t wire_bytes, const float* shared,
                                    int64_t h, int64_t m, float* const* outs, int32_t* status, cudaStream_t stream);
+// Decode directly into the compute layout used by the GEMM (w_up^T [m][h], w_down^T
+// [h][m]) in out_dt; shared_c is the shared expert already in that layout/dtype.
+cudaError_t launch_sr_decode_layout_batch(const uint8_t* const* wires, int batch, size_t wire_bytes,
+                                          const float* shared, const void* shared_c, DType out_dt, int64_t h,
+                                          int64_t m, void* const* up, void* const* down, int32_t* status,
+                                          cudaStream_t stream);
 // out = mean over experts (fp64 accumulate in list order, times 1/n, round to fp32).
 cudaError_t launch_shared_mean(DType dt, const void* const* experts, int n, int64_t P, float* out,
                                cudaStream_t stream);

@@ -616,6 +616,65 @@ __global__ void __launch_bounds__(256) sr_decode_scatter_kernel(DecBatch batch, 
   batch.out[b][idx] = __double2float_rn(__dadd_rn(static_cast<double>(shared[idx]), entry_value(wire, v, j)));
 }
 
+// Decode straight into the GEMM's compute layout (K-major w_up^T [m][h], w_down^T [h][m])
+// in the layer dtype: the slot was pre-filled with the shared expert in that layout (a
+// copy-engine memcpy), so only the k entries are scattered, each to its transposed
+// position, with the same double-precision add and round as the flat decode.
+struct DecLayoutBatch {
+  const uint8_t* wire[kMaxSrBatch];
+  void* up[kMaxSrBatch];
+  void* down[kMaxSrBatch];
+};
+
+template <bool BF16OUT>
+__global__ void __launch_bounds__(256) sr_decode_scatter_layout_kernel(DecLayoutBatch batch, size_t bytes,
+                                                                       const float* __restrict__ shared, int64_t h,
+                                                                       int64_t m, int32_t* status) {
+  const int b = blockIdx.y;
+  const uint8_t* wire = batch.wire[b];
+  int code;
+  const WireView v = read_header(wire, bytes, h, m, &code);
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (!v.ok_header) {
+    if (j == 0) status[4 * b] = code;
+    return;
+  }
+  if (j >= v.k) return;
+  const uint64_t up = static_cast<uint64_t>(h * m), P = 2 * up;
+  const uint64_t idx = entry_index(wire, v, j);
+  int c = 0;
+  if (idx >= P) c = 5;
+  else if (j > 0 && idx <= entry_index(wire, v, j - 1)) c = 6;
+  if (c) {
+    atomicMin(reinterpret_cast<unsigned long long*>(status + 4 * b + 2),
+              static_cast<unsigned long long>(j) * 8ull + static_cast<unsigned long long>(c));
+    return;
+  }
+  const float val = __double2float_rn(__dadd_rn(static_cast<double>(shared[idx]), entry_value(wire, v, j)));
+  int64_t off;
+  void* base;
+  if (idx < up) {  // w_up is h x m: (r, c) -> w_up^T[c][r]
+    const int64_t r = static_cast<int64_t>(idx) / m, cc = static_cast<int64_t>(idx) % m;
+    off = cc * h + r;
+    base = batch.up[b];
+  } else {         // w_down is m x h: (r, c) -> w_down^T[c][r]
+    const int64_t i2 = static_cast<int64_t>(idx - up);
+    const int64_t r = i2 / h, cc = i2 % h;
+    off = cc * m + r;
+    base = batch.down[b];
+  }
+  if (BF16OUT) static_cast<__nv_bfloat16*>(base)[off] = __float2bfloat16_rn(val);
+  else static_cast<float*>(base)[off] = val;
+}
+
+__global__ void sr_status_init_kernel(int32_t* status, int n) {
+  const int b = threadIdx.x;
+  if (b >= n) return;
+  status[4 * b] = 0;
+  status[4 * b + 1] = 0;
+  *reinterpret_cast<unsigned long long*>(status + 4 * b + 2) = ~0ull;
+}
+
 __global__ void sr_status_finalize_kernel(int32_t* status, int n) {
   const int b = threadIdx.x;
   if (b >= n || status[4 * b] != 0) return;
@@ -746,6 +805,35 @@ cudaError_t launch_sr_decode_batch(const uint8_t* const* wires, int batch, size_
   const int64_t kmax = wire_bytes > 28 ? static_cast<int64_t>((wire_bytes - 28) / 8) : 0;
   const int vblocks = static_cast<int>(std::max<int64_t>(1, (kmax + 255) / 256));
   sr_decode_scatter_kernel<<<dim3(vblocks, batch), 256, 0, stream>>>(db, wire_bytes, shared, h, m, status);
+  sr_status_finalize_kernel<<<1, kMaxSrBatch, 0, stream>>>(status, batch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sr_decode_layout_batch(const uint8_t* const* wires, int batch, size_t wire_bytes,
+                                          const float* shared, const void* shared_c, DType out_dt, int64_t h,
+                                          int64_t m, void* const* up, void* const* down, int32_t* status,
+                                          cudaStream_t stream) {
+  if (batch <= 0 || batch > kMaxSrBatch) return cudaErrorInvalidValue;
+  DecLayoutBatch db{};
+  const size_t eb = out_dt == DType::BF16 ? 2 : 4;
+  const size_t half = static_cast<size_t>(h * m) * eb;
+  for (int i = 0; i < batch; ++i) {
+    db.wire[i] = wires[i];
+    db.up[i] = up[i];
+    db.down[i] = down[i];
+    // shared expert in the compute layout -> the slot (copy engine)
+    cudaError_t e = cudaMemcpyAsync(up[i], shared_c, half, cudaMemcpyDeviceToDevice, stream);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(down[i], static_cast<const uint8_t*>(shared_c) + half, half, cudaMemcpyDeviceToDevice, stream);
+    if (e != cudaSuccess) return e;
+  }
+  sr_status_init_kernel<<<1, kMaxSrBatch, 0, stream>>>(status, batch);
+  const int64_t kmax = wire_bytes > 28 ? static_cast<int64_t>((wire_bytes - 28) / 8) : 0;
+  const int vblocks = static_cast<int>(std::max<int64_t>(1, (kmax + 255) / 256));
+  if (out_dt == DType::BF16)
+    sr_decode_scatter_layout_kernel<true><<<dim3(vblocks, batch), 256, 0, stream>>>(db, wire_bytes, shared, h, m, status);
+  else
+    sr_decode_scatter_layout_kernel<false><<<dim3(vblocks, batch), 256, 0, stream>>>(db, wire_bytes, shared, h, m, status);
   sr_status_finalize_kernel<<<1, kMaxSrBatch, 0, stream>>>(status, batch);
   return cudaGetLastError();
 }

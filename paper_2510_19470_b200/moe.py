@@ -116,6 +116,16 @@ class MoELayer:
     def host_fence(self, stream=None):
         check(lib.hep_layer_host_fence(self.handle, _stream(stream)))
 
+    def comm_bench(self, x: torch.Tensor, iters: int = 10, stream=None) -> dict:
+        """Per-GPU exchange microbenchmark (collective): NVLink A2A dispatch and expert
+        All-Gather bytes and times; bus GB/s = bytes / time."""
+        out = (C.c_double * 6)()
+        check(lib.hep_layer_comm_bench(self.handle, x.data_ptr(), x.shape[0], iters, out, _stream(stream)))
+        r = {"a2a_ms": out[0], "a2a_bytes": out[1], "ag_ms": out[3], "ag_bytes": out[4]}
+        r["a2a_bus_gbs"] = r["a2a_bytes"] / (r["a2a_ms"] * 1e6) if r["a2a_ms"] > 0 else None
+        r["ag_bus_gbs"] = r["ag_bytes"] / (r["ag_ms"] * 1e6) if r["ag_ms"] > 0 else None
+        return r
+
     def debug(self, T: int):
         """Device views of the last forward's routing: topk_idx, topk_w, pos, key_counts."""
         ti, tw, pos, packed, kc = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
