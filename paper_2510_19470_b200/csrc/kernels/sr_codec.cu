@@ -6,12 +6,23 @@
 //   keep the k entries ranked by (|r| desc, index asc) -- the reference's
 //   nth_element order (:44-62) -- emitted in ascending index order as SRC1 wire
 //   entries (index, value) with value = (float)r for 32-bit wires (:26-28).
-//   GPU algorithm: key = IEEE bits of |r| (monotone for non-negative doubles);
-//   MSB-first radix select with 12-bit digits (block-private shared-memory
-//   histograms, early exit once the threshold bucket is exactly consumed) finds
-//   the threshold prefix T and how many key==T ties to take; then ONE ordered
-//   stream compaction with a decoupled look-back scan writes the entries already
-//   sorted by index (no sort pass), taking ties lowest-index first.
+//   GPU algorithm (key = IEEE bits of |r|, monotone for non-negative doubles):
+//   1. sample: 32768 evenly spaced keys per range; two order statistics of the sample
+//      bracket the k-th largest key's top word [lo32, hi32] with a 4-sigma margin;
+//   2. split (one full read): keys above hi32 are "sure", keys in the bracket are
+//      "candidates"; both are compacted in index order into a short list (residual,
+//      index) with a decoupled look-back scan.  The exact counts validate the
+//      bracket (sure < k <= sure + candidates, list within capacity); a failed
+//      bracket switches the range to the full-range path below, so the result never
+//      depends on the sample;
+//   3. select: MSB radix select with 12-bit digits over the candidates (or the full
+//      range) for the remaining rank, one fused histogram+select launch per digit
+//      (block-private histograms, last-arriving block picks the bucket, early exit
+//      once the bucket is exactly consumed or no key has lower bits);
+//   4. emit: ordered compaction of the list (or range) into the wire, ties at the
+//      threshold taken lowest index first.
+//   Full reads: 2 (sample and list work are ~1-2% of the range) instead of one per
+//   radix pass plus the compaction.
 // Decode (K6, "unpack"), :226-246: out = shared, then out[i] = (float)((double)
 //   shared[i] + v) for every entry; entries are validated in parallel and the
 //   first failing entry (lowest j) decides the error code, like the reference's
@@ -19,6 +30,10 @@
 // Shared mean (K7), :147-168: fp64 sum over experts in list order, times (1/n).
 // All fp64 arithmetic uses explicit _rn intrinsics so no FMA contraction can
 // change a rounding.
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -29,32 +44,60 @@ namespace {
 
 constexpr int kDigitBits = 12;
 constexpr int kBins = 1 << kDigitBits;
-constexpr int kPasses = 6;
-__constant__ int c_shift[kPasses] = {51, 39, 27, 15, 3, 0};
-__constant__ int c_width[kPasses] = {12, 12, 12, 12, 12, 3};
+constexpr int kPasses = 6;  // 12-bit digits cover the 63 key bits below the sign in 6 passes
 
 constexpr int kTileThreads = 256;
 constexpr int kPerThread = 16;
 constexpr int kTile = kTileThreads * kPerThread;  // 4096 elements per compaction tile
+constexpr int kSample = 8192;                      // sampled keys per range
+constexpr int kSplitPer = 64;                      // split: elements per thread per tile
+constexpr int kSplitTile = kTileThreads * kSplitPer;
+constexpr int kSampleThreads = 1024;
+constexpr int kSampleSmem = (kSample + 2 * kBins) * sizeof(unsigned int);
+
+constexpr int kModeList = 0;  // select and emit over the sure + candidate list
+constexpr int kModeFull = 1;  // select and emit over the whole range (static choice or failed bracket)
 
 struct SelState {
   unsigned long long prefix;
   unsigned long long mask;
-  long long need;
-  int done;
-  int ticket;
-  unsigned long long keyor;  // OR of every key in the range (pass 0): bits that never vary are skipped
-  unsigned int hist[kBins];
+  long long need;    // rank still to place (list mode: among the candidates)
+  long long need0;   // min(k, n)
+  long long n_sure, n_super;
+  unsigned long long keyor;  // OR of every key taking part in pass 0: bits that never vary are skipped
+  unsigned int lo32, hi32;   // candidate bracket on the top key word
+  int done, mode;
+  int top;  // bits [top, 63] of the threshold key are resolved (prefix/mask); next digit ends at top-1
+  int ticket, ticket2, arrive;
+  alignas(16) unsigned int hist[kBins];
 };
 
-// Workspace of a batch: SelState per (expert, range) followed by the look-back words of
-// every (expert, range), `tiles` apiece.
+struct RangeArgs {
+  int64_t lo[2], hi[2], k[2], out_base[2];
+  int full[2];  // static full-range mode
+  int nr;
+  int force_fallback;
+};
+
+// Selects a per-range argument without a dynamically indexed (local-memory) param copy.
+__host__ __device__ __forceinline__ int64_t pick(const int64_t (&a)[2], int r) { return r ? a[1] : a[0]; }
+
+// Workspace: one slot per (expert, range): SelState | split look-back words | emit
+// look-back words | list residuals (f64) | list indices (u32, relative to the range).
 struct WsView {
-  SelState* sel;
-  unsigned long long* status;
-  int64_t tiles;
-  __device__ SelState& st(int b, int r) const { return sel[b * 2 + r]; }
-  __device__ unsigned long long* stat(int b, int r) const { return status + (static_cast<int64_t>(b) * 2 + r) * tiles; }
+  uint8_t* base;
+  size_t per, off_stat, off_stat2, off_res, off_idx;
+  int64_t tiles, cap;
+  __device__ uint8_t* slot(int b, int r) const { return base + (static_cast<size_t>(b) * 2 + r) * per; }
+  __device__ SelState& st(int b, int r) const { return *reinterpret_cast<SelState*>(slot(b, r)); }
+  __device__ unsigned long long* stat(int b, int r) const {
+    return reinterpret_cast<unsigned long long*>(slot(b, r) + off_stat);
+  }
+  __device__ unsigned long long* stat2(int b, int r) const {
+    return reinterpret_cast<unsigned long long*>(slot(b, r) + off_stat2);
+  }
+  __device__ double* lres(int b, int r) const { return reinterpret_cast<double*>(slot(b, r) + off_res); }
+  __device__ uint32_t* lidx(int b, int r) const { return reinterpret_cast<uint32_t*>(slot(b, r) + off_idx); }
 };
 
 struct EncBatch {
@@ -74,33 +117,192 @@ __device__ __forceinline__ double residual_at(const void* expert, bool bf16, con
   return __dsub_rn(e, static_cast<double>(shared[i]));
 }
 
+// Residuals of elements i0 .. i0+3 (0 past hi).  vec: i0 is 4-aligned, so one float4
+// of the shared expert and one 8- or 16-byte load of the expert cover the group.
+__device__ __forceinline__ void load_res4(const void* expert, int bf16, const float* __restrict__ shared,
+                                          int64_t i0, int64_t hi, bool vec, double (&r)[4]) {
+  float e4[4] = {0.f, 0.f, 0.f, 0.f}, s4[4] = {0.f, 0.f, 0.f, 0.f};
+  if (vec && i0 + 3 < hi) {
+    const float4 sv = *reinterpret_cast<const float4*>(shared + i0);
+    s4[0] = sv.x; s4[1] = sv.y; s4[2] = sv.z; s4[3] = sv.w;
+    if (bf16) {
+      const uint2 raw = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(expert) + i0);
+      e4[0] = bf16_lo(raw.x); e4[1] = bf16_hi(raw.x); e4[2] = bf16_lo(raw.y); e4[3] = bf16_hi(raw.y);
+    } else {
+      const float4 ev = *reinterpret_cast<const float4*>(static_cast<const float*>(expert) + i0);
+      e4[0] = ev.x; e4[1] = ev.y; e4[2] = ev.z; e4[3] = ev.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + q < hi) {
+        s4[q] = shared[i0 + q];
+        e4[q] = bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(expert)[i0 + q])
+                     : static_cast<const float*>(expert)[i0 + q];
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) r[q] = __dsub_rn(static_cast<double>(e4[q]), static_cast<double>(s4[q]));
+}
+
 __device__ __forceinline__ unsigned long long key_of(double r) {
   return static_cast<unsigned long long>(__double_as_longlong(fabs(r)));
 }
+__device__ __forceinline__ uint32_t key32_of(double r) { return static_cast<uint32_t>(key_of(r) >> 32); }
 
 __device__ __forceinline__ void put_u32(uint8_t* p, uint32_t v) { *reinterpret_cast<uint32_t*>(p) = v; }
 
-// Block b: reset the selection state of expert b, zero its look-back words, write its
-// SRC1 header.
-__global__ void sr_init_kernel(WsView ws, EncBatch batch, int64_t n0, int64_t k0, int64_t n1, int64_t k1,
-                               int64_t h, int64_t m, int64_t k_total, uint32_t iw, uint32_t vw) {
-  const int b = blockIdx.x, t = threadIdx.x;
-  for (int r = 0; r < 2; ++r) {
-    SelState& s = ws.st(b, r);
-    const int64_t n = r ? n1 : n0, k = r ? k1 : k0;
-    for (int i = t; i < kBins; i += blockDim.x) s.hist[i] = 0;
-    unsigned long long* st = ws.stat(b, r);
-    for (int64_t i = t; i < ws.tiles; i += blockDim.x) st[i] = 0;
-    if (t == 0) {
-      s.prefix = 0;
-      s.mask = 0;
-      s.need = k >= n ? n : k;
-      s.done = (k <= 0 || k >= n) ? 1 : 0;
-      s.ticket = 0;
-      s.keyor = 0;
+// Residual magnitudes cluster in a few bins, so lanes holding the same digit are merged
+// with match.any and one leader adds the population count.
+__device__ __forceinline__ void hist_add(unsigned int* sh, int d) {
+  const unsigned int peers = __match_any_sync(__activemask(), d);
+  if (d >= 0 && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&sh[d], __popc(peers));
+}
+
+// Finds, scanning bins from the top (nb-1) down, the bin holding the need-th largest
+// key (1 <= need <= total): writes the bin, the count above it and its own count to
+// shared memory.  Any block size that is a multiple of 32 (<= 1024).
+template <typename Count>
+__device__ void find_bucket(Count cnt, int nb, long long need, int* sh_bin, long long* sh_before,
+                            long long* sh_count, unsigned long long* wsum) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  unsigned long long mine = 0;
+  for (int i = 0; i < per; ++i) {
+    const int b = nb - 1 - (t * per + i);
+    if (b >= 0) mine += cnt(b);
+  }
+  unsigned long long incl = mine;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += o;
+    }
+    if (lane < nw) wsum[lane] = w;
+  }
+  __syncthreads();
+  if (warp) incl += wsum[warp - 1];
+  const long long excl = static_cast<long long>(incl - mine);
+  if (excl < need && static_cast<long long>(incl) >= need) {  // exactly one owner
+    long long before = excl;
+    for (int i = 0; i < per; ++i) {
+      const int b = nb - 1 - (t * per + i);
+      if (b < 0) break;
+      const long long c = cnt(b);
+      if (before + c >= need) {
+        *sh_bin = b;
+        *sh_before = before;
+        *sh_count = c;
+        break;
+      }
+      before += c;
     }
   }
-  if (t == 0) {
+  __syncthreads();
+}
+
+// Decoupled look-back over tiles taken in ticket order, two 31-bit counters per tile
+// (warp 0; a 32-tile window per step, one predecessor per lane).  Returns the
+// exclusive prefix of both counters in every lane.
+__device__ __forceinline__ void lookback(unsigned long long* status, int tile, unsigned long long ta,
+                                         unsigned long long tb, unsigned long long& pa, unsigned long long& pb) {
+  constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 31) - 1;
+  const int lane = threadIdx.x & 31;
+  pa = 0;
+  pb = 0;
+  if (tile == 0) {
+    if (lane == 0) atomicExch(&status[0], kInc | (ta << 31) | tb);
+    return;
+  }
+  if (lane == 0) atomicExch(&status[tile], kAgg | (ta << 31) | tb);
+  for (int t0 = tile - 1; t0 >= 0; t0 -= 32) {
+    const int t = t0 - lane;
+    unsigned long long w = 0;
+    if (t >= 0) {
+      do { w = *reinterpret_cast<volatile unsigned long long*>(&status[t]); } while ((w >> 62) == 0);
+    }
+    const unsigned int inc = __ballot_sync(0xffffffffu, t >= 0 && (w >> 62) == 2);
+    const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest predecessor with an inclusive prefix
+    unsigned long long a = (t >= 0 && lane <= stop) ? (w >> 31) & kVal : 0;
+    unsigned long long b = (t >= 0 && lane <= stop) ? w & kVal : 0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+      b += __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    pa += a;
+    pb += b;
+    if (inc) break;
+  }
+  if (lane == 0) {
+    __threadfence();
+    atomicExch(&status[tile], kInc | ((pa + ta) << 31) | (pb + tb));
+  }
+}
+
+// Exclusive in-warp prefix of two per-lane counts (each < 2^16 per warp step).
+__device__ __forceinline__ void warp_scan2(unsigned int a, unsigned int b, unsigned int& ea, unsigned int& eb,
+                                           unsigned int& ta, unsigned int& tb) {
+  const int lane = threadIdx.x & 31;
+  const unsigned int mine = (a << 16) | b;
+  unsigned int incl = mine;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  const unsigned int total = __shfl_sync(0xffffffffu, incl, 31);
+  ea = (incl - mine) >> 16;
+  eb = (incl - mine) & 0xffffu;
+  ta = total >> 16;
+  tb = total & 0xffffu;
+}
+
+// grid (16, batch): reset the selection state and look-back words of expert b's two
+// ranges, write its SRC1 header.
+__global__ void sr_init_kernel(WsView ws, EncBatch batch, RangeArgs ra, int64_t h, int64_t m, int64_t k_total,
+                               uint32_t iw, uint32_t vw) {
+  const int b = blockIdx.y, t = threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int r = 0; r < 2; ++r) {
+    SelState& s = ws.st(b, r);
+    unsigned long long* s1 = ws.stat(b, r);
+    unsigned long long* s2 = ws.stat2(b, r);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + t; i < ws.tiles; i += stride) {
+      s1[i] = 0;
+      s2[i] = 0;
+    }
+    if (blockIdx.x) continue;
+    for (int i = t; i < kBins; i += blockDim.x) s.hist[i] = 0;
+    if (t == 0) {
+      const bool live = r < ra.nr;
+      const int64_t n = live ? pick(ra.hi, r) - pick(ra.lo, r) : 0, k = live ? pick(ra.k, r) : 0;
+      s.prefix = 0;
+      s.mask = 0;
+      s.top = 63;
+      s.need0 = s.need = k >= n ? n : (k > 0 ? k : 0);
+      s.done = (k <= 0 || k >= n) ? 1 : 0;
+      s.mode = (!live || s.done || (r ? ra.full[1] : ra.full[0])) ? kModeFull : kModeList;
+      s.n_sure = 0;
+      s.n_super = 0;
+      s.keyor = 0;
+      s.lo32 = 0;
+      s.hi32 = 0xffffffffu;
+      s.ticket = 0;
+      s.ticket2 = 0;
+      s.arrive = 0;
+    }
+  }
+  if (blockIdx.x == 0 && t == 0) {
     uint8_t* wire = batch.wire[b];
     wire[0] = 'S'; wire[1] = 'R'; wire[2] = 'C'; wire[3] = '1';
     put_u32(wire + 4, static_cast<uint32_t>(h));
@@ -112,412 +314,527 @@ __global__ void sr_init_kernel(WsView ws, EncBatch batch, int64_t n0, int64_t k0
   }
 }
 
-// Residual magnitudes cluster in a few bins, so lanes holding the same digit are merged
-// with match.any and one leader adds the population count.
-__device__ __forceinline__ void hist_add(unsigned int* sh, int d) {
-  const unsigned int peers = __match_any_sync(__activemask(), d);
-  if (d >= 0 && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&sh[d], __popc(peers));
-}
-
-// Histogram of the current digit over the keys matching the prefix (grid.y = expert).
-__global__ void __launch_bounds__(256) sr_hist_kernel(EncBatch batch, int bf16, const float* __restrict__ shared,
-                                                      int64_t lo, int64_t hi, WsView ws, int range, int pass) {
-  SelState& s = ws.st(blockIdx.y, range);
-  if (s.done) return;
-  const void* expert = batch.expert[blockIdx.y];
-  __shared__ unsigned int sh[kBins];
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x) sh[b] = 0;
-  __syncthreads();
-  const unsigned long long mask = s.mask, prefix = s.prefix;
-  const int shift = c_shift[pass];
-  const unsigned int dmask = (1u << c_width[pass]) - 1u;
-  unsigned long long kor = 0;
-  auto digit = [&](double r) {
-    const unsigned long long key = key_of(r);
-    kor |= key;
-    return (key & mask) == prefix ? static_cast<int>((key >> shift) & dmask) : -1;
-  };
-  // Vector body over 4-element groups (aligned to the range start), scalar ends.
-  const int64_t head_end = min(hi, (lo + 3) & ~static_cast<int64_t>(3));
-  const int64_t body_end = head_end + ((hi - head_end) & ~static_cast<int64_t>(3));
-  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t groups = (body_end - head_end) >> 2;
-  for (int64_t gi = tid; gi - (threadIdx.x & 31) < groups; gi += nthreads) {  // warp-uniform trip count
-    int d0 = -1, d1 = -1, d2 = -1, d3 = -1;
-    if (gi < groups) {
-      const int64_t i = head_end + 4 * gi;
-      const float4 sv = *reinterpret_cast<const float4*>(shared + i);
-      float e0, e1, e2, e3;
-      if (bf16) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(expert) + i);
-        e0 = bf16_lo(raw.x); e1 = bf16_hi(raw.x); e2 = bf16_lo(raw.y); e3 = bf16_hi(raw.y);
-      } else {
-        const float4 ev = *reinterpret_cast<const float4*>(static_cast<const float*>(expert) + i);
-        e0 = ev.x; e1 = ev.y; e2 = ev.z; e3 = ev.w;
-      }
-      d0 = digit(__dsub_rn(static_cast<double>(e0), static_cast<double>(sv.x)));
-      d1 = digit(__dsub_rn(static_cast<double>(e1), static_cast<double>(sv.y)));
-      d2 = digit(__dsub_rn(static_cast<double>(e2), static_cast<double>(sv.z)));
-      d3 = digit(__dsub_rn(static_cast<double>(e3), static_cast<double>(sv.w)));
-    }
-    hist_add(sh, d0);
-    hist_add(sh, d1);
-    hist_add(sh, d2);
-    hist_add(sh, d3);
-  }
-  if (blockIdx.x == 0) {
-    for (int64_t i = lo + threadIdx.x; i < head_end; i += blockDim.x) {
-      const int d = digit(residual_at(expert, bf16, shared, i));
-      if (d >= 0) atomicAdd(&sh[d], 1u);
-    }
-    for (int64_t i = body_end + threadIdx.x; i < hi; i += blockDim.x) {
-      const int d = digit(residual_at(expert, bf16, shared, i));
-      if (d >= 0) atomicAdd(&sh[d], 1u);
-    }
-  }
-  if (pass == 0) {
-    const unsigned int lo32 = __reduce_or_sync(0xffffffffu, static_cast<unsigned int>(kor));
-    const unsigned int hi32 = __reduce_or_sync(0xffffffffu, static_cast<unsigned int>(kor >> 32));
-    if ((threadIdx.x & 31) == 0 && (lo32 | hi32))
-      atomicOr(&s.keyor, (static_cast<unsigned long long>(hi32) << 32) | lo32);
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x)
-    if (sh[b]) atomicAdd(&s.hist[b], sh[b]);
-}
-
-// Block b (1024 threads): pick the digit bucket of expert b holding the need-th largest key.
-__global__ void __launch_bounds__(1024) sr_select_kernel(WsView ws, int range, int pass) {
-  SelState& s = ws.st(blockIdx.x, range);
-  if (s.done) return;
+// grid (nr, batch), 1024 threads: sample kSample evenly spaced keys of the range and
+// bracket the need-th largest key's top word between two sample order statistics,
+// each located to 24 bits (a 12-bit digit, then 12 more bits inside its bin; the
+// bracket is widened to the bins' outer edges, so it only ever grows).
+__global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(EncBatch batch, int bf16,
+                                                                   const float* __restrict__ shared, RangeArgs ra,
+                                                                   WsView ws) {
+  extern __shared__ unsigned int smem[];
+  uint32_t* ks = smem;                    // kSample keys
+  unsigned int* h_hi = smem + kSample;    // kBins
+  unsigned int* h_lo = h_hi + kBins;      // kBins
   __shared__ unsigned long long wsum[32];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int shift = c_shift[pass], width = c_width[pass], nb = 1 << width;
-  const int per = (nb + 1023) / 1024;
-  // Thread t owns bins nb-1-(t*per) .. nb-per-(t*per), counting down from the top.
-  unsigned long long mine = 0;
-  for (int i = 0; i < per; ++i) {
-    const int b = nb - 1 - (t * per + i);
-    if (b >= 0) mine += s.hist[b];
+  __shared__ int sh_bin;
+  __shared__ long long sh_before, sh_count;
+  const int r = blockIdx.x, b = blockIdx.y;
+  SelState& s = ws.st(b, r);
+  if (s.mode != kModeList) return;
+  const void* expert = batch.expert[b];
+  const int64_t lo = pick(ra.lo, r), n = pick(ra.hi, r) - lo;
+  const int S = static_cast<int>(n < kSample ? n : kSample);
+  constexpr int kPer = kSample / kSampleThreads;
+  const int64_t stride = n / S;  // evenly spaced over [0, S * stride), the tail < S elements
+  double rs[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {  // all loads in flight at once
+    const int j = threadIdx.x + u * kSampleThreads;
+    rs[u] = j < S ? residual_at(expert, bf16, shared, lo + static_cast<int64_t>(j) * stride) : 0.0;
   }
-  unsigned long long incl = mine;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int j = threadIdx.x + u * kSampleThreads;
+    if (j < S) ks[j] = key32_of(rs[u]);
+  }
+  for (int i = threadIdx.x; i < kBins; i += blockDim.x) h_hi[i] = 0;
+  __syncthreads();
+  const double q = static_cast<double>(s.need0) / static_cast<double>(n);
+  const double mean = q * S;
+  const double dev = 4.0 * sqrt(mean * (1.0 - q)) + 8.0;
+  const long long r_hi = static_cast<long long>(floor(mean - dev));
+  const long long r_lo = static_cast<long long>(ceil(mean + dev));
+  const bool has_hi = r_hi >= 0, has_lo = r_lo < S;
+  // digit 1: bits 20..31 of the top word
+  for (int j = threadIdx.x; j < S; j += blockDim.x) hist_add(h_hi, static_cast<int>(ks[j] >> 20));
+  __syncthreads();
+  int b_hi = 0, b_lo = 0;
+  long long w_hi = r_hi + 1, w_lo = r_lo + 1;
+  auto c1 = [&](int i) { return static_cast<unsigned long long>(h_hi[i]); };
+  if (has_hi) {
+    find_bucket(c1, kBins, w_hi, &sh_bin, &sh_before, &sh_count, wsum);
+    b_hi = sh_bin;
+    w_hi -= sh_before;
+    __syncthreads();
+  }
+  if (has_lo) {
+    find_bucket(c1, kBins, w_lo, &sh_bin, &sh_before, &sh_count, wsum);
+    b_lo = sh_bin;
+    w_lo -= sh_before;
+    __syncthreads();
+  }
+  // digit 2: bits 8..19 inside each bin
+  for (int i = threadIdx.x; i < kBins; i += blockDim.x) { h_hi[i] = 0; h_lo[i] = 0; }
+  __syncthreads();
+  for (int j = threadIdx.x; j < S; j += blockDim.x) {
+    const uint32_t key = ks[j];
+    const int top = static_cast<int>(key >> 20), d = static_cast<int>((key >> 8) & 0xfffu);
+    hist_add(h_hi, has_hi && top == b_hi ? d : -1);
+    hist_add(h_lo, has_lo && top == b_lo ? d : -1);
+  }
+  __syncthreads();
+  uint32_t hi32 = 0xffffffffu, lo32 = 0;
+  if (has_hi) {
+    find_bucket([&](int i) { return static_cast<unsigned long long>(h_hi[i]); }, kBins, w_hi, &sh_bin, &sh_before,
+                &sh_count, wsum);
+    hi32 = (static_cast<uint32_t>(b_hi) << 20) | (static_cast<uint32_t>(sh_bin) << 8) | 0xffu;
+    __syncthreads();
+  }
+  if (has_lo) {
+    find_bucket([&](int i) { return static_cast<unsigned long long>(h_lo[i]); }, kBins, w_lo, &sh_bin, &sh_before,
+                &sh_count, wsum);
+    lo32 = (static_cast<uint32_t>(b_lo) << 20) | (static_cast<uint32_t>(sh_bin) << 8);
+  }
+  if (ra.force_fallback) hi32 = lo32 = 0;  // test hook: an invalid bracket
+  if (threadIdx.x == 0) {
+    s.hi32 = hi32;
+    s.lo32 = lo32;
+  }
+}
+
+// v[j] for a run-time j without local memory: a 4-level select tree.
+__device__ __forceinline__ float pick16(const float (&v)[16], int j) {
+  float a[8], c[4], d[2];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = (j & 1) ? v[2 * k + 1] : v[2 * k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k] = (j & 2) ? a[2 * k + 1] : a[2 * k];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) d[k] = (j & 4) ? c[2 * k + 1] : c[2 * k];
+  return (j & 8) ? d[1] : d[0];
+}
+
+// grid (tiles, batch * nr): one full read of the range; sure (key32 > hi32) and
+// candidate (lo32 <= key32 <= hi32) entries are compacted in index order into the
+// list.  A tile is 16384 elements (64 per thread, as flag bits), so the look-back is
+// amortised and several tiles stay resident per SM.
+// Fast phase (branch-free): the listed set is {|d| >= B0}, B0 the double whose top
+// word is lo32 (d the fp64 residual).  f = |e - s| in fp32 is within 2^-24 relative of
+// the exact difference, so f < B0 (1 - 2^-22) proves "not listed"; the rest (the
+// ~1-2% listed plus a 2^-22-wide band) are marked "maybe" and reclassified in fp64
+// from the registers; the first listed residuals of a lane are stashed in shared
+// memory for the write.  The last tile validates the
+// bracket from the exact totals.
+__global__ void __launch_bounds__(kTileThreads, 4) sr_split_kernel(EncBatch batch, int bf16,
+                                                                   const float* __restrict__ shared, RangeArgs ra,
+                                                                   WsView ws) {
+  const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
+  SelState& s = ws.st(b, r);
+  if (s.mode != kModeList) return;
+  constexpr int kStash = 4;  // first listed residuals of a lane, kept for the write
+  __shared__ int tile_sh;
+  __shared__ unsigned int wsp[8], wsu[8];
+  __shared__ unsigned long long excl_sp;
+  __shared__ double stash[kTileThreads * kStash];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) tile_sh = atomicAdd(&s.ticket, 1);
+  __syncthreads();
+  const int tile = tile_sh;
+  const int64_t lo = pick(ra.lo, r), hi = pick(ra.hi, r);
+  const int64_t ntiles = (hi - lo + kSplitTile - 1) / kSplitTile;
+  if (tile >= ntiles) return;
+  const void* expert = batch.expert[b];
+  const bool vec = (lo & 3) == 0;
+  const uint32_t lo32 = s.lo32, hi32 = s.hi32;
+  // fp32 "surely below B0" threshold; outside [2^-100, 2^126] every element is exact
+  const double b0 = __hiloint2double(static_cast<int>(lo32), 0);
+  const float t_below = (b0 >= 0x1p-100 && b0 <= 0x1p126) ? __double2float_rd(b0 * (1.0 - 0x1p-22)) : -1.0f;
+  const int64_t base = lo + static_cast<int64_t>(tile) * kSplitTile + warp * (kSplitPer * 32);
+  constexpr int kSteps = kSplitPer / 4;  // 128 elements per warp step
+  // bit 4*it+q of a lane's masks: element base + 128 it + 4 lane + q
+  unsigned long long fsu = 0, fsp = 0;
+  double* my_stash = stash + threadIdx.x * kStash;
+  int nst = 0;
+#pragma unroll 1
+  for (int grp = 0; grp < kSteps / 4; ++grp) {
+    float e[16], sv[16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i0 = base + (grp * 4 + u) * 128 + 4 * lane;
+      if (vec && i0 + 3 < hi) {
+        const float4 s4 = *reinterpret_cast<const float4*>(shared + i0);
+        sv[4 * u] = s4.x; sv[4 * u + 1] = s4.y; sv[4 * u + 2] = s4.z; sv[4 * u + 3] = s4.w;
+        if (bf16) {
+          const uint2 raw = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(expert) + i0);
+          e[4 * u] = bf16_lo(raw.x); e[4 * u + 1] = bf16_hi(raw.x);
+          e[4 * u + 2] = bf16_lo(raw.y); e[4 * u + 3] = bf16_hi(raw.y);
+        } else {
+          const float4 ev = *reinterpret_cast<const float4*>(static_cast<const float*>(expert) + i0);
+          e[4 * u] = ev.x; e[4 * u + 1] = ev.y; e[4 * u + 2] = ev.z; e[4 * u + 3] = ev.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool in = i0 + q < hi;
+          sv[4 * u + q] = in ? shared[i0 + q] : 0.f;
+          e[4 * u + q] = in ? (bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(expert)[i0 + q])
+                                    : static_cast<const float*>(expert)[i0 + q])
+                            : 0.f;
+        }
+      }
+    }
+    unsigned int m = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) m |= static_cast<unsigned int>(!(fabsf(e[j] - sv[j]) < t_below)) << j;
+    // exact phase over this group's maybe elements (register select, no reload)
+    for (; m; m &= m - 1) {
+      const int j = __ffs(m) - 1, bit = 16 * grp + j;
+      const int64_t i = base + (bit >> 2) * 128 + 4 * lane + (bit & 3);
+      if (i >= hi) continue;
+      const double rr = __dsub_rn(static_cast<double>(pick16(e, j)), static_cast<double>(pick16(sv, j)));
+      const uint32_t k32 = key32_of(rr);
+      if (k32 >= lo32) {
+        fsp |= 1ull << bit;
+        if (k32 > hi32) fsu |= 1ull << bit;
+        if (nst < kStash) my_stash[nst] = rr;
+        ++nst;
+      }
+    }
+  }
+
+  const unsigned int wu = __reduce_add_sync(0xffffffffu, __popcll(fsu));
+  const unsigned int wp = __reduce_add_sync(0xffffffffu, __popcll(fsp));
+  if (lane == 0) { wsu[warp] = wu; wsp[warp] = wp; }
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long tsu = 0, tsp = 0;
+    for (int w = 0; w < 8; ++w) { tsu += wsu[w]; tsp += wsp[w]; }
+    unsigned long long psu, psp;
+    lookback(ws.stat(b, r), tile, tsu, tsp, psu, psp);
+    if (lane == 0) {
+      excl_sp = psp;
+      if (tile == ntiles - 1) {  // exact totals: validate the bracket
+        const long long n_sure = static_cast<long long>(psu + tsu), n_super = static_cast<long long>(psp + tsp);
+        s.n_sure = n_sure;
+        s.n_super = n_super;
+        if (n_super <= ws.cap && n_sure < s.need0 && n_super >= s.need0) {
+          s.need = s.need0 - n_sure;
+          if (n_super == s.need0) s.done = 1;  // every candidate is taken
+          // every candidate shares the leading bits of lo32 and hi32: start the digits below
+          const int c = __clz(lo32 ^ hi32);  // >= 1 (bit 63 of a key is 0)
+          const unsigned long long msk = c >= 32 ? 0xffffffff00000000ull : (~0ull << (64 - c));
+          s.mask = msk;
+          s.prefix = (static_cast<unsigned long long>(hi32) << 32) & msk;
+          s.top = 64 - c;
+        } else {
+          s.mode = kModeFull;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (!wp) return;
+
+  // Write: position of (step it, lane, q) = warp base + listed entries of the warp in
+  // earlier steps + of lower lanes in step it + lower q of this lane.  Per-step lane
+  // counts (0..4) sit in 8-bit fields, 4 steps per word, and are scanned across lanes.
+  unsigned int cnt[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    unsigned int v = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      v |= static_cast<unsigned int>(__popc(static_cast<unsigned int>(fsp >> (4 * (4 * w + k))) & 0xfu)) << (8 * k);
+    cnt[w] = v;
+  }
+  unsigned int incl[4] = {cnt[0], cnt[1], cnt[2], cnt[3]};
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += o;
-  }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    unsigned long long w = wsum[lane];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const unsigned long long o = __shfl_up_sync(0xffffffffu, w, off);
-      if (lane >= off) w += o;
+    for (int w = 0; w < 4; ++w) {
+      const unsigned int o = __shfl_up_sync(0xffffffffu, incl[w], off);
+      if (lane >= off) incl[w] += o;
     }
-    wsum[lane] = w;
   }
-  __syncthreads();
-  if (warp) incl += wsum[warp - 1];
-  const long long need = s.need;
-  const long long excl = static_cast<long long>(incl - mine);
-  if (excl < need && static_cast<long long>(incl) >= need) {  // exactly one owner
-    long long before = excl;
-    for (int i = 0; i < per; ++i) {
-      const int b = nb - 1 - (t * per + i);
-      if (b < 0) break;
-      const long long c = s.hist[b];
-      if (before + c >= need) {
-        const long long rem = need - before;
-        s.prefix |= static_cast<unsigned long long>(b) << shift;
-        s.mask |= static_cast<unsigned long long>(nb - 1) << shift;
-        s.need = rem;
-        if (c == rem || pass == kPasses - 1) s.done = 1;
-        if ((s.keyor & ((1ull << shift) - 1ull)) == 0) {
-          // No key has a bit below this digit: the remaining bucket is all ties.
-          s.mask = ~0ull;
-          s.done = 1;
-        }
-        break;
+  unsigned long long run = excl_sp;
+  for (int w = 0; w < warp; ++w) run += wsp[w];
+  unsigned int step_base[kSteps];  // listed entries of the warp before each step
+  {
+    unsigned int acc = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const unsigned int tot = __shfl_sync(0xffffffffu, incl[w], 31);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        step_base[4 * w + k] = acc;
+        acc += (tot >> (8 * k)) & 0xffu;
       }
-      before += c;
     }
   }
-  __syncthreads();
-  for (int b = t; b < kBins; b += blockDim.x) s.hist[b] = 0;
+  double* lres = ws.lres(b, r);
+  uint32_t* lidx = ws.lidx(b, r);
+  int used = 0;
+  for (unsigned long long mm = fsp; mm; mm &= mm - 1) {
+    const int bit = __ffsll(static_cast<long long>(mm)) - 1;
+    const int it = bit >> 2, q = bit & 3;
+    const unsigned int lane_excl = ((incl[it >> 2] - cnt[it >> 2]) >> (8 * (it & 3))) & 0xffu;
+    const unsigned int in_lane = __popc(static_cast<unsigned int>(fsp >> (4 * it)) & ((1u << q) - 1u));
+    const unsigned long long pos = run + step_base[it] + lane_excl + in_lane;
+    const int64_t i = base + it * 128 + 4 * lane + q;
+    const double rr = used < kStash ? my_stash[used] : residual_at(expert, bf16, shared, i);
+    if (pos < static_cast<unsigned long long>(ws.cap)) {
+      lres[pos] = rr;
+      lidx[pos] = static_cast<uint32_t>(i - lo);
+    }
+    ++used;
+  }
 }
 
-// Ordered compaction of the selected entries of [lo, hi) into the wire (grid.y = expert):
-// per-tile counts, decoupled look-back for the tile's global prefix, then ballot ranks.
-__global__ void __launch_bounds__(kTileThreads) sr_compact_kernel(EncBatch batch, int bf16,
-                                                                  const float* __restrict__ shared, int64_t lo,
-                                                                  int64_t hi, WsView ws, int range, int64_t out_base,
-                                                                  uint32_t iw, uint32_t vw) {
-  const int bexp = blockIdx.y;
-  SelState& s = ws.st(bexp, range);
-  const void* expert = batch.expert[bexp];
-  uint8_t* wire = batch.wire[bexp];
+// grid (blocks, batch * nr): histogram of the current digit over the keys matching the
+// prefix (candidates of the list, or the full range), block-private in shared memory;
+// the last block to arrive picks the bucket of the need-th largest and resets the
+// global histogram for the next digit.
+__global__ void __launch_bounds__(kTileThreads) sr_select_kernel(EncBatch batch, int bf16,
+                                                                 const float* __restrict__ shared, RangeArgs ra,
+                                                                 WsView ws, int pass) {
+  const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
+  SelState& s = ws.st(b, r);
+  if (s.done) return;
+  __shared__ unsigned int sh[kBins];
+  __shared__ unsigned long long wsum[32];
+  __shared__ int sh_bin, sh_last;
+  __shared__ long long sh_before, sh_count;
+  const int mode = s.mode;
+  const unsigned long long mask = s.mask, prefix = s.prefix;
+  const int top = s.top, width = top < kDigitBits ? top : kDigitBits, shift = top - width;
+  const unsigned int dmask = (1u << width) - 1u;
+  const int64_t lo = pick(ra.lo, r), hi = pick(ra.hi, r);
+  const int64_t units = mode == kModeList ? s.n_super : hi - lo;
+  const int64_t chunk = static_cast<int64_t>(kTile);  // units per block per sweep
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * chunk;
+  const bool work = first < units;
+  unsigned long long kor = 0;
+  if (work) {
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    auto digit = [&](unsigned long long key, bool in) {
+      kor |= in ? key : 0ull;
+      return in && (key & mask) == prefix ? static_cast<int>((key >> shift) & dmask) : -1;
+    };
+    const int64_t sweep = static_cast<int64_t>(gridDim.x) * chunk;
+    if (mode == kModeList) {
+      const double* lres = ws.lres(b, r);
+      const uint32_t hi32 = s.hi32;
+      for (int64_t c0 = first; c0 < units; c0 += sweep) {
+        for (int it = 0; it < kPerThread / 4; ++it) {
+          const int64_t j0 = c0 + it * (kTileThreads * 4) + 4 * threadIdx.x;
+          double r4[4] = {0.0, 0.0, 0.0, 0.0};
+          if (j0 + 3 < units) {
+            const double2 a = *reinterpret_cast<const double2*>(lres + j0);
+            const double2 c = *reinterpret_cast<const double2*>(lres + j0 + 2);
+            r4[0] = a.x; r4[1] = a.y; r4[2] = c.x; r4[3] = c.y;
+          } else {
+            for (int q = 0; q < 4; ++q)
+              if (j0 + q < units) r4[q] = lres[j0 + q];
+          }
+          int d[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const unsigned long long key = key_of(r4[q]);
+            d[q] = digit(key, j0 + q < units && static_cast<uint32_t>(key >> 32) <= hi32);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) hist_add(sh, d[q]);
+        }
+      }
+    } else {
+      const void* expert = batch.expert[b];
+      const bool vec = (lo & 3) == 0;
+      for (int64_t c0 = first; c0 < units; c0 += sweep) {
+        for (int it = 0; it < kPerThread / 4; ++it) {
+          const int64_t i0 = lo + c0 + it * (kTileThreads * 4) + 4 * threadIdx.x;
+          double r4[4];
+          load_res4(expert, bf16, shared, i0, hi, vec, r4);
+          int d[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) d[q] = digit(key_of(r4[q]), i0 + q < hi);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) hist_add(sh, d[q]);
+        }
+      }
+    }
+    if (pass == 0) {
+      const unsigned int lo_w = __reduce_or_sync(0xffffffffu, static_cast<unsigned int>(kor));
+      const unsigned int hi_w = __reduce_or_sync(0xffffffffu, static_cast<unsigned int>(kor >> 32));
+      if ((threadIdx.x & 31) == 0 && (lo_w | hi_w))
+        atomicOr(&s.keyor, (static_cast<unsigned long long>(hi_w) << 32) | lo_w);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x)
+      if (sh[i]) atomicAdd(&s.hist[i], sh[i]);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) sh_last = atomicAdd(&s.arrive, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!sh_last) return;
+  __threadfence();
+  const int nb = 1 << width;
+  const long long need = s.need;
+  // the global histogram -> shared memory in one coalesced sweep, then the scan
+  for (int i = threadIdx.x; i < nb / 4; i += blockDim.x)
+    reinterpret_cast<uint4*>(sh)[i] = __ldcg(reinterpret_cast<const uint4*>(s.hist) + i);
+  if (nb < 4 && threadIdx.x < nb) sh[threadIdx.x] = __ldcg(&s.hist[threadIdx.x]);
+  __syncthreads();
+  find_bucket([&](int i) { return static_cast<unsigned long long>(sh[i]); }, nb, need, &sh_bin, &sh_before,
+              &sh_count, wsum);
+  if (threadIdx.x == 0) {
+    const int bin = sh_bin;
+    const long long rem = need - sh_before;
+    s.prefix |= static_cast<unsigned long long>(bin) << shift;
+    s.mask |= static_cast<unsigned long long>(nb - 1) << shift;
+    s.need = rem;
+    s.top = shift;
+    if (sh_count == rem || shift == 0) s.done = 1;
+    if ((__ldcg(&s.keyor) & ((1ull << shift) - 1ull)) == 0) {
+      // No key has a bit below this digit: the remaining bucket is all ties.
+      s.mask = ~0ull;
+      s.done = 1;
+    }
+    s.arrive = 0;
+  }
+  for (int i = threadIdx.x; i < kBins / 4; i += blockDim.x) reinterpret_cast<uint4*>(s.hist)[i] = make_uint4(0, 0, 0, 0);
+}
+
+// grid (blocks, batch * nr), persistent over tiles taken in ticket order: ordered
+// compaction of the selected entries of the list (or of the full range) into the wire.
+// Selected: sure, or (key & mask) > prefix, or a threshold tie among the first `need`.
+__global__ void __launch_bounds__(kTileThreads) sr_emit_kernel(EncBatch batch, int bf16,
+                                                               const float* __restrict__ shared, RangeArgs ra,
+                                                               WsView ws, uint32_t iw, uint32_t vw) {
+  const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
+  SelState& s = ws.st(b, r);
+  if (s.need0 == 0) return;
   __shared__ int tile_sh;
   __shared__ unsigned int wgt[8], weq[8];
   __shared__ unsigned long long excl_gt_sh, excl_eq_sh;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) tile_sh = atomicAdd(&s.ticket, 1);
-  __syncthreads();
-  const int tile = tile_sh;
-  const int64_t base = lo + static_cast<int64_t>(tile) * kTile + warp * (kPerThread * 32);
+  constexpr int kSteps = kPerThread / 4;
+  const int mode = s.mode;
   const unsigned long long mask = s.mask, prefix = s.prefix;
   const long long need = s.need;
-
-  float rv[kPerThread];  // (float)r for 32-bit wires; 64-bit wires recompute r
-  unsigned int bgt[kPerThread], beq[kPerThread];
-  unsigned int cgt = 0, ceq = 0;
-#pragma unroll
-  for (int it = 0; it < kPerThread; ++it) {
-    const int64_t i = base + it * 32 + lane;
-    bool gt = false, eq = false;
-    rv[it] = 0.f;
-    if (i < hi) {
-      const double r = residual_at(expert, bf16, shared, i);
-      rv[it] = __double2float_rn(r);
-      const unsigned long long km = key_of(r) & mask;
-      gt = km > prefix;
-      eq = km == prefix;
-    }
-    bgt[it] = __ballot_sync(0xffffffffu, gt);
-    beq[it] = __ballot_sync(0xffffffffu, eq);
-    cgt += __popc(bgt[it]);
-    ceq += __popc(beq[it]);
-  }
-  if (lane == 0) { wgt[warp] = cgt; weq[warp] = ceq; }
-  __syncthreads();
-
-  unsigned long long* status = ws.stat(bexp, range);
-  if (warp == 0) {
-    // Decoupled look-back, a 32-tile window per step (one predecessor per lane): with
-    // ~1000 resident tiles a serial walk would chain hundreds of dependent L2 reads.
-    constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 31) - 1;
-    unsigned long long tgt = 0, teq = 0;
-    for (int w = 0; w < 8; ++w) { tgt += wgt[w]; teq += weq[w]; }
-    unsigned long long pgt = 0, peq = 0;
-    if (tile == 0) {
-      if (lane == 0) atomicExch(&status[0], kInc | (tgt << 31) | teq);
-    } else {
-      if (lane == 0) atomicExch(&status[tile], kAgg | (tgt << 31) | teq);
-      for (int t0 = tile - 1; t0 >= 0; t0 -= 32) {
-        const int t = t0 - lane;
-        unsigned long long w = 0;
-        if (t >= 0) {
-          do { w = *reinterpret_cast<volatile unsigned long long*>(&status[t]); } while ((w >> 62) == 0);
-        }
-        const unsigned int inc = __ballot_sync(0xffffffffu, t >= 0 && (w >> 62) == 2);
-        const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest predecessor with an inclusive prefix
-        unsigned long long g = (t >= 0 && lane <= stop) ? (w >> 31) & kVal : 0;
-        unsigned long long e = (t >= 0 && lane <= stop) ? w & kVal : 0;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          g += __shfl_xor_sync(0xffffffffu, g, off);
-          e += __shfl_xor_sync(0xffffffffu, e, off);
-        }
-        pgt += g;
-        peq += e;
-        if (inc) break;
-      }
-      if (lane == 0) {
-        __threadfence();
-        atomicExch(&status[tile], kInc | ((pgt + tgt) << 31) | (peq + teq));
-      }
-    }
-    if (lane == 0) {
-      excl_gt_sh = pgt;
-      excl_eq_sh = peq;
-    }
-  }
-  __syncthreads();
-
-  unsigned long long run_gt = excl_gt_sh, run_eq = excl_eq_sh;
-  for (int w = 0; w < warp; ++w) { run_gt += wgt[w]; run_eq += weq[w]; }
-  const unsigned int lt = (1u << lane) - 1u;
+  const uint32_t hi32 = s.hi32;
+  const int64_t lo = pick(ra.lo, r), hi = pick(ra.hi, r);
+  const int64_t units = mode == kModeList ? s.n_super : hi - lo;
+  const int64_t ntiles = (units + kTile - 1) / kTile;
+  const void* expert = batch.expert[b];
+  const bool vec = (lo & 3) == 0;
+  const double* lres = ws.lres(b, r);
+  const uint32_t* lidx = ws.lidx(b, r);
+  uint8_t* wire = batch.wire[b];
   const int eb = static_cast<int>((iw + vw) / 8);
+  const int64_t out_base = pick(ra.out_base, r);
+
+  for (;;) {
+    if (threadIdx.x == 0) tile_sh = atomicAdd(&s.ticket2, 1);
+    __syncthreads();
+    const int tile = tile_sh;
+    if (tile >= ntiles) break;
+    const int64_t base = static_cast<int64_t>(tile) * kTile + warp * (kPerThread * 32);  // unit offset
+
+    double rv[kPerThread];
+    uint32_t ix[kPerThread];
+    unsigned int fl[kSteps];  // bits 0-3 gt, 4-7 eq
+    unsigned int cgt = 0, ceq = 0;
 #pragma unroll
-  for (int it = 0; it < kPerThread; ++it) {
-    const bool gt = (bgt[it] >> lane) & 1u, eq = (beq[it] >> lane) & 1u;
-    const unsigned long long gbefore = run_gt + __popc(bgt[it] & lt);
-    const unsigned long long ebefore = run_eq + __popc(beq[it] & lt);
-    if (gt || (eq && static_cast<long long>(ebefore) < need)) {
-      const unsigned long long taken_eq =
-          static_cast<long long>(ebefore) < need ? ebefore : static_cast<unsigned long long>(need);
-      const int64_t j = out_base + static_cast<int64_t>(gbefore + taken_eq);
-      uint8_t* p = wire + 28 + j * eb;
-      const uint64_t idx = static_cast<uint64_t>(base + it * 32 + lane);
-      put_u32(p, static_cast<uint32_t>(idx));
-      if (iw == 64) { put_u32(p + 4, static_cast<uint32_t>(idx >> 32)); p += 8; } else { p += 4; }
-      if (vw == 32) {
-        put_u32(p, __float_as_uint(rv[it]));
+    for (int it = 0; it < kSteps; ++it) {
+      const int64_t u0 = base + it * 128 + 4 * lane;
+      double r4[4] = {0.0, 0.0, 0.0, 0.0};
+      uint32_t i4[4] = {0u, 1u, 2u, 3u};
+      if (mode == kModeList) {
+        if (u0 + 3 < units) {
+          const double2 a = *reinterpret_cast<const double2*>(lres + u0);
+          const double2 c = *reinterpret_cast<const double2*>(lres + u0 + 2);
+          const uint4 iv = *reinterpret_cast<const uint4*>(lidx + u0);
+          r4[0] = a.x; r4[1] = a.y; r4[2] = c.x; r4[3] = c.y;
+          i4[0] = iv.x; i4[1] = iv.y; i4[2] = iv.z; i4[3] = iv.w;
+        } else {
+          for (int q = 0; q < 4; ++q)
+            if (u0 + q < units) { r4[q] = lres[u0 + q]; i4[q] = lidx[u0 + q]; }
+        }
       } else {
-        const double r = residual_at(expert, bf16, shared, static_cast<int64_t>(idx));
-        const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(r));
-        put_u32(p, static_cast<uint32_t>(b));
-        put_u32(p + 4, static_cast<uint32_t>(b >> 32));
+        load_res4(expert, bf16, shared, lo + u0, hi, vec, r4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) i4[q] = static_cast<uint32_t>(u0 + q);
       }
-    }
-    run_gt += __popc(bgt[it]);
-    run_eq += __popc(beq[it]);
-  }
-}
-
-// Vectorised compaction (range start 4-aligned): lane l of a warp handles 4 consecutive
-// elements per 128-element step, so the per-element work is a float4 load pair, the key
-// test and a nibble of flags; in-warp ranks come from one packed (gt, eq) prefix scan.
-__global__ void __launch_bounds__(kTileThreads) sr_compact4_kernel(EncBatch batch, int bf16,
-                                                                   const float* __restrict__ shared, int64_t lo,
-                                                                   int64_t hi, WsView ws, int range, int64_t out_base,
-                                                                   uint32_t iw, uint32_t vw) {
-  constexpr int kSteps = kPerThread / 4;  // 4 steps x 128 elements = 512 per warp
-  const int bexp = blockIdx.y;
-  SelState& s = ws.st(bexp, range);
-  const void* expert = batch.expert[bexp];
-  uint8_t* wire = batch.wire[bexp];
-  __shared__ int tile_sh;
-  __shared__ unsigned int wgt[8], weq[8];
-  __shared__ unsigned long long excl_gt_sh, excl_eq_sh;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) tile_sh = atomicAdd(&s.ticket, 1);
-  __syncthreads();
-  const int tile = tile_sh;
-  const int64_t base = lo + static_cast<int64_t>(tile) * kTile + warp * (kPerThread * 32);
-  const unsigned long long mask = s.mask, prefix = s.prefix;
-  const long long need = s.need;
-
-  float rv[kPerThread];
-  unsigned int fl[kSteps];  // bits 0-3: gt of the 4 elements, bits 4-7: eq
-  unsigned int cgt = 0, ceq = 0;
-#pragma unroll
-  for (int it = 0; it < kSteps; ++it) {
-    const int64_t i0 = base + it * 128 + 4 * lane;
-    float e4[4] = {0.f, 0.f, 0.f, 0.f}, s4[4] = {0.f, 0.f, 0.f, 0.f};
-    if (i0 + 3 < hi) {
-      const float4 sv = *reinterpret_cast<const float4*>(shared + i0);
-      s4[0] = sv.x; s4[1] = sv.y; s4[2] = sv.z; s4[3] = sv.w;
-      if (bf16) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(expert) + i0);
-        e4[0] = bf16_lo(raw.x); e4[1] = bf16_hi(raw.x); e4[2] = bf16_lo(raw.y); e4[3] = bf16_hi(raw.y);
-      } else {
-        const float4 ev = *reinterpret_cast<const float4*>(static_cast<const float*>(expert) + i0);
-        e4[0] = ev.x; e4[1] = ev.y; e4[2] = ev.z; e4[3] = ev.w;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (i0 + q < hi) {
-          s4[q] = shared[i0 + q];
-          e4[q] = bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(expert)[i0 + q])
-                       : static_cast<const float*>(expert)[i0 + q];
-        }
-    }
-    unsigned int f = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double r = __dsub_rn(static_cast<double>(e4[q]), static_cast<double>(s4[q]));
-      rv[it * 4 + q] = __double2float_rn(r);
-      const unsigned long long km = key_of(r) & mask;
-      const bool in = i0 + q < hi;
-      f |= (in && km > prefix ? 1u : 0u) << q;
-      f |= (in && km == prefix ? 1u : 0u) << (4 + q);
-    }
-    fl[it] = f;
-    cgt += __popc(f & 0xfu);
-    ceq += __popc(f >> 4);
-  }
-  const unsigned int wg = __reduce_add_sync(0xffffffffu, cgt), we = __reduce_add_sync(0xffffffffu, ceq);
-  if (lane == 0) { wgt[warp] = wg; weq[warp] = we; }
-  __syncthreads();
-
-  unsigned long long* status = ws.stat(bexp, range);
-  if (warp == 0) {
-    constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 31) - 1;
-    unsigned long long tgt = 0, teq = 0;
-    for (int w = 0; w < 8; ++w) { tgt += wgt[w]; teq += weq[w]; }
-    unsigned long long pgt = 0, peq = 0;
-    if (tile == 0) {
-      if (lane == 0) atomicExch(&status[0], kInc | (tgt << 31) | teq);
-    } else {
-      if (lane == 0) atomicExch(&status[tile], kAgg | (tgt << 31) | teq);
-      for (int t0 = tile - 1; t0 >= 0; t0 -= 32) {
-        const int t = t0 - lane;
-        unsigned long long w = 0;
-        if (t >= 0) {
-          do { w = *reinterpret_cast<volatile unsigned long long*>(&status[t]); } while ((w >> 62) == 0);
-        }
-        const unsigned int inc = __ballot_sync(0xffffffffu, t >= 0 && (w >> 62) == 2);
-        const int stop = inc ? __ffs(inc) - 1 : 31;
-        unsigned long long g = (t >= 0 && lane <= stop) ? (w >> 31) & kVal : 0;
-        unsigned long long e = (t >= 0 && lane <= stop) ? w & kVal : 0;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          g += __shfl_xor_sync(0xffffffffu, g, off);
-          e += __shfl_xor_sync(0xffffffffu, e, off);
-        }
-        pgt += g;
-        peq += e;
-        if (inc) break;
-      }
-      if (lane == 0) {
-        __threadfence();
-        atomicExch(&status[tile], kInc | ((pgt + tgt) << 31) | (peq + teq));
-      }
-    }
-    if (lane == 0) {
-      excl_gt_sh = pgt;
-      excl_eq_sh = peq;
-    }
-  }
-  __syncthreads();
-
-  unsigned long long run_gt = excl_gt_sh, run_eq = excl_eq_sh;
-  for (int w = 0; w < warp; ++w) { run_gt += wgt[w]; run_eq += weq[w]; }
-  const int eb = static_cast<int>((iw + vw) / 8);
-#pragma unroll
-  for (int it = 0; it < kSteps; ++it) {
-    const unsigned int f = fl[it];
-    // exclusive in-warp prefix of (gt count << 16 | eq count)
-    const unsigned int mine = (static_cast<unsigned int>(__popc(f & 0xfu)) << 16) | __popc(f >> 4);
-    unsigned int incl = mine;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += o;
-    }
-    const unsigned int total = __shfl_sync(0xffffffffu, incl, 31);
-    unsigned long long gb = run_gt + ((incl - mine) >> 16);
-    unsigned long long ebf = run_eq + ((incl - mine) & 0xffffu);
-    if (f) {
+      unsigned int f = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const bool gt = (f >> q) & 1u, eq = (f >> (4 + q)) & 1u;
-        if (gt || (eq && static_cast<long long>(ebf) < need)) {
-          const unsigned long long taken_eq =
-              static_cast<long long>(ebf) < need ? ebf : static_cast<unsigned long long>(need);
-          const int64_t j = out_base + static_cast<int64_t>(gb + taken_eq);
-          uint8_t* p = wire + 28 + j * eb;
-          const uint64_t idx = static_cast<uint64_t>(base + it * 128 + 4 * lane + q);
-          put_u32(p, static_cast<uint32_t>(idx));
-          if (iw == 64) { put_u32(p + 4, static_cast<uint32_t>(idx >> 32)); p += 8; } else { p += 4; }
-          if (vw == 32) {
-            put_u32(p, __float_as_uint(rv[it * 4 + q]));
-          } else {
-            const double r = residual_at(expert, bf16, shared, static_cast<int64_t>(idx));
-            const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(r));
-            put_u32(p, static_cast<uint32_t>(b));
-            put_u32(p + 4, static_cast<uint32_t>(b >> 32));
-          }
-        }
-        gb += gt;
-        ebf += eq;
+        rv[it * 4 + q] = r4[q];
+        ix[it * 4 + q] = i4[q];
+        const unsigned long long key = key_of(r4[q]);
+        const bool in = u0 + q < units;
+        const bool sure = mode == kModeList && static_cast<uint32_t>(key >> 32) > hi32;
+        const unsigned long long km = key & mask;
+        f |= (in && (sure || km > prefix) ? 1u : 0u) << q;
+        f |= (in && !sure && km == prefix ? 1u : 0u) << (4 + q);
+      }
+      fl[it] = f;
+      cgt += __popc(f & 0xfu);
+      ceq += __popc(f >> 4);
+    }
+    const unsigned int wg = __reduce_add_sync(0xffffffffu, cgt), we = __reduce_add_sync(0xffffffffu, ceq);
+    if (lane == 0) { wgt[warp] = wg; weq[warp] = we; }
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long tgt = 0, teq = 0;
+      for (int w = 0; w < 8; ++w) { tgt += wgt[w]; teq += weq[w]; }
+      unsigned long long pgt, peq;
+      lookback(ws.stat2(b, r), tile, tgt, teq, pgt, peq);
+      if (lane == 0) {
+        excl_gt_sh = pgt;
+        excl_eq_sh = peq;
       }
     }
-    run_gt += total >> 16;
-    run_eq += total & 0xffffu;
+    __syncthreads();
+
+    unsigned long long run_gt = excl_gt_sh, run_eq = excl_eq_sh;
+    for (int w = 0; w < warp; ++w) { run_gt += wgt[w]; run_eq += weq[w]; }
+#pragma unroll
+    for (int it = 0; it < kSteps; ++it) {
+      const unsigned int f = fl[it];
+      unsigned int egt, eeq, tgt, teq;
+      warp_scan2(__popc(f & 0xfu), __popc(f >> 4), egt, eeq, tgt, teq);
+      unsigned long long gb = run_gt + egt, ebf = run_eq + eeq;
+      if (f) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool gt = (f >> q) & 1u, eq = (f >> (4 + q)) & 1u;
+          if (gt || (eq && static_cast<long long>(ebf) < need)) {
+            const unsigned long long taken_eq =
+                static_cast<long long>(ebf) < need ? ebf : static_cast<unsigned long long>(need);
+            const int64_t j = out_base + static_cast<int64_t>(gb + taken_eq);
+            uint8_t* p = wire + 28 + j * eb;
+            const uint64_t idx = static_cast<uint64_t>(lo) + ix[it * 4 + q];
+            put_u32(p, static_cast<uint32_t>(idx));
+            if (iw == 64) { put_u32(p + 4, static_cast<uint32_t>(idx >> 32)); p += 8; } else { p += 4; }
+            const double rr = rv[it * 4 + q];
+            if (vw == 32) {
+              put_u32(p, __float_as_uint(__double2float_rn(rr)));
+            } else {
+              const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(rr));
+              put_u32(p, static_cast<uint32_t>(bits));
+              put_u32(p + 4, static_cast<uint32_t>(bits >> 32));
+            }
+          }
+          gb += gt;
+          ebf += eq;
+        }
+      }
+      run_gt += tgt;
+      run_eq += teq;
+    }
+    __syncthreads();  // tile_sh / wgt / excl reuse
   }
 }
 
@@ -732,11 +1049,39 @@ __global__ void transpose_convert_kernel(const Tin* __restrict__ in, int64_t row
 
 }  // namespace
 
-int64_t sr_tiles(int64_t P) { return (P + kTile - 1) / kTile; }
+namespace {
+
+size_t round256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+// Per-(expert, range) workspace slot; tiles and list capacity sized for a range of the
+// whole expert (P elements), so one layout serves both wire layouts.
+WsView make_ws(void* base, int64_t P) {
+  WsView ws{};
+  ws.base = static_cast<uint8_t*>(base);
+  ws.tiles = (P + kTile - 1) / kTile;
+  ws.cap = std::min<int64_t>(P, P / 32 + 4096);
+  ws.off_stat = round256(sizeof(SelState));
+  ws.off_stat2 = ws.off_stat + round256(sizeof(unsigned long long) * ws.tiles);
+  ws.off_res = ws.off_stat2 + round256(sizeof(unsigned long long) * ws.tiles);
+  ws.off_idx = ws.off_res + round256(sizeof(double) * ws.cap);
+  ws.per = ws.off_idx + round256(sizeof(uint32_t) * ws.cap);
+  return ws;
+}
+
+// HEP_SR_SELECT=full forces the full-range select, =fallback an invalid sample bracket
+// (both exercise the fallback in tests); anything else picks per range.
+int select_override() {
+  const char* v = std::getenv("HEP_SR_SELECT");
+  if (!v) return 0;
+  if (!std::strcmp(v, "full")) return 1;
+  if (!std::strcmp(v, "fallback")) return 2;
+  return 0;
+}
+
+}  // namespace
 
 size_t sr_workspace_bytes(int64_t h, int64_t m, int batch) {
-  const int64_t tiles = sr_tiles(2 * h * m);
-  return static_cast<size_t>(batch) * 2 * (sizeof(SelState) + sizeof(unsigned long long) * tiles) + 256;
+  return static_cast<size_t>(batch) * 2 * make_ws(nullptr, 2 * h * m).per + 256;
 }
 
 cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, int batch, const float* shared,
@@ -748,46 +1093,65 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
     eb.expert[i] = experts[i];
     eb.wire[i] = wires[i];
   }
-  const int64_t tiles = sr_tiles(plan.total);
-  WsView ws{static_cast<SelState*>(workspace),
-            reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(workspace) + sizeof(SelState) * 2 * batch),
-            tiles};
+  const int64_t P = plan.total, up = plan.h * plan.m;
+  // 256-byte align the slots (the workspace pointer itself may be any cudaMalloc offset)
+  uint8_t* wbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+  const WsView ws = make_ws(wbase, P);
   const int bf16 = expert_dt == DType::BF16;
-  const int64_t up = plan.h * plan.m, P = plan.total;
-  struct Range { int64_t lo, hi, k, out_base; };
-  Range ranges[2];
-  int nr;
+  const int ovr = select_override();
+  RangeArgs ra{};
   if (plan.per_matrix) {
-    ranges[0] = {0, up, plan.k_up, 0};
-    ranges[1] = {up, P, plan.k_down, plan.k_up};
-    nr = 2;
+    ra.lo[0] = 0;  ra.hi[0] = up; ra.k[0] = plan.k_up;   ra.out_base[0] = 0;
+    ra.lo[1] = up; ra.hi[1] = P;  ra.k[1] = plan.k_down; ra.out_base[1] = plan.k_up;
+    ra.nr = 2;
   } else {
-    ranges[0] = {0, P, plan.k, 0};
-    ranges[1] = {0, 0, 0, 0};
-    nr = 1;
+    ra.lo[0] = 0; ra.hi[0] = P; ra.k[0] = plan.k; ra.out_base[0] = 0;
+    ra.nr = 1;
   }
-  sr_init_kernel<<<batch, 256, 0, stream>>>(ws, eb, ranges[0].hi - ranges[0].lo, ranges[0].k,
-                                            ranges[1].hi - ranges[1].lo, ranges[1].k, plan.h, plan.m, plan.k,
-                                            plan.index_bits, plan.value_bits);
-  for (int r = 0; r < nr; ++r) {
-    const int64_t n = ranges[r].hi - ranges[r].lo;
-    if (n <= 0) continue;
-    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 8 / batch, (n + 1023) / 1024)));
-    for (int pass = 0; pass < kPasses; ++pass) {
-      sr_hist_kernel<<<dim3(blocks, batch), 256, 0, stream>>>(eb, bf16, shared, ranges[r].lo, ranges[r].hi, ws, r,
-                                                               pass);
-      sr_select_kernel<<<batch, 1024, 0, stream>>>(ws, r, pass);
+  ra.force_fallback = ovr == 2;
+  bool any_list = false, any_full = false;
+  double expect_max = 0.0;
+  for (int r = 0; r < ra.nr; ++r) {
+    const int64_t n = pick(ra.hi, r) - pick(ra.lo, r), k = pick(ra.k, r);
+    bool full = ovr == 1 || n <= 0 || k <= 0 || k >= n || n >= (int64_t{1} << 31);
+    if (!full) {
+      // expected list size: k plus the sample's +-dev bracket scaled to the range
+      const double S = static_cast<double>(std::min<int64_t>(n, kSample)), q = static_cast<double>(k) / n;
+      const double dev = 4.0 * std::sqrt(q * S * (1.0 - q)) + 8.0;
+      const double expect = static_cast<double>(k) + 2.0 * dev / S * static_cast<double>(n);
+      full = expect > 0.75 * static_cast<double>(ws.cap);
+      if (!full) expect_max = std::max(expect_max, expect);
     }
-    const int ntiles = static_cast<int>((n + kTile - 1) / kTile);
-    if ((ranges[r].lo & 3) == 0)
-      sr_compact4_kernel<<<dim3(ntiles, batch), kTileThreads, 0, stream>>>(eb, bf16, shared, ranges[r].lo,
-                                                                            ranges[r].hi, ws, r, ranges[r].out_base,
-                                                                            plan.index_bits, plan.value_bits);
-    else
-      sr_compact_kernel<<<dim3(ntiles, batch), kTileThreads, 0, stream>>>(eb, bf16, shared, ranges[r].lo,
-                                                                           ranges[r].hi, ws, r, ranges[r].out_base,
-                                                                           plan.index_bits, plan.value_bits);
+    ra.full[r] = full;
+    any_list |= !full && k > 0;
+    any_full |= full && k > 0;
   }
+  const int slots = batch * ra.nr;
+  const int64_t nmax = std::max(ra.hi[0] - ra.lo[0], ra.nr > 1 ? ra.hi[1] - ra.lo[1] : int64_t{0});
+  const int64_t tiles_max = std::max<int64_t>(1, (nmax + kSplitTile - 1) / kSplitTile);
+  const int wide = std::max(1, 148 * 8 / slots);  // blocks per slot for full-range sweeps
+
+  sr_init_kernel<<<dim3(16, batch), 256, 0, stream>>>(ws, eb, ra, plan.h, plan.m, plan.k, plan.index_bits,
+                                                      plan.value_bits);
+  if (any_list) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(sr_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSampleSmem);
+      attr = true;
+    }
+    sr_sample_kernel<<<dim3(ra.nr, batch), kSampleThreads, kSampleSmem, stream>>>(eb, bf16, shared,
+                                                                                                  ra, ws);
+    sr_split_kernel<<<dim3(static_cast<unsigned>(tiles_max), slots), kTileThreads, 0, stream>>>(eb, bf16, shared,
+                                                                                                 ra, ws);
+  }
+  // A failed bracket falls back to the full range with the list-sized grid (rare);
+  // a statically full range gets the wide grid.
+  const int list_blocks = static_cast<int>(std::min<double>(wide, std::ceil(1.25 * expect_max / kTile)));
+  const int blocks = any_full ? std::max(wide, 1) : std::max(list_blocks, 1);
+  for (int pass = 0; pass < kPasses; ++pass)
+    sr_select_kernel<<<dim3(blocks, slots), kTileThreads, 0, stream>>>(eb, bf16, shared, ra, ws, pass);
+  sr_emit_kernel<<<dim3(blocks, slots), kTileThreads, 0, stream>>>(eb, bf16, shared, ra, ws, plan.index_bits,
+                                                                   plan.value_bits);
   return cudaGetLastError();
 }
 

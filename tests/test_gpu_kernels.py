@@ -104,7 +104,9 @@ def _demo_expert_pair(h, m, seed, quantize=False):
     (8, 8, None, 10 ** 9, 32, 32, False, False),
     (333, 77, 7.0, None, 64, 32, False, True),
 ])
-def test_sr_encode_decode_bitexact(h, m, ratio, k, iw, vw, per_matrix, quant):
+@pytest.mark.parametrize("select", ["auto", "full", "fallback"])
+def test_sr_encode_decode_bitexact(h, m, ratio, k, iw, vw, per_matrix, quant, select, monkeypatch):
+    monkeypatch.setenv("HEP_SR_SELECT", select)
     e, s = _demo_expert_pair(h, m, seed=h * 1000 + m, quantize=quant)
     want = oracle.sr_encode(e, s, h, m, ratio=ratio, k=k, iw=iw, vw=vw, per_matrix=per_matrix,
                             use_ref=oracle.ref is not None)
@@ -130,8 +132,10 @@ def test_sr_bf16_expert_upcast():
     assert wire.cpu().numpy().tobytes() == want.tobytes()
 
 
-def test_sr_cfg4_expert_bitexact():
+@pytest.mark.parametrize("select", ["auto", "fallback"])
+def test_sr_cfg4_expert_bitexact(select, monkeypatch):
     """Full cfg4 expert (H=2048, F=1408, P=5,767,168) at CR=50 against the reference."""
+    monkeypatch.setenv("HEP_SR_SELECT", select)
     h, m = 2048, 1408
     e, s = _demo_expert_pair(h, m, seed=11)
     want = oracle.sr_encode(e, s, h, m, ratio=50.0, use_ref=oracle.ref is not None)
@@ -181,9 +185,30 @@ def test_transpose_convert():
     assert torch.equal(out, x.T.contiguous().to(torch.bfloat16))
 
 
+@pytest.mark.parametrize("h,m,ratio,per_matrix,quant,bf16", [
+    (512, 1536, 50.0, True, False, True),    # sampled bracket (ranges >> 32768 keys)
+    (512, 1536, 50.0, False, False, False),
+    (512, 1536, 20.0, True, True, False),    # ~9 distinct |r|: list overflows -> full-range fallback
+    (300, 1001, 100.0, True, False, False),  # odd range start (unaligned second matrix)
+])
+def test_sr_encode_sampled_bracket(h, m, ratio, per_matrix, quant, bf16):
+    """Medium experts where the bracket comes from a sparse sample of each range."""
+    e, s = _demo_expert_pair(h, m, seed=h + m, quantize=quant)
+    et = torch.from_numpy(e)
+    if bf16:
+        et = et.to(torch.bfloat16)
+        e = et.float().numpy()
+    want = oracle.sr_encode(e, s, h, m, ratio=ratio, per_matrix=per_matrix, use_ref=oracle.ref is not None)
+    cfg = srmod.CompressionConfig(ratio_CR=ratio, per_matrix_budget=per_matrix)
+    wire = srmod.sr_encode(et.cuda(), torch.from_numpy(s).cuda(), h, m, cfg)
+    assert wire.cpu().numpy().tobytes() == want.tobytes()
+
+
 @pytest.mark.parametrize("per_matrix", [False, True])
-def test_sr_batched_encode_decode_bitexact(per_matrix):
+@pytest.mark.parametrize("select", ["auto", "full", "fallback"])
+def test_sr_batched_encode_decode_bitexact(per_matrix, select, monkeypatch):
     """One launch sequence for several experts (the layer encodes all owned experts at once)."""
+    monkeypatch.setenv("HEP_SR_SELECT", select)
     h, m, n = 40, 56, 5
     s = _demo_expert_pair(h, m, seed=99)[1]
     experts = [_demo_expert_pair(h, m, seed=100 + i, quantize=bool(i % 2))[0] for i in range(n)]
