@@ -50,8 +50,8 @@ constexpr int kTileThreads = 256;
 constexpr int kPerThread = 16;
 constexpr int kTile = kTileThreads * kPerThread;  // 4096 elements per compaction tile
 constexpr int kSample = 8192;                      // sampled keys per range
-constexpr int kSplitPer = 64;                      // split: elements per thread per tile
-constexpr int kSplitTile = kTileThreads * kSplitPer;
+constexpr int kSplitTile = 8192;                   // split: elements per tile (staged in shared memory)
+constexpr unsigned int kStageCap = kSplitTile / 16;  // staged list entries per split tile
 constexpr int kSampleThreads = 1024;
 constexpr int kSampleSmem = (kSample + 2 * kBins) * sizeof(unsigned int);
 
@@ -68,6 +68,7 @@ struct SelState {
   unsigned int lo32, hi32;   // candidate bracket on the top key word
   int done, mode;
   int top;  // bits [top, 63] of the threshold key are resolved (prefix/mask); next digit ends at top-1
+  int overflow;  // a split tile listed more than its staging segment holds
   int ticket, ticket2, arrive;
   alignas(16) unsigned int hist[kBins];
 };
@@ -86,7 +87,7 @@ __host__ __device__ __forceinline__ int64_t pick(const int64_t (&a)[2], int r) {
 // look-back words | list residuals (f64) | list indices (u32, relative to the range).
 struct WsView {
   uint8_t* base;
-  size_t per, off_stat, off_stat2, off_res, off_idx;
+  size_t per, off_stat, off_stat2, off_res, off_idx, off_sres, off_sidx, off_skeys;
   int64_t tiles, cap;
   __device__ uint8_t* slot(int b, int r) const { return base + (static_cast<size_t>(b) * 2 + r) * per; }
   __device__ SelState& st(int b, int r) const { return *reinterpret_cast<SelState*>(slot(b, r)); }
@@ -98,6 +99,11 @@ struct WsView {
   }
   __device__ double* lres(int b, int r) const { return reinterpret_cast<double*>(slot(b, r) + off_res); }
   __device__ uint32_t* lidx(int b, int r) const { return reinterpret_cast<uint32_t*>(slot(b, r) + off_idx); }
+  __device__ uint32_t* skeys(int b, int r) const { return reinterpret_cast<uint32_t*>(slot(b, r) + off_skeys); }
+  __device__ double* sres(int b, int r) const { return reinterpret_cast<double*>(slot(b, r) + off_sres); }
+  __device__ uint32_t* sidx(int b, int r) const { return reinterpret_cast<uint32_t*>(slot(b, r) + off_sidx); }
+  // listed count per split tile (the split look-back words are not used in list mode)
+  __device__ unsigned int* tcount(int b, int r) const { return reinterpret_cast<unsigned int*>(stat(b, r)); }
 };
 
 struct EncBatch {
@@ -269,10 +275,25 @@ __device__ __forceinline__ void warp_scan2(unsigned int a, unsigned int b, unsig
 
 // grid (16, batch): reset the selection state and look-back words of expert b's two
 // ranges, write its SRC1 header.
-__global__ void sr_init_kernel(WsView ws, EncBatch batch, RangeArgs ra, int64_t h, int64_t m, int64_t k_total,
-                               uint32_t iw, uint32_t vw) {
+__global__ void sr_init_kernel(WsView ws, EncBatch batch, int bf16, const float* __restrict__ shared, RangeArgs ra,
+                               int64_t h, int64_t m, int64_t k_total, uint32_t iw, uint32_t vw) {
   const int b = blockIdx.y, t = threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int r = 0; r < ra.nr; ++r) {
+    // list-mode range: its kSample evenly spaced keys, spread over the grid's blocks so
+    // the scattered DRAM reads are not limited by one SM's outstanding misses
+    const int64_t n = pick(ra.hi, r) - pick(ra.lo, r), k = pick(ra.k, r);
+    if ((r ? ra.full[1] : ra.full[0]) || k <= 0 || k >= n) continue;
+    const int S = static_cast<int>(n < kSample ? n : kSample);
+    const int64_t step = n / S, lo = pick(ra.lo, r);
+    uint32_t* keys = ws.skeys(b, r);
+    for (int j = blockIdx.x * blockDim.x + t; j < S; j += static_cast<int>(stride)) {
+      const int64_t i = lo + static_cast<int64_t>(j) * step;
+      const float e = bf16 ? __uint_as_float(static_cast<uint32_t>(__ldcs(static_cast<const unsigned short*>(batch.expert[b]) + i)) << 16)
+                           : __ldcs(static_cast<const float*>(batch.expert[b]) + i);
+      keys[j] = key32_of(__dsub_rn(static_cast<double>(e), static_cast<double>(__ldcs(shared + i))));
+    }
+  }
   for (int r = 0; r < 2; ++r) {
     SelState& s = ws.st(b, r);
     unsigned long long* s1 = ws.stat(b, r);
@@ -294,6 +315,7 @@ __global__ void sr_init_kernel(WsView ws, EncBatch batch, RangeArgs ra, int64_t 
       s.mode = (!live || s.done || (r ? ra.full[1] : ra.full[0])) ? kModeFull : kModeList;
       s.n_sure = 0;
       s.n_super = 0;
+      s.overflow = 0;
       s.keyor = 0;
       s.lo32 = 0;
       s.hi32 = 0xffffffffu;
@@ -314,13 +336,12 @@ __global__ void sr_init_kernel(WsView ws, EncBatch batch, RangeArgs ra, int64_t 
   }
 }
 
-// grid (nr, batch), 1024 threads: sample kSample evenly spaced keys of the range and
-// bracket the need-th largest key's top word between two sample order statistics,
+// grid (nr, batch), 1024 threads: from the kSample evenly spaced keys of the range
+// (gathered by sr_init_kernel), bracket the need-th largest key's top word between two
+// sample order statistics,
 // each located to 24 bits (a 12-bit digit, then 12 more bits inside its bin; the
 // bracket is widened to the bins' outer edges, so it only ever grows).
-__global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(EncBatch batch, int bf16,
-                                                                   const float* __restrict__ shared, RangeArgs ra,
-                                                                   WsView ws) {
+__global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(RangeArgs ra, WsView ws) {
   extern __shared__ unsigned int smem[];
   uint32_t* ks = smem;                    // kSample keys
   unsigned int* h_hi = smem + kSample;    // kBins
@@ -331,22 +352,10 @@ __global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(EncBatch batc
   const int r = blockIdx.x, b = blockIdx.y;
   SelState& s = ws.st(b, r);
   if (s.mode != kModeList) return;
-  const void* expert = batch.expert[b];
-  const int64_t lo = pick(ra.lo, r), n = pick(ra.hi, r) - lo;
+  const int64_t n = pick(ra.hi, r) - pick(ra.lo, r);
   const int S = static_cast<int>(n < kSample ? n : kSample);
-  constexpr int kPer = kSample / kSampleThreads;
-  const int64_t stride = n / S;  // evenly spaced over [0, S * stride), the tail < S elements
-  double rs[kPer];
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {  // all loads in flight at once
-    const int j = threadIdx.x + u * kSampleThreads;
-    rs[u] = j < S ? residual_at(expert, bf16, shared, lo + static_cast<int64_t>(j) * stride) : 0.0;
-  }
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const int j = threadIdx.x + u * kSampleThreads;
-    if (j < S) ks[j] = key32_of(rs[u]);
-  }
+  const uint32_t* gk = ws.skeys(b, r);  // sampled by sr_init_kernel across many SMs
+  for (int j = threadIdx.x; j < S; j += blockDim.x) ks[j] = gk[j];
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) h_hi[i] = 0;
   __syncthreads();
   const double q = static_cast<double>(s.need0) / static_cast<double>(n);
@@ -379,8 +388,10 @@ __global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(EncBatch batc
   for (int j = threadIdx.x; j < S; j += blockDim.x) {
     const uint32_t key = ks[j];
     const int top = static_cast<int>(key >> 20), d = static_cast<int>((key >> 8) & 0xfffu);
-    hist_add(h_hi, has_hi && top == b_hi ? d : -1);
-    hist_add(h_lo, has_lo && top == b_lo ? d : -1);
+    const bool in_hi = has_hi && top == b_hi, in_lo = has_lo && top == b_lo;
+    const unsigned int act = __activemask();
+    if (__any_sync(act, in_hi)) hist_add(h_hi, in_hi ? d : -1);  // most warps hold neither bin
+    if (__any_sync(act, in_lo)) hist_add(h_lo, in_lo ? d : -1);
   }
   __syncthreads();
   uint32_t hi32 = 0xffffffffu, lo32 = 0;
@@ -402,191 +413,244 @@ __global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(EncBatch batc
   }
 }
 
-// v[j] for a run-time j without local memory: a 4-level select tree.
-__device__ __forceinline__ float pick16(const float (&v)[16], int j) {
-  float a[8], c[4], d[2];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) a[k] = (j & 1) ? v[2 * k + 1] : v[2 * k];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) c[k] = (j & 2) ? a[2 * k + 1] : a[2 * k];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) d[k] = (j & 4) ? c[2 * k + 1] : c[2 * k];
-  return (j & 8) ? d[1] : d[0];
-}
-
-// grid (tiles, batch * nr): one full read of the range; sure (key32 > hi32) and
-// candidate (lo32 <= key32 <= hi32) entries are compacted in index order into the
-// list.  A tile is 16384 elements (64 per thread, as flag bits), so the look-back is
-// amortised and several tiles stay resident per SM.
-// Fast phase (branch-free): the listed set is {|d| >= B0}, B0 the double whose top
-// word is lo32 (d the fp64 residual).  f = |e - s| in fp32 is within 2^-24 relative of
-// the exact difference, so f < B0 (1 - 2^-22) proves "not listed"; the rest (the
-// ~1-2% listed plus a 2^-22-wide band) are marked "maybe" and reclassified in fp64
-// from the registers; the first listed residuals of a lane are stashed in shared
-// memory for the write.  The last tile validates the
-// bracket from the exact totals.
-__global__ void __launch_bounds__(kTileThreads, 4) sr_split_kernel(EncBatch batch, int bf16,
-                                                                   const float* __restrict__ shared, RangeArgs ra,
-                                                                   WsView ws) {
+// grid (tiles, batch * nr), 256 threads: one full read of the range.  A tile (8192
+// elements) is staged into shared memory by two bulk async copies (TMA engine, no
+// registers held in flight; plain loads for an unaligned range start and the last
+// < 8 elements), then classified from shared memory:
+//   fast phase (branch-free): the listed set is {|d| >= B0}, B0 the double whose top
+//   word is lo32 (d the fp64 residual).  f = |e - s| in fp32 is within 2^-24 relative
+//   of the exact difference, so f < B0 (1 - 2^-22) proves "not listed"; the rest (the
+//   ~1-2% listed plus a 2^-22-wide band) are marked "maybe" and reclassified in fp64.
+// Sure (key32 > hi32) and candidate (lo32 <= key32 <= hi32) entries of the tile are
+// written in index order into its fixed staging segment (kStageCap entries) with the
+// tile's count; totals accumulate atomically.  No tile waits on another; sr_pack_kernel
+// later packs the segments into the dense list.
+template <bool BULK>
+__global__ void __launch_bounds__(kTileThreads) sr_split_kernel(EncBatch batch, int bf16,
+                                                                const float* __restrict__ shared, RangeArgs ra,
+                                                                WsView ws) {
+  extern __shared__ __align__(128) uint8_t smem_split[];
+  float* s_sh = reinterpret_cast<float*>(smem_split);              // kSplitTile floats
+  uint8_t* s_ex = smem_split + kSplitTile * sizeof(float);          // kSplitTile bf16 or floats
+  __shared__ __align__(8) uint64_t full_bar;
+  __shared__ unsigned int wtot[8][2];                               // per-warp step counts (8-bit fields)
   const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
   SelState& s = ws.st(b, r);
   if (s.mode != kModeList) return;
-  constexpr int kStash = 4;  // first listed residuals of a lane, kept for the write
-  __shared__ int tile_sh;
-  __shared__ unsigned int wsp[8], wsu[8];
-  __shared__ unsigned long long excl_sp;
-  __shared__ double stash[kTileThreads * kStash];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) tile_sh = atomicAdd(&s.ticket, 1);
-  __syncthreads();
-  const int tile = tile_sh;
+  const int tile = blockIdx.x;
   const int64_t lo = pick(ra.lo, r), hi = pick(ra.hi, r);
-  const int64_t ntiles = (hi - lo + kSplitTile - 1) / kSplitTile;
-  if (tile >= ntiles) return;
+  const int64_t t_lo = lo + static_cast<int64_t>(tile) * kSplitTile;
+  if (t_lo >= hi) return;
+  const int count = static_cast<int>(hi - t_lo < kSplitTile ? hi - t_lo : kSplitTile);
   const void* expert = batch.expert[b];
-  const bool vec = (lo & 3) == 0;
+  const int eb = bf16 ? 2 : 4;
+  // bulk part: the first count8 elements (multiple of 8 = 16 B of bf16, 32 B of f32)
+  const int count8 = BULK ? (count & ~7) : 0;
+  if (BULK) {
+    if (threadIdx.x == 0) {
+      mbar_init(&full_bar, 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && count8) {
+      const uint64_t pol = l2_policy_evict_first();
+      mbar_arrive_expect_tx(&full_bar, static_cast<uint32_t>(count8 * (4 + eb)));
+      bulk_load(s_sh, shared + t_lo, static_cast<uint32_t>(count8 * 4), &full_bar, pol);
+      bulk_load(s_ex, static_cast<const uint8_t*>(expert) + t_lo * eb, static_cast<uint32_t>(count8 * eb), &full_bar,
+                pol);
+    }
+  }
+  for (int p = count8 + threadIdx.x; p < count; p += blockDim.x) {  // plain-load part
+    s_sh[p] = shared[t_lo + p];
+    if (bf16) reinterpret_cast<uint16_t*>(s_ex)[p] = static_cast<const uint16_t*>(expert)[t_lo + p];
+    else reinterpret_cast<float*>(s_ex)[p] = static_cast<const float*>(expert)[t_lo + p];
+  }
   const uint32_t lo32 = s.lo32, hi32 = s.hi32;
   // fp32 "surely below B0" threshold; outside [2^-100, 2^126] every element is exact
   const double b0 = __hiloint2double(static_cast<int>(lo32), 0);
   const float t_below = (b0 >= 0x1p-100 && b0 <= 0x1p126) ? __double2float_rd(b0 * (1.0 - 0x1p-22)) : -1.0f;
-  const int64_t base = lo + static_cast<int64_t>(tile) * kSplitTile + warp * (kSplitPer * 32);
-  constexpr int kSteps = kSplitPer / 4;  // 128 elements per warp step
-  // bit 4*it+q of a lane's masks: element base + 128 it + 4 lane + q
-  unsigned long long fsu = 0, fsp = 0;
-  double* my_stash = stash + threadIdx.x * kStash;
-  int nst = 0;
-#pragma unroll 1
-  for (int grp = 0; grp < kSteps / 4; ++grp) {
-    float e[16], sv[16];
+  if (BULK && count8) mbar_wait(&full_bar, 0);
+  __syncthreads();
+
+  // element p = 1024 it + 4 tid + q  ->  bit 4 it + q
+  constexpr int kSteps = kSplitTile / (kTileThreads * 4);  // 8
+  auto ex_at = [&](int p) {
+    return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(s_ex)[p]) : reinterpret_cast<const float*>(s_ex)[p];
+  };
+  uint32_t maybe = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t i0 = base + (grp * 4 + u) * 128 + 4 * lane;
-      if (vec && i0 + 3 < hi) {
-        const float4 s4 = *reinterpret_cast<const float4*>(shared + i0);
-        sv[4 * u] = s4.x; sv[4 * u + 1] = s4.y; sv[4 * u + 2] = s4.z; sv[4 * u + 3] = s4.w;
-        if (bf16) {
-          const uint2 raw = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(expert) + i0);
-          e[4 * u] = bf16_lo(raw.x); e[4 * u + 1] = bf16_hi(raw.x);
-          e[4 * u + 2] = bf16_lo(raw.y); e[4 * u + 3] = bf16_hi(raw.y);
-        } else {
-          const float4 ev = *reinterpret_cast<const float4*>(static_cast<const float*>(expert) + i0);
-          e[4 * u] = ev.x; e[4 * u + 1] = ev.y; e[4 * u + 2] = ev.z; e[4 * u + 3] = ev.w;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const bool in = i0 + q < hi;
-          sv[4 * u + q] = in ? shared[i0 + q] : 0.f;
-          e[4 * u + q] = in ? (bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(expert)[i0 + q])
-                                    : static_cast<const float*>(expert)[i0 + q])
-                            : 0.f;
-        }
-      }
+  for (int it = 0; it < kSteps; ++it) {
+    const int p0 = it * 1024 + 4 * threadIdx.x;
+    const float4 sv = *reinterpret_cast<const float4*>(s_sh + p0);
+    float e4[4];
+    if (bf16) {
+      const uint2 raw = *reinterpret_cast<const uint2*>(s_ex + p0 * 2);
+      e4[0] = bf16_lo(raw.x); e4[1] = bf16_hi(raw.x); e4[2] = bf16_lo(raw.y); e4[3] = bf16_hi(raw.y);
+    } else {
+      const float4 ev = *reinterpret_cast<const float4*>(s_ex + p0 * 4);
+      e4[0] = ev.x; e4[1] = ev.y; e4[2] = ev.z; e4[3] = ev.w;
     }
-    unsigned int m = 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) m |= static_cast<unsigned int>(!(fabsf(e[j] - sv[j]) < t_below)) << j;
-    // exact phase over this group's maybe elements (register select, no reload)
-    for (; m; m &= m - 1) {
-      const int j = __ffs(m) - 1, bit = 16 * grp + j;
-      const int64_t i = base + (bit >> 2) * 128 + 4 * lane + (bit & 3);
-      if (i >= hi) continue;
-      const double rr = __dsub_rn(static_cast<double>(pick16(e, j)), static_cast<double>(pick16(sv, j)));
-      const uint32_t k32 = key32_of(rr);
-      if (k32 >= lo32) {
-        fsp |= 1ull << bit;
-        if (k32 > hi32) fsu |= 1ull << bit;
-        if (nst < kStash) my_stash[nst] = rr;
-        ++nst;
-      }
+    maybe |= static_cast<uint32_t>(!(fabsf(e4[0] - sv.x) < t_below)) << (4 * it);
+    maybe |= static_cast<uint32_t>(!(fabsf(e4[1] - sv.y) < t_below)) << (4 * it + 1);
+    maybe |= static_cast<uint32_t>(!(fabsf(e4[2] - sv.z) < t_below)) << (4 * it + 2);
+    maybe |= static_cast<uint32_t>(!(fabsf(e4[3] - sv.w) < t_below)) << (4 * it + 3);
+  }
+  uint32_t fsp = 0, fsu = 0;
+  for (uint32_t mm = maybe; mm; mm &= mm - 1) {
+    const int bit = __ffs(mm) - 1;
+    const int p = (bit >> 2) * 1024 + 4 * threadIdx.x + (bit & 3);
+    if (p >= count) continue;
+    const double rr = __dsub_rn(static_cast<double>(ex_at(p)), static_cast<double>(s_sh[p]));
+    const uint32_t k32 = key32_of(rr);
+    if (k32 >= lo32) {
+      fsp |= 1u << bit;
+      if (k32 > hi32) fsu |= 1u << bit;
     }
   }
 
-  const unsigned int wu = __reduce_add_sync(0xffffffffu, __popcll(fsu));
-  const unsigned int wp = __reduce_add_sync(0xffffffffu, __popcll(fsp));
-  if (lane == 0) { wsu[warp] = wu; wsp[warp] = wp; }
-  __syncthreads();
-  if (warp == 0) {
-    unsigned long long tsu = 0, tsp = 0;
-    for (int w = 0; w < 8; ++w) { tsu += wsu[w]; tsp += wsp[w]; }
-    unsigned long long psu, psp;
-    lookback(ws.stat(b, r), tile, tsu, tsp, psu, psp);
-    if (lane == 0) {
-      excl_sp = psp;
-      if (tile == ntiles - 1) {  // exact totals: validate the bracket
-        const long long n_sure = static_cast<long long>(psu + tsu), n_super = static_cast<long long>(psp + tsp);
-        s.n_sure = n_sure;
-        s.n_super = n_super;
-        if (n_super <= ws.cap && n_sure < s.need0 && n_super >= s.need0) {
-          s.need = s.need0 - n_sure;
-          if (n_super == s.need0) s.done = 1;  // every candidate is taken
-          // every candidate shares the leading bits of lo32 and hi32: start the digits below
-          const int c = __clz(lo32 ^ hi32);  // >= 1 (bit 63 of a key is 0)
-          const unsigned long long msk = c >= 32 ? 0xffffffff00000000ull : (~0ull << (64 - c));
-          s.mask = msk;
-          s.prefix = (static_cast<unsigned long long>(hi32) << 32) & msk;
-          s.top = 64 - c;
-        } else {
-          s.mode = kModeFull;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (!wp) return;
-
-  // Write: position of (step it, lane, q) = warp base + listed entries of the warp in
-  // earlier steps + of lower lanes in step it + lower q of this lane.  Per-step lane
-  // counts (0..4) sit in 8-bit fields, 4 steps per word, and are scanned across lanes.
-  unsigned int cnt[4];
+  // per-step counts (0..4) in 8-bit fields, 4 steps per word, scanned across lanes
+  unsigned int cnt[2], incl[2];
 #pragma unroll
-  for (int w = 0; w < 4; ++w) {
+  for (int w = 0; w < 2; ++w) {
     unsigned int v = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      v |= static_cast<unsigned int>(__popc(static_cast<unsigned int>(fsp >> (4 * (4 * w + k))) & 0xfu)) << (8 * k);
-    cnt[w] = v;
+    for (int k = 0; k < 4; ++k) v |= static_cast<unsigned int>(__popc((fsp >> (4 * (4 * w + k))) & 0xfu)) << (8 * k);
+    cnt[w] = incl[w] = v;
   }
-  unsigned int incl[4] = {cnt[0], cnt[1], cnt[2], cnt[3]};
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < 2; ++w) {
       const unsigned int o = __shfl_up_sync(0xffffffffu, incl[w], off);
       if (lane >= off) incl[w] += o;
     }
   }
-  unsigned long long run = excl_sp;
-  for (int w = 0; w < warp; ++w) run += wsp[w];
-  unsigned int step_base[kSteps];  // listed entries of the warp before each step
-  {
-    unsigned int acc = 0;
+  const unsigned int nsu = __reduce_add_sync(0xffffffffu, __popc(fsu));
+  if (lane == 31) { wtot[warp][0] = incl[0]; wtot[warp][1] = incl[1]; }
+  __shared__ unsigned int wsu[8];
+  if (lane == 0) wsu[warp] = nsu;
+  __syncthreads();
+  // step s offset = all warps' entries in steps < s + lower warps' entries in step s
+  unsigned int step_off[kSteps];
+  unsigned int total = 0;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const unsigned int tot = __shfl_sync(0xffffffffu, incl[w], 31);
+  for (int st = 0; st < kSteps; ++st) {
+    unsigned int below = 0, all = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        step_base[4 * w + k] = acc;
-        acc += (tot >> (8 * k)) & 0xffu;
-      }
+    for (int w = 0; w < 8; ++w) {
+      const unsigned int c = (wtot[w][st >> 2] >> (8 * (st & 3))) & 0xffu;
+      all += c;
+      below += w < warp ? c : 0u;
     }
+    step_off[st] = total + below;
+    total += all;
   }
-  double* lres = ws.lres(b, r);
-  uint32_t* lidx = ws.lidx(b, r);
-  int used = 0;
-  for (unsigned long long mm = fsp; mm; mm &= mm - 1) {
-    const int bit = __ffsll(static_cast<long long>(mm)) - 1;
+  if (threadIdx.x == 0) {
+    unsigned int tsu = 0;
+    for (int w = 0; w < 8; ++w) tsu += wsu[w];
+    ws.tcount(b, r)[tile] = total;
+    if (tsu) atomicAdd(reinterpret_cast<unsigned long long*>(&s.n_sure), static_cast<unsigned long long>(tsu));
+    if (total) atomicAdd(reinterpret_cast<unsigned long long*>(&s.n_super), static_cast<unsigned long long>(total));
+    if (total > kStageCap) atomicOr(&s.overflow, 1);
+  }
+  double* sres = ws.sres(b, r) + static_cast<int64_t>(tile) * kStageCap;
+  uint32_t* sidx = ws.sidx(b, r) + static_cast<int64_t>(tile) * kStageCap;
+  for (uint32_t mm = fsp; mm; mm &= mm - 1) {
+    const int bit = __ffs(mm) - 1;
     const int it = bit >> 2, q = bit & 3;
     const unsigned int lane_excl = ((incl[it >> 2] - cnt[it >> 2]) >> (8 * (it & 3))) & 0xffu;
-    const unsigned int in_lane = __popc(static_cast<unsigned int>(fsp >> (4 * it)) & ((1u << q) - 1u));
-    const unsigned long long pos = run + step_base[it] + lane_excl + in_lane;
-    const int64_t i = base + it * 128 + 4 * lane + q;
-    const double rr = used < kStash ? my_stash[used] : residual_at(expert, bf16, shared, i);
-    if (pos < static_cast<unsigned long long>(ws.cap)) {
-      lres[pos] = rr;
-      lidx[pos] = static_cast<uint32_t>(i - lo);
+    const unsigned int pos = step_off[it] + lane_excl + __popc((fsp >> (4 * it)) & ((1u << q) - 1u));
+    const int p = it * 1024 + 4 * threadIdx.x + q;
+    if (pos < kStageCap) {
+      sres[pos] = __dsub_rn(static_cast<double>(ex_at(p)), static_cast<double>(s_sh[p]));
+      sidx[pos] = static_cast<uint32_t>(t_lo + p - lo);
     }
-    ++used;
+  }
+}
+
+// grid (batch * nr), 1024 threads: validate the bracket from the exact totals and turn
+// the tiles' listed counts into exclusive offsets in the dense list.
+__global__ void __launch_bounds__(1024) sr_scan_kernel(RangeArgs ra, WsView ws) {
+  const int r = blockIdx.x % ra.nr, b = blockIdx.x / ra.nr;
+  SelState& s = ws.st(b, r);
+  if (s.mode != kModeList) return;
+  __shared__ unsigned int wsum[32];
+  const long long n_sure = s.n_sure, n_super = s.n_super;
+  const bool valid = !s.overflow && n_super <= ws.cap && n_sure < s.need0 && n_super >= s.need0;
+  if (!valid) {
+    if (threadIdx.x == 0) s.mode = kModeFull;
+    return;
+  }
+  if (threadIdx.x == 0) {
+    const uint32_t lo32 = s.lo32, hi32 = s.hi32;
+    s.need = s.need0 - n_sure;
+    if (n_super == s.need0) s.done = 1;  // every candidate is taken
+    // every candidate shares the leading bits of lo32 and hi32: start the digits below
+    const int c = __clz(lo32 ^ hi32);  // >= 1 (bit 63 of a key is 0)
+    const unsigned long long msk = c >= 32 ? 0xffffffff00000000ull : (~0ull << (64 - c));
+    s.mask = msk;
+    s.prefix = (static_cast<unsigned long long>(hi32) << 32) & msk;
+    s.top = 64 - c;
+  }
+  const int64_t n = pick(ra.hi, r) - pick(ra.lo, r);
+  const int ntiles = static_cast<int>((n + kSplitTile - 1) / kSplitTile);
+  unsigned int* cnt = ws.tcount(b, r);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned int carry = 0;
+  for (int c0 = 0; c0 < ntiles; c0 += blockDim.x) {
+    const int t = c0 + threadIdx.x;
+    const unsigned int c = t < ntiles ? cnt[t] : 0u;
+    unsigned int incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned int w = wsum[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned int o = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += o;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const unsigned int wb = warp ? wsum[warp - 1] : 0u;
+    if (t < ntiles) cnt[t] = carry + wb + incl - c;  // exclusive offset
+    carry += wsum[31];
+    __syncthreads();
+  }
+}
+
+// grid (blocks, batch * nr): one warp per split tile copies its staged entries to the
+// tile's offset in the dense list.
+__global__ void __launch_bounds__(kTileThreads) sr_pack_kernel(RangeArgs ra, WsView ws) {
+  const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
+  SelState& s = ws.st(b, r);
+  if (s.mode != kModeList) return;
+  const int64_t n = pick(ra.hi, r) - pick(ra.lo, r);
+  const int ntiles = static_cast<int>((n + kSplitTile - 1) / kSplitTile);
+  const unsigned int* off = ws.tcount(b, r);
+  const long long n_super = s.n_super;
+  const int lane = threadIdx.x & 31;
+  double* lres = ws.lres(b, r);
+  uint32_t* lidx = ws.lidx(b, r);
+  const double* sres = ws.sres(b, r);
+  const uint32_t* sidx = ws.sidx(b, r);
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += warps) {
+    const unsigned int o = off[t];
+    const unsigned int c = (t + 1 < ntiles ? off[t + 1] : static_cast<unsigned int>(n_super)) - o;
+    const int64_t src = static_cast<int64_t>(t) * kStageCap;
+#pragma unroll 4
+    for (unsigned int j = lane; j < c; j += 32) {
+      lres[o + j] = sres[src + j];
+      lidx[o + j] = sidx[src + j];
+    }
   }
 }
 
@@ -626,25 +690,27 @@ __global__ void __launch_bounds__(kTileThreads) sr_select_kernel(EncBatch batch,
       const double* lres = ws.lres(b, r);
       const uint32_t hi32 = s.hi32;
       for (int64_t c0 = first; c0 < units; c0 += sweep) {
+        double rv[kPerThread];  // all loads first (in-order issue), then the digits
+#pragma unroll
         for (int it = 0; it < kPerThread / 4; ++it) {
           const int64_t j0 = c0 + it * (kTileThreads * 4) + 4 * threadIdx.x;
-          double r4[4] = {0.0, 0.0, 0.0, 0.0};
           if (j0 + 3 < units) {
             const double2 a = *reinterpret_cast<const double2*>(lres + j0);
             const double2 c = *reinterpret_cast<const double2*>(lres + j0 + 2);
-            r4[0] = a.x; r4[1] = a.y; r4[2] = c.x; r4[3] = c.y;
+            rv[4 * it] = a.x; rv[4 * it + 1] = a.y; rv[4 * it + 2] = c.x; rv[4 * it + 3] = c.y;
           } else {
-            for (int q = 0; q < 4; ++q)
-              if (j0 + q < units) r4[q] = lres[j0 + q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rv[4 * it + q] = j0 + q < units ? lres[j0 + q] : 0.0;
           }
-          int d[4];
+        }
+#pragma unroll
+        for (int it = 0; it < kPerThread / 4; ++it) {
+          const int64_t j0 = c0 + it * (kTileThreads * 4) + 4 * threadIdx.x;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const unsigned long long key = key_of(r4[q]);
-            d[q] = digit(key, j0 + q < units && static_cast<uint32_t>(key >> 32) <= hi32);
+            const unsigned long long key = key_of(rv[4 * it + q]);
+            hist_add(sh, digit(key, j0 + q < units && static_cast<uint32_t>(key >> 32) <= hi32));
           }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) hist_add(sh, d[q]);
         }
       }
     } else {
@@ -746,33 +812,41 @@ __global__ void __launch_bounds__(kTileThreads) sr_emit_kernel(EncBatch batch, i
     uint32_t ix[kPerThread];
     unsigned int fl[kSteps];  // bits 0-3 gt, 4-7 eq
     unsigned int cgt = 0, ceq = 0;
+    // all loads of the tile first (in-order issue), then the flags
 #pragma unroll
     for (int it = 0; it < kSteps; ++it) {
       const int64_t u0 = base + it * 128 + 4 * lane;
-      double r4[4] = {0.0, 0.0, 0.0, 0.0};
-      uint32_t i4[4] = {0u, 1u, 2u, 3u};
       if (mode == kModeList) {
         if (u0 + 3 < units) {
           const double2 a = *reinterpret_cast<const double2*>(lres + u0);
           const double2 c = *reinterpret_cast<const double2*>(lres + u0 + 2);
           const uint4 iv = *reinterpret_cast<const uint4*>(lidx + u0);
-          r4[0] = a.x; r4[1] = a.y; r4[2] = c.x; r4[3] = c.y;
-          i4[0] = iv.x; i4[1] = iv.y; i4[2] = iv.z; i4[3] = iv.w;
+          rv[it * 4] = a.x; rv[it * 4 + 1] = a.y; rv[it * 4 + 2] = c.x; rv[it * 4 + 3] = c.y;
+          ix[it * 4] = iv.x; ix[it * 4 + 1] = iv.y; ix[it * 4 + 2] = iv.z; ix[it * 4 + 3] = iv.w;
         } else {
-          for (int q = 0; q < 4; ++q)
-            if (u0 + q < units) { r4[q] = lres[u0 + q]; i4[q] = lidx[u0 + q]; }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            rv[it * 4 + q] = u0 + q < units ? lres[u0 + q] : 0.0;
+            ix[it * 4 + q] = u0 + q < units ? lidx[u0 + q] : 0u;
+          }
         }
       } else {
+        double r4[4];
         load_res4(expert, bf16, shared, lo + u0, hi, vec, r4);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) i4[q] = static_cast<uint32_t>(u0 + q);
+        for (int q = 0; q < 4; ++q) {
+          rv[it * 4 + q] = r4[q];
+          ix[it * 4 + q] = static_cast<uint32_t>(u0 + q);
+        }
       }
+    }
+#pragma unroll
+    for (int it = 0; it < kSteps; ++it) {
+      const int64_t u0 = base + it * 128 + 4 * lane;
       unsigned int f = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        rv[it * 4 + q] = r4[q];
-        ix[it * 4 + q] = i4[q];
-        const unsigned long long key = key_of(r4[q]);
+        const unsigned long long key = key_of(rv[it * 4 + q]);
         const bool in = u0 + q < units;
         const bool sure = mode == kModeList && static_cast<uint32_t>(key >> 32) > hi32;
         const unsigned long long km = key & mask;
@@ -1064,7 +1138,11 @@ WsView make_ws(void* base, int64_t P) {
   ws.off_stat2 = ws.off_stat + round256(sizeof(unsigned long long) * ws.tiles);
   ws.off_res = ws.off_stat2 + round256(sizeof(unsigned long long) * ws.tiles);
   ws.off_idx = ws.off_res + round256(sizeof(double) * ws.cap);
-  ws.per = ws.off_idx + round256(sizeof(uint32_t) * ws.cap);
+  const int64_t staged = (P + kSplitTile - 1) / kSplitTile * kStageCap;
+  ws.off_sres = ws.off_idx + round256(sizeof(uint32_t) * ws.cap);
+  ws.off_sidx = ws.off_sres + round256(sizeof(double) * staged);
+  ws.off_skeys = ws.off_sidx + round256(sizeof(uint32_t) * staged);
+  ws.per = ws.off_skeys + round256(sizeof(uint32_t) * kSample);
   return ws;
 }
 
@@ -1131,18 +1209,24 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
   const int64_t tiles_max = std::max<int64_t>(1, (nmax + kSplitTile - 1) / kSplitTile);
   const int wide = std::max(1, 148 * 8 / slots);  // blocks per slot for full-range sweeps
 
-  sr_init_kernel<<<dim3(16, batch), 256, 0, stream>>>(ws, eb, ra, plan.h, plan.m, plan.k, plan.index_bits,
-                                                      plan.value_bits);
+  sr_init_kernel<<<dim3(16, batch), 256, 0, stream>>>(ws, eb, bf16, shared, ra, plan.h, plan.m, plan.k,
+                                                      plan.index_bits, plan.value_bits);
   if (any_list) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(sr_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSampleSmem);
+      cudaFuncSetAttribute(sr_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 8);
+      cudaFuncSetAttribute(sr_split_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 8);
       attr = true;
     }
-    sr_sample_kernel<<<dim3(ra.nr, batch), kSampleThreads, kSampleSmem, stream>>>(eb, bf16, shared,
-                                                                                                  ra, ws);
-    sr_split_kernel<<<dim3(static_cast<unsigned>(tiles_max), slots), kTileThreads, 0, stream>>>(eb, bf16, shared,
-                                                                                                 ra, ws);
+    sr_sample_kernel<<<dim3(ra.nr, batch), kSampleThreads, kSampleSmem, stream>>>(ra, ws);
+    const bool bulk = ((ra.lo[0] | (ra.nr > 1 ? ra.lo[1] : 0)) & 7) == 0;
+    const int smem = kSplitTile * (4 + (bf16 ? 2 : 4));
+    const dim3 sgrid(static_cast<unsigned>(tiles_max), slots);
+    if (bulk) sr_split_kernel<true><<<sgrid, kTileThreads, smem, stream>>>(eb, bf16, shared, ra, ws);
+    else sr_split_kernel<false><<<sgrid, kTileThreads, smem, stream>>>(eb, bf16, shared, ra, ws);
+    sr_scan_kernel<<<slots, 1024, 0, stream>>>(ra, ws);
+    sr_pack_kernel<<<dim3(std::max(1, 148 * 4 / slots), slots), kTileThreads, 0, stream>>>(ra, ws);
   }
   // A failed bracket falls back to the full range with the list-sized grid (rare);
   // a statically full range gets the wide grid.
