@@ -35,6 +35,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -57,6 +59,7 @@ constexpr int kSampleSmem = (kSample + 2 * kBins) * sizeof(unsigned int);
 
 constexpr int kModeList = 0;  // select and emit over the sure + candidate list
 constexpr int kModeFull = 1;  // select and emit over the whole range (static choice or failed bracket)
+constexpr int kModeDone = 2;  // the wire range is written (sr_finish_kernel)
 
 struct SelState {
   unsigned long long prefix;
@@ -115,13 +118,6 @@ struct DecBatch {
   const uint8_t* wire[kMaxSrBatch];
   float* out[kMaxSrBatch];
 };
-
-__device__ __forceinline__ double residual_at(const void* expert, bool bf16, const float* shared,
-                                              int64_t i) {
-  const double e = bf16 ? static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(expert)[i]))
-                        : static_cast<double>(static_cast<const float*>(expert)[i]);
-  return __dsub_rn(e, static_cast<double>(shared[i]));
-}
 
 // Residuals of elements i0 .. i0+3 (0 past hi).  vec: i0 is 4-aligned, so one float4
 // of the shared expert and one 8- or 16-byte load of the expert cover the group.
@@ -423,8 +419,8 @@ __global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(RangeArgs ra,
 //   ~1-2% listed plus a 2^-22-wide band) are marked "maybe" and reclassified in fp64.
 // Sure (key32 > hi32) and candidate (lo32 <= key32 <= hi32) entries of the tile are
 // written in index order into its fixed staging segment (kStageCap entries) with the
-// tile's count; totals accumulate atomically.  No tile waits on another; sr_pack_kernel
-// later packs the segments into the dense list.
+// tile's count; totals accumulate atomically.  No tile waits on another;
+// sr_finish_kernel later packs the segments into the dense list.
 template <bool BULK>
 __global__ void __launch_bounds__(kTileThreads) sr_split_kernel(EncBatch batch, int bf16,
                                                                 const float* __restrict__ shared, RangeArgs ra,
@@ -569,6 +565,356 @@ __global__ void __launch_bounds__(kTileThreads) sr_split_kernel(EncBatch batch, 
   }
 }
 
+// ---------------------------------------------------------------- finish (cluster)
+// One 8-CTA cluster per (expert, range) in list mode, everything after the split in
+// one launch, CTAs exchanging through distributed shared memory:
+//   1. validate the bracket from the exact totals; pack the tiles' staging segments
+//      into the dense list (CTA c: split tiles [c T/8, (c+1) T/8));
+//   2. radix select over the candidates (the sure entries are excluded), digits starting
+//      below the common prefix of lo32 and hi32: block histograms, reduced across the
+//      cluster (CTA c sums bins [c nb/8, (c+1) nb/8)), the owner of the target bin
+//      broadcasts it;
+//   3. ordered emit: per-CTA (gt, eq) counts exchanged for the CTA's offset, then
+//      block scans place every selected entry at its wire position.
+// A failed bracket (rare) runs steps 2-3 over the full range instead of the list, with
+// the same cluster (slower, same result).
+constexpr int kFinCta = 8;
+constexpr int kFinThreads = 512;
+constexpr int kFinPer = 8;                        // consecutive units per thread per round
+constexpr int kFinRound = kFinThreads * kFinPer;  // 4096
+constexpr double kFinMaxList = 262144.0;          // longest expected list per slot on the cluster path
+
+struct FinXch {
+  unsigned long long tot[kFinCta];  // per-CTA slice totals / counts (written by the peers)
+  unsigned long long aux[kFinCta];
+  int bin;
+  long long before, count;
+};
+
+// Inclusive block scan of one 32-bit value per thread (512 threads); returns the
+// exclusive prefix and writes the block total to *total.
+__device__ __forceinline__ unsigned int block_scan_excl(unsigned int v, unsigned int* wtot, unsigned int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned int incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) wtot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned int w = lane < (kFinThreads >> 5) ? wtot[lane] : 0u;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned int o = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += o;
+    }
+    if (lane < (kFinThreads >> 5)) wtot[lane] = w;
+  }
+  __syncthreads();
+  const unsigned int ex = (warp ? wtot[warp - 1] : 0u) + incl - v;
+  *total = wtot[(kFinThreads >> 5) - 1];
+  __syncthreads();
+  return ex;
+}
+
+__global__ void __cluster_dims__(kFinCta, 1, 1) __launch_bounds__(kFinThreads)
+    sr_finish_kernel(EncBatch batch, int bf16, const float* __restrict__ shared, RangeArgs ra, WsView ws,
+                     uint32_t iw, uint32_t vw) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = static_cast<int>(cl.block_rank());
+  const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
+  SelState& s = ws.st(b, r);
+  if (s.mode != kModeList) return;  // uniform over the cluster (no CTA writes it before the end)
+  __shared__ unsigned int hist[kBins];
+  __shared__ unsigned int slice[kBins / kFinCta];
+  __shared__ unsigned int wtot[32];
+  __shared__ unsigned long long wsum[32];
+  __shared__ FinXch xch;
+  __shared__ int sh_bin;
+  __shared__ long long sh_before, sh_count;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t lo = pick(ra.lo, r), hi = pick(ra.hi, r), n = hi - lo;
+  const void* expert = batch.expert[b];
+  const bool vec = (lo & 3) == 0;
+  const uint32_t lo32 = s.lo32, hi32 = s.hi32;
+  const long long n_sure = s.n_sure, n_super = s.n_super, need0 = s.need0;
+  const bool list = !s.overflow && n_super <= ws.cap && n_sure < need0 && n_super >= need0;
+  double* lres = ws.lres(b, r);
+  uint32_t* lidx = ws.lidx(b, r);
+
+  // 1. pack the staging segments into the dense list
+  if (list) {
+    const unsigned int* cnt = ws.tcount(b, r);
+    const int ntiles = static_cast<int>((n + kSplitTile - 1) / kSplitTile);
+    const int t0 = static_cast<int>(static_cast<int64_t>(ntiles) * crank / kFinCta);
+    const int t1 = static_cast<int>(static_cast<int64_t>(ntiles) * (crank + 1) / kFinCta);
+    unsigned int before = 0;
+    for (int t = threadIdx.x; t < t0; t += blockDim.x) before += cnt[t];
+    unsigned int tot;
+    before = block_scan_excl(before, wtot, &tot), before = tot;  // sum over the block
+    const double* sres = ws.sres(b, r);
+    const uint32_t* sidx = ws.sidx(b, r);
+    unsigned int run = before;
+    __shared__ unsigned int toff[kFinThreads + 1];
+    for (int c0 = t0; c0 < t1; c0 += blockDim.x) {
+      const int t = c0 + threadIdx.x;
+      const int nt = min(static_cast<int>(blockDim.x), t1 - c0);
+      const unsigned int c = t < t1 ? cnt[t] : 0u;
+      unsigned int chunk;
+      toff[threadIdx.x] = block_scan_excl(c, wtot, &chunk);
+      if (threadIdx.x == 0) toff[nt] = chunk;
+      __syncthreads();
+      // flattened copy: entry p of the chunk lives in tile upper_bound(toff, p) - 1;
+      // eight entries per thread per round, all loads issued before the stores
+      for (unsigned int p0 = 0; p0 < chunk; p0 += 8 * kFinThreads) {
+        double v[8];
+        uint32_t ii[8];
+        unsigned int pp[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const unsigned int p = p0 + q * kFinThreads + threadIdx.x;
+          pp[q] = p;
+          if (p < chunk) {
+            int lo_k = 0, hi_k = nt;  // first k with toff[k] > p, in (0, nt]
+            while (lo_k < hi_k) {
+              const int mid = (lo_k + hi_k) >> 1;
+              if (toff[mid] <= p) lo_k = mid + 1; else hi_k = mid;
+            }
+            const int k = lo_k - 1;
+            const int64_t src = static_cast<int64_t>(c0 + k) * kStageCap + (p - toff[k]);
+            v[q] = sres[src];
+            ii[q] = sidx[src];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (pp[q] < chunk) {
+            lres[run + pp[q]] = v[q];
+            lidx[run + pp[q]] = ii[q];
+          }
+      }
+      run += chunk;
+      __syncthreads();
+    }
+  }
+  cl.sync();  // the dense list is complete (release/acquire across the cluster)
+
+  // units: list entries, or the full range after a failed bracket
+  const int64_t units = list ? n_super : n;
+  const int64_t per_cta = ((units + kFinCta - 1) / kFinCta + 7) & ~static_cast<int64_t>(7);
+  const int64_t u_lo = min(units, per_cta * crank), u_hi = min(units, u_lo + per_cta);
+  // residuals and relative indices of units u0 .. u0+7 (u0 a multiple of 8)
+  auto load8 = [&](int64_t u0, double (&rv)[kFinPer], uint32_t (&ix)[kFinPer]) {
+    if (list) {
+      if (u0 + kFinPer <= u_hi) {
+#pragma unroll
+        for (int q = 0; q < kFinPer; q += 2) {
+          const double2 d = *reinterpret_cast<const double2*>(lres + u0 + q);
+          rv[q] = d.x; rv[q + 1] = d.y;
+        }
+        const uint4 a = *reinterpret_cast<const uint4*>(lidx + u0), c = *reinterpret_cast<const uint4*>(lidx + u0 + 4);
+        ix[0] = a.x; ix[1] = a.y; ix[2] = a.z; ix[3] = a.w; ix[4] = c.x; ix[5] = c.y; ix[6] = c.z; ix[7] = c.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < kFinPer; ++q) {
+          rv[q] = u0 + q < u_hi ? lres[u0 + q] : 0.0;
+          ix[q] = u0 + q < u_hi ? lidx[u0 + q] : 0u;
+        }
+      }
+    } else {
+      double a[4], c[4];
+      load_res4(expert, bf16, shared, lo + u0, lo + u_hi, vec, a);
+      load_res4(expert, bf16, shared, lo + u0 + 4, lo + u_hi, vec, c);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { rv[q] = a[q]; rv[4 + q] = c[q]; }
+#pragma unroll
+      for (int q = 0; q < kFinPer; ++q) ix[q] = static_cast<uint32_t>(u0 + q);
+    }
+  };
+
+  // 2. radix select
+  long long need = list ? need0 - n_sure : need0;
+  bool done = list && n_super == need0;  // every candidate is taken
+  unsigned long long prefix = 0, mask = 0;
+  int top = 63;
+  if (list) {  // every candidate shares the leading bits of lo32 and hi32
+    const int c = __clz(lo32 ^ hi32);
+    mask = c >= 32 ? 0xffffffff00000000ull : (~0ull << (64 - c));
+    prefix = (static_cast<unsigned long long>(hi32) << 32) & mask;
+    top = 64 - c;
+  }
+  unsigned long long keyor = 0;
+  for (int pass = 0; pass < kPasses && !done; ++pass) {
+    const int width = top < kDigitBits ? top : kDigitBits, shift = top - width, nb = 1 << width;
+    const unsigned int dmask = static_cast<unsigned int>(nb - 1);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    unsigned long long kor = 0;
+    for (int64_t u0 = u_lo + kFinPer * threadIdx.x; u0 - kFinPer * threadIdx.x < u_hi; u0 += kFinRound) {
+      double rv[kFinPer];
+      uint32_t ix[kFinPer];
+      load8(u0, rv, ix);
+#pragma unroll
+      for (int q = 0; q < kFinPer; ++q) {
+        const unsigned long long key = key_of(rv[q]);
+        const bool cand = u0 + q < u_hi && (!list || static_cast<uint32_t>(key >> 32) <= hi32);
+        kor |= cand ? key : 0ull;
+        // candidates spread over the bins below their common prefix: plain atomics
+        if (cand && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & dmask], 1u);
+      }
+    }
+    if (pass == 0) {
+      const unsigned int lw = __reduce_or_sync(0xffffffffu, static_cast<unsigned int>(kor));
+      const unsigned int hw = __reduce_or_sync(0xffffffffu, static_cast<unsigned int>(kor >> 32));
+      if (lane == 0) wsum[warp] = (static_cast<unsigned long long>(hw) << 32) | lw;
+    }
+    __syncthreads();
+    if (pass == 0 && threadIdx.x == 0) {
+      unsigned long long o = 0;
+      for (int w = 0; w < kFinThreads / 32; ++w) o |= wsum[w];
+      kor = o;
+    }
+    cl.sync();  // every CTA's histogram is complete
+    // my slice of bins, summed over the cluster
+    const int per = (nb + kFinCta - 1) / kFinCta, b0 = crank * per, b1 = min(nb, b0 + per);
+    unsigned int mine = 0;
+    for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      unsigned int v = 0;
+#pragma unroll
+      for (int c = 0; c < kFinCta; ++c) v += cl.map_shared_rank(hist, c)[i];
+      slice[i - b0] = v;
+      mine += v;
+    }
+    unsigned int stot;
+    block_scan_excl(mine, wtot, &stot);
+    if (threadIdx.x == 0)
+      for (int c = 0; c < kFinCta; ++c) {
+        cl.map_shared_rank(&xch, c)->tot[crank] = stot;
+        if (pass == 0) cl.map_shared_rank(&xch, c)->aux[crank] = kor;
+      }
+    cl.sync();  // slice totals (and the pass-0 key OR) everywhere
+    if (pass == 0)
+      for (int c = 0; c < kFinCta; ++c) keyor |= xch.aux[c];
+    // the slice holding the need-th largest: bins descend from the top slice
+    long long above = 0;
+    int owner = 0;
+    for (int c = kFinCta - 1; c >= 0; --c) {
+      if (above + static_cast<long long>(xch.tot[c]) >= need) { owner = c; break; }
+      above += static_cast<long long>(xch.tot[c]);
+    }
+    if (crank == owner) {
+      find_bucket([&](int i) { return static_cast<unsigned long long>(slice[i]); }, b1 - b0, need - above, &sh_bin,
+                  &sh_before, &sh_count, wsum);
+      if (threadIdx.x == 0)
+        for (int c = 0; c < kFinCta; ++c) {
+          FinXch* x = cl.map_shared_rank(&xch, c);
+          x->bin = b0 + sh_bin;
+          x->before = above + sh_before;
+          x->count = sh_count;
+        }
+    }
+    cl.sync();  // the chosen bin everywhere
+    const long long rem = need - xch.before;
+    prefix |= static_cast<unsigned long long>(xch.bin) << shift;
+    mask |= static_cast<unsigned long long>(nb - 1) << shift;
+    need = rem;
+    top = shift;
+    if (xch.count == rem || shift == 0) done = true;
+    if ((keyor & ((1ull << shift) - 1ull)) == 0) {  // no key has a lower bit: the bucket is all ties
+      mask = ~0ull;
+      done = true;
+    }
+    cl.sync();  // xch is rewritten by the next pass
+  }
+
+  // 3. emit.  Selected: sure (list), or (key & mask) > prefix, or one of the first
+  // `need` ties (key & mask) == prefix in index order.
+  auto flags = [&](double rr, bool in, bool& gt, bool& eq) {
+    const unsigned long long key = key_of(rr);
+    const bool sure = list && static_cast<uint32_t>(key >> 32) > hi32;
+    const unsigned long long km = key & mask;
+    gt = in && (sure || km > prefix);
+    eq = in && !sure && km == prefix;
+  };
+  unsigned int cgt = 0, ceq = 0;
+  for (int64_t u0 = u_lo + kFinPer * threadIdx.x; u0 - kFinPer * threadIdx.x < u_hi; u0 += kFinRound) {
+    double rv[kFinPer];
+    uint32_t ix[kFinPer];
+    load8(u0, rv, ix);
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) {
+      bool gt, eq;
+      flags(rv[q], u0 + q < u_hi, gt, eq);
+      cgt += gt;
+      ceq += eq;
+    }
+  }
+  unsigned int tgt, teq;
+  block_scan_excl(cgt, wtot, &tgt);  // block sums (the count sweep can exceed 16-bit fields)
+  block_scan_excl(ceq, wtot, &teq);
+  if (threadIdx.x == 0)
+    for (int c = 0; c < kFinCta; ++c) {
+      cl.map_shared_rank(&xch, c)->tot[crank] = tgt;
+      cl.map_shared_rank(&xch, c)->aux[crank] = teq;
+    }
+  cl.sync();
+  unsigned long long run_gt = 0, run_eq = 0;
+  for (int c = 0; c < crank; ++c) { run_gt += xch.tot[c]; run_eq += xch.aux[c]; }
+  uint8_t* wire = batch.wire[b];
+  const int ebytes = static_cast<int>((iw + vw) / 8);
+  const int64_t out_base = pick(ra.out_base, r);
+  for (int64_t u0 = u_lo + kFinPer * threadIdx.x; u0 - kFinPer * threadIdx.x < u_hi; u0 += kFinRound) {
+    double rv[kFinPer];
+    uint32_t ix[kFinPer];
+    load8(u0, rv, ix);
+    unsigned int fg = 0, fe = 0;
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) {
+      bool gt, eq;
+      flags(rv[q], u0 + q < u_hi, gt, eq);
+      fg |= static_cast<unsigned int>(gt) << q;
+      fe |= static_cast<unsigned int>(eq) << q;
+    }
+    unsigned int rt;  // (gt << 16 | eq) packed: at most 4096 of each per round
+    const unsigned int xp = block_scan_excl((static_cast<unsigned int>(__popc(fg)) << 16) | __popc(fe), wtot, &rt);
+    const unsigned int rg = rt >> 16, re = rt & 0xffffu;
+    unsigned long long gb = run_gt + (xp >> 16), ebf = run_eq + (xp & 0xffffu);
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) {
+      const bool gt = (fg >> q) & 1u, eq = (fe >> q) & 1u;
+      if (gt || (eq && static_cast<long long>(ebf) < need)) {
+        const unsigned long long taken_eq =
+            static_cast<long long>(ebf) < need ? ebf : static_cast<unsigned long long>(need);
+        uint8_t* p = wire + 28 + (out_base + static_cast<int64_t>(gb + taken_eq)) * ebytes;
+        const uint64_t idx = static_cast<uint64_t>(lo) + ix[q];
+        put_u32(p, static_cast<uint32_t>(idx));
+        if (iw == 64) { put_u32(p + 4, static_cast<uint32_t>(idx >> 32)); p += 8; } else { p += 4; }
+        if (vw == 32) {
+          put_u32(p, __float_as_uint(__double2float_rn(rv[q])));
+        } else {
+          const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(rv[q]));
+          put_u32(p, static_cast<uint32_t>(bits));
+          put_u32(p + 4, static_cast<uint32_t>(bits >> 32));
+        }
+      }
+      gb += gt;
+      ebf += eq;
+    }
+    run_gt += rg;
+    run_eq += re;
+  }
+  if (crank == 0 && threadIdx.x == 0) {  // the later multi-block kernels skip this slot
+    s.done = 1;
+    s.mode = kModeDone;
+  }
+}
+
+// Multi-block path (large lists, and statically full-range slots): scan, pack, one
+// select launch per digit, emit.  Grids span all SMs, so a list of millions of entries
+// per slot streams at HBM rate instead of through one cluster.
 // grid (batch * nr), 1024 threads: validate the bracket from the exact totals and turn
 // the tiles' listed counts into exclusive offsets in the dense list.
 __global__ void __launch_bounds__(1024) sr_scan_kernel(RangeArgs ra, WsView ws) {
@@ -663,7 +1009,7 @@ __global__ void __launch_bounds__(kTileThreads) sr_select_kernel(EncBatch batch,
                                                                  WsView ws, int pass) {
   const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
   SelState& s = ws.st(b, r);
-  if (s.done) return;
+  if (s.done || s.mode == kModeDone) return;
   __shared__ unsigned int sh[kBins];
   __shared__ unsigned long long wsum[32];
   __shared__ int sh_bin, sh_last;
@@ -780,7 +1126,7 @@ __global__ void __launch_bounds__(kTileThreads) sr_emit_kernel(EncBatch batch, i
                                                                WsView ws, uint32_t iw, uint32_t vw) {
   const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
   SelState& s = ws.st(b, r);
-  if (s.need0 == 0) return;
+  if (s.need0 == 0 || s.mode == kModeDone) return;
   __shared__ int tile_sh;
   __shared__ unsigned int wgt[8], weq[8];
   __shared__ unsigned long long excl_gt_sh, excl_eq_sh;
@@ -1146,13 +1492,16 @@ WsView make_ws(void* base, int64_t P) {
   return ws;
 }
 
-// HEP_SR_SELECT=full forces the full-range select, =fallback an invalid sample bracket
-// (both exercise the fallback in tests); anything else picks per range.
+// HEP_SR_SELECT=full forces the full-range select, =fallback an invalid sample bracket,
+// =multiblock the multi-block list path (all exercised in tests); anything else picks
+// per call.
 int select_override() {
   const char* v = std::getenv("HEP_SR_SELECT");
   if (!v) return 0;
   if (!std::strcmp(v, "full")) return 1;
   if (!std::strcmp(v, "fallback")) return 2;
+  if (!std::strcmp(v, "multiblock")) return 3;
+  if (!std::strcmp(v, "fallback-multiblock")) return 4;
   return 0;
 }
 
@@ -1186,11 +1535,11 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
     ra.lo[0] = 0; ra.hi[0] = P; ra.k[0] = plan.k; ra.out_base[0] = 0;
     ra.nr = 1;
   }
-  ra.force_fallback = ovr == 2;
+  ra.force_fallback = ovr == 2 || ovr == 4;
   bool any_list = false, any_full = false;
   double expect_max = 0.0;
   for (int r = 0; r < ra.nr; ++r) {
-    const int64_t n = pick(ra.hi, r) - pick(ra.lo, r), k = pick(ra.k, r);
+    const int64_t n = ra.hi[r] - ra.lo[r], k = ra.k[r];
     bool full = ovr == 1 || n <= 0 || k <= 0 || k >= n || n >= (int64_t{1} << 31);
     if (!full) {
       // expected list size: k plus the sample's +-dev bracket scaled to the range
@@ -1208,6 +1557,9 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
   const int64_t nmax = std::max(ra.hi[0] - ra.lo[0], ra.nr > 1 ? ra.hi[1] - ra.lo[1] : int64_t{0});
   const int64_t tiles_max = std::max<int64_t>(1, (nmax + kSplitTile - 1) / kSplitTile);
   const int wide = std::max(1, 148 * 8 / slots);  // blocks per slot for full-range sweeps
+  // lists up to kFinMaxList entries finish in one cluster launch per slot; longer ones
+  // (experts of ~100M parameters) take the multi-block path across all SMs
+  const bool cluster = expect_max <= kFinMaxList && ovr != 3 && ovr != 4;
 
   sr_init_kernel<<<dim3(16, batch), 256, 0, stream>>>(ws, eb, bf16, shared, ra, plan.h, plan.m, plan.k,
                                                       plan.index_bits, plan.value_bits);
@@ -1225,17 +1577,24 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
     const dim3 sgrid(static_cast<unsigned>(tiles_max), slots);
     if (bulk) sr_split_kernel<true><<<sgrid, kTileThreads, smem, stream>>>(eb, bf16, shared, ra, ws);
     else sr_split_kernel<false><<<sgrid, kTileThreads, smem, stream>>>(eb, bf16, shared, ra, ws);
-    sr_scan_kernel<<<slots, 1024, 0, stream>>>(ra, ws);
-    sr_pack_kernel<<<dim3(std::max(1, 148 * 4 / slots), slots), kTileThreads, 0, stream>>>(ra, ws);
+    if (cluster) {
+      sr_finish_kernel<<<dim3(kFinCta, slots), kFinThreads, 0, stream>>>(eb, bf16, shared, ra, ws, plan.index_bits,
+                                                                         plan.value_bits);
+    } else {
+      sr_scan_kernel<<<slots, 1024, 0, stream>>>(ra, ws);
+      sr_pack_kernel<<<dim3(std::max(1, 148 * 4 / slots), slots), kTileThreads, 0, stream>>>(ra, ws);
+    }
   }
-  // A failed bracket falls back to the full range with the list-sized grid (rare);
-  // a statically full range gets the wide grid.
-  const int list_blocks = static_cast<int>(std::min<double>(wide, std::ceil(1.25 * expect_max / kTile)));
-  const int blocks = any_full ? std::max(wide, 1) : std::max(list_blocks, 1);
-  for (int pass = 0; pass < kPasses; ++pass)
-    sr_select_kernel<<<dim3(blocks, slots), kTileThreads, 0, stream>>>(eb, bf16, shared, ra, ws, pass);
-  sr_emit_kernel<<<dim3(blocks, slots), kTileThreads, 0, stream>>>(eb, bf16, shared, ra, ws, plan.index_bits,
-                                                                   plan.value_bits);
+  if (any_full || (any_list && !cluster)) {
+    // A failed bracket on the multi-block path runs with the list-sized grid (rare);
+    // a statically full range gets the wide grid.
+    const int list_blocks = static_cast<int>(std::min<double>(wide, std::ceil(1.25 * expect_max / kTile)));
+    const int blocks = any_full ? wide : std::max(list_blocks, 1);
+    for (int pass = 0; pass < kPasses; ++pass)
+      sr_select_kernel<<<dim3(blocks, slots), kTileThreads, 0, stream>>>(eb, bf16, shared, ra, ws, pass);
+    sr_emit_kernel<<<dim3(blocks, slots), kTileThreads, 0, stream>>>(eb, bf16, shared, ra, ws, plan.index_bits,
+                                                                     plan.value_bits);
+  }
   return cudaGetLastError();
 }
 

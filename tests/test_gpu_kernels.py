@@ -94,6 +94,11 @@ def _demo_expert_pair(h, m, seed, quantize=False):
     return e, s
 
 
+# every select path of the encoder: sampled bracket on the cluster or the multi-block
+# path, forced full-range select, and a forced invalid bracket on either path
+SELECT_PATHS = ["auto", "full", "fallback", "multiblock", "fallback-multiblock"]
+
+
 @pytest.mark.parametrize("h,m,ratio,k,iw,vw,per_matrix,quant", [
     (16, 24, None, 40, 32, 32, False, False),
     (16, 24, None, 40, 64, 64, False, True),
@@ -104,7 +109,7 @@ def _demo_expert_pair(h, m, seed, quantize=False):
     (8, 8, None, 10 ** 9, 32, 32, False, False),
     (333, 77, 7.0, None, 64, 32, False, True),
 ])
-@pytest.mark.parametrize("select", ["auto", "full", "fallback"])
+@pytest.mark.parametrize("select", SELECT_PATHS)
 def test_sr_encode_decode_bitexact(h, m, ratio, k, iw, vw, per_matrix, quant, select, monkeypatch):
     monkeypatch.setenv("HEP_SR_SELECT", select)
     e, s = _demo_expert_pair(h, m, seed=h * 1000 + m, quantize=quant)
@@ -132,7 +137,7 @@ def test_sr_bf16_expert_upcast():
     assert wire.cpu().numpy().tobytes() == want.tobytes()
 
 
-@pytest.mark.parametrize("select", ["auto", "fallback"])
+@pytest.mark.parametrize("select", ["auto", "fallback", "multiblock"])
 def test_sr_cfg4_expert_bitexact(select, monkeypatch):
     """Full cfg4 expert (H=2048, F=1408, P=5,767,168) at CR=50 against the reference."""
     monkeypatch.setenv("HEP_SR_SELECT", select)
@@ -191,8 +196,10 @@ def test_transpose_convert():
     (512, 1536, 20.0, True, True, False),    # ~9 distinct |r|: list overflows -> full-range fallback
     (300, 1001, 100.0, True, False, False),  # odd range start (unaligned second matrix)
 ])
-def test_sr_encode_sampled_bracket(h, m, ratio, per_matrix, quant, bf16):
+@pytest.mark.parametrize("select", ["auto", "multiblock"])
+def test_sr_encode_sampled_bracket(h, m, ratio, per_matrix, quant, bf16, select, monkeypatch):
     """Medium experts where the bracket comes from a sparse sample of each range."""
+    monkeypatch.setenv("HEP_SR_SELECT", select)
     e, s = _demo_expert_pair(h, m, seed=h + m, quantize=quant)
     et = torch.from_numpy(e)
     if bf16:
@@ -205,7 +212,7 @@ def test_sr_encode_sampled_bracket(h, m, ratio, per_matrix, quant, bf16):
 
 
 @pytest.mark.parametrize("per_matrix", [False, True])
-@pytest.mark.parametrize("select", ["auto", "full", "fallback"])
+@pytest.mark.parametrize("select", SELECT_PATHS)
 def test_sr_batched_encode_decode_bitexact(per_matrix, select, monkeypatch):
     """One launch sequence for several experts (the layer encodes all owned experts at once)."""
     monkeypatch.setenv("HEP_SR_SELECT", select)
