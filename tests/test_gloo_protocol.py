@@ -1,4 +1,4 @@
-"""The N > 1 protocol on CPU: two processes over gloo (world size 2 and 4), no GPU.
+"""The N > 1 protocol on CPU: processes over gloo (world size 2, 4 and 8), no GPU.
 
 Each rank takes its placement and routing from libhep.so's host library (route table,
 peer lists, held experts) and gates its own tokens with the oracle.  The ranks then
@@ -19,7 +19,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-HIER = {2: [([2], [1]), ([2], [2])], 4: [([2, 2], [1, 1]), ([2, 2], [1, 2]), ([4], [2])]}
+HIER = {2: [([2], [1]), ([2], [2])], 4: [([2, 2], [1, 1]), ([2, 2], [1, 2]), ([4], [2])],
+        8: [([2, 2, 2], [1, 2, 2]), ([2, 4], [1, 1])]}  # the N=8 bench topologies (cfg4, cfg3)
 
 
 def _port():
