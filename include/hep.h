@@ -168,6 +168,16 @@ int hep_layer_set_expert(hep_layer_t layer, int64_t expert, const void* w_up, co
                          hep_dtype dtype, void* stream);
 /* SR mode: the shared expert (fp32 flat P, device) that residuals are coded against. */
 int hep_layer_set_shared(hep_layer_t layer, const float* shared, void* stream);
+/* SR mode: recompute the shared expert from the owned experts of every rank — the
+ * element-wise mean over ALL E experts, fp64 sum in expert order times 1/E, rounded to
+ * fp32 (replaces sr::init_shared / sr::update_shared, sparsecomp.cpp:147-173, whose
+ * update_shared is the single-process stand-in for the paper's async all-reduce).
+ * Bit-exact with the reference: a chain over ranks 0..G-1 (experts are owned in rank
+ * order), pipelined in chunks over NVLink peer memory (NCCL send/recv + broadcast on the
+ * HEP_COMM=nccl path).  Collective: every rank calls it on its stream. */
+int hep_layer_refresh_shared(hep_layer_t layer, void* stream);
+/* SR mode: copy of the current fp32 shared expert (flat P) into `out` (device). */
+int hep_layer_get_shared(hep_layer_t layer, float* out, void* stream);
 /* Expert-domain All-Gather of the owned experts (dense or SR-migrated), so that every
  * held expert is resident.  Issued on `stream`. */
 int hep_layer_gather_experts(hep_layer_t layer, void* stream);

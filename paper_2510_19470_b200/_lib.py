@@ -133,6 +133,8 @@ SIGNATURES = {
     "hep_layer_set_gate": [VP, VP, I32, VP],
     "hep_layer_set_expert": [VP, I64, VP, VP, I32, VP],
     "hep_layer_set_shared": [VP, VP, VP],
+    "hep_layer_refresh_shared": [VP, VP],
+    "hep_layer_get_shared": [VP, VP, VP],
     "hep_layer_gather_experts": [VP, VP],
     "hep_layer_forward": [VP, VP, I64, VP, VP],
     "hep_layer_forward_host": [VP, VP, I64, VP, VP],

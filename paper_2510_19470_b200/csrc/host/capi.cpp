@@ -389,6 +389,14 @@ int hep_layer_set_shared(hep_layer_t layer, const float* shared, void* stream) {
   return guarded([&] { layer->impl->set_shared(shared, st(stream)); });
 }
 
+int hep_layer_refresh_shared(hep_layer_t layer, void* stream) {
+  return guarded([&] { layer->impl->refresh_shared(st(stream)); });
+}
+
+int hep_layer_get_shared(hep_layer_t layer, float* out, void* stream) {
+  return guarded([&] { layer->impl->get_shared(out, st(stream)); });
+}
+
 int hep_layer_gather_experts(hep_layer_t layer, void* stream) {
   return guarded([&] { layer->impl->gather_experts(st(stream)); });
 }

@@ -153,6 +153,7 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
     sr_tmp_.alloc(sizeof(float) * P);
     sr_status_.alloc(16 * kMaxSrBatch);
     shared_c_.alloc(static_cast<size_t>(dtype_bytes(dt_)) * P);
+    if (G_ > 1) partial_.alloc(sizeof(double) * P);  // shared-expert refresh chain
   }
   for (int b = 0; b < 2; ++b) {
     x_dev_[b].alloc(eb * Tmax_ * H_);
@@ -185,14 +186,23 @@ void Layer::setup_p2p() {
   send_base_.alloc(sizeof(int) * NK_);
   // Exchange CUDA IPC handles of xall / oall / sync (token path) and of the expert
   // compute copies and SR wires (expert All-Gather pulls) through NCCL.
-  constexpr int kBufs = 6;
+  constexpr int kBufs = 9;
   cudaIpcMemHandle_t mine[kBufs] = {};
   ck(cudaIpcGetMemHandle(&mine[0], xall_.p), "ipc handle");
   ck(cudaIpcGetMemHandle(&mine[1], oall_.p), "ipc handle");
   ck(cudaIpcGetMemHandle(&mine[2], sync_.p), "ipc handle");
   ck(cudaIpcGetMemHandle(&mine[3], w_up_c_.p), "ipc handle");
   ck(cudaIpcGetMemHandle(&mine[4], w_down_c_.p), "ipc handle");
-  if (use_sr_) ck(cudaIpcGetMemHandle(&mine[5], wires_.p), "ipc handle");
+  if (use_sr_) {
+    // + the shared-expert refresh chain: fp64 partials, chunk flags, the fp32 mean
+    const int64_t P = 2 * H_ * F_;
+    chain_flags_.alloc(sizeof(uint32_t) * ((P + kChainChunk - 1) / kChainChunk + kMaxG));
+    ck(cudaMemset(chain_flags_.p, 0, chain_flags_.bytes), "chain flags");
+    ck(cudaIpcGetMemHandle(&mine[5], wires_.p), "ipc handle");
+    ck(cudaIpcGetMemHandle(&mine[6], partial_.p), "ipc handle");
+    ck(cudaIpcGetMemHandle(&mine[7], chain_flags_.p), "ipc handle");
+    ck(cudaIpcGetMemHandle(&mine[8], shared_.p), "ipc handle");
+  }
   DevBuf dmine, dall;
   dmine.alloc(sizeof(mine));
   dall.alloc(sizeof(mine) * G_);
@@ -215,6 +225,8 @@ void Layer::setup_p2p() {
   peer_w_up_.assign(static_cast<size_t>(G_), nullptr);
   peer_w_down_.assign(static_cast<size_t>(G_), nullptr);
   peer_wires_.assign(static_cast<size_t>(G_), nullptr);
+  peer_chain_flags_.assign(static_cast<size_t>(G_), nullptr);
+  if (use_sr_) peer_chain_flags_[static_cast<size_t>(rank_)] = chain_flags_.as<uint32_t>();
   for (int r = 0; r < G_; ++r) {
     if (r == rank_) {
       a.xall[r] = xall_.p;
@@ -223,7 +235,7 @@ void Layer::setup_p2p() {
       continue;
     }
     void* ptrs[kBufs] = {};
-    const int nb = use_sr_ ? kBufs : kBufs - 1;
+    const int nb = use_sr_ ? kBufs : 5;
     for (int b = 0; b < nb; ++b) {
       ck(cudaIpcOpenMemHandle(&ptrs[b], all[static_cast<size_t>(kBufs * r + b)], cudaIpcMemLazyEnablePeerAccess), "ipc open");
       ipc_opened_.push_back(ptrs[b]);
@@ -234,6 +246,15 @@ void Layer::setup_p2p() {
     peer_w_up_[static_cast<size_t>(r)] = ptrs[3];
     peer_w_down_[static_cast<size_t>(r)] = ptrs[4];
     peer_wires_[static_cast<size_t>(r)] = ptrs[5];
+    if (use_sr_) peer_chain_flags_[static_cast<size_t>(r)] = static_cast<uint32_t*>(ptrs[7]);
+    if (use_sr_ && r == rank_ - 1) {
+      peer_partial_prev_ = static_cast<const double*>(ptrs[6]);
+      peer_flags_prev_ = static_cast<const uint32_t*>(ptrs[7]);
+    }
+    if (use_sr_ && r == G_ - 1) {
+      peer_shared_last_ = static_cast<const float*>(ptrs[8]);
+      peer_flags_last_ = static_cast<const uint32_t*>(ptrs[7]);
+    }
   }
   a.n_ag = 0;
   for (int64_t p : ag_peers_) a.ag_list[a.n_ag++] = static_cast<int>(p);
@@ -309,6 +330,62 @@ void Layer::set_expert(int64_t e, const void* w_up, const void* w_down, DType dt
 void Layer::set_shared(const float* shared, cudaStream_t s) {
   if (!use_sr_) throw std::invalid_argument("shared expert is only used with SR migration");
   ck(cudaMemcpyAsync(shared_.p, shared, sizeof(float) * 2 * H_ * F_, cudaMemcpyDeviceToDevice, s), "shared");
+  finish_shared(s);
+}
+
+void Layer::get_shared(float* out, cudaStream_t s) const {
+  if (!use_sr_) throw std::invalid_argument("shared expert is only used with SR migration");
+  ck(cudaMemcpyAsync(out, shared_.p, sizeof(float) * 2 * H_ * F_, cudaMemcpyDeviceToDevice, s), "get shared");
+}
+
+void Layer::refresh_shared(cudaStream_t s) {
+  if (!use_sr_) throw std::invalid_argument("shared expert is only used with SR migration");
+  const int64_t P = 2 * H_ * F_;
+  if (G_ == 1) {  // every expert is local: the plain kernel over the list
+    std::vector<const void*> ex(static_cast<size_t>(n_));
+    for (int64_t j = 0; j < n_; ++j) ex[static_cast<size_t>(j)] = master_.as<float>() + j * P;
+    ck(launch_shared_mean(DType::F32, ex.data(), static_cast<int>(n_), P, shared_.as<float>(), s), "shared mean");
+    finish_shared(s);
+    return;
+  }
+  ChainArgs c{};
+  c.master = master_.as<float>();
+  c.partial = partial_.as<double>();
+  c.shared = shared_.as<float>();
+  c.P = P;
+  c.chunk = kChainChunk;
+  c.n = static_cast<int>(n_);
+  c.rank = rank_;
+  c.G = static_cast<int>(G_);
+  c.inv = 1.0 / static_cast<double>(E_);
+  if (p2p_) {
+    // peer-memory chain: chunks pipeline from rank 0 to rank G-1, then every rank
+    // copies the mean from the last one
+    c.pred_partial = peer_partial_prev_;
+    c.pred_flags = peer_flags_prev_;
+    c.my_flags = chain_flags_.as<uint32_t>();
+    c.last_shared = peer_shared_last_;
+    c.last_flags = peer_flags_last_;
+    const int64_t nchunks = (P + kChainChunk - 1) / kChainChunk;
+    for (int r = 0; r < G_; ++r) c.bar[r] = peer_chain_flags_[static_cast<size_t>(r)] + nchunks;
+    c.epoch = ++chain_epoch_;
+    ck(launch_shared_chain(c, s), "shared chain");
+  } else {
+    // NCCL: the same chain with whole-vector hops, then a broadcast from the last rank
+    nck(ncclGroupStart(), "group");
+    if (rank_ > 0) nck(ncclRecv(partial_.p, static_cast<size_t>(P), ncclFloat64, rank_ - 1, comm_->nccl, s), "recv");
+    nck(ncclGroupEnd(), "group");
+    c.pred_partial = partial_.as<double>();
+    c.epoch = 0;  // no flags
+    ck(launch_shared_chain(c, s), "shared chain");
+    if (rank_ < G_ - 1) nck(ncclSend(partial_.p, static_cast<size_t>(P), ncclFloat64, rank_ + 1, comm_->nccl, s), "send");
+    nck(ncclBroadcast(shared_.p, shared_.p, static_cast<size_t>(P), ncclFloat32, static_cast<int>(G_ - 1), comm_->nccl, s),
+        "broadcast");
+  }
+  finish_shared(s);
+}
+
+void Layer::finish_shared(cudaStream_t s) {
   // the shared expert in the GEMM's layout, the base every migrated expert is decoded onto
   const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
   ck(launch_transpose_convert(DType::F32, shared_.p, H_, F_, dt_, shared_c_.p, s), "shared up");

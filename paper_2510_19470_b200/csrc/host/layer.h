@@ -45,6 +45,11 @@ class Layer {
   void set_gate(const void* w_gate, DType dt, cudaStream_t s);
   void set_expert(int64_t e, const void* w_up, const void* w_down, DType dt, cudaStream_t s);
   void set_shared(const float* shared, cudaStream_t s);  // SR mode: fp32 flat P
+  // SR mode: recompute the shared expert as the mean of ALL experts across the ranks
+  // (reference init_shared / update_shared, sparsecomp.cpp:147-173), bit-exact with
+  // the reference's sequential fp64 sum in expert order; every rank ends with it.
+  void refresh_shared(cudaStream_t s);
+  void get_shared(float* out, cudaStream_t s) const;  // SR mode: copy of the fp32 shared expert
   void gather_experts(cudaStream_t s);
   void forward(const void* x, int64_t T, void* y, cudaStream_t s);
   void forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s);
@@ -111,6 +116,16 @@ class Layer {
   cudaEvent_t ev_ag_start_ = nullptr, ev_ag_done_ = nullptr;
   std::vector<void*> peer_w_up_, peer_w_down_, peer_wires_;
   uint32_t ag_epoch_ = 0;
+  // shared-expert refresh chain (SR mode): fp64 partial sums and per-chunk flags,
+  // peer-mapped from the neighbouring ranks
+  DevBuf partial_, chain_flags_;
+  const double* peer_partial_prev_ = nullptr;
+  const uint32_t* peer_flags_prev_ = nullptr;
+  const float* peer_shared_last_ = nullptr;
+  const uint32_t* peer_flags_last_ = nullptr;
+  std::vector<uint32_t*> peer_chain_flags_;  // every rank's chain flags (own included)
+  uint32_t chain_epoch_ = 0;
+  void finish_shared(cudaStream_t s);  // shared_ -> shared_c_ (GEMM layout)
   bool ag_pending_ = false;
   std::vector<void*> ipc_opened_;
   uint32_t epoch_ = 0;

@@ -247,6 +247,53 @@ __global__ void __launch_bounds__(256) combine_p2p_kernel(P2PArgs a, const int* 
   }
 }
 
+// ---------------------------------------------------------------- shared-expert refresh
+// Deterministic cross-GPU shared mean, bit-exact with the reference's sequential fp64
+// sum in expert order (sparsecomp.cpp:147-168): experts 0..E-1 live on ranks 0..G-1 in
+// order, so the sum is a chain.  Rank g, chunk by chunk: wait for rank g-1's partial of
+// the chunk (peer memory flag), continue the fp64 sum over its own experts, publish its
+// partial (or, on the last rank, the fp32 mean).  Chunks pipeline across the chain.
+// Entry barrier: every rank has finished the previous refresh (stream order), so no
+// partial or mean of the previous epoch is still being read when this one overwrites it.
+__global__ void chain_barrier_kernel(ChainArgs c) {
+  const int r = threadIdx.x;
+  if (r < c.G) st_release_sys(c.bar[r] + c.rank, c.epoch);
+  __syncthreads();
+  if (r < c.G) wait_flag(c.bar[c.rank] + r, c.epoch);
+}
+
+__global__ void __launch_bounds__(256) shared_chain_kernel(ChainArgs c) {
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * c.chunk;
+  const int64_t i1 = min(c.P, i0 + c.chunk);
+  if (c.rank > 0 && c.epoch) {
+    if (threadIdx.x == 0) wait_flag(c.pred_flags + blockIdx.x, c.epoch);
+    __syncthreads();
+  }
+  const bool last = c.rank == c.G - 1;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    double acc = c.rank > 0 ? __ldcv(c.pred_partial + i) : 0.0;
+    for (int j = 0; j < c.n; ++j) acc = __dadd_rn(acc, static_cast<double>(c.master[static_cast<int64_t>(j) * c.P + i]));
+    if (last) c.shared[i] = __double2float_rn(__dmul_rn(acc, c.inv));
+    else c.partial[i] = acc;
+  }
+  if (!c.epoch) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(c.my_flags + blockIdx.x, c.epoch);
+  }
+}
+
+// Ranks before the last: copy each chunk of the mean from the last rank once its flag
+// is up.
+__global__ void __launch_bounds__(256) shared_fetch_kernel(ChainArgs c) {
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * c.chunk;
+  const int64_t i1 = min(c.P, i0 + c.chunk);
+  if (threadIdx.x == 0) wait_flag(c.last_flags + blockIdx.x, c.epoch);
+  __syncthreads();
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) c.shared[i] = __ldcv(c.last_shared + i);
+}
+
 }  // namespace
 
 const uint32_t* p2p_dispatch_flags(const P2PArgs& a) {
@@ -283,6 +330,14 @@ cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T,
   }
   permute_p2p_kernel<<<(T + 7) / 8, 256, 0, s>>>(a, static_cast<const uint8_t*>(x), T, row_bytes, k, keys, ranks,
                                                  chunk_off, key_off, send_base, pos, mode);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shared_chain(const ChainArgs& c, cudaStream_t s) {
+  const int blocks = static_cast<int>((c.P + c.chunk - 1) / c.chunk);
+  if (c.epoch) chain_barrier_kernel<<<1, 32, 0, s>>>(c);
+  shared_chain_kernel<<<blocks, 256, 0, s>>>(c);
+  if (c.epoch && c.rank != c.G - 1) shared_fetch_kernel<<<blocks, 256, 0, s>>>(c);
   return cudaGetLastError();
 }
 

@@ -47,4 +47,24 @@ cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, cons
                                const int* send_base, const float* w, int T, int H, int k, void* y,
                                cudaStream_t s);
 
+// Shared-expert refresh across the ranks (comm_p2p.cu): the fp64 sum over every expert in
+// expert order as a chain over ranks 0..G-1, chunked so the ranks pipeline.
+struct ChainArgs {
+  const float* master;          // this rank's n fp32 experts, flat [n][P]
+  const double* pred_partial;   // rank-1's partial (peer memory); unused on rank 0
+  const uint32_t* pred_flags;   // rank-1's chunk flags (peer memory)
+  double* partial;              // this rank's partial (read by rank+1)
+  uint32_t* my_flags;           // this rank's chunk flags
+  const float* last_shared;     // the last rank's mean (peer memory)
+  const uint32_t* last_flags;   // the last rank's chunk flags (peer memory)
+  float* shared;                // this rank's copy of the mean
+  uint32_t* bar[kMaxG];         // every rank's barrier flags ([kMaxG], after its chunk flags)
+  int64_t P, chunk;
+  int n, rank, G;
+  double inv;                   // 1 / E
+  uint32_t epoch;               // 0: no flags (the NCCL path moves the partials)
+};
+constexpr int64_t kChainChunk = 65536;  // elements per pipelined chunk
+cudaError_t launch_shared_chain(const ChainArgs& c, cudaStream_t s);
+
 }  // namespace hep

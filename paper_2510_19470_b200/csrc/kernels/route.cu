@@ -159,9 +159,11 @@ __global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ x,
 // tensor core's summation order.
 constexpr int kGT = 64;          // tokens per block
 constexpr int kGC = 64;          // hidden columns per stage
-constexpr int kGStages = 4;
 constexpr int kGPitch = kGC + 8; // bf16 elements per smem row (16-byte pad: no ldmatrix conflicts)
-constexpr size_t kGateSmem = static_cast<size_t>(kGStages) * 2 * kGT * kGPitch * 2;
+// Pipeline depth and gate-weight rows staged per stage: with few experts the x stream
+// gets a deeper pipeline (more bytes in flight per SM).
+template <int STAGES, int EROWS>
+constexpr size_t gate_smem() { return static_cast<size_t>(STAGES) * (kGT + EROWS) * kGPitch * 2; }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
@@ -186,6 +188,7 @@ __device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+template <int kGStages, int EROWS>
 __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __restrict__ x,
                                                       const __nv_bfloat16* __restrict__ wg_t, int T_tok,
                                                       int H, int E, int k,
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
                                                       int* __restrict__ chunk_counts) {
   extern __shared__ __align__(128) uint8_t gsm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(gsm);                      // [S][64][pitch]
-  __nv_bfloat16* ws = xs + static_cast<size_t>(kGStages) * kGT * kGPitch;         // [S][64][pitch]
+  __nv_bfloat16* ws = xs + static_cast<size_t>(kGStages) * kGT * kGPitch;         // [S][EROWS][pitch]
   __shared__ float logits[kGT][kMaxE + 1];
   __shared__ int skey[kGT][kMaxK];
 
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
   auto load_stage = [&](int s, int kc) {
     const int hc = kc * kGC;
     __nv_bfloat16* xd = xs + static_cast<size_t>(s) * kGT * kGPitch;
-    __nv_bfloat16* wd = ws + static_cast<size_t>(s) * kGT * kGPitch;
+    __nv_bfloat16* wd = ws + static_cast<size_t>(s) * EROWS * kGPitch;
 #pragma unroll
     for (int i = tid; i < kGT * (kGC / 8); i += 128) {
       const int r = i >> 3, c8 = (i & 7) * 8;
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
     cp_async_commit();
     const int s = kc % kGStages;
     const __nv_bfloat16* xa = xs + static_cast<size_t>(s) * kGT * kGPitch + (warp * 16) * kGPitch;
-    const __nv_bfloat16* wb = ws + static_cast<size_t>(s) * kGT * kGPitch;
+    const __nv_bfloat16* wb = ws + static_cast<size_t>(s) * EROWS * kGPitch;
 #pragma unroll
     for (int ks = 0; ks < kGC / 16; ++ks) {
       uint32_t a[4];
@@ -546,17 +549,25 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
   if (dt == DType::BF16) {
     // wg_t is bf16 [E, H] for bf16 layers.
     if (H % kGC || E % 8) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-      const cudaError_t e = cudaFuncSetAttribute(gate_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(kGateSmem));
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
     const int blocks = (T + kGT - 1) / kGT;
-    gate_mma_kernel<<<blocks, 128, kGateSmem, stream>>>(
-        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg_t), T, H, E, k, dest_of_owner,
-        experts_per_gpu, NK, topk_idx, topk_w, keys, ranks, chunk_counts);
+    auto go = [&](auto kern, size_t smem, bool& attr) {
+      if (!attr) {  // once per instantiation
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      kern<<<blocks, 128, smem, stream>>>(static_cast<const __nv_bfloat16*>(x),
+                                          static_cast<const __nv_bfloat16*>(wg_t), T, H, E, k, dest_of_owner,
+                                          experts_per_gpu, NK, topk_idx, topk_w, keys, ranks, chunk_counts);
+      return cudaSuccess;
+    };
+    static bool a8 = false, a16 = false, a64 = false;
+    cudaError_t e;
+    if (E <= 8) e = go(gate_mma_kernel<8, 8>, gate_smem<8, 8>(), a8);
+    else if (E <= 16) e = go(gate_mma_kernel<8, 16>, gate_smem<8, 16>(), a16);
+    else e = go(gate_mma_kernel<4, kMaxE>, gate_smem<4, kMaxE>(), a64);
+    if (e != cudaSuccess) return e;
   } else {
     const int nchunks = (T + kChunk - 1) / kChunk;
     gate_kernel<float><<<nchunks, 256, 0, stream>>>(static_cast<const float*>(x), static_cast<const float*>(wg_t),

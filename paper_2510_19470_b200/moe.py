@@ -95,6 +95,16 @@ class MoELayer:
     def set_shared(self, shared_flat_f32: torch.Tensor, stream=None):
         check(lib.hep_layer_set_shared(self.handle, shared_flat_f32.data_ptr(), _stream(stream)))
 
+    def refresh_shared(self, stream=None):
+        """Shared expert := mean of all E experts across the ranks (collective; bit-exact
+        with the reference's init_shared / update_shared, sparsecomp.cpp:147-173)."""
+        check(lib.hep_layer_refresh_shared(self.handle, _stream(stream)))
+
+    def get_shared(self, stream=None) -> torch.Tensor:
+        out = torch.empty(2 * self.H * self.F, dtype=torch.float32, device="cuda")
+        check(lib.hep_layer_get_shared(self.handle, out.data_ptr(), _stream(stream)))
+        return out
+
     def gather_experts(self, stream=None):
         check(lib.hep_layer_gather_experts(self.handle, _stream(stream)))
 

@@ -61,10 +61,15 @@ def main():
     P = 2 * a.H * a.F
     flat = [torch.cat([w_up[e].float().reshape(-1), w_down[e].float().reshape(-1)]).numpy() for e in range(a.E)]
     shared = oracle.shared_mean(flat)
-    if a.sr:
-        layer.set_shared(torch.from_numpy(shared).cuda())
     for e in layer.owned_experts():
         layer.set_expert(e, w_up[e].cuda(), w_down[e].cuda())
+    if a.sr:
+        # the shared expert from every rank's owned experts (cross-GPU chain), twice: the
+        # second refresh must reuse the partial buffers safely and give the same bytes
+        for _ in range(2):
+            layer.refresh_shared()
+            got = layer.get_shared().cpu().numpy()
+            assert got.tobytes() == shared.tobytes(), "refreshed shared expert differs from the reference mean"
     layer.gather_experts()
     y = layer.forward(x_all[rank].cuda())
     dbg = layer.debug(a.T)

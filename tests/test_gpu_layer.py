@@ -115,3 +115,23 @@ def test_layer_forward_host_matches_device():
     torch.cuda.synchronize()
     assert torch.equal(y_dev, yh)
     layer.close()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_refresh_shared_single_gpu(dtype):
+    """refresh_shared with every expert local: the mean over the owned fp32 masters,
+    bit-exact with the reference's init_shared (sparsecomp.cpp:147-168)."""
+    from paper_2510_19470_b200.sr import CompressionConfig
+
+    H, F, E = 96, 160, 8
+    g = torch.Generator().manual_seed(3)
+    w_up, w_down = synthetic.experts(E, H, F, g, dtype=dtype)
+    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=2, max_tokens=64, dtype=dtype,
+                     sr=CompressionConfig(ratio_CR=8.0))
+    for e in range(E):
+        layer.set_expert(e, w_up[e].cuda(), w_down[e].cuda())
+    layer.refresh_shared()
+    got = layer.get_shared().cpu().numpy()
+    flat = [torch.cat([w_up[e].float().reshape(-1), w_down[e].float().reshape(-1)]).numpy() for e in range(E)]
+    assert got.tobytes() == oracle.shared_mean(flat).tobytes()
+    layer.close()
