@@ -413,6 +413,11 @@ void Layer::gather_experts(cudaStream_t s) {
     if (use_sr_) {
       if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
       stride = (wb + 15) / 16 * 16;
+      if (ag.epoch > 1) {  // every AG peer has pulled last epoch's wires before they are rewritten
+        P2PArgs prev = ag;
+        prev.epoch = ag.epoch - 1;
+        ck(launch_signal_wait(prev, 4, ag_s_, true, true, false), "wires pulled");
+      }
       std::vector<const void*> ex;
       std::vector<void*> wo;
       for (int64_t i = 0; i < n_; ++i) {
@@ -439,7 +444,10 @@ void Layer::gather_experts(cudaStream_t s) {
                            eb * n_ * per_slot_down, cudaMemcpyDeviceToDevice, ag_s_), "pull down");
       }
     }
-    if (use_sr_) decode_gathered(wb, stride, ag_s_);
+    if (use_sr_) {
+      ck(launch_signal_wait(ag, 4, ag_s_, false, true, true), "wires pulled");
+      decode_gathered(wb, stride, ag_s_);
+    }
     ck(cudaEventRecord(ev_ag_done_, ag_s_), "record");
     ag_pending_ = true;
     return;

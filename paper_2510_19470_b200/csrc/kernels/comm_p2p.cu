@@ -47,14 +47,15 @@ __device__ void wait_flag(const uint32_t* f, uint32_t epoch) {
 
 // Sync buffer of one rank (in its HBM, written by peers).
 struct SyncView {
-  uint32_t* flags;  // [4][kMaxG]: 0 counts, 1 dispatched, 2 outputs ready, 3 experts final; index = source
+  uint32_t* flags;  // [5][kMaxG]: 0 counts, 1 dispatched, 2 outputs ready, 3 experts final,
+                    // 4 "pulled your wires"; index = source
   int* inbox;       // [2][kMaxG][NK]: counts of every source, double-buffered by epoch parity
 };
 
 __device__ __forceinline__ SyncView view(void* base, int NK) {
   SyncView v;
   v.flags = static_cast<uint32_t*>(base);
-  v.inbox = reinterpret_cast<int*>(static_cast<uint8_t*>(base) + 4 * kMaxG * sizeof(uint32_t));
+  v.inbox = reinterpret_cast<int*>(static_cast<uint8_t*>(base) + kSyncSlots * kMaxG * sizeof(uint32_t));
   (void)NK;
   return v;
 }
@@ -191,13 +192,13 @@ __global__ void __launch_bounds__(256) permute_p2p_kernel(P2PArgs a, const uint8
 }
 
 // Raise flag `slot` on every A2A peer, then (if `wait`) wait for theirs.
-__global__ void signal_wait_kernel(P2PArgs a, int slot, int wait, int ag) {
+__global__ void signal_wait_kernel(P2PArgs a, int slot, int wait, int ag, int sig) {
   __threadfence_system();
   const int NK = a.G * a.E;
   const int i = threadIdx.x;
   const int n = ag ? a.n_ag : a.n_src[a.rank];
   const int* list = ag ? a.ag_list : a.src_list + a.rank * kMaxG;
-  if (i < n) st_release_sys(view(a.sync[list[i]], NK).flags + slot * kMaxG + a.rank, a.epoch);
+  if (sig && i < n) st_release_sys(view(a.sync[list[i]], NK).flags + slot * kMaxG + a.rank, a.epoch);
   if (!wait) return;
   __syncthreads();
   if (i < n) wait_flag(view(a.sync[a.rank], NK).flags + slot * kMaxG + list[i], a.epoch);
@@ -301,7 +302,7 @@ const uint32_t* p2p_dispatch_flags(const P2PArgs& a) {
 }
 
 size_t p2p_sync_bytes(int G, int E) {
-  return 4 * kMaxG * sizeof(uint32_t) + 2 * kMaxG * static_cast<size_t>(G) * E * sizeof(int) + 256;
+  return kSyncSlots * kMaxG * sizeof(uint32_t) + 2 * kMaxG * static_cast<size_t>(G) * E * sizeof(int) + 256;
 }
 
 cudaError_t launch_count_exchange(const P2PArgs& a, const int* key_total, const int* key_off,
@@ -341,8 +342,8 @@ cudaError_t launch_shared_chain(const ChainArgs& c, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait, bool ag_peers) {
-  signal_wait_kernel<<<1, 32, 0, s>>>(a, slot, wait ? 1 : 0, ag_peers ? 1 : 0);
+cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait, bool ag_peers, bool sig) {
+  signal_wait_kernel<<<1, 32, 0, s>>>(a, slot, wait ? 1 : 0, ag_peers ? 1 : 0, sig ? 1 : 0);
   return cudaGetLastError();
 }
 

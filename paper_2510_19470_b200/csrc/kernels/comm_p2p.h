@@ -9,6 +9,7 @@
 namespace hep {
 
 constexpr int kMaxG = 8;
+constexpr int kSyncSlots = 5;  // flag slots per rank's sync buffer (see launch_signal_wait)
 constexpr int kMaxE = 64;
 
 // Passed by value to every kernel: peer-mapped base pointers (index = rank; own rank
@@ -39,8 +40,11 @@ cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T,
                                const int* ranks, const int* chunk_off, const int* key_off, const int* send_base,
                                int* pos, cudaStream_t s, int mode = 0);
 // slot 1: "my rows are in your receive area"; slot 2: "your outputs are ready";
-// slot 3 (AG peers): "my experts for this epoch are final, pull them".
-cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait = true, bool ag_peers = false);
+// slot 3 (AG peers): "my experts for this epoch are final, pull them";
+// slot 4 (AG peers): "I have pulled your wires of this epoch" (before they are rewritten).
+// sig = false: wait only; wait = false: signal only.
+cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool wait = true, bool ag_peers = false,
+                               bool sig = true);
 // This rank's dispatch flags (indexed by source rank), for GEMM-side gating.
 const uint32_t* p2p_dispatch_flags(const P2PArgs& a);
 cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, const int* pos, const int* key_off,

@@ -583,6 +583,9 @@ constexpr int kFinThreads = 512;
 constexpr int kFinPer = 8;                        // consecutive units per thread per round
 constexpr int kFinRound = kFinThreads * kFinPer;  // 4096
 constexpr double kFinMaxList = 262144.0;          // longest expected list per slot on the cluster path
+constexpr int kFinSmemCap = 12288;                // list entries a CTA keeps in shared memory
+constexpr int kFinSmemPadded = kFinSmemCap + kFinSmemCap / 8;
+constexpr int kFinSmem = kFinSmemPadded * (sizeof(double) + sizeof(uint32_t));
 
 struct FinXch {
   unsigned long long tot[kFinCta];  // per-CTA slice totals / counts (written by the peers)
@@ -628,6 +631,11 @@ __global__ void __cluster_dims__(kFinCta, 1, 1) __launch_bounds__(kFinThreads)
   const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
   SelState& s = ws.st(b, r);
   if (s.mode != kModeList) return;  // uniform over the cluster (no CTA writes it before the end)
+  // the CTA's share of the list, resident across the passes and the emit when it fits
+  // (one pad word per 8 keeps the per-thread runs of 8 conflict-free)
+  extern __shared__ __align__(16) uint8_t fin_dyn[];
+  double* s_res = reinterpret_cast<double*>(fin_dyn);
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(fin_dyn + sizeof(double) * kFinSmemPadded);
   __shared__ unsigned int hist[kBins];
   __shared__ unsigned int slice[kBins / kFinCta];
   __shared__ unsigned int wtot[32];
@@ -645,16 +653,25 @@ __global__ void __cluster_dims__(kFinCta, 1, 1) __launch_bounds__(kFinThreads)
   double* lres = ws.lres(b, r);
   uint32_t* lidx = ws.lidx(b, r);
 
-  // 1. pack the staging segments into the dense list
+  // 1. gather this CTA's split tiles' staging segments (in index order): into shared
+  // memory when they fit, else into the dense list in global memory
+  int64_t my_lo = 0, my_hi = 0;  // this CTA's entries in list order
+  bool in_smem = false;
   if (list) {
     const unsigned int* cnt = ws.tcount(b, r);
     const int ntiles = static_cast<int>((n + kSplitTile - 1) / kSplitTile);
     const int t0 = static_cast<int>(static_cast<int64_t>(ntiles) * crank / kFinCta);
     const int t1 = static_cast<int>(static_cast<int64_t>(ntiles) * (crank + 1) / kFinCta);
-    unsigned int before = 0;
-    for (int t = threadIdx.x; t < t0; t += blockDim.x) before += cnt[t];
+    unsigned int before = 0, mine = 0;
+    for (int t = threadIdx.x; t < t1; t += blockDim.x) (t < t0 ? before : mine) += cnt[t];
     unsigned int tot;
-    before = block_scan_excl(before, wtot, &tot), before = tot;  // sum over the block
+    block_scan_excl(before, wtot, &tot);
+    before = tot;
+    block_scan_excl(mine, wtot, &tot);
+    mine = tot;
+    my_lo = before;
+    my_hi = static_cast<int64_t>(before) + mine;
+    in_smem = mine <= static_cast<unsigned int>(kFinSmemCap);
     const double* sres = ws.sres(b, r);
     const uint32_t* sidx = ws.sidx(b, r);
     unsigned int run = before;
@@ -692,24 +709,41 @@ __global__ void __cluster_dims__(kFinCta, 1, 1) __launch_bounds__(kFinThreads)
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           if (pp[q] < chunk) {
-            lres[run + pp[q]] = v[q];
-            lidx[run + pp[q]] = ii[q];
+            const unsigned int d = run + pp[q];
+            if (in_smem) {
+              const unsigned int l = d - before;
+              s_res[l + (l >> 3)] = v[q];
+              s_idx[l + (l >> 3)] = ii[q];
+            } else {
+              lres[d] = v[q];
+              lidx[d] = ii[q];
+            }
           }
       }
       run += chunk;
       __syncthreads();
     }
   }
-  cl.sync();  // the dense list is complete (release/acquire across the cluster)
+  __syncthreads();
 
-  // units: list entries, or the full range after a failed bracket
+  // units: this CTA's list entries, or an equal share of the full range after a failed
+  // bracket
   const int64_t units = list ? n_super : n;
   const int64_t per_cta = ((units + kFinCta - 1) / kFinCta + 7) & ~static_cast<int64_t>(7);
-  const int64_t u_lo = min(units, per_cta * crank), u_hi = min(units, u_lo + per_cta);
-  // residuals and relative indices of units u0 .. u0+7 (u0 a multiple of 8)
+  const int64_t u_lo = list ? my_lo : min(units, per_cta * crank);
+  const int64_t u_hi = list ? my_hi : min(units, u_lo + per_cta);
+  // residuals and relative indices of units u0 .. u0+7
   auto load8 = [&](int64_t u0, double (&rv)[kFinPer], uint32_t (&ix)[kFinPer]) {
-    if (list) {
-      if (u0 + kFinPer <= u_hi) {
+    if (list && in_smem) {
+#pragma unroll
+      for (int q = 0; q < kFinPer; ++q) {
+        const int64_t l = u0 + q - u_lo;
+        const bool in = u0 + q < u_hi;
+        rv[q] = in ? s_res[l + (l >> 3)] : 0.0;
+        ix[q] = in ? s_idx[l + (l >> 3)] : 0u;
+      }
+    } else if (list) {
+      if (((u0 & 7) == 0) && u0 + kFinPer <= u_hi) {
 #pragma unroll
         for (int q = 0; q < kFinPer; q += 2) {
           const double2 d = *reinterpret_cast<const double2*>(lres + u0 + q);
@@ -1569,6 +1603,7 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
       cudaFuncSetAttribute(sr_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSampleSmem);
       cudaFuncSetAttribute(sr_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 8);
       cudaFuncSetAttribute(sr_split_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 8);
+      cudaFuncSetAttribute(sr_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFinSmem);
       attr = true;
     }
     sr_sample_kernel<<<dim3(ra.nr, batch), kSampleThreads, kSampleSmem, stream>>>(ra, ws);
@@ -1578,8 +1613,8 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
     if (bulk) sr_split_kernel<true><<<sgrid, kTileThreads, smem, stream>>>(eb, bf16, shared, ra, ws);
     else sr_split_kernel<false><<<sgrid, kTileThreads, smem, stream>>>(eb, bf16, shared, ra, ws);
     if (cluster) {
-      sr_finish_kernel<<<dim3(kFinCta, slots), kFinThreads, 0, stream>>>(eb, bf16, shared, ra, ws, plan.index_bits,
-                                                                         plan.value_bits);
+      sr_finish_kernel<<<dim3(kFinCta, slots), kFinThreads, kFinSmem, stream>>>(eb, bf16, shared, ra, ws,
+                                                                                plan.index_bits, plan.value_bits);
     } else {
       sr_scan_kernel<<<slots, 1024, 0, stream>>>(ra, ws);
       sr_pack_kernel<<<dim3(std::max(1, 148 * 4 / slots), slots), kTileThreads, 0, stream>>>(ra, ws);
