@@ -123,7 +123,7 @@ def test_refresh_shared_single_gpu(dtype):
     bit-exact with the reference's init_shared (sparsecomp.cpp:147-168)."""
     from paper_2510_19470_b200.sr import CompressionConfig
 
-    H, F, E = 96, 160, 8
+    H, F, E = 128, 192, 8
     g = torch.Generator().manual_seed(3)
     w_up, w_down = synthetic.experts(E, H, F, g, dtype=dtype)
     layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=2, max_tokens=64, dtype=dtype,
