@@ -23,6 +23,7 @@ constexpr int kChunk = 32;      // tokens per gate block == ranking chunk
 constexpr int kHc = 64;         // hidden columns staged per step
 constexpr int kMaxE = 64;       // experts supported by the gate kernel
 constexpr int kMaxK = 8;
+constexpr int kMaxNK = 512;    // (destination, expert) keys: G * E, G <= 8 GPUs of one box
 
 template <typename T>
 __device__ __forceinline__ float to_f32(T v) { return static_cast<float>(v); }
@@ -202,6 +203,7 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
   __nv_bfloat16* ws = xs + static_cast<size_t>(kGStages) * kGT * kGPitch;         // [S][EROWS][pitch]
   __shared__ float logits[kGT][kMaxE + 1];
   __shared__ int skey[kGT][kMaxK];
+  __shared__ int kcount[kGT / kChunk][kMaxNK];  // per-chunk running key counts
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t0 = blockIdx.x * kGT;
@@ -269,76 +271,71 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
   }
   __syncthreads();
 
-  for (int q = 0; q < 16; ++q) {
-    const int r = warp * 16 + q;
+  // Top-k per token, two threads per token (each scans half of the E logits): k rounds
+  // of (local best among unused) -> pair exchange; order (logit desc, expert id asc).
+  {
+    const int r = tid >> 1, h = tid & 1;  // 128 threads = 64 tokens x 2
     const int t = t0 + r;
-    if (t >= T_tok) break;  // warp-uniform
-    float v0 = lane < E ? logits[r][lane] : -FLT_MAX;
-    float v1 = lane + 32 < E ? logits[r][lane + 32] : -FLT_MAX;
-    bool used0 = lane >= E, used1 = lane + 32 >= E;
+    const int half = E >> 1, e0 = h * half;
+    uint32_t used = 0;  // bit i: logit e0 + i taken (half <= 32)
     float sel_v[kMaxK];
     int sel_e[kMaxK];
     for (int j = 0; j < k; ++j) {
       float bv = -FLT_MAX;
       int be = 0x7fffffff;
-      if (!used0) { bv = v0; be = lane; }
-      if (!used1 && (be == 0x7fffffff || v1 > bv)) { bv = v1; be = lane + 32; }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
-        if (oe != 0x7fffffff && (be == 0x7fffffff || ov > bv || (ov == bv && oe < be))) {
-          bv = ov;
-          be = oe;
-        }
+      for (int i = 0; i < half; ++i) {
+        const float v = logits[r][e0 + i];
+        if (!((used >> i) & 1u) && (be == 0x7fffffff || v > bv)) { bv = v; be = e0 + i; }  // ids ascend
       }
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, 1);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, 1);
+      if (oe != 0x7fffffff && (be == 0x7fffffff || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
       sel_v[j] = bv;
       sel_e[j] = be;
-      if (be == lane) used0 = true;
-      if (be == lane + 32) used1 = true;
+      if (be >= e0 && be < e0 + half) used |= 1u << (be - e0);
     }
-    if (lane < k) {
-      float s = 0.f, mine = 0.f;
-      for (int j = 0; j < k; ++j) {
-        const float ex = expf(sel_v[j] - sel_v[0]);
-        s += ex;
-        if (j == lane) mine = ex;
+    if (t < T_tok) {
+      float s = 0.f;
+      for (int j = 0; j < k; ++j) s += expf(sel_v[j] - sel_v[0]);
+      for (int j = h; j < k; j += 2) {  // the pair splits the k slots
+        const size_t o = static_cast<size_t>(t) * k + j;
+        const int e = sel_e[j];
+        const int key = dest_of_owner[e / n_per_gpu] * E + e;
+        topk_idx[o] = e;
+        topk_w[o] = expf(sel_v[j] - sel_v[0]) / s;
+        keys[o] = key;
+        skey[r][j] = key;
       }
-      const size_t o = static_cast<size_t>(t) * k + lane;
-      const int e = sel_e[lane];
-      const int key = dest_of_owner[e / n_per_gpu] * E + e;
-      topk_idx[o] = e;
-      topk_w[o] = mine / s;
-      keys[o] = key;
-      skey[r][lane] = key;
     }
   }
   __syncthreads();
 
-  // Ranking per 32-token chunk (two chunks per block).
-  for (int sub = 0; sub < kGT / kChunk; ++sub) {
+  // Ranking per 32-token chunk (two chunks per block, one warp each): entries in
+  // (token, slot) order, 32 per round; lanes holding the same key find each other with
+  // match.any, the rank is the key's running count plus the lower lanes of the group.
+  if (warp < kGT / kChunk) {
+    const int sub = warp;
     const int chunk = blockIdx.x * (kGT / kChunk) + sub;
     const int c0 = sub * kChunk;
     const int valid = min(kChunk, T_tok - (t0 + c0));
-    if (valid <= 0) break;
-    int* counts = chunk_counts + static_cast<size_t>(chunk) * NK;
-    for (int i = tid; i < NK; i += blockDim.x) counts[i] = 0;
-    __syncthreads();
-    for (int i = tid; i < valid * k; i += blockDim.x) {
-      const int r = i / k, j = i % k;
-      const int key = skey[c0 + r][j];
-      int before = 0, after = 0;
-      for (int r2 = 0; r2 < valid; ++r2) {
-        if (r2 == r) continue;
-        for (int j2 = 0; j2 < k; ++j2)
-          if (skey[c0 + r2][j2] == key) {
-            if (r2 < r) ++before; else ++after;
-          }
+    if (valid > 0) {
+      int* cnt = kcount[sub];
+      for (int i = lane; i < NK; i += 32) cnt[i] = 0;
+      __syncwarp();
+      const int n_ent = valid * k;
+      for (int base = 0; base < n_ent; base += 32) {
+        const int i = base + lane;
+        const int key = i < n_ent ? skey[c0 + i / k][i % k] : -1;
+        const unsigned int peers = __match_any_sync(0xffffffffu, key);
+        const int before = __popc(peers & ((1u << lane) - 1u));
+        if (i < n_ent) ranks[static_cast<size_t>(t0 + c0) * k + i] = cnt[key] + before;
+        __syncwarp();
+        if (i < n_ent && before == 0) cnt[key] += __popc(peers);
+        __syncwarp();
       }
-      ranks[static_cast<size_t>(t0 + c0 + r) * k + j] = before;
-      if (after == 0) counts[key] = before + 1;
+      int* counts = chunk_counts + static_cast<size_t>(chunk) * NK;
+      for (int i = lane; i < NK; i += 32) counts[i] = cnt[i];
     }
-    __syncthreads();
   }
 }
 
@@ -548,7 +545,7 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
   if (E > kMaxE || k > kMaxK || k > E || T <= 0) return cudaErrorInvalidValue;
   if (dt == DType::BF16) {
     // wg_t is bf16 [E, H] for bf16 layers.
-    if (H % kGC || E % 8) return cudaErrorInvalidValue;
+    if (H % kGC || E % 8 || NK > kMaxNK || k > kMaxK) return cudaErrorInvalidValue;
     const int blocks = (T + kGT - 1) / kGT;
     auto go = [&](auto kern, size_t smem, bool& attr) {
       if (!attr) {  // once per instantiation
