@@ -159,12 +159,12 @@ __global__ void __launch_bounds__(256) gate_kernel(const T* __restrict__ x,
 // every partial sum is exactly representable, so the logits do not depend on the
 // tensor core's summation order.
 constexpr int kGT = 64;          // tokens per block
-constexpr int kGC = 64;          // hidden columns per stage
-constexpr int kGPitch = kGC + 8; // bf16 elements per smem row (16-byte pad: no ldmatrix conflicts)
+constexpr int kGCMin = 64;       // hidden columns per stage: H must be a multiple
 // Pipeline depth and gate-weight rows staged per stage: with few experts the x stream
 // gets a deeper pipeline (more bytes in flight per SM).
-template <int STAGES, int EROWS>
-constexpr size_t gate_smem() { return static_cast<size_t>(STAGES) * (kGT + EROWS) * kGPitch * 2; }
+// Wider stages read longer runs of each token row (128 or 256 B per row per stage).
+template <int STAGES, int EROWS, int GC>
+constexpr size_t gate_smem() { return static_cast<size_t>(STAGES) * (kGT + EROWS) * (GC + 8) * 2; }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
@@ -189,8 +189,8 @@ __device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int kGStages, int EROWS>
-__global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __restrict__ x,
+template <int kGStages, int EROWS, int kGC>
+__global__ void __launch_bounds__(256) gate_mma_kernel(const __nv_bfloat16* __restrict__ x,
                                                       const __nv_bfloat16* __restrict__ wg_t, int T_tok,
                                                       int H, int E, int k,
                                                       const int* __restrict__ dest_of_owner, int n_per_gpu,
@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
                                                       float* __restrict__ topk_w, int* __restrict__ keys,
                                                       int* __restrict__ ranks,
                                                       int* __restrict__ chunk_counts) {
+  constexpr int kGPitch = kGC + 8;  // bf16 elements per smem row (16-byte pad: no ldmatrix conflicts)
   extern __shared__ __align__(128) uint8_t gsm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(gsm);                      // [S][64][pitch]
   __nv_bfloat16* ws = xs + static_cast<size_t>(kGStages) * kGT * kGPitch;         // [S][EROWS][pitch]
@@ -215,13 +216,14 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
     __nv_bfloat16* xd = xs + static_cast<size_t>(s) * kGT * kGPitch;
     __nv_bfloat16* wd = ws + static_cast<size_t>(s) * EROWS * kGPitch;
 #pragma unroll
-    for (int i = tid; i < kGT * (kGC / 8); i += 128) {
-      const int r = i >> 3, c8 = (i & 7) * 8;
+    constexpr int kCh = kGC / 8;  // 16-byte chunks per row per stage
+    for (int i = tid; i < kGT * kCh; i += 256) {
+      const int r = i / kCh, c8 = (i % kCh) * 8;
       const int t = t0 + r;
       cp_async16(xd + r * kGPitch + c8, x + static_cast<size_t>(t < T_tok ? t : 0) * H + hc + c8, t < T_tok);
     }
-    for (int i = tid; i < E * (kGC / 8); i += 128) {
-      const int r = i >> 3, c8 = (i & 7) * 8;
+    for (int i = tid; i < E * kCh; i += 256) {
+      const int r = i / kCh, c8 = (i % kCh) * 8;
       cp_async16(wd + r * kGPitch + c8, wg_t + static_cast<size_t>(r) * H + hc + c8, true);
     }
   };
@@ -242,10 +244,13 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
     if (pre < nkc) load_stage(pre % kGStages, pre);
     cp_async_commit();
     const int s = kc % kGStages;
-    const __nv_bfloat16* xa = xs + static_cast<size_t>(s) * kGT * kGPitch + (warp * 16) * kGPitch;
+    const __nv_bfloat16* xa = xs + static_cast<size_t>(s) * kGT * kGPitch + ((warp & 3) * 16) * kGPitch;
     const __nv_bfloat16* wb = ws + static_cast<size_t>(s) * EROWS * kGPitch;
+    // split-K inside the block: warps 0-3 take the stage's first half of 16-column
+    // steps, warps 4-7 the second half (8 warps in flight per block)
+    constexpr int kHalf = kGC / 32;
 #pragma unroll
-    for (int ks = 0; ks < kGC / 16; ++ks) {
+    for (int ks = (warp >> 2) * kHalf; ks < (warp >> 2) * kHalf + kHalf; ++ks) {
       uint32_t a[4];
       ldsm_x4(xa + (lane & 15) * kGPitch + ks * 16 + (lane >> 4) * 8, a[0], a[1], a[2], a[3]);
 #pragma unroll
@@ -260,24 +265,41 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
     }
   }
   cp_async_wait<0>();
+  __syncthreads();  // the stage buffers are free: the k-half partials go there
+  float (*part)[kMaxE + 1] = reinterpret_cast<float (*)[kMaxE + 1]>(gsm);
+  if (warp >= 4) {
 #pragma unroll
-  for (int nt = 0; nt < kMaxE / 8; ++nt) {
-    if (nt >= ntiles) break;
-    const int r = warp * 16 + (lane >> 2), c = nt * 8 + (lane & 3) * 2;
-    logits[r][c] = acc[nt][0];
-    logits[r][c + 1] = acc[nt][1];
-    logits[r + 8][c] = acc[nt][2];
-    logits[r + 8][c + 1] = acc[nt][3];
+    for (int nt = 0; nt < kMaxE / 8; ++nt) {
+      if (nt >= ntiles) break;
+      const int r = (warp & 3) * 16 + (lane >> 2), c = nt * 8 + (lane & 3) * 2;
+      part[r][c] = acc[nt][0];
+      part[r][c + 1] = acc[nt][1];
+      part[r + 8][c] = acc[nt][2];
+      part[r + 8][c + 1] = acc[nt][3];
+    }
+  }
+  __syncthreads();
+  if (warp < 4) {
+#pragma unroll
+    for (int nt = 0; nt < kMaxE / 8; ++nt) {
+      if (nt >= ntiles) break;
+      const int r = warp * 16 + (lane >> 2), c = nt * 8 + (lane & 3) * 2;
+      logits[r][c] = acc[nt][0] + part[r][c];
+      logits[r][c + 1] = acc[nt][1] + part[r][c + 1];
+      logits[r + 8][c] = acc[nt][2] + part[r + 8][c];
+      logits[r + 8][c + 1] = acc[nt][3] + part[r + 8][c + 1];
+    }
   }
   __syncthreads();
 
-  // Top-k per token, two threads per token (each scans half of the E logits): k rounds
-  // of (local best among unused) -> pair exchange; order (logit desc, expert id asc).
+  // Top-k per token, four threads per token (each scans a quarter of the E logits): k
+  // rounds of (local best among unused) -> exchange within the quad; order (logit desc,
+  // expert id asc).
   {
-    const int r = tid >> 1, h = tid & 1;  // 128 threads = 64 tokens x 2
+    const int r = tid >> 2, h = tid & 3;  // 256 threads = 64 tokens x 4
     const int t = t0 + r;
-    const int half = E >> 1, e0 = h * half;
-    uint32_t used = 0;  // bit i: logit e0 + i taken (half <= 32)
+    const int half = E >> 2, e0 = h * half;
+    uint32_t used = 0;  // bit i: logit e0 + i taken (quarter <= 16)
     float sel_v[kMaxK];
     int sel_e[kMaxK];
     for (int j = 0; j < k; ++j) {
@@ -287,9 +309,12 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
         const float v = logits[r][e0 + i];
         if (!((used >> i) & 1u) && (be == 0x7fffffff || v > bv)) { bv = v; be = e0 + i; }  // ids ascend
       }
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, 1);
-      const int oe = __shfl_xor_sync(0xffffffffu, be, 1);
-      if (oe != 0x7fffffff && (be == 0x7fffffff || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
+#pragma unroll
+      for (int off = 1; off <= 2; off <<= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (oe != 0x7fffffff && (be == 0x7fffffff || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
+      }
       sel_v[j] = bv;
       sel_e[j] = be;
       if (be >= e0 && be < e0 + half) used |= 1u << (be - e0);
@@ -297,7 +322,7 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
     if (t < T_tok) {
       float s = 0.f;
       for (int j = 0; j < k; ++j) s += expf(sel_v[j] - sel_v[0]);
-      for (int j = h; j < k; j += 2) {  // the pair splits the k slots
+      for (int j = h; j < k; j += 4) {  // the quad splits the k slots
         const size_t o = static_cast<size_t>(t) * k + j;
         const int e = sel_e[j];
         const int key = dest_of_owner[e / n_per_gpu] * E + e;
@@ -545,7 +570,7 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
   if (E > kMaxE || k > kMaxK || k > E || T <= 0) return cudaErrorInvalidValue;
   if (dt == DType::BF16) {
     // wg_t is bf16 [E, H] for bf16 layers.
-    if (H % kGC || E % 8 || NK > kMaxNK || k > kMaxK) return cudaErrorInvalidValue;
+    if (H % kGCMin || E % 8 || NK > kMaxNK || k > kMaxK) return cudaErrorInvalidValue;
     const int blocks = (T + kGT - 1) / kGT;
     auto go = [&](auto kern, size_t smem, bool& attr) {
       if (!attr) {  // once per instantiation
@@ -554,16 +579,17 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
         if (e != cudaSuccess) return e;
         attr = true;
       }
-      kern<<<blocks, 128, smem, stream>>>(static_cast<const __nv_bfloat16*>(x),
+      kern<<<blocks, 256, smem, stream>>>(static_cast<const __nv_bfloat16*>(x),
                                           static_cast<const __nv_bfloat16*>(wg_t), T, H, E, k, dest_of_owner,
                                           experts_per_gpu, NK, topk_idx, topk_w, keys, ranks, chunk_counts);
       return cudaSuccess;
     };
-    static bool a8 = false, a16 = false, a64 = false;
+    static bool a8 = false, a8w = false, a16 = false, a64 = false;
     cudaError_t e;
-    if (E <= 8) e = go(gate_mma_kernel<8, 8>, gate_smem<8, 8>(), a8);
-    else if (E <= 16) e = go(gate_mma_kernel<8, 16>, gate_smem<8, 16>(), a16);
-    else e = go(gate_mma_kernel<4, kMaxE>, gate_smem<4, kMaxE>(), a64);
+    if (E <= 8 && H % 128 == 0) e = go(gate_mma_kernel<4, 8, 128>, gate_smem<4, 8, 128>(), a8w);
+    else if (E <= 8) e = go(gate_mma_kernel<8, 8, 64>, gate_smem<8, 8, 64>(), a8);
+    else if (E <= 16) e = go(gate_mma_kernel<8, 16, 64>, gate_smem<8, 16, 64>(), a16);
+    else e = go(gate_mma_kernel<4, kMaxE, 64>, gate_smem<4, kMaxE, 64>(), a64);
     if (e != cudaSuccess) return e;
   } else {
     const int nchunks = (T + kChunk - 1) / kChunk;
