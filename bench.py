@@ -220,6 +220,28 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def bind_to_gpu_numa(device_index):
+    """Pin this rank's host threads to the CPUs NVML reports as local to its GPU, so the
+    pinned host buffers of the e2e leg are first-touched on the GPU's NUMA node (the
+    H2D/D2H traffic of all ranks then stays off the socket interconnect)."""
+    try:
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        bus = torch.cuda.get_device_properties(device_index).pci_bus_id
+        dom = torch.cuda.get_device_properties(device_index).pci_domain_id
+        dev = torch.cuda.get_device_properties(device_index).pci_device_id
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{dom:08x}:{bus:02x}:{dev:02x}.0")
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return sorted(cpus)
+    except Exception:
+        return None
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
@@ -237,6 +259,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     torch.cuda.set_device(local)
+    numa_cpus = bind_to_gpu_numa(local) if world > 1 else None
     dev = torch.device("cuda", local)
     comm = None
     if world > 1:
@@ -421,6 +444,7 @@ def main():
             "dtype": cfg["dtype"], "data": "synthetic (dyadic tokens/gate, reference demo expert population)",
             "config": {"workload": cfg["workload"], "tokens_per_gpu": T, "hidden": H, "ffn": F, "experts": E,
                        "top_k": k, "sf": sf, "sed": sed, "layers": cfg["layers"], "sr_migration": use_sr,
+                       "e2e_host_threads": f"bound to {len(numa_cpus)} GPU-local cores (NVML affinity)" if numa_cpus else "unbound",
                        "planner_p": p_plan, "sed_source": sed_source, "comm": "nccl" if os.environ.get("HEP_COMM") == "nccl" else "nvlink-p2p",
                        "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per GPU)" %
                              (T * row_bytes / 1e6, cfg["layers"] * len(layer.owned_experts()) * 2 * H * F * (row_bytes // H) / 1e9)},
