@@ -138,7 +138,30 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
     ck(make_tmap_bf16_2d(&map_b1_, w_up_c_.p, slots_ * F_, H_, b_box, 64), "tmap b1");
     ck(make_tmap_bf16_2d(&map_a2_, hbuf_.p, rows_cap_, F_, 128, 64), "tmap a2");
     ck(make_tmap_bf16_2d(&map_b2_, w_down_c_.p, slots_ * H_, F_, b_box, 64), "tmap b2");
+  } else {
+    const char* f32 = std::getenv("HEP_F32_GEMM");
+    tf32_ = !(f32 && std::string(f32) == "simt") && H_ % 32 == 0 && F_ % 32 == 0;
+    if (tf32_) {
+      const size_t fb = sizeof(float);
+      xhi_.alloc(fb * rows_cap_ * H_);
+      xlo_.alloc(fb * rows_cap_ * H_);
+      hhi_.alloc(fb * rows_cap_ * F_);
+      hlo_.alloc(fb * rows_cap_ * F_);
+      wuhi_.alloc(fb * slots_ * F_ * H_);
+      wulo_.alloc(fb * slots_ * F_ * H_);
+      wdhi_.alloc(fb * slots_ * H_ * F_);
+      wdlo_.alloc(fb * slots_ * H_ * F_);
+      ck(make_tmap_f32_2d(&t_xhi_, xhi_.p, rows_cap_, H_, 128, 32), "tmap xhi");
+      ck(make_tmap_f32_2d(&t_xlo_, xlo_.p, rows_cap_, H_, 128, 32), "tmap xlo");
+      ck(make_tmap_f32_2d(&t_hhi_, hhi_.p, rows_cap_, F_, 128, 32), "tmap hhi");
+      ck(make_tmap_f32_2d(&t_hlo_, hlo_.p, rows_cap_, F_, 128, 32), "tmap hlo");
+      ck(make_tmap_f32_2d(&t_wuhi_, wuhi_.p, slots_ * F_, H_, 256, 32), "tmap wuhi");
+      ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, slots_ * F_, H_, 256, 32), "tmap wulo");
+      ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, slots_ * H_, F_, 256, 32), "tmap wdhi");
+      ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, slots_ * H_, F_, 256, 32), "tmap wdlo");
+    }
   }
+  slot_dirty_.assign(static_cast<size_t>(slots_), 1);
 
   if (use_sr_) {
     const int64_t P = 2 * H_ * F_;
@@ -310,6 +333,7 @@ void Layer::set_expert(int64_t e, const void* w_up, const void* w_down, DType dt
   uint8_t* down = w_down_c_.as<uint8_t>() + eb * slot * H_ * F_;
   ck(launch_transpose_convert(dt, w_up, H_, F_, dt_, up, s), "w_up layout");
   ck(launch_transpose_convert(dt, w_down, F_, H_, dt_, down, s), "w_down layout");
+  slot_dirty_[static_cast<size_t>(slot)] = 1;
   if (use_sr_) {
     // fp32 master copy in the reference flat layout (w_up then w_down) for encode.
     const int64_t P = 2 * H_ * F_;
@@ -393,8 +417,30 @@ void Layer::finish_shared(cudaStream_t s) {
                               shared_c_.as<uint8_t>() + eb * H_ * F_, s), "shared down");
 }
 
+void Layer::mark_gathered_dirty() {
+  for (int64_t p : ag_peers_)
+    for (int64_t i = 0; i < n_; ++i)
+      slot_dirty_[static_cast<size_t>(slot_of_expert_[static_cast<size_t>(p * n_ + i)])] = 1;
+}
+
+void Layer::split_dirty_slots(cudaStream_t s) {
+  const int64_t per = F_ * H_;
+  for (int64_t a = 0; a < slots_;) {
+    if (!slot_dirty_[static_cast<size_t>(a)]) { ++a; continue; }
+    int64_t b = a;
+    while (b < slots_ && slot_dirty_[static_cast<size_t>(b)]) slot_dirty_[static_cast<size_t>(b++)] = 0;
+    ck(launch_split_tf32(w_up_c_.as<float>() + a * per, wuhi_.as<float>() + a * per, wulo_.as<float>() + a * per,
+                         (b - a) * per, s), "split w_up");
+    ck(launch_split_tf32(w_down_c_.as<float>() + a * per, wdhi_.as<float>() + a * per,
+                         wdlo_.as<float>() + a * per, (b - a) * per, s), "split w_down");
+    launches_ += 2;
+    a = b;
+  }
+}
+
 void Layer::gather_experts(cudaStream_t s) {
   if (G_ == 1 || ag_peers_.empty()) return;
+  mark_gathered_dirty();  // the gathered slots' compute copies are rewritten below
   const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
   const size_t per_slot_up = static_cast<size_t>(F_ * H_), per_slot_down = static_cast<size_t>(H_ * F_);
   auto first_slot_of = [&](int64_t owner) { return slot_of_expert_[static_cast<size_t>(owner * n_)]; };
@@ -622,6 +668,18 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     ck(gemm(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_), "gemm up");
     mark(down.c_str(), s);
     ck(gemm(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_), "gemm down");
+  } else if (tf32_) {
+    mark(up.c_str(), s);
+    split_dirty_slots(s);
+    ck(launch_split_tf32(xall_.as<float>(), xhi_.as<float>(), xlo_.as<float>(), rows_cap_ * H_, s), "split x");
+    ck(launch_grouped_gemm_tf32x3(t_xhi_, t_xlo_, t_wuhi_, t_wulo_, hhi_.as<float>(), hlo_.as<float>(),
+                                  static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s),
+       "gemm up");
+    mark(down.c_str(), s);
+    ck(launch_grouped_gemm_tf32x3(t_hhi_, t_hlo_, t_wdhi_, t_wdlo_, oall_.as<float>(), nullptr, static_cast<int>(H_),
+                                  static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s),
+       "gemm down");
+    launches_ += 1;
   } else {
     mark(up.c_str(), s);
     ck(launch_grouped_gemm_f32(xall_.as<float>(), static_cast<int>(H_), w_up_c_.as<float>(), hbuf_.as<float>(), static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_ * 2, s), "gemm up");

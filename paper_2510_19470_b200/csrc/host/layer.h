@@ -102,6 +102,13 @@ class Layer {
   DevBuf pos_, xall_, hbuf_, oall_;
   int64_t rows_cap_;
   CUtensorMap map_a1_, map_b1_, map_a2_, map_b2_;
+  // fp32 layers on the tensor cores (3xTF32): every GEMM operand as a tf32 hi/lo pair
+  bool tf32_ = false;
+  DevBuf xhi_, xlo_, hhi_, hlo_, wuhi_, wulo_, wdhi_, wdlo_;
+  CUtensorMap t_xhi_, t_xlo_, t_hhi_, t_hlo_, t_wuhi_, t_wulo_, t_wdhi_, t_wdlo_;
+  std::vector<char> slot_dirty_;  // compute-copy slots whose hi/lo split is stale
+  void split_dirty_slots(cudaStream_t s);
+  void mark_gathered_dirty();
   uint32_t sched_up_ = 0, sched_down_ = 0;
   bool cta_pair_ = true;
 

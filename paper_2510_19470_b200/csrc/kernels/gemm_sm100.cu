@@ -538,6 +538,277 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+
+// ============================================================================
+// fp32 layers (cfg1/cfg2): the same persistent 1-CTA structure on kind::tf32 with the
+// 3xTF32 split.  Every fp32 operand x is carried as x_hi = rna_tf32(x) and
+// x_lo = rna_tf32(x - x_hi); D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi in fp32 TMEM
+// accumulators drops only the lo*lo term (~2^-22 relative per product), so the result
+// meets the fp32 1e-4 bound that single TF32 (10-bit mantissa) cannot, at tensor-core
+// rates.  A stage holds 32 fp32 of K (one 128-byte swizzle row) for A_hi, A_lo, B_hi,
+// B_lo: 16 + 16 + 32 + 32 KB, two stages.  Epilogue: fp32 rows, or (split mode) the
+// ReLU'd rows already split into hi/lo for the next GEMM.
+constexpr int T_BK = 32;
+constexpr int T_STAGES = 2;
+constexpr int T_A_BYTES = BM * T_BK * 4;
+constexpr int T_B_BYTES = BN * T_BK * 4;
+constexpr int T_STAGE_BYTES = 2 * T_A_BYTES + 2 * T_B_BYTES;
+
+struct SmemCtlT {
+  uint64_t full[T_STAGES];
+  uint64_t empty[T_STAGES];
+  uint64_t tfull[ACC];
+  uint64_t tempty[ACC];
+  uint32_t tmem_base;
+  int num_tiles;
+  int tile_start[kMaxGroups + 1];
+  int row_start[kMaxGroups];
+  int rows[kMaxGroups];
+  int slot[kMaxGroups];
+};
+constexpr size_t kSmemBytesT = 1024 + T_STAGES * T_STAGE_BYTES + sizeof(SmemCtlT);
+
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
+  return (1u << 4)                                   // D format fp32
+         | (2u << 7)                                 // A format tf32
+         | (2u << 10)                                // B format tf32
+         | (static_cast<uint32_t>(N >> 3) << 17)     // N / 8
+         | (static_cast<uint32_t>(M >> 4) << 24);    // M / 16
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
+                           const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
+                           float* __restrict__ C, float* __restrict__ C_lo, int ldc, int N, int K,
+                           const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
+                           const int* __restrict__ g_slot, int ng, int relu) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  SmemCtlT& s = *reinterpret_cast<SmemCtlT*>(smem + T_STAGES * T_STAGE_BYTES);
+  auto a_hi_at = [&](int st) { return smem + st * T_STAGE_BYTES; };
+  auto a_lo_at = [&](int st) { return smem + st * T_STAGE_BYTES + T_A_BYTES; };
+  auto b_hi_at = [&](int st) { return smem + st * T_STAGE_BYTES + 2 * T_A_BYTES; };
+  auto b_lo_at = [&](int st) { return smem + st * T_STAGE_BYTES + 2 * T_A_BYTES + T_B_BYTES; };
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_kb = K / T_BK;
+
+  if (warp == 2) {
+    int carry = 0;
+    for (int base = 0; base < ng; base += 32) {
+      const int g = base + lane;
+      int tiles = 0;
+      if (g < ng) {
+        const int r = g_rows[g];
+        s.row_start[g] = g_row_start[g];
+        s.rows[g] = r;
+        s.slot[g] = g_slot[g];
+        tiles = ((r + BM - 1) / BM) * n_tiles;
+      }
+      int incl = tiles;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+      }
+      if (g < ng) s.tile_start[g] = carry + incl - tiles;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      s.tile_start[ng] = carry;
+      s.num_tiles = carry;
+    }
+  } else if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a_hi);
+    tma_prefetch_desc(&map_a_lo);
+    tma_prefetch_desc(&map_b_hi);
+    tma_prefetch_desc(&map_b_lo);
+    for (int i = 0; i < T_STAGES; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < ACC; ++i) {
+      mbar_init(&s.tfull[i], 1);
+      mbar_init(&s.tempty[i], 4);
+    }
+    fence_barrier_init();
+  } else if (warp == 1) {
+    tmem_alloc(&s.tmem_base, TMEM_COLS);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  const int total = s.num_tiles;
+  const uint32_t tmem_base = s.tmem_base;
+  // tiles walk (group, m-tile, n-tile) with m fastest: a group's A rows stay in L2
+  // across its n-tiles
+
+  if (warp == 0) {
+    if (lane == 0) {  // ================= TMA producer =================
+      const uint64_t pol = make_policy(0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        int lo = 0, hi = ng - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s.tile_start[mid] <= tile) lo = mid; else hi = mid - 1;
+        }
+        const int g = lo;
+        const int local = tile - s.tile_start[g];
+        const int m_tiles = (s.rows[g] + BM - 1) / BM;
+        const int mt = local % m_tiles, nt = local / m_tiles;
+        const int a_row = s.row_start[g] + mt * BM;
+        const int b_row = s.slot[g] * N + nt * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&s.empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&s.full[stage], T_STAGE_BYTES);
+          tma_load_2d(a_hi_at(stage), &map_a_hi, &s.full[stage], kb * T_BK, a_row, pol);
+          tma_load_2d(a_lo_at(stage), &map_a_lo, &s.full[stage], kb * T_BK, a_row, pol);
+          tma_load_2d(b_hi_at(stage), &map_b_hi, &s.full[stage], kb * T_BK, b_row, pol);
+          tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], kb * T_BK, b_row, pol);
+          if (++stage == T_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ================= MMA issuer =================
+      constexpr uint32_t idesc = umma_idesc_tf32(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&s.full[stage], phase);
+          tc_fence_after();
+          const uint32_t ah = smem_addr(a_hi_at(stage)), al = smem_addr(a_lo_at(stage));
+          const uint32_t bh = smem_addr(b_hi_at(stage)), bl = smem_addr(b_lo_at(stage));
+#pragma unroll
+          for (int k = 0; k < T_BK / 8; ++k) {  // K = 8 tf32 (32 bytes) per instruction
+            const uint32_t off = 32u * k;
+            umma_tf32(d_tmem, umma_desc_k_sw128(al + off), umma_desc_k_sw128(bh + off), idesc, (kb | k) != 0);
+            umma_tf32(d_tmem, umma_desc_k_sw128(ah + off), umma_desc_k_sw128(bl + off), idesc, 1);
+            umma_tf32(d_tmem, umma_desc_k_sw128(ah + off), umma_desc_k_sw128(bh + off), idesc, 1);
+          }
+          umma_commit(&s.empty[stage]);
+          if (++stage == T_STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&s.tfull[acc]);
+        if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ================= epilogue (warps 2..5) =================
+    const uint32_t quarter = warp & 3u;
+    const int row_in_tile = static_cast<int>(quarter * 32 + lane);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int lo = 0, hi = ng - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s.tile_start[mid] <= tile) lo = mid; else hi = mid - 1;
+      }
+      const int g = lo;
+      const int local = tile - s.tile_start[g];
+      const int m_tiles = (s.rows[g] + BM - 1) / BM;
+      const int mt = local % m_tiles, nt = local / m_tiles;
+      const int r_local = mt * BM + row_in_tile;
+      const bool row_ok = r_local < s.rows[g];
+      const size_t row_off = static_cast<size_t>(s.row_start[g] + r_local) * ldc + nt * BN;
+
+      mbar_wait(&s.tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_base = tmem_base + static_cast<uint32_t>(acc * BN) + ((quarter * 32u) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        if (nt * BN + c >= N) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_base + static_cast<uint32_t>(c), v);
+        tmem_ld_wait();
+        if (row_ok) {
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = __uint_as_float(v[i]);
+            f[i] = relu ? fmaxf(x, 0.f) : x;
+          }
+          if (C_lo) {  // split for the next GEMM
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 h, l;
+              h.x = rna_tf32(f[4 * q]);     l.x = rna_tf32(f[4 * q] - h.x);
+              h.y = rna_tf32(f[4 * q + 1]); l.y = rna_tf32(f[4 * q + 1] - h.y);
+              h.z = rna_tf32(f[4 * q + 2]); l.z = rna_tf32(f[4 * q + 2] - h.z);
+              h.w = rna_tf32(f[4 * q + 3]); l.w = rna_tf32(f[4 * q + 3] - h.w);
+              *reinterpret_cast<float4*>(C + row_off + c + 4 * q) = h;
+              *reinterpret_cast<float4*>(C_lo + row_off + c + 4 * q) = l;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(C + row_off + c + 4 * q) =
+                  make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.tempty[acc]);
+      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+__global__ void split_tf32_kernel(const float* __restrict__ in, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t n4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = reinterpret_cast<const float4*>(in)[i];
+    float4 h, l;
+    h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
+    h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
+    h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
+    h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
+    reinterpret_cast<float4*>(hi)[i] = h;
+    reinterpret_cast<float4*>(lo)[i] = l;
+  }
+}
+
 }  // namespace
 
 bool gemm_use_cta_pair() {
@@ -578,6 +849,44 @@ cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows,
                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                             uint32_t box_cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 4};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
+                                       const CUtensorMap& b_lo, float* C, float* C_lo, int ldc, int N, int K,
+                                       const GroupTable& groups, int relu, int num_sms, cudaStream_t stream) {
+  if (K % T_BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(kSmemBytesT));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  grouped_gemm_tf32x3_kernel<<<num_sms, kThreads, kSmemBytesT, stream>>>(
+      a_hi, a_lo, b_hi, b_lo, C, C_lo, ldc, N, K, groups.row_start, groups.rows, groups.slot, groups.num_groups, relu);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_tf32(const float* in, float* hi, float* lo, int64_t n, cudaStream_t stream) {
+  if (n % 4) return cudaErrorInvalidValue;
+  const int64_t n4 = n / 4;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n4 + 255) / 256)));
+  split_tf32_kernel<<<blocks, 256, 0, stream>>>(in, hi, lo, n4);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C,

@@ -88,6 +88,15 @@ bool gemm_use_cta_pair();
 uint32_t gemm_schedule(int rows_per_expert, int N, int K, bool up);
 
 // fp32 SIMT grouped GEMM (gemm_f32.cu), same contract with fp32 operands.
+// fp32 layers on the tensor cores: 3xTF32 (gemm_sm100.cu).  Operands come as hi/lo tf32
+// pairs (launch_split_tf32); C_lo != nullptr stores the ReLU'd result split the same way.
+cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                             uint32_t box_cols);
+cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
+                                       const CUtensorMap& b_lo, float* C, float* C_lo, int ldc, int N, int K,
+                                       const GroupTable& groups, int relu, int num_sms, cudaStream_t stream);
+cudaError_t launch_split_tf32(const float* in, float* hi, float* lo, int64_t n, cudaStream_t stream);
+
 cudaError_t launch_grouped_gemm_f32(const float* A, int lda, const float* B, float* C, int ldc,
                                     int N, int K, const GroupTable& groups, int relu,
                                     int num_blocks, cudaStream_t stream);
