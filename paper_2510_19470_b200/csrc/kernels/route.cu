@@ -364,6 +364,108 @@ __global__ void __launch_bounds__(256) gate_mma_kernel(const __nv_bfloat16* __re
   }
 }
 
+// fp32 gate with the whole chunk resident: one block = one 32-token ranking chunk; x
+// rows and W_g^T land in shared memory through cp.async in one shot (no per-column
+// round trips), logits on the CUDA cores (exact for the dyadic parity inputs), top-k by
+// eight threads per token, ranking by match.any as in the bf16 kernel.
+__global__ void __launch_bounds__(256) gate_f32_oneshot_kernel(const float* __restrict__ x,
+                                                               const float* __restrict__ wg_t, int T_tok, int H,
+                                                               int E, int k, const int* __restrict__ dest_of_owner,
+                                                               int n_per_gpu, int NK, int* __restrict__ topk_idx,
+                                                               float* __restrict__ topk_w, int* __restrict__ keys,
+                                                               int* __restrict__ ranks,
+                                                               int* __restrict__ chunk_counts) {
+  extern __shared__ __align__(16) float fsm[];
+  const int pitch = H + 4;  // floats; rows stay 16-byte aligned
+  float* xs = fsm;                   // [kChunk][pitch]
+  float* ws = fsm + kChunk * pitch;  // [E][pitch]
+  __shared__ float logits[kChunk][kMaxE + 1];
+  __shared__ int skey[kChunk][kMaxK];
+  __shared__ int kcount[kMaxNK];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int chunk = blockIdx.x, t0 = chunk * kChunk;
+  const int c4 = H / 4;
+  for (int i = tid; i < kChunk * c4; i += blockDim.x) {
+    const int r = i / c4, c = (i % c4) * 4, t = t0 + r;
+    cp_async16(xs + r * pitch + c, x + static_cast<size_t>(t < T_tok ? t : 0) * H + c, t < T_tok);
+  }
+  for (int i = tid; i < E * c4; i += blockDim.x) {
+    const int r = i / c4, c = (i % c4) * 4;
+    cp_async16(ws + r * pitch + c, wg_t + static_cast<size_t>(r) * H + c, true);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  {
+    const int tok = tid >> 3, eg = tid & 7;  // experts eg, eg + 8, ... (only the real ones)
+    const float* xr = xs + tok * pitch;
+    for (int e = eg; e < E; e += 8) {
+      const float* wr = ws + e * pitch;
+      float acc = 0.f;
+#pragma unroll 8
+      for (int c = 0; c < H; ++c) acc = fmaf(xr[c], wr[c], acc);
+      logits[tok][e] = acc;
+    }
+  }
+  __syncthreads();
+  {  // top-k: eight threads per token, each scans E/8 logits
+    const int r = tid >> 3, h = tid & 7, t = t0 + r;
+    const int part = E >> 3, e0 = h * part;
+    uint32_t used = 0;
+    float sel_v[kMaxK];
+    int sel_e[kMaxK];
+    for (int j = 0; j < k; ++j) {
+      float bv = -FLT_MAX;
+      int be = 0x7fffffff;
+      for (int i = 0; i < part; ++i) {
+        const float v = logits[r][e0 + i];
+        if (!((used >> i) & 1u) && (be == 0x7fffffff || v > bv)) { bv = v; be = e0 + i; }
+      }
+#pragma unroll
+      for (int off = 1; off <= 4; off <<= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (oe != 0x7fffffff && (be == 0x7fffffff || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
+      }
+      sel_v[j] = bv;
+      sel_e[j] = be;
+      if (be >= e0 && be < e0 + part) used |= 1u << (be - e0);
+    }
+    if (t < T_tok) {
+      float ssum = 0.f;
+      for (int j = 0; j < k; ++j) ssum += expf(sel_v[j] - sel_v[0]);
+      for (int j = h; j < k; j += 8) {
+        const size_t o = static_cast<size_t>(t) * k + j;
+        const int e = sel_e[j];
+        const int key = dest_of_owner[e / n_per_gpu] * E + e;
+        topk_idx[o] = e;
+        topk_w[o] = expf(sel_v[j] - sel_v[0]) / ssum;
+        keys[o] = key;
+        skey[r][j] = key;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {  // ranking of the chunk's (token, slot) entries
+    const int valid = min(kChunk, T_tok - t0);
+    for (int i = lane; i < NK; i += 32) kcount[i] = 0;
+    __syncwarp();
+    const int n_ent = valid * k;
+    for (int base = 0; base < n_ent; base += 32) {
+      const int i = base + lane;
+      const int key = i < n_ent ? skey[i / k][i % k] : -1;
+      const unsigned int peers = __match_any_sync(0xffffffffu, key);
+      const int before = __popc(peers & ((1u << lane) - 1u));
+      if (i < n_ent) ranks[static_cast<size_t>(t0) * k + i] = kcount[key] + before;
+      __syncwarp();
+      if (i < n_ent && before == 0) kcount[key] += __popc(peers);
+      __syncwarp();
+    }
+    int* counts = chunk_counts + static_cast<size_t>(chunk) * NK;
+    for (int i = lane; i < NK; i += 32) counts[i] = kcount[i];
+  }
+}
+
 // One block per key: exclusive scan of chunk_counts[:, key] over chunks.
 __global__ void __launch_bounds__(1024) chunk_scan_kernel(const int* __restrict__ chunk_counts,
                                                           int nchunks, int NK,
@@ -593,9 +695,23 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
     if (e != cudaSuccess) return e;
   } else {
     const int nchunks = (T + kChunk - 1) / kChunk;
-    gate_kernel<float><<<nchunks, 256, 0, stream>>>(static_cast<const float*>(x), static_cast<const float*>(wg_t),
-                                                    T, H, E, k, dest_of_owner, experts_per_gpu, NK, topk_idx,
-                                                    topk_w, keys, ranks, chunk_counts);
+    const size_t smem = static_cast<size_t>(kChunk + E) * (H + 4) * sizeof(float);
+    if (H % 4 == 0 && smem <= 200 * 1024 && NK <= kMaxNK && k <= kMaxK && E % 8 == 0) {
+      static bool attr = false;
+      if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute(gate_f32_oneshot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      gate_f32_oneshot_kernel<<<nchunks, 256, smem, stream>>>(
+          static_cast<const float*>(x), static_cast<const float*>(wg_t), T, H, E, k, dest_of_owner, experts_per_gpu,
+          NK, topk_idx, topk_w, keys, ranks, chunk_counts);
+    } else {
+      gate_kernel<float><<<nchunks, 256, 0, stream>>>(static_cast<const float*>(x), static_cast<const float*>(wg_t),
+                                                      T, H, E, k, dest_of_owner, experts_per_gpu, NK, topk_idx,
+                                                      topk_w, keys, ranks, chunk_counts);
+    }
   }
   return cudaGetLastError();
 }
