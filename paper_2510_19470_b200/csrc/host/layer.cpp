@@ -159,6 +159,22 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
       ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, slots_ * F_, H_, 256, 32), "tmap wulo");
       ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, slots_ * H_, F_, 256, 32), "tmap wdhi");
       ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, slots_ * H_, F_, 256, 32), "tmap wdlo");
+      // split-K when (groups x m-tiles x n-tiles) of an even routing leaves SMs idle
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t groups = slots_ * (1 + static_cast<int64_t>(a2a_peers_.size()));
+      const int64_t m_tiles = std::max<int64_t>(1, (Tmax_ * k_ / E_ + 127) / 128);
+      auto pick = [&](int64_t N, int64_t K) {
+        const int64_t tiles = groups * m_tiles * ((N + 255) / 256);
+        int ks = 1;
+        while (ks < 8 && tiles * ks * 2 <= sms && K % (32 * ks * 2) == 0) ks *= 2;
+        return ks;
+      };
+      ksplit_up_ = pick(F_, H_);
+      ksplit_down_ = pick(H_, F_);
+      const int ks = std::max(ksplit_up_, ksplit_down_);
+      if (ks > 1) kpart_.alloc(sizeof(float) * ks * rows_cap_ * std::max(F_, H_));
     }
   }
   slot_dirty_.assign(static_cast<size_t>(slots_), 1);
@@ -673,11 +689,13 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     split_dirty_slots(s);
     ck(launch_split_tf32(xall_.as<float>(), xhi_.as<float>(), xlo_.as<float>(), rows_cap_ * H_, s), "split x");
     ck(launch_grouped_gemm_tf32x3(t_xhi_, t_xlo_, t_wuhi_, t_wulo_, hhi_.as<float>(), hlo_.as<float>(),
-                                  static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s),
+                                  static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s,
+                                  ksplit_up_, kpart_.as<float>(), rows_cap_),
        "gemm up");
     mark(down.c_str(), s);
     ck(launch_grouped_gemm_tf32x3(t_hhi_, t_hlo_, t_wdhi_, t_wdlo_, oall_.as<float>(), nullptr, static_cast<int>(H_),
-                                  static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s),
+                                  static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, ksplit_down_,
+                                  kpart_.as<float>(), rows_cap_),
        "gemm down");
     launches_ += 1;
   } else {

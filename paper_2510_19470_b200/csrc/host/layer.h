@@ -107,6 +107,8 @@ class Layer {
   DevBuf xhi_, xlo_, hhi_, hlo_, wuhi_, wulo_, wdhi_, wdlo_;
   CUtensorMap t_xhi_, t_xlo_, t_hhi_, t_hlo_, t_wuhi_, t_wulo_, t_wdhi_, t_wdlo_;
   std::vector<char> slot_dirty_;  // compute-copy slots whose hi/lo split is stale
+  int ksplit_up_ = 1, ksplit_down_ = 1;  // split-K when the tiles alone cannot fill the SMs
+  DevBuf kpart_;
   void split_dirty_slots(cudaStream_t s);
   void mark_gathered_dirty();
   uint32_t sched_up_ = 0, sched_down_ = 0;

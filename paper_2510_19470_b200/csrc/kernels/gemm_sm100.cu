@@ -599,7 +599,7 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
                            const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
                            float* __restrict__ C, float* __restrict__ C_lo, int ldc, int N, int K,
                            const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
-                           const int* __restrict__ g_slot, int ng, int relu) {
+                           const int* __restrict__ g_slot, int ng, int relu, int ksplit, size_t split_stride) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -612,7 +612,9 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int n_tiles = (N + BN - 1) / BN;
-  const int num_kb = K / T_BK;
+  // split-K (ksplit > 1): tile t covers K-part t % ksplit and stores raw fp32 partials
+  // at C + part * split_stride; a reduce kernel sums the parts in order
+  const int num_kb = K / T_BK / ksplit;
 
   if (warp == 2) {
     int carry = 0;
@@ -637,7 +639,7 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
     }
     if (lane == 0) {
       s.tile_start[ng] = carry;
-      s.num_tiles = carry;
+      s.num_tiles = carry * ksplit;
     }
   } else if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a_hi);
@@ -671,24 +673,26 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int part = tile % ksplit, gt = tile / ksplit;
         int lo = 0, hi = ng - 1;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (s.tile_start[mid] <= tile) lo = mid; else hi = mid - 1;
+          if (s.tile_start[mid] <= gt) lo = mid; else hi = mid - 1;
         }
         const int g = lo;
-        const int local = tile - s.tile_start[g];
+        const int local = gt - s.tile_start[g];
         const int m_tiles = (s.rows[g] + BM - 1) / BM;
         const int mt = local % m_tiles, nt = local / m_tiles;
         const int a_row = s.row_start[g] + mt * BM;
         const int b_row = s.slot[g] * N + nt * BN;
+        const int k0 = part * num_kb * T_BK;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&s.full[stage], T_STAGE_BYTES);
-          tma_load_2d(a_hi_at(stage), &map_a_hi, &s.full[stage], kb * T_BK, a_row, pol);
-          tma_load_2d(a_lo_at(stage), &map_a_lo, &s.full[stage], kb * T_BK, a_row, pol);
-          tma_load_2d(b_hi_at(stage), &map_b_hi, &s.full[stage], kb * T_BK, b_row, pol);
-          tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], kb * T_BK, b_row, pol);
+          tma_load_2d(a_hi_at(stage), &map_a_hi, &s.full[stage], k0 + kb * T_BK, a_row, pol);
+          tma_load_2d(a_lo_at(stage), &map_a_lo, &s.full[stage], k0 + kb * T_BK, a_row, pol);
+          tma_load_2d(b_hi_at(stage), &map_b_hi, &s.full[stage], k0 + kb * T_BK, b_row, pol);
+          tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], k0 + kb * T_BK, b_row, pol);
           if (++stage == T_STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -730,18 +734,20 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int part = tile % ksplit, gt = tile / ksplit;
       int lo = 0, hi = ng - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (s.tile_start[mid] <= tile) lo = mid; else hi = mid - 1;
+        if (s.tile_start[mid] <= gt) lo = mid; else hi = mid - 1;
       }
       const int g = lo;
-      const int local = tile - s.tile_start[g];
+      const int local = gt - s.tile_start[g];
       const int m_tiles = (s.rows[g] + BM - 1) / BM;
       const int mt = local % m_tiles, nt = local / m_tiles;
       const int r_local = mt * BM + row_in_tile;
       const bool row_ok = r_local < s.rows[g];
-      const size_t row_off = static_cast<size_t>(s.row_start[g] + r_local) * ldc + nt * BN;
+      const size_t row_off = static_cast<size_t>(s.row_start[g] + r_local) * ldc + nt * BN + part * split_stride;
+      const bool raw = ksplit > 1;  // partials: no ReLU, no split
 
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
@@ -757,9 +763,9 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float x = __uint_as_float(v[i]);
-            f[i] = relu ? fmaxf(x, 0.f) : x;
+            f[i] = (relu && !raw) ? fmaxf(x, 0.f) : x;
           }
-          if (C_lo) {  // split for the next GEMM
+          if (C_lo && !raw) {  // split for the next GEMM
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               float4 h, l;
@@ -791,6 +797,31 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// Sum the split-K partials in part order (deterministic), then ReLU / hi-lo split.
+__global__ void ksplit_reduce_kernel(const float* __restrict__ P, int ksplit, size_t stride, int64_t n4, int relu,
+                                     float* __restrict__ out, float* __restrict__ out_lo) {
+  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += step) {
+    float4 a = reinterpret_cast<const float4*>(P)[i];
+    for (int p = 1; p < ksplit; ++p) {
+      const float4 b = reinterpret_cast<const float4*>(P + p * stride)[i];
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    if (relu) { a.x = fmaxf(a.x, 0.f); a.y = fmaxf(a.y, 0.f); a.z = fmaxf(a.z, 0.f); a.w = fmaxf(a.w, 0.f); }
+    if (out_lo) {
+      float4 h, l;
+      h.x = rna_tf32(a.x); l.x = rna_tf32(a.x - h.x);
+      h.y = rna_tf32(a.y); l.y = rna_tf32(a.y - h.y);
+      h.z = rna_tf32(a.z); l.z = rna_tf32(a.z - h.z);
+      h.w = rna_tf32(a.w); l.w = rna_tf32(a.w - h.w);
+      reinterpret_cast<float4*>(out)[i] = h;
+      reinterpret_cast<float4*>(out_lo)[i] = l;
+    } else {
+      reinterpret_cast<float4*>(out)[i] = a;
+    }
   }
 }
 
@@ -867,8 +898,11 @@ cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, 
 
 cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
                                        const CUtensorMap& b_lo, float* C, float* C_lo, int ldc, int N, int K,
-                                       const GroupTable& groups, int relu, int num_sms, cudaStream_t stream) {
-  if (K % T_BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0) return cudaErrorInvalidValue;
+                                       const GroupTable& groups, int relu, int num_sms, cudaStream_t stream,
+                                       int ksplit, float* partial, int64_t rows_total) {
+  if (ksplit < 1 || K % (T_BK * ksplit) || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
+    return cudaErrorInvalidValue;
+  if (ksplit > 1 && !partial) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
     const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -876,8 +910,15 @@ cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMa
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  const size_t stride = static_cast<size_t>(rows_total) * ldc;
   grouped_gemm_tf32x3_kernel<<<num_sms, kThreads, kSmemBytesT, stream>>>(
-      a_hi, a_lo, b_hi, b_lo, C, C_lo, ldc, N, K, groups.row_start, groups.rows, groups.slot, groups.num_groups, relu);
+      a_hi, a_lo, b_hi, b_lo, ksplit > 1 ? partial : C, C_lo, ldc, N, K, groups.row_start, groups.rows, groups.slot,
+      groups.num_groups, relu, ksplit, stride);
+  if (ksplit > 1) {
+    const int64_t n4 = static_cast<int64_t>(stride) / 4;
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n4 + 255) / 256)));
+    ksplit_reduce_kernel<<<blocks, 256, 0, stream>>>(partial, ksplit, stride, n4, relu, C, C_lo);
+  }
   return cudaGetLastError();
 }
 
