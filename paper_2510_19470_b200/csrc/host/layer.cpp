@@ -261,6 +261,11 @@ void Layer::setup_p2p() {
   ck(cudaStreamCreateWithFlags(&side_s_, cudaStreamNonBlocking), "side stream");
   ck(cudaEventCreateWithFlags(&ev_counts_, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&ev_remote_, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&ev_arrived_, cudaEventDisableTiming), "event");
+  {
+    const char* spin = std::getenv("HEP_GEMM_SPIN");  // 1: GEMM producers wait on dispatch flags (old)
+    spin_ = spin && spin[0] == '1';
+  }
   peer_w_up_.assign(static_cast<size_t>(G_), nullptr);
   peer_w_down_.assign(static_cast<size_t>(G_), nullptr);
   peer_wires_.assign(static_cast<size_t>(G_), nullptr);
@@ -322,6 +327,7 @@ Layer::~Layer() {
   if (ev_ag_done_) cudaEventDestroy(ev_ag_done_);
   if (ev_counts_) cudaEventDestroy(ev_counts_);
   if (ev_remote_) cudaEventDestroy(ev_remote_);
+  if (ev_arrived_) cudaEventDestroy(ev_arrived_);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   if (h2d_s_) cudaStreamSynchronize(h2d_s_);
   if (d2h_s_) cudaStreamSynchronize(d2h_s_);
@@ -743,6 +749,14 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
                             pos_.as<int>(), side_s_, 2), "permute remote");
       ck(launch_signal_wait(p2p_args_, 1, side_s_, false), "dispatch flags");
       ck(cudaEventRecord(ev_remote_, side_s_), "record");
+      if (!spin_) {
+        // every source's rows have landed: only this one-warp kernel spins, never the
+        // persistent GEMM (which could otherwise hold every SM while a peer's dispatch
+        // waits for SM space behind it)
+        ck(launch_signal_wait(p2p_args_, 1, side_s_, true, false, false), "dispatch arrived");
+        ck(cudaEventRecord(ev_arrived_, side_s_), "record");
+        ++launches_;
+      }
       ck(launch_permute_p2p(p2p_args_, dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), keys_.as<int>(),
                             ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
                             pos_.as<int>(), s, 1), "permute local");
@@ -750,17 +764,31 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
       // The down-projection writes received rows' outputs straight into their source
       // GPU's oall (fused GEMM + combine exchange); the combine reads local HBM only.
       const int n_src = p2p_args_.n_src[rank_];
-      if (ag_pending_) {
+      const int own_local = static_cast<int>(n_), own = static_cast<int>(n_ * (1 + n_src));
+      const unsigned long long* out_down = g_out_down_.as<unsigned long long>();
+      if (!spin_) {
+        // Own experts' local rows overlap the remote dispatch; received rows follow once
+        // they have all landed; gathered experts once the All-Gather is resident.
+        run_expert_gemms(s, out_down, nullptr, 0, own_local);
+        ck(cudaStreamWaitEvent(s, ev_arrived_, 0), "wait dispatch");
+        if (own > own_local) run_expert_gemms(s, out_down, nullptr, own_local, own - own_local, "_remote");
+        if (num_groups_ > own) {
+          if (ag_pending_) {
+            mark("ag_wait", s);
+            ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");
+          }
+          run_expert_gemms(s, out_down, nullptr, own, num_groups_ - own, "_gathered");
+        }
+        ag_pending_ = false;
+      } else if (ag_pending_) {
         // own experts first (weights already resident), gathered ones after the AG lands
-        const int own = static_cast<int>(n_ * (1 + n_src));
-        run_expert_gemms(s, g_out_down_.as<unsigned long long>(), g_wait_.as<int>(), 0, own);
+        run_expert_gemms(s, out_down, g_wait_.as<int>(), 0, own);
         mark("ag_wait", s);
         ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");
         ag_pending_ = false;
-        run_expert_gemms(s, g_out_down_.as<unsigned long long>(), g_wait_.as<int>(), own, num_groups_ - own,
-                         "_gathered");
+        run_expert_gemms(s, out_down, g_wait_.as<int>(), own, num_groups_ - own, "_gathered");
       } else {
-        run_expert_gemms(s, g_out_down_.as<unsigned long long>(), g_wait_.as<int>());
+        run_expert_gemms(s, out_down, g_wait_.as<int>());
       }
       ck(cudaStreamWaitEvent(s, ev_remote_, 0), "wait");
       mark("combine", s);

@@ -119,7 +119,8 @@ class Layer {
   P2PArgs p2p_args_{};
   DevBuf sync_, send_base_, g_out_down_, g_wait_;
   cudaStream_t side_s_ = nullptr;
-  cudaEvent_t ev_counts_ = nullptr, ev_remote_ = nullptr;
+  cudaEvent_t ev_counts_ = nullptr, ev_remote_ = nullptr, ev_arrived_ = nullptr;
+  bool spin_ = false;  // HEP_GEMM_SPIN=1: GEMM producers spin on per-source dispatch flags
   // expert All-Gather overlapped with the step (copy-engine pulls over NVLink)
   cudaStream_t ag_s_ = nullptr;
   cudaEvent_t ev_ag_start_ = nullptr, ev_ag_done_ = nullptr;
