@@ -24,6 +24,10 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# separate hardware queues for the step's streams (see paper_2510_19470_b200/__init__.py);
+# set before torch creates the CUDA context
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import subprocess
 import sys

@@ -15,6 +15,8 @@
 // the same layout the NCCL path produces, so both paths feed the same GEMM groups.
 // Flags carry a per-forward epoch; spins time out (trap) instead of hanging.
 
+#include <cstdio>
+
 #include "common.cuh"
 #include "comm_p2p.h"
 
@@ -36,11 +38,17 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-__device__ void wait_flag(const uint32_t* f, uint32_t epoch) {
+// who: (rank << 16) | (site << 8) | peer, printed if the wait times out.  Sites: 0 counts,
+// 11..14 signal slots 1..4, 20 refresh barrier, 21 refresh chain, 22 refresh fetch.
+__device__ void wait_flag(const uint32_t* f, uint32_t epoch, uint32_t who = 0) {
   const uint64_t t0 = globaltimer();
   // Epochs only grow; a peer that already moved on to a later epoch also satisfies us.
   while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
-    if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();  // peer never arrived
+    if (globaltimer() - t0 > 60ull * 1000000000ull) {  // peer never arrived
+      printf("hep: flag wait timed out: rank %u site %u peer %u epoch %u flag %u\n", who >> 16, (who >> 8) & 0xffu,
+             who & 0xffu, epoch, ld_acquire_sys(f));
+      __trap();
+    }
     __nanosleep(64);
   }
 }
@@ -82,7 +90,8 @@ __global__ void __launch_bounds__(256) count_exchange_kernel(P2PArgs a, const in
     st_release_sys(view(a.sync[threadIdx.x], NK).flags + 0 * kMaxG + me, a.epoch);
   // 2) wait for everyone's counts.
   const SyncView mine = view(a.sync[me], NK);
-  if (threadIdx.x < G && static_cast<int>(threadIdx.x) != me) wait_flag(mine.flags + 0 * kMaxG + threadIdx.x, a.epoch);
+  if (threadIdx.x < G && static_cast<int>(threadIdx.x) != me)
+    wait_flag(mine.flags + 0 * kMaxG + threadIdx.x, a.epoch, (static_cast<uint32_t>(me) << 16) | threadIdx.x);
   __syncthreads();
   for (int i = threadIdx.x; i < G * NK; i += blockDim.x) {
     const int s = i / NK, key = i % NK;
@@ -201,7 +210,9 @@ __global__ void signal_wait_kernel(P2PArgs a, int slot, int wait, int ag, int si
   if (sig && i < n) st_release_sys(view(a.sync[list[i]], NK).flags + slot * kMaxG + a.rank, a.epoch);
   if (!wait) return;
   __syncthreads();
-  if (i < n) wait_flag(view(a.sync[a.rank], NK).flags + slot * kMaxG + list[i], a.epoch);
+  if (i < n)
+    wait_flag(view(a.sync[a.rank], NK).flags + slot * kMaxG + list[i], a.epoch,
+              (static_cast<uint32_t>(a.rank) << 16) | ((10u + slot) << 8) | static_cast<uint32_t>(list[i]));
 }
 
 template <bool BF16>
@@ -260,14 +271,14 @@ __global__ void chain_barrier_kernel(ChainArgs c) {
   const int r = threadIdx.x;
   if (r < c.G) st_release_sys(c.bar[r] + c.rank, c.epoch);
   __syncthreads();
-  if (r < c.G) wait_flag(c.bar[c.rank] + r, c.epoch);
+  if (r < c.G) wait_flag(c.bar[c.rank] + r, c.epoch, (static_cast<uint32_t>(c.rank) << 16) | (20u << 8) | r);
 }
 
 __global__ void __launch_bounds__(256) shared_chain_kernel(ChainArgs c) {
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * c.chunk;
   const int64_t i1 = min(c.P, i0 + c.chunk);
   if (c.rank > 0 && c.epoch) {
-    if (threadIdx.x == 0) wait_flag(c.pred_flags + blockIdx.x, c.epoch);
+    if (threadIdx.x == 0) wait_flag(c.pred_flags + blockIdx.x, c.epoch, (static_cast<uint32_t>(c.rank) << 16) | (21u << 8));
     __syncthreads();
   }
   const bool last = c.rank == c.G - 1;
@@ -290,7 +301,7 @@ __global__ void __launch_bounds__(256) shared_chain_kernel(ChainArgs c) {
 __global__ void __launch_bounds__(256) shared_fetch_kernel(ChainArgs c) {
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * c.chunk;
   const int64_t i1 = min(c.P, i0 + c.chunk);
-  if (threadIdx.x == 0) wait_flag(c.last_flags + blockIdx.x, c.epoch);
+  if (threadIdx.x == 0) wait_flag(c.last_flags + blockIdx.x, c.epoch, (static_cast<uint32_t>(c.rank) << 16) | (22u << 8));
   __syncthreads();
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) c.shared[i] = __ldcv(c.last_shared + i);
 }

@@ -14,6 +14,7 @@
 // w2..w5 epilogue (warp w drains TMEM lanes 32*(w%4) .. +31).
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -92,7 +93,10 @@ __device__ __forceinline__ void wait_dispatch(const uint32_t* flag, uint32_t epo
     if (static_cast<int32_t>(v - epoch) >= 0) break;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 60ull * 1000000000ull) __trap();
+    if (t - t0 > 60ull * 1000000000ull) {
+      printf("hep: GEMM dispatch wait timed out: epoch %u flag %u\n", epoch, v);
+      __trap();
+    }
     __nanosleep(100);
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");

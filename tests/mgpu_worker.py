@@ -12,6 +12,8 @@ import json
 import os
 import sys
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before torch creates the context
+
 import numpy as np
 import torch
 import torch.distributed as dist
