@@ -1,11 +1,12 @@
 """The reference's OWN test programs, compiled unmodified from /root/reference by
 oracle/Makefile, run against this repository's C++ implementation of the API:
 
-* ref_unit_vs_ours   : proj/tests/test_{topology,sparsecomp,perfmodel}.cpp (46 doctest
-                       cases) built with include/hybridep/ and csrc/host/ (doctest shim)
-* acceptance_vs_ours : proj/tests/acceptance.cpp (12 release criteria) with our topology,
-                       plan, perfmodel, SR codec and step-DAG builder; the reference's own
-                       discrete-event engine (out of scope here) drives our schedule
+* ref_unit_vs_ours   : proj/tests/test_{topology,sparsecomp,perfmodel,simcore}.cpp (61
+                       doctest cases) built with include/hybridep/ and csrc/host/ (doctest
+                       shim)
+* acceptance_vs_ours : proj/tests/acceptance.cpp (12 release criteria) linked against our
+                       host library only: topology, plan, perfmodel, SR codec, step-DAG
+                       builder and discrete-event engine (csrc/host/simrun.cpp)
 * ref_unit_vs_ref    : control, the same suites against the reference itself
 """
 import os
@@ -26,7 +27,7 @@ def _run(name):
 def test_reference_unit_suites_pass_against_our_library():
     r = _run("ref_unit_vs_ours")
     assert r.returncode == 0, r.stdout[-4000:]
-    assert "46 passed | 0 failed" in r.stdout, r.stdout[-2000:]
+    assert "61 passed | 0 failed" in r.stdout, r.stdout[-2000:]
 
 
 def test_reference_unit_suites_control():
