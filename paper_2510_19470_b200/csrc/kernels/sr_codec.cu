@@ -81,6 +81,7 @@ struct RangeArgs {
   int full[2];  // static full-range mode
   int nr;
   int force_fallback;
+  int lookback;  // the multi-block emit runs: its look-back words need zeroing
 };
 
 // Selects a per-range argument without a dynamically indexed (local-memory) param copy.
@@ -212,6 +213,62 @@ __device__ void find_bucket(Count cnt, int nb, long long need, int* sh_bin, long
   __syncthreads();
 }
 
+// Two bucket searches in one scan: counts A and B (each < 2^32 in total) packed in one
+// 64-bit lane value; slot q of the outputs is the bin holding needq-th largest of
+// counts q (needq <= 0: skipped).  Used by the sample bracket (both order statistics).
+template <typename CountA, typename CountB>
+__device__ void find_bucket_pair(CountA ca, CountB cb, int nb, long long need_a, long long need_b, int* bin,
+                                 long long* before, unsigned long long* wsum) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  unsigned long long mine = 0;  // (sum A << 32) | sum B
+  for (int i = 0; i < per; ++i) {
+    const int b = nb - 1 - (t * per + i);
+    if (b >= 0) mine += (static_cast<unsigned long long>(ca(b)) << 32) | cb(b);
+  }
+  unsigned long long incl = mine;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += o;
+    }
+    if (lane < nw) wsum[lane] = w;
+  }
+  __syncthreads();
+  if (warp) incl += wsum[warp - 1];
+  const unsigned long long excl = incl - mine;
+  for (int q = 0; q < 2; ++q) {
+    const long long need = q ? need_b : need_a;
+    const int sh = q ? 0 : 32;
+    const long long ex = static_cast<long long>((excl >> sh) & 0xffffffffull);
+    const long long in = static_cast<long long>((incl >> sh) & 0xffffffffull);
+    if (need > 0 && ex < need && in >= need) {
+      long long acc = ex;
+      for (int i = 0; i < per; ++i) {
+        const int b = nb - 1 - (t * per + i);
+        if (b < 0) break;
+        const long long c = static_cast<long long>(q ? cb(b) : ca(b));
+        if (acc + c >= need) {
+          bin[q] = b;
+          before[q] = acc;
+          break;
+        }
+        acc += c;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // Decoupled look-back over tiles taken in ticket order, two 31-bit counters per tile
 // (warp 0; a 32-tile window per step, one predecessor per lane).  Returns the
 // exclusive prefix of both counters in every lane.
@@ -294,10 +351,11 @@ __global__ void sr_init_kernel(WsView ws, EncBatch batch, int bf16, const float*
     SelState& s = ws.st(b, r);
     unsigned long long* s1 = ws.stat(b, r);
     unsigned long long* s2 = ws.stat2(b, r);
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + t; i < ws.tiles; i += stride) {
-      s1[i] = 0;
-      s2[i] = 0;
-    }
+    // only the multi-block emit walks look-back words (the split's per-tile counts are
+    // written for every tile before they are read)
+    if (ra.lookback)
+      for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + t; i < ws.tiles; i += stride) s2[i] = 0;
+    (void)s1;
     if (blockIdx.x) continue;
     for (int i = t; i < kBins; i += blockDim.x) s.hist[i] = 0;
     if (t == 0) {
@@ -343,8 +401,8 @@ __global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(RangeArgs ra,
   unsigned int* h_hi = smem + kSample;    // kBins
   unsigned int* h_lo = h_hi + kBins;      // kBins
   __shared__ unsigned long long wsum[32];
-  __shared__ int sh_bin;
-  __shared__ long long sh_before, sh_count;
+  __shared__ int pbin[2];
+  __shared__ long long pbefore[2];
   const int r = blockIdx.x, b = blockIdx.y;
   SelState& s = ws.st(b, r);
   if (s.mode != kModeList) return;
@@ -363,21 +421,13 @@ __global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(RangeArgs ra,
   // digit 1: bits 20..31 of the top word
   for (int j = threadIdx.x; j < S; j += blockDim.x) hist_add(h_hi, static_cast<int>(ks[j] >> 20));
   __syncthreads();
-  int b_hi = 0, b_lo = 0;
   long long w_hi = r_hi + 1, w_lo = r_lo + 1;
-  auto c1 = [&](int i) { return static_cast<unsigned long long>(h_hi[i]); };
-  if (has_hi) {
-    find_bucket(c1, kBins, w_hi, &sh_bin, &sh_before, &sh_count, wsum);
-    b_hi = sh_bin;
-    w_hi -= sh_before;
-    __syncthreads();
-  }
-  if (has_lo) {
-    find_bucket(c1, kBins, w_lo, &sh_bin, &sh_before, &sh_count, wsum);
-    b_lo = sh_bin;
-    w_lo -= sh_before;
-    __syncthreads();
-  }
+  // both order statistics' first digits from one scan of the shared histogram
+  find_bucket_pair([&](int i) { return h_hi[i]; }, [&](int i) { return h_hi[i]; }, kBins, has_hi ? w_hi : 0,
+                   has_lo ? w_lo : 0, pbin, pbefore, wsum);
+  const int b_hi = has_hi ? pbin[0] : 0, b_lo = has_lo ? pbin[1] : 0;
+  if (has_hi) w_hi -= pbefore[0];
+  if (has_lo) w_lo -= pbefore[1];
   // digit 2: bits 8..19 inside each bin
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) { h_hi[i] = 0; h_lo[i] = 0; }
   __syncthreads();
@@ -390,18 +440,11 @@ __global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(RangeArgs ra,
     if (__any_sync(act, in_lo)) hist_add(h_lo, in_lo ? d : -1);
   }
   __syncthreads();
+  find_bucket_pair([&](int i) { return h_hi[i]; }, [&](int i) { return h_lo[i]; }, kBins, has_hi ? w_hi : 0,
+                   has_lo ? w_lo : 0, pbin, pbefore, wsum);
   uint32_t hi32 = 0xffffffffu, lo32 = 0;
-  if (has_hi) {
-    find_bucket([&](int i) { return static_cast<unsigned long long>(h_hi[i]); }, kBins, w_hi, &sh_bin, &sh_before,
-                &sh_count, wsum);
-    hi32 = (static_cast<uint32_t>(b_hi) << 20) | (static_cast<uint32_t>(sh_bin) << 8) | 0xffu;
-    __syncthreads();
-  }
-  if (has_lo) {
-    find_bucket([&](int i) { return static_cast<unsigned long long>(h_lo[i]); }, kBins, w_lo, &sh_bin, &sh_before,
-                &sh_count, wsum);
-    lo32 = (static_cast<uint32_t>(b_lo) << 20) | (static_cast<uint32_t>(sh_bin) << 8);
-  }
+  if (has_hi) hi32 = (static_cast<uint32_t>(b_hi) << 20) | (static_cast<uint32_t>(pbin[0]) << 8) | 0xffu;
+  if (has_lo) lo32 = (static_cast<uint32_t>(b_lo) << 20) | (static_cast<uint32_t>(pbin[1]) << 8);
   if (ra.force_fallback) hi32 = lo32 = 0;  // test hook: an invalid bracket
   if (threadIdx.x == 0) {
     s.hi32 = hi32;
@@ -1595,6 +1638,7 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
   // (experts of ~100M parameters) take the multi-block path across all SMs
   const bool cluster = expect_max <= kFinMaxList && ovr != 3 && ovr != 4;
 
+  ra.lookback = (any_full || (any_list && !cluster)) ? 1 : 0;
   sr_init_kernel<<<dim3(16, batch), 256, 0, stream>>>(ws, eb, bf16, shared, ra, plan.h, plan.m, plan.k,
                                                       plan.index_bits, plan.value_bits);
   if (any_list) {
