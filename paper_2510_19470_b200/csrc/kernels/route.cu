@@ -12,6 +12,9 @@
 
 #include <float.h>
 
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -466,6 +469,189 @@ __global__ void __launch_bounds__(256) gate_f32_oneshot_kernel(const float* __re
   }
 }
 
+// ---------------------------------------------------------------------------------
+// bf16 gate on the 5th-gen tensor cores: one CTA per 128 tokens; TMA streams the x
+// tile (128 x 64, SW128) and W_g^T (NE x 64; rows past E are zero-filled) through a
+// 4-stage mbarrier ring; one thread issues tcgen05.mma M=128 N=NE K=16 into TMEM; the
+// four epilogue warps each own 32 tokens (= one ranking chunk): tcgen05.ld of their
+// logit rows, top-k and softmax per thread, match.any ranking per warp.  Warp roles as
+// in the expert GEMM: w0 TMA, w1 TMEM + MMA, w2..w5 epilogue.
+constexpr int kUGT = 128;      // tokens per CTA
+constexpr int kUGK = 64;       // K per stage (128 B of bf16 = one swizzle row)
+template <int NE, int KS>
+constexpr int ug_stages() { return KS > 1 ? (NE <= 16 ? 4 : 3) : (NE <= 16 ? 8 : 6); }  // split: 2 CTAs per SM
+
+// KS = 2: a 2-CTA cluster per tile splits K; the second CTA hands its partial logits
+// over DSMEM, so the x stream spreads over all SMs (128-token tiles alone leave SMs idle).
+template <int NE, int KS>
+__global__ void __launch_bounds__(192, 1) gate_umma_kernel(const __grid_constant__ CUtensorMap map_x,
+                                                           const __grid_constant__ CUtensorMap map_w, int T_tok,
+                                                           int H, int E, int k, const int* __restrict__ dest_of_owner,
+                                                           int n_per_gpu, int NK, int* __restrict__ topk_idx,
+                                                           float* __restrict__ topk_w, int* __restrict__ keys,
+                                                           int* __restrict__ ranks, int* __restrict__ chunk_counts) {
+  constexpr int A_BYTES = kUGT * kUGK * 2;
+  constexpr int B_BYTES = NE * kUGK * 2;
+  constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr int TCOLS = NE < 32 ? 32 : NE;
+  extern __shared__ uint8_t ug_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ug_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  constexpr int kUGStages = ug_stages<NE, KS>();
+  __shared__ __align__(8) uint64_t full[kUGStages], empty[kUGStages], tfull;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int skey[4][32][kMaxK];
+  __shared__ int kcount[4][kMaxNK];
+  // the second K half's logits (KS = 2) reuse the stage ring once the MMAs are done
+  float (*part)[NE] = reinterpret_cast<float (*)[NE]>(sm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int crank = KS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int tile = blockIdx.x / KS;
+  const int t0 = tile * kUGT;
+  const int kb_all = H / kUGK, num_kb = kb_all / KS, kb0 = crank * num_kb;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_x);
+    tma_prefetch_desc(&map_w);
+    for (int i = 0; i < kUGStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&tfull, 1);
+    fence_barrier_init();
+  } else if (warp == 1) {
+    tmem_alloc(&tmem_base_sh, TCOLS);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      const uint64_t pol_x = l2_policy_evict_first(), pol_w = l2_policy_evict_last();
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int st = kb % kUGStages;
+        mbar_wait(&empty[st], ((kb / kUGStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[st], STAGE);
+        tma_load_2d(sm + st * STAGE, &map_x, &full[st], (kb0 + kb) * kUGK, t0, pol_x);
+        tma_load_2d(sm + st * STAGE + A_BYTES, &map_w, &full[st], (kb0 + kb) * kUGK, 0, pol_w);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(kUGT, NE);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int st = kb % kUGStages;
+        mbar_wait(&full[st], (kb / kUGStages) & 1);
+        tc_fence_after();
+        const uint32_t a = smem_addr(sm + st * STAGE), b = smem_addr(sm + st * STAGE + A_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < kUGK / 16; ++kk)
+          umma_bf16(tmem, umma_desc_k_sw128(a + 32 * kk), umma_desc_k_sw128(b + 32 * kk), idesc, (kb | kk) != 0);
+        umma_commit(&empty[st]);
+      }
+      umma_commit(&tfull);
+    }
+  }
+  // epilogue warps: warp w owns TMEM lanes 32 (w % 4) .. +31 = tokens of one ranking chunk
+  const bool epi = warp >= 2;
+  const int q = warp & 3;
+  const int r = q * 32 + lane, t = t0 + r;
+  float v[NE < 32 ? 32 : NE];
+  if (epi) {
+    mbar_wait(&tfull, 0);
+    tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < (NE < 32 ? 32 : NE); c += 32) {
+      uint32_t u[32];
+      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, u);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[c + i] = __uint_as_float(u[i]);
+    }
+    tc_fence_before();
+    if (KS > 1 && crank == 1) {
+#pragma unroll
+      for (int e = 0; e < NE; ++e) part[r][e] = v[e];
+    }
+  }
+  if (KS > 1) {
+    __syncwarp();
+    cluster_sync();  // the second half's logits are in its shared memory
+    if (epi && crank == 0) {
+      const float* peer = cooperative_groups::this_cluster().map_shared_rank(&part[0][0], 1);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) v[e] += peer[r * NE + e];
+    }
+  }
+  if (epi && crank == 0) {
+    // top-k by (logit desc, expert id asc), softmax over the k selected
+    unsigned long long used = 0;
+    float sel_v[kMaxK];
+    int sel_e[kMaxK];
+    for (int j = 0; j < k; ++j) {
+      float bv = 0.f;
+      int be = -1;
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        if (e < E && !((used >> e) & 1ull) && (be < 0 || v[e] > bv)) { bv = v[e]; be = e; }
+      sel_v[j] = bv;
+      sel_e[j] = be;
+      used |= 1ull << be;
+    }
+    const int valid = min(32, T_tok - (t0 + q * 32));
+    if (t < T_tok) {
+      float ssum = 0.f;
+      for (int j = 0; j < k; ++j) ssum += expf(sel_v[j] - sel_v[0]);
+      for (int j = 0; j < k; ++j) {
+        const size_t o = static_cast<size_t>(t) * k + j;
+        const int e = sel_e[j];
+        const int key = dest_of_owner[e / n_per_gpu] * E + e;
+        topk_idx[o] = e;
+        topk_w[o] = expf(sel_v[j] - sel_v[0]) / ssum;
+        keys[o] = key;
+        skey[q][lane][j] = key;
+      }
+    }
+    __syncwarp();
+    if (valid > 0) {  // ranking of this chunk's (token, slot) entries
+      int* cnt = kcount[q];
+      for (int i = lane; i < NK; i += 32) cnt[i] = 0;
+      __syncwarp();
+      const int n_ent = valid * k;
+      for (int base = 0; base < n_ent; base += 32) {
+        const int i = base + lane;
+        const int key = i < n_ent ? skey[q][i / k][i % k] : -1;
+        const unsigned int peers = __match_any_sync(0xffffffffu, key);
+        const int before = __popc(peers & ((1u << lane) - 1u));
+        if (i < n_ent) ranks[static_cast<size_t>(t0 + q * 32) * k + i] = cnt[key] + before;
+        __syncwarp();
+        if (i < n_ent && before == 0) cnt[key] += __popc(peers);
+        __syncwarp();
+      }
+      int* counts = chunk_counts + static_cast<size_t>(tile * 4 + q) * NK;
+      for (int i = lane; i < NK; i += 32) counts[i] = cnt[i];
+    }
+  }
+  if (KS > 1) {
+    __syncwarp();
+    cluster_sync();  // the peer's logits were read before it may exit
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TCOLS);
+  }
+}
+
+template <int NE, int KS>
+constexpr size_t gate_umma_smem() {
+  return 1024 + static_cast<size_t>(ug_stages<NE, KS>()) * (kUGT + NE) * kUGK * 2;
+}
+
+
 // One block per key: exclusive scan of chunk_counts[:, key] over chunks.
 __global__ void __launch_bounds__(1024) chunk_scan_kernel(const int* __restrict__ chunk_counts,
                                                           int nchunks, int NK,
@@ -673,6 +859,60 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
   if (dt == DType::BF16) {
     // wg_t is bf16 [E, H] for bf16 layers.
     if (H % kGCMin || E % 8 || NK > kMaxNK || k > kMaxK) return cudaErrorInvalidValue;
+    const char* gate_env = std::getenv("HEP_GATE");
+    if (!(gate_env && gate_env[0] == 'm') && H % kUGK == 0 && E <= 64 && NK <= kMaxNK && k <= kMaxK) {
+      // tensor-core gate; TMA descriptors cached per (pointer, shape)
+      struct MapCache { const void* p = nullptr; int rows = 0, cols = 0, box = 0; CUtensorMap m; };
+      static MapCache xc[4], wc[2];
+      static int xnext = 0;
+      auto get = [](MapCache* c, int n, int* next, const void* ptr, int rows, int cols, int box) -> const CUtensorMap* {
+        for (int i = 0; i < n; ++i)
+          if (c[i].p == ptr && c[i].rows == rows && c[i].cols == cols && c[i].box == box) return &c[i].m;
+        MapCache& e = c[next ? (*next)++ % n : 0];
+        if (make_tmap_bf16_2d(&e.m, ptr, rows, cols, box, kUGK) != cudaSuccess) return nullptr;
+        e.p = ptr; e.rows = rows; e.cols = cols; e.box = box;
+        return &e.m;
+      };
+      const int NE = E <= 16 ? 16 : 64;
+      const CUtensorMap* mx = get(xc, 4, &xnext, x, T, H, kUGT);
+      const CUtensorMap* mw = get(wc, 1, nullptr, wg_t, E, H, NE);
+      if (!mx || !mw) return cudaErrorInvalidValue;
+      const int tiles = (T + kUGT - 1) / kUGT;
+      // HEP_GATE_SPLIT=1: split K over a CTA pair (DSMEM hand-off of the partial logits).
+      // Measured no faster for cfg3 and slower for cfg4 (profiles/README.md), so off.
+      const char* split_env = std::getenv("HEP_GATE_SPLIT");
+      const bool split = split_env && split_env[0] == '1' && (H / kUGK) % 2 == 0;
+      auto launch = [&](auto kern, size_t smem, int ks, bool& attr) {
+        if (!attr) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+          attr = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(tiles * ks));
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(ks);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, *mx, *mw, T, H, E, k, dest_of_owner, experts_per_gpu, NK, topk_idx,
+                                  topk_w, keys, ranks, chunk_counts);
+      };
+      static bool a[4] = {false, false, false, false};
+      cudaError_t err;
+      if (NE == 16)
+        err = split ? launch(gate_umma_kernel<16, 2>, gate_umma_smem<16, 2>(), 2, a[0])
+                    : launch(gate_umma_kernel<16, 1>, gate_umma_smem<16, 1>(), 1, a[1]);
+      else
+        err = split ? launch(gate_umma_kernel<64, 2>, gate_umma_smem<64, 2>(), 2, a[2])
+                    : launch(gate_umma_kernel<64, 1>, gate_umma_smem<64, 1>(), 1, a[3]);
+      if (err != cudaSuccess) return err;
+      return cudaGetLastError();
+    }
     const int blocks = (T + kGT - 1) / kGT;
     auto go = [&](auto kern, size_t smem, bool& attr) {
       if (!attr) {  // once per instantiation
