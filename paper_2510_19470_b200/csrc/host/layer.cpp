@@ -147,29 +147,18 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
       xlo_.alloc(fb * rows_cap_ * H_);
       hhi_.alloc(fb * rows_cap_ * F_);
       hlo_.alloc(fb * rows_cap_ * F_);
+      wuhi_.alloc(fb * slots_ * F_ * H_);
+      wulo_.alloc(fb * slots_ * F_ * H_);
+      wdhi_.alloc(fb * slots_ * H_ * F_);
+      wdlo_.alloc(fb * slots_ * H_ * F_);
       ck(make_tmap_f32_2d(&t_xhi_, xhi_.p, rows_cap_, H_, 128, 32), "tmap xhi");
       ck(make_tmap_f32_2d(&t_xlo_, xlo_.p, rows_cap_, H_, 128, 32), "tmap xlo");
       ck(make_tmap_f32_2d(&t_hhi_, hhi_.p, rows_cap_, F_, 128, 32), "tmap hhi");
       ck(make_tmap_f32_2d(&t_hlo_, hlo_.p, rows_cap_, F_, 128, 32), "tmap hlo");
-      // Weights: by default the GEMM splits the staged fp32 tiles itself (one HBM read);
-      // HEP_TF32_PRESPLIT=1 keeps pre-split hi/lo copies instead.
-      const char* pre = std::getenv("HEP_TF32_PRESPLIT");
-      tf32_presplit_ = pre && pre[0] == '1';
-      if (tf32_presplit_) {
-        wuhi_.alloc(fb * slots_ * F_ * H_);
-        wulo_.alloc(fb * slots_ * F_ * H_);
-        wdhi_.alloc(fb * slots_ * H_ * F_);
-        wdlo_.alloc(fb * slots_ * H_ * F_);
-        ck(make_tmap_f32_2d(&t_wuhi_, wuhi_.p, slots_ * F_, H_, 256, 32), "tmap wuhi");
-        ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, slots_ * F_, H_, 256, 32), "tmap wulo");
-        ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, slots_ * H_, F_, 256, 32), "tmap wdhi");
-        ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, slots_ * H_, F_, 256, 32), "tmap wdlo");
-      } else {
-        ck(make_tmap_f32_2d(&t_wuhi_, w_up_c_.p, slots_ * F_, H_, 256, 32), "tmap wu");
-        ck(make_tmap_f32_2d(&t_wdhi_, w_down_c_.p, slots_ * H_, F_, 256, 32), "tmap wd");
-        t_wulo_ = t_wuhi_;
-        t_wdlo_ = t_wdhi_;
-      }
+      ck(make_tmap_f32_2d(&t_wuhi_, wuhi_.p, slots_ * F_, H_, 256, 32), "tmap wuhi");
+      ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, slots_ * F_, H_, 256, 32), "tmap wulo");
+      ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, slots_ * H_, F_, 256, 32), "tmap wdhi");
+      ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, slots_ * H_, F_, 256, 32), "tmap wdlo");
       // split-K when (groups x m-tiles x n-tiles) of an even routing leaves SMs idle
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
@@ -703,17 +692,16 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     ck(gemm(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_), "gemm down");
   } else if (tf32_) {
     mark(up.c_str(), s);
-    if (tf32_presplit_) split_dirty_slots(s);
+    split_dirty_slots(s);
     ck(launch_split_tf32(xall_.as<float>(), xhi_.as<float>(), xlo_.as<float>(), rows_cap_ * H_, s), "split x");
-    const bool sb = !tf32_presplit_;
     ck(launch_grouped_gemm_tf32x3(t_xhi_, t_xlo_, t_wuhi_, t_wulo_, hhi_.as<float>(), hlo_.as<float>(),
                                   static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s,
-                                  ksplit_up_, kpart_.as<float>(), rows_cap_, sb),
+                                  ksplit_up_, kpart_.as<float>(), rows_cap_),
        "gemm up");
     mark(down.c_str(), s);
     ck(launch_grouped_gemm_tf32x3(t_hhi_, t_hlo_, t_wdhi_, t_wdlo_, oall_.as<float>(), nullptr, static_cast<int>(H_),
                                   static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, ksplit_down_,
-                                  kpart_.as<float>(), rows_cap_, sb),
+                                  kpart_.as<float>(), rows_cap_),
        "gemm down");
     launches_ += 1;
   } else {

@@ -104,7 +104,6 @@ class Layer {
   CUtensorMap map_a1_, map_b1_, map_a2_, map_b2_;
   // fp32 layers on the tensor cores (3xTF32): every GEMM operand as a tf32 hi/lo pair
   bool tf32_ = false;
-  bool tf32_presplit_ = false;  // HEP_TF32_PRESPLIT=1: pre-split weight copies instead of in-GEMM split
   DevBuf xhi_, xlo_, hhi_, hlo_, wuhi_, wulo_, wdhi_, wdlo_;
   CUtensorMap t_xhi_, t_xlo_, t_hhi_, t_hlo_, t_wuhi_, t_wulo_, t_wdhi_, t_wdlo_;
   std::vector<char> slot_dirty_;  // compute-copy slots whose hi/lo split is stale

@@ -561,7 +561,6 @@ constexpr int T_STAGE_BYTES = 2 * T_A_BYTES + 2 * T_B_BYTES;
 struct SmemCtlT {
   uint64_t full[T_STAGES];
   uint64_t empty[T_STAGES];
-  uint64_t conv[T_STAGES];  // B tile split into hi/lo (SB variant)
   uint64_t tfull[ACC];
   uint64_t tempty[ACC];
   uint32_t tmem_base;
@@ -599,10 +598,7 @@ __device__ __forceinline__ float rna_tf32(float x) {
   return __uint_as_float(r);
 }
 
-// SB: B arrives as plain fp32 (one HBM read of the weights); converter warps 6..9
-// split each staged B tile in place into hi (rna_tf32) and lo before the MMA reads it.
-template <bool SB>
-__global__ void __launch_bounds__(SB ? kThreads + 128 : kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
                            const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
                            float* __restrict__ C, float* __restrict__ C_lo, int ldc, int N, int K,
@@ -653,11 +649,10 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
     tma_prefetch_desc(&map_a_hi);
     tma_prefetch_desc(&map_a_lo);
     tma_prefetch_desc(&map_b_hi);
-    if (!SB) tma_prefetch_desc(&map_b_lo);
+    tma_prefetch_desc(&map_b_lo);
     for (int i = 0; i < T_STAGES; ++i) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
-      mbar_init(&s.conv[i], 4);
     }
     for (int i = 0; i < ACC; ++i) {
       mbar_init(&s.tfull[i], 1);
@@ -697,11 +692,11 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
         const int k0 = part * num_kb * T_BK;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&s.full[stage], SB ? T_STAGE_BYTES - T_B_BYTES : T_STAGE_BYTES);
+          mbar_arrive_expect_tx(&s.full[stage], T_STAGE_BYTES);
           tma_load_2d(a_hi_at(stage), &map_a_hi, &s.full[stage], k0 + kb * T_BK, a_row, pol);
           tma_load_2d(a_lo_at(stage), &map_a_lo, &s.full[stage], k0 + kb * T_BK, a_row, pol);
           tma_load_2d(b_hi_at(stage), &map_b_hi, &s.full[stage], k0 + kb * T_BK, b_row, pol);
-          if (!SB) tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], k0 + kb * T_BK, b_row, pol);
+          tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], k0 + kb * T_BK, b_row, pol);
           if (++stage == T_STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -718,7 +713,7 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(SB ? &s.conv[stage] : &s.full[stage], phase);
+          mbar_wait(&s.full[stage], phase);
           tc_fence_after();
           const uint32_t ah = smem_addr(a_hi_at(stage)), al = smem_addr(a_lo_at(stage));
           const uint32_t bh = smem_addr(b_hi_at(stage)), bl = smem_addr(b_lo_at(stage));
@@ -734,33 +729,6 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
         }
         umma_commit(&s.tfull[acc]);
         if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
-      }
-    }
-  } else if (SB && warp >= 6) {
-    // ================= B converters (warps 6..9) =================
-    const int ct = static_cast<int>(threadIdx.x) - 192;  // 0..127
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&s.full[stage], phase);
-        float4* hi4 = reinterpret_cast<float4*>(b_hi_at(stage));
-        float4* lo4 = reinterpret_cast<float4*>(b_lo_at(stage));
-#pragma unroll 4
-        for (int i = ct; i < T_B_BYTES / 16; i += 128) {  // elementwise: the swizzle is layout-neutral
-          const float4 v = hi4[i];
-          float4 h, l;
-          h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
-          h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
-          h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
-          h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
-          hi4[i] = h;
-          lo4[i] = l;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tcgen05 reads
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s.conv[stage]);
-        if (++stage == T_STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else {
@@ -935,20 +903,19 @@ cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, 
 cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
                                        const CUtensorMap& b_lo, float* C, float* C_lo, int ldc, int N, int K,
                                        const GroupTable& groups, int relu, int num_sms, cudaStream_t stream,
-                                       int ksplit, float* partial, int64_t rows_total, bool split_b) {
+                                       int ksplit, float* partial, int64_t rows_total) {
   if (ksplit < 1 || K % (T_BK * ksplit) || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
     return cudaErrorInvalidValue;
   if (ksplit > 1 && !partial) return cudaErrorInvalidValue;
-  static bool attr_set[2] = {false, false};
-  auto kern = split_b ? grouped_gemm_tf32x3_kernel<true> : grouped_gemm_tf32x3_kernel<false>;
-  if (!attr_set[split_b]) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytesT));
+  static bool attr_set = false;
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(kSmemBytesT));
     if (e != cudaSuccess) return e;
-    attr_set[split_b] = true;
+    attr_set = true;
   }
   const size_t stride = static_cast<size_t>(rows_total) * ldc;
-  kern<<<num_sms, split_b ? kThreads + 128 : kThreads, kSmemBytesT, stream>>>(
+  grouped_gemm_tf32x3_kernel<<<num_sms, kThreads, kSmemBytesT, stream>>>(
       a_hi, a_lo, b_hi, b_lo, ksplit > 1 ? partial : C, C_lo, ldc, N, K, groups.row_start, groups.rows, groups.slot,
       groups.num_groups, relu, ksplit, stride);
   if (ksplit > 1) {
