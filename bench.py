@@ -359,6 +359,14 @@ def main():
     flops = 4.0 * H * F * rows
     achieved = flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
     peak = pk.get("bf16_tflops_sustained", 1400.0)
+    peak_source = "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside the step loop)"
+    gemm_kernel = "grouped expert GEMM (up+down, tcgen05 kind::f16)"
+    if cfg["dtype"] == "f32":
+        # fp32 layers run 3xTF32 on the tensor cores: TF32 is half the bf16 rate and every
+        # fp32 product costs three TF32 MMAs, so the fp32-equivalent ceiling is bf16 / 6
+        peak = peak / 6.0
+        peak_source = "derived: MEASURED_PEAKS.json bf16_tflops_sustained / 2 (tf32 rate) / 3 (3xTF32 MMAs per product)"
+        gemm_kernel = "grouped expert GEMM (up+down, tcgen05 kind::tf32, 3xTF32)"
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
@@ -454,10 +462,10 @@ def main():
                              (T * row_bytes / 1e6, cfg["layers"] * len(layer.owned_experts()) * 2 * H * F * (row_bytes // H) / 1e9)},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": T * row_bytes,
                     "d2h_bytes_per_step": T * row_bytes},
-            "roofline": {"bound": "tensor", "kernel": "grouped expert GEMM (up+down, tcgen05)",
+            "roofline": {"bound": "tensor", "kernel": gemm_kernel,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside the step loop)",
+                         "peak_source": peak_source,
                          "flops_per_launch_pair": flops},
             "phase_ms": phases,
             "gpu_launches": launches,
