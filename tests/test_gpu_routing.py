@@ -68,6 +68,19 @@ def test_cfg4_hierarchy_routing_bitexact(sed):
     check_hierarchy([2, 2, 2], sed, x_all, wg, 6, bf16=True)
 
 
+@pytest.mark.parametrize("gate,split", [("mma", "0"), ("umma", "1")])
+@pytest.mark.parametrize("E,k,T", [(8, 2, 300), (64, 6, 200)])
+def test_gate_variants_routing_bitexact(gate, split, E, k, T, monkeypatch):
+    """The mma.sync gate (HEP_GATE=mma) and the K-split tcgen05 gate (HEP_GATE_SPLIT=1)
+    route exactly like the default tcgen05 gate and the oracle (ragged token counts)."""
+    monkeypatch.setenv("HEP_GATE", gate)
+    monkeypatch.setenv("HEP_GATE_SPLIT", split)
+    g = torch.Generator().manual_seed(22 + E)
+    x_all = synthetic.dyadic((8, T, 1024), g, dtype=torch.bfloat16)
+    wg = synthetic.dyadic((1024, E), g, dtype=torch.bfloat16)
+    check_hierarchy([2, 4], [1, 2], x_all, wg, k, bf16=True)
+
+
 def test_cfg1_full_layer_vs_8_simulated_gpus():
     """cfg1: 4096 tokens total (8 simulated GPUs x 512), H=1024, F=4096, E=8, top-2, fp32,
     SF=[2,4], S_ED=[1,4].  Dense experts make every GPU's output independent of where its
