@@ -14,6 +14,7 @@
 
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -865,6 +866,8 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
       struct MapCache { const void* p = nullptr; int rows = 0, cols = 0, box = 0; CUtensorMap m; };
       static MapCache xc[4], wc[2];
       static int xnext = 0;
+      static std::mutex mu;  // layers may be driven from several host threads
+      std::lock_guard<std::mutex> lock(mu);
       auto get = [](MapCache* c, int n, int* next, const void* ptr, int rows, int cols, int box) -> const CUtensorMap* {
         for (int i = 0; i < n; ++i)
           if (c[i].p == ptr && c[i].rows == rows && c[i].cols == cols && c[i].box == box) return &c[i].m;
