@@ -301,11 +301,13 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
 // and both epilogues release the accumulator on the leader's tempty barrier.
 constexpr int P_BM = 256;          // rows per cluster tile (128 per CTA)
 constexpr int P_BN = 256;
-constexpr int P_STAGES = 4;
-// Epilogue staging: each epilogue warp assembles its 32 rows x 256 bf16 columns in shared
-// memory so global (and NVLink peer) stores go out as whole 512-byte row segments
-// instead of 32 scattered 16-byte pieces per instruction.
-constexpr int P_STG_PITCH = P_BN * 2 + 16;              // bytes per staged row (+16 B pad)
+constexpr int P_STAGES = 5;
+// Epilogue staging: each epilogue warp assembles its 32 rows x 128 bf16 columns (half a
+// tile, twice per tile) in shared memory so global (and NVLink peer) stores go out as
+// whole 256-byte row segments instead of scattered 16-byte pieces; the half-width
+// buffer leaves room for a fifth operand stage.
+constexpr int P_STG_COLS = P_BN / 2;
+constexpr int P_STG_PITCH = P_STG_COLS * 2 + 16;        // bytes per staged row (+16 B pad)
 constexpr int P_STG_BYTES = 4 * 32 * P_STG_PITCH;       // 4 epilogue warps
 constexpr int P_A_BYTES = 128 * BK * 2;
 constexpr int P_B_BYTES = 128 * BK * 2;
@@ -480,38 +482,46 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_base = tmem_base + static_cast<uint32_t>(acc * P_BN) + ((quarter * 32u) << 16);
-      // TMEM -> registers -> (relu, bf16) -> staged row `lane`
-#pragma unroll 1
-      for (int c = 0; c < ncols; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_base + static_cast<uint32_t>(c), v);
-        tmem_ld_wait();
-        float f[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float x = __uint_as_float(v[i]);
-          f[i] = relu ? fmaxf(x, 0.f) : x;
-        }
-        uint4* dst = reinterpret_cast<uint4*>(stg + lane * P_STG_PITCH + c * 2);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = pack8(f + 8 * q);
-      }
-      // The accumulator is free as soon as it has been read.
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(&s.tempty[acc]);
-      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
-      // Staged rows -> global, one row per instruction: lane l writes bytes [16l, 16l+16).
-      const int row_bytes = ncols * 2;
       const int rows_here = min(32, s.rows[g] - row0);
       __nv_bfloat16* out0 = s.out[g] + static_cast<size_t>(row0) * ldc + nt * P_BN;
-      for (int r = 0; r < rows_here; ++r) {
-        if (lane * 16 < row_bytes) {
-          const uint4 val = *reinterpret_cast<const uint4*>(stg + r * P_STG_PITCH + lane * 16);
-          st_v4(reinterpret_cast<uint8_t*>(out0 + static_cast<size_t>(r) * ldc) + lane * 16, val);
+      // two column halves: TMEM -> registers -> (relu, bf16) -> staged row `lane` -> global
+#pragma unroll 1
+      for (int h = 0; h < P_BN; h += P_STG_COLS) {
+        const int hcols = min(P_STG_COLS, ncols - h);
+        if (hcols <= 0) break;  // warp-uniform
+#pragma unroll 1
+        for (int c = 0; c < hcols; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_base + static_cast<uint32_t>(h + c), v);
+          tmem_ld_wait();
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = __uint_as_float(v[i]);
+            f[i] = relu ? fmaxf(x, 0.f) : x;
+          }
+          uint4* dst = reinterpret_cast<uint4*>(stg + lane * P_STG_PITCH + c * 2);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = pack8(f + 8 * q);
         }
+        if (h + P_STG_COLS >= ncols) {
+          // the accumulator is free as soon as its last columns have been read
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(&s.tempty[acc]);
+        }
+        __syncwarp();
+        // staged rows -> global, one row per instruction: lane l writes bytes [16l, 16l+16)
+        const int row_bytes = hcols * 2;
+        for (int r = 0; r < rows_here; ++r) {
+          if (lane * 16 < row_bytes) {
+            const uint4 val = *reinterpret_cast<const uint4*>(stg + r * P_STG_PITCH + lane * 16);
+            st_v4(reinterpret_cast<uint8_t*>(out0 + static_cast<size_t>(r) * ldc + h) + lane * 16, val);
+          }
+        }
+        __syncwarp();  // the staging buffer is rewritten next
       }
-      __syncwarp();  // staging buffer is rewritten by the next tile
+      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
     }
     if (g_out) __threadfence_system();  // outputs may live in a peer GPU's HBM
   }
