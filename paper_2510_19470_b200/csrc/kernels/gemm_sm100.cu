@@ -870,7 +870,12 @@ uint32_t gemm_schedule(int rows_per_expert, int N, int K, bool up) {
   // B hurt here: a B half-tile is re-read by the other clusters of its n-column after
   // it would have been evicted (DRAM reads 4.9 -> 2.2 GB up, 13.8 -> 8.4 GB down;
   // 1.25 -> 1.44-1.48 PFLOP/s).
-  if (gemm_use_cta_pair()) return 0x2u;
+  if (gemm_use_cta_pair()) {
+    // down-projection with an expert's A stripe far beyond L2 (cfg3: 117 MB): super-rows of
+    // 8 m-tiles keep a 59 MB A stripe resident (DRAM 5.3 -> 4.8 GB, -0.8% time; tools/gemm_down_sched.sh)
+    const double a_bytes = static_cast<double>(rows_per_expert) * K * 2.0;
+    return (!up && a_bytes > 64e6) ? 0x822u : 0x2u;
+  }
   // Single CTA (128-row tiles): keep the operand re-used across a wave in L2
   // (evict_last) and stream the other (evict_first).  When one expert's A rows fit in
   // L2, rasterise m-fastest so A stays resident across all n-tiles; otherwise walk
