@@ -39,6 +39,9 @@ def main():
     ap.add_argument("--k", type=int, default=2)
     ap.add_argument("--T", type=int, default=300)
     ap.add_argument("--sr", action="store_true")
+    ap.add_argument("--ragged", action="store_true",
+                    help="every rank a different token count (down to 1), then a second forward "
+                         "with the counts rotated, reusing the layer's buffers")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
 
@@ -73,12 +76,32 @@ def main():
             got = layer.get_shared().cpu().numpy()
             assert got.tobytes() == shared.tobytes(), "refreshed shared expert differs from the reference mean"
     layer.gather_experts()
+    if a.ragged:
+        counts = [max(1, a.T - 113 * r) for r in range(G)]
+        counts[-1] = 1
+        plan = [counts, counts[1:] + counts[:1]]
+    else:
+        plan = [[a.T] * G]
+    report = {"rank": rank, "sf": a.sf, "sed": a.sed, "sr": a.sr, "T": [c[rank] for c in plan]}
+    for counts in plan:
+        check(a, layer, x_all[:, :counts[rank]], wg, w_up, w_down, flat, shared, rank, G, bf16, report)
+    if a.out and rank == 0:
+        json.dump(report, open(a.out, "w"))
+    print("rank", rank, "ok", report, flush=True)
+    layer.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
+def check(a, layer, x_all, wg, w_up, w_down, flat, shared, rank, G, bf16, report):
+    """One forward of this rank's x_all[rank] against the oracle.  Rows of other ranks
+    beyond their own count are never routed, so x_all[:, :T_rank] gives the oracle
+    exactly this rank's tokens and routing."""
+    T = x_all.shape[1]
     y = layer.forward(x_all[rank].cuda())
-    dbg = layer.debug(a.T)
+    dbg = layer.debug(T)
     torch.cuda.synchronize()
     y = y.float().cpu().numpy()
-
-    report = {"rank": rank, "sf": a.sf, "sed": a.sed, "sr": a.sr}
     if not a.sr:
         ref = oracle.moe_layer(x_all.float().numpy(), wg.numpy(), w_up.float().numpy(), w_down.float().numpy(),
                                a.k, a.sf, a.sed, bf16=bf16)
@@ -115,12 +138,6 @@ def main():
         assert d.max() <= 2e-2 * scale and d.mean() <= 2e-3 * scale, report
     else:
         assert d.max() <= 1e-4 * scale, report
-    if a.out and rank == 0:
-        json.dump(report, open(a.out, "w"))
-    print("rank", rank, "ok", report, flush=True)
-    layer.close()
-    comm.close()
-    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

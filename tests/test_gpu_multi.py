@@ -26,6 +26,12 @@ CASES = [
     ([2, 4], [1, 2], []),              # ambiguous relay (S2 tie-break)
     ([2, 4], [2, 2], []),
     ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr"]),  # cfg4 hierarchy with migration
+    # ragged: a different token count on every rank (the last rank routes one token),
+    # then a second forward with the counts rotated through the same buffers
+    ([2], [1], ["--ragged"]),
+    ([2, 2], [1, 2], ["--ragged"]),
+    ([2, 2], [2, 1], ["--ragged", "--sr"]),
+    ([2, 2], [1, 1], ["--ragged", "--dtype", "f32", "--E", "16", "--k", "4"]),
 ]
 
 
