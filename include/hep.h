@@ -190,7 +190,8 @@ int hep_layer_get_shared(hep_layer_t layer, float* out, void* stream);
  * held expert is resident.  Issued on `stream`. */
 int hep_layer_gather_experts(hep_layer_t layer, void* stream);
 /* The step: gate -> permute -> dispatch -> expert FFN -> combine.  x, y: device
- * [tokens, H] in the layer dtype. */
+ * [tokens, H] in the layer dtype, 0 <= tokens <= max_tokens (tokens may differ between
+ * GPUs; a GPU with tokens = 0 still takes part and serves its peers' rows). */
 int hep_layer_forward(hep_layer_t layer, const void* x, int64_t tokens, void* y, void* stream);
 /* Same step with host buffers (pinned recommended): H2D copy, forward, D2H copy.
  * Asynchronous and double-buffered: the H2D of the next call and the D2H of the

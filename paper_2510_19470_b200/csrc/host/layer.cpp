@@ -714,16 +714,24 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
 }
 
 void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
-  if (T <= 0 || T > Tmax_) throw std::invalid_argument("token count must be in [1, max_tokens]");
+  // T = 0 is legal: a rank with an empty batch still takes part in the exchange (it
+  // sends no rows, receives its peers' rows and runs their experts).
+  if (T < 0 || T > Tmax_) throw std::invalid_argument("token count must be in [0, max_tokens]");
   launches_ = 0;
   const int Ti = static_cast<int>(T);
   const int nchunks = (Ti + 31) / 32;
   mark("gate", s);
-  ck(launch_gate(dt_, x, wg_t_.p, Ti, static_cast<int>(H_), static_cast<int>(E_), static_cast<int>(k_),
-                 d_route_.as<int>(), static_cast<int>(n_), static_cast<int>(NK_), topk_idx_.as<int>(),
-                 topk_w_.as<float>(), keys_.as<int>(), ranks_.as<int>(), chunk_counts_.as<int>(), s), "gate");
+  if (Ti > 0) {
+    ck(launch_gate(dt_, x, wg_t_.p, Ti, static_cast<int>(H_), static_cast<int>(E_), static_cast<int>(k_),
+                   d_route_.as<int>(), static_cast<int>(n_), static_cast<int>(NK_), topk_idx_.as<int>(),
+                   topk_w_.as<float>(), keys_.as<int>(), ranks_.as<int>(), chunk_counts_.as<int>(), s), "gate");
+  }
   mark("scan", s);
-  ck(launch_chunk_scan(chunk_counts_.as<int>(), nchunks, static_cast<int>(NK_), chunk_off_.as<int>(), key_total_.as<int>(), s), "chunk scan");
+  if (Ti > 0) {
+    ck(launch_chunk_scan(chunk_counts_.as<int>(), nchunks, static_cast<int>(NK_), chunk_off_.as<int>(), key_total_.as<int>(), s), "chunk scan");
+  } else {
+    ck(cudaMemsetAsync(key_total_.p, 0, sizeof(int32_t) * static_cast<size_t>(NK_), s), "zero counts");
+  }
   ck(launch_key_scan(key_total_.as<int>(), static_cast<int>(G_), static_cast<int>(E_), rank_, d_slot_of_expert_.as<int>(),
                      key_off_.as<int>(), dest_rows_.as<int>(), dest_off_.as<int>(), g_row_start_.as<int>(),
                      g_rows_.as<int>(), g_slot_.as<int>(), s), "key scan");
@@ -923,7 +931,7 @@ void Layer::collect_timings(char* names, size_t names_cap, float* ms, int cap, i
 
 void Layer::forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s) {
   const size_t bytes = static_cast<size_t>(T * H_ * dtype_bytes(dt_));
-  if (T <= 0 || T > Tmax_) throw std::invalid_argument("token count must be in [1, max_tokens]");
+  if (T < 0 || T > Tmax_) throw std::invalid_argument("token count must be in [0, max_tokens]");
   const int b = hslot_;
   hslot_ ^= 1;
   // H2D on its own stream once the step that last used this slot stopped reading it.

@@ -331,6 +331,7 @@ cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T,
                                int* pos, cudaStream_t s, int mode) {
   const int row_bytes = H * dtype_bytes(dt);
   if (row_bytes % 16 || k > 8) return cudaErrorInvalidValue;
+  if (T == 0) return cudaSuccess;  // empty batch: nothing to send
   static bool carveout = false;
   if (!carveout) {
     // Same L1/shared split as the persistent GEMM, so remote-row blocks can run on SMs
@@ -362,6 +363,7 @@ cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, cons
                                const int* send_base, const float* w, int T, int H, int k, void* y,
                                cudaStream_t s) {
   if (k > 8) return cudaErrorInvalidValue;
+  if (T == 0) return cudaSuccess;
   if (dt == DType::BF16)
     combine_p2p_kernel<true><<<(T + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y);
   else

@@ -980,6 +980,7 @@ cudaError_t launch_permute(DType dt, const void* x, int T, int H, int k, int NK,
                            void* packed, cudaStream_t stream) {
   const int row_bytes = H * dtype_bytes(dt);
   if (row_bytes % 16) return cudaErrorInvalidValue;
+  if (T == 0) return cudaSuccess;
   const int blocks = (T + 7) / 8;
   permute_kernel<<<blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(x), T, row_bytes, k, NK,
                                              keys, ranks, chunk_off, key_off, pos,
@@ -995,6 +996,7 @@ cudaError_t launch_positions(int T, int k, int NK, const int* keys, const int* r
 
 cudaError_t launch_combine(DType dt, const void* out, const int* pos, const float* topk_w, int T,
                            int H, int k, void* y, cudaStream_t stream) {
+  if (T == 0) return cudaSuccess;
   const int blocks = (T + 7) / 8;
   if (dt == DType::BF16) {
     if (H % 8) return cudaErrorInvalidValue;

@@ -41,7 +41,8 @@ def main():
     ap.add_argument("--sr", action="store_true")
     ap.add_argument("--ragged", action="store_true",
                     help="every rank a different token count (down to 1), then a second forward "
-                         "with the counts rotated, reusing the layer's buffers")
+                         "with the counts rotated and a third with rank 0 empty, reusing the "
+                         "layer's buffers")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
 
@@ -79,7 +80,9 @@ def main():
     if a.ragged:
         counts = [max(1, a.T - 113 * r) for r in range(G)]
         counts[-1] = 1
-        plan = [counts, counts[1:] + counts[:1]]
+        zero = list(counts)
+        zero[0] = 0  # an empty batch on rank 0: it still serves its peers' rows
+        plan = [counts, counts[1:] + counts[:1], zero]
     else:
         plan = [[a.T] * G]
     report = {"rank": rank, "sf": a.sf, "sed": a.sed, "sr": a.sr, "T": [c[rank] for c in plan]}
@@ -99,8 +102,11 @@ def check(a, layer, x_all, wg, w_up, w_down, flat, shared, rank, G, bf16, report
     exactly this rank's tokens and routing."""
     T = x_all.shape[1]
     y = layer.forward(x_all[rank].cuda())
-    dbg = layer.debug(T)
     torch.cuda.synchronize()
+    if T == 0:
+        assert tuple(y.shape) == (0, a.H)
+        return
+    dbg = layer.debug(T)
     y = y.float().cpu().numpy()
     if not a.sr:
         ref = oracle.moe_layer(x_all.float().numpy(), wg.numpy(), w_up.float().numpy(), w_down.float().numpy(),

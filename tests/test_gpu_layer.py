@@ -13,6 +13,7 @@ import torch
 
 import oracle
 from paper_2510_19470_b200 import synthetic
+from paper_2510_19470_b200 import InvalidArgument
 from paper_2510_19470_b200.moe import MoELayer
 
 pytestmark = pytest.mark.gpu
@@ -78,23 +79,37 @@ def test_layer_bf16_cfg4_shape():
     assert d.max() <= 2e-2 * scale and d.mean() <= 2e-3 * scale, (d.max() / scale, d.mean() / scale)
 
 
-def test_layer_single_token_and_repeat():
-    """Edge cases: T=1, and a second forward on the same layer reuses buffers."""
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
+def test_layer_single_token_empty_and_repeat(dtype):
+    """Edge cases: T=1, an empty batch (T=0: no rows, an empty result, state intact), and
+    further forwards on the same layer reusing its buffers."""
     H, F, E, k = 256, 512, 8, 2
+    bf16 = dtype == torch.bfloat16
     g = torch.Generator().manual_seed(9)
     wg = synthetic.dyadic((H, E), g)
-    w_up, w_down = synthetic.experts(E, H, F, g, dtype=torch.bfloat16)
-    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=64, dtype=torch.bfloat16)
+    w_up, w_down = synthetic.experts(E, H, F, g, dtype=dtype)
+    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=64, dtype=dtype)
     layer.set_gate(wg.cuda())
     for e in range(E):
         layer.set_expert(e, w_up[e].cuda(), w_down[e].cuda())
-    for T in (1, 64, 33):
-        x = synthetic.dyadic((T, H), g, dtype=torch.bfloat16)
-        y = layer.forward(x.cuda()).float().cpu().numpy()
+    for T in (1, 0, 64, 0, 33):
+        x = synthetic.dyadic((T, H), g, dtype=dtype)
+        y = layer.forward(x.cuda())
+        yh = torch.empty(T, H, dtype=dtype).pin_memory()
+        layer.forward_host(x.pin_memory(), yh)
+        layer.host_fence()
+        torch.cuda.synchronize()
+        assert tuple(y.shape) == (T, H) and tuple(yh.shape) == (T, H)
+        if T == 0:
+            continue
+        y = y.float().cpu().numpy()
         ref = oracle.moe_layer(x.float().numpy()[None], wg.numpy(), w_up.float().numpy(), w_down.float().numpy(),
-                               k, [1], [1], bf16=True)
+                               k, [1], [1], bf16=bf16)
         scale = np.abs(ref["y"][0]).max()
-        assert np.abs(y - ref["y"][0]).max() <= 2e-2 * scale
+        assert np.abs(y - ref["y"][0]).max() <= (2e-2 if bf16 else 1e-4) * scale
+        assert np.array_equal(yh.float().numpy(), y)
+    with pytest.raises(InvalidArgument):
+        layer.forward(torch.zeros(65, H, dtype=dtype, device="cuda"))
     layer.close()
 
 
