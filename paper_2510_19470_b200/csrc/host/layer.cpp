@@ -11,6 +11,8 @@
 #include "layer.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
@@ -151,14 +153,14 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
       wulo_.alloc(fb * slots_ * F_ * H_);
       wdhi_.alloc(fb * slots_ * H_ * F_);
       wdlo_.alloc(fb * slots_ * H_ * F_);
-      ck(make_tmap_f32_2d(&t_xhi_, xhi_.p, rows_cap_, H_, 128, 32), "tmap xhi");
-      ck(make_tmap_f32_2d(&t_xlo_, xlo_.p, rows_cap_, H_, 128, 32), "tmap xlo");
-      ck(make_tmap_f32_2d(&t_hhi_, hhi_.p, rows_cap_, F_, 128, 32), "tmap hhi");
-      ck(make_tmap_f32_2d(&t_hlo_, hlo_.p, rows_cap_, F_, 128, 32), "tmap hlo");
-      ck(make_tmap_f32_2d(&t_wuhi_, wuhi_.p, slots_ * F_, H_, 256, 32), "tmap wuhi");
-      ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, slots_ * F_, H_, 256, 32), "tmap wulo");
-      ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, slots_ * H_, F_, 256, 32), "tmap wdhi");
-      ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, slots_ * H_, F_, 256, 32), "tmap wdlo");
+      ck(make_tmap_f32_2d(&t_xhi_, xhi_.p, rows_cap_, H_, 128, kTf32BK), "tmap xhi");
+      ck(make_tmap_f32_2d(&t_xlo_, xlo_.p, rows_cap_, H_, 128, kTf32BK), "tmap xlo");
+      ck(make_tmap_f32_2d(&t_hhi_, hhi_.p, rows_cap_, F_, 128, kTf32BK), "tmap hhi");
+      ck(make_tmap_f32_2d(&t_hlo_, hlo_.p, rows_cap_, F_, 128, kTf32BK), "tmap hlo");
+      ck(make_tmap_f32_2d(&t_wuhi_, wuhi_.p, slots_ * F_, H_, 256, kTf32BK), "tmap wuhi");
+      ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, slots_ * F_, H_, 256, kTf32BK), "tmap wulo");
+      ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, slots_ * H_, F_, 256, kTf32BK), "tmap wdhi");
+      ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, slots_ * H_, F_, 256, kTf32BK), "tmap wdlo");
       // split-K when (groups x m-tiles x n-tiles) of an even routing leaves SMs idle
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
@@ -173,6 +175,14 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
       };
       ksplit_up_ = pick(F_, H_);
       ksplit_down_ = pick(H_, F_);
+      if (const char* env = std::getenv("HEP_TF32_KSPLIT")) {  // "up,down" override (sweeps)
+        int u = 0, d = 0;
+        if (std::sscanf(env, "%d,%d", &u, &d) == 2 && u >= 1 && d >= 1 && H_ % (kTf32BK * u) == 0 &&
+            F_ % (kTf32BK * d) == 0) {
+          ksplit_up_ = u;
+          ksplit_down_ = d;
+        }
+      }
       const int ks = std::max(ksplit_up_, ksplit_down_);
       if (ks > 1) kpart_.alloc(sizeof(float) * ks * rows_cap_ * std::max(F_, H_));
     }

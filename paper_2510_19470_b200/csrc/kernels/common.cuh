@@ -185,6 +185,17 @@ __device__ __forceinline__ void tmem_ld_wait() {
 // Shared-memory matrix descriptor: K-major operand, 128-byte swizzle, rows of 128 B,
 // 8-row core groups 1024 B apart (SBO).  Bits: start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version=1 [46,48), layout SWIZZLE_128B=2 [61,64).
+// Same for 64-byte swizzle: rows of 64 B, 8-row core groups 512 B apart, SWIZZLE_64B=4.
+__device__ __forceinline__ uint64_t umma_desc_k_sw64(uint32_t smem_byte_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_byte_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>(512u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(4u) << 61;
+  return d;
+}
+
 __device__ __forceinline__ uint64_t umma_desc_k_sw128(uint32_t smem_byte_addr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((smem_byte_addr >> 4) & 0x3FFFu);

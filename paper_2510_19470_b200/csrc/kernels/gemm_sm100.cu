@@ -562,8 +562,8 @@ EncodeTiledFn encode_fn() {
 // rates.  A stage holds 32 fp32 of K (one 128-byte swizzle row) for A_hi, A_lo, B_hi,
 // B_lo: 16 + 16 + 32 + 32 KB, two stages.  Epilogue: fp32 rows, or (split mode) the
 // ReLU'd rows already split into hi/lo for the next GEMM.
-constexpr int T_BK = 32;
-constexpr int T_STAGES = 2;
+constexpr int T_BK = kTf32BK;
+constexpr int T_STAGES = T_BK == 32 ? 2 : 4;
 constexpr int T_A_BYTES = BM * T_BK * 4;
 constexpr int T_B_BYTES = BN * T_BK * 4;
 constexpr int T_STAGE_BYTES = 2 * T_A_BYTES + 2 * T_B_BYTES;
@@ -600,6 +600,12 @@ __host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
          | (2u << 10)                                // B format tf32
          | (static_cast<uint32_t>(N >> 3) << 17)     // N / 8
          | (static_cast<uint32_t>(M >> 4) << 24);    // M / 16
+}
+
+// K-major descriptor of a stage operand: 128-byte rows (BK=32, SW128) or 64-byte rows
+// (BK=16, SW64)
+__device__ __forceinline__ uint64_t t_desc(uint32_t addr) {
+  return T_BK == 32 ? umma_desc_k_sw128(addr) : umma_desc_k_sw64(addr);
 }
 
 __device__ __forceinline__ float rna_tf32(float x) {
@@ -730,9 +736,9 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
 #pragma unroll
           for (int k = 0; k < T_BK / 8; ++k) {  // K = 8 tf32 (32 bytes) per instruction
             const uint32_t off = 32u * k;
-            umma_tf32(d_tmem, umma_desc_k_sw128(al + off), umma_desc_k_sw128(bh + off), idesc, (kb | k) != 0);
-            umma_tf32(d_tmem, umma_desc_k_sw128(ah + off), umma_desc_k_sw128(bl + off), idesc, 1);
-            umma_tf32(d_tmem, umma_desc_k_sw128(ah + off), umma_desc_k_sw128(bh + off), idesc, 1);
+            umma_tf32(d_tmem, t_desc(al + off), t_desc(bh + off), idesc, (kb | k) != 0);
+            umma_tf32(d_tmem, t_desc(ah + off), t_desc(bl + off), idesc, 1);
+            umma_tf32(d_tmem, t_desc(ah + off), t_desc(bh + off), idesc, 1);
           }
           umma_commit(&s.empty[stage]);
           if (++stage == T_STAGES) { stage = 0; phase ^= 1; }
@@ -909,8 +915,10 @@ cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, 
   const cuuint64_t strides[1] = {cols * 4};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
+  if (box_cols != 32 && box_cols != 16) return cudaErrorInvalidValue;
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }

@@ -88,6 +88,10 @@ bool gemm_use_cta_pair();
 uint32_t gemm_schedule(int rows_per_expert, int N, int K, bool up);
 
 // fp32 SIMT grouped GEMM (gemm_f32.cu), same contract with fp32 operands.
+// K-extent (fp32 columns) of one 3xTF32 pipeline stage; tensor maps of its operands use
+// this box width (32: 128-byte swizzle, 2 stages of 96 KB; 16: 64-byte swizzle, 4 stages
+// of 48 KB -- 3% faster on cfg1, profiles/README.md).
+constexpr int kTf32BK = 16;
 // fp32 layers on the tensor cores: 3xTF32 (gemm_sm100.cu).  Operands come as hi/lo tf32
 // pairs (launch_split_tf32); C_lo != nullptr stores the ReLU'd result split the same way.
 cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,

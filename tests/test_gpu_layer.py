@@ -19,9 +19,9 @@ from paper_2510_19470_b200.moe import MoELayer
 pytestmark = pytest.mark.gpu
 
 
-def run_layer(H, F, E, k, T, dtype, seed=0):
+def run_layer(H, F, E, k, T, dtype, seed=0, gaussian=False):
     g = torch.Generator().manual_seed(seed)
-    x = synthetic.dyadic((T, H), g, dtype=dtype)
+    x = torch.randn((T, H), generator=g).to(dtype) if gaussian else synthetic.dyadic((T, H), g, dtype=dtype)
     wg = synthetic.dyadic((H, E), g)
     w_up, w_down = synthetic.experts(E, H, F, g, dtype=dtype)
     layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype)
@@ -57,6 +57,15 @@ def test_layer_fp32_cfg1_shape():
     x, y, dbg, ref = run_layer(1024, 4096, 8, 2, 512, torch.float32)
     check_routing(dbg, ref)
     check_packed(x, dbg, 2)
+    err = np.abs(y - ref["y"][0]).max() / np.abs(ref["y"][0]).max()
+    assert err <= 1e-4, err
+
+
+def test_layer_fp32_gaussian_inputs():
+    """fp32 accuracy on full-mantissa activations (N(0,1) tokens: the 3xTF32 split of x
+    has a non-zero lo part, unlike dyadic inputs): max error <= 1e-4 of max |y|."""
+    x, y, dbg, ref = run_layer(1024, 4096, 8, 2, 512, torch.float32, seed=5, gaussian=True)
+    assert np.array_equal(dbg["topk_idx"].cpu().numpy(), ref["topk_idx"][0])
     err = np.abs(y - ref["y"][0]).max() / np.abs(ref["y"][0]).max()
     assert err <= 1e-4, err
 
