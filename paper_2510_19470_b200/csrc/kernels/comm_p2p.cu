@@ -171,10 +171,11 @@ __global__ void __launch_bounds__(256) permute_p2p_kernel(P2PArgs a, const uint8
                                                           const int* __restrict__ chunk_off,
                                                           const int* __restrict__ key_off,
                                                           const int* __restrict__ send_base, int* __restrict__ pos,
-                                                          int mode) {
+                                                          int mode, int seg) {
   // mode 0: every row; 1: rows staying on this GPU (and all of pos); 2: remote rows only.
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int t, sg, v0, v1;
+  row_segment(row_bytes >> 4, seg, t, sg, v0, v1);
   if (t >= T_tok) return;
   const int NK = a.G * a.E;
   const int chunk = t / 32;
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(256) permute_p2p_kernel(P2PArgs a, const uint8
     const size_t o = static_cast<size_t>(t) * k + j;
     const int key = keys[o];
     const int p = key_off[key] + chunk_off[static_cast<size_t>(chunk) * NK + key] + ranks[o];
-    if (lane == 0 && mode != 2) pos[o] = p;
+    if (lane == 0 && sg == 0 && mode != 2) pos[o] = p;
     const int d = key / a.E;
     const bool skip = (mode == 1 && d != a.rank) || (mode == 2 && d == a.rank);
     const int row = d == a.rank ? p : send_base[key] + (p - key_off[key]);
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(256) permute_p2p_kernel(P2PArgs a, const uint8
   bool any = false;
   for (int j = 0; j < k; ++j) any |= dst[j] != nullptr;
   if (!any) return;
-  for (int v = lane; v < (row_bytes >> 4); v += 32) {
+  for (int v = v0 + lane; v < v1; v += 32) {
     const uint4 val = ld_nc_v4(src + 16 * v);
     for (int j = 0; j < k; ++j)
       if (dst[j]) st_v4(dst[j] + 16 * v, val);
@@ -221,11 +222,12 @@ __global__ void __launch_bounds__(256) combine_p2p_kernel(P2PArgs a, const int* 
                                                           const int* __restrict__ key_off,
                                                           const int* __restrict__ send_base,
                                                           const float* __restrict__ w, int T_tok, int H, int k,
-                                                          void* __restrict__ y) {
+                                                          void* __restrict__ y, int seg) {
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= T_tok) return;
   const int eb = BF16 ? 2 : 4;
+  int t, sg, v0, v1;
+  row_segment(H * eb / 16, seg, t, sg, v0, v1);
+  if (t >= T_tok) return;
   const uint8_t* row[8];
   float wt[8];
   for (int j = 0; j < k; ++j) {
@@ -235,8 +237,7 @@ __global__ void __launch_bounds__(256) combine_p2p_kernel(P2PArgs a, const int* 
     row[j] = static_cast<const uint8_t*>(a.oall[d]) + static_cast<size_t>(r) * H * eb;
     wt[j] = w[o];
   }
-  const int per = 16 / eb;
-  for (int v = lane; v < H / per; v += 32) {
+  for (int v = v0 + lane; v < v1; v += 32) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = 0; j < k; ++j) {
       const uint4 r = *reinterpret_cast<const uint4*>(row[j] + 16 * v);
@@ -341,8 +342,9 @@ cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T,
     if (e != cudaSuccess) return e;
     carveout = true;
   }
-  permute_p2p_kernel<<<(T + 7) / 8, 256, 0, s>>>(a, static_cast<const uint8_t*>(x), T, row_bytes, k, keys, ranks,
-                                                 chunk_off, key_off, send_base, pos, mode);
+  const int seg = row_segments(T, row_bytes >> 4);
+  permute_p2p_kernel<<<(T * seg + 7) / 8, 256, 0, s>>>(a, static_cast<const uint8_t*>(x), T, row_bytes, k, keys,
+                                                       ranks, chunk_off, key_off, send_base, pos, mode, seg);
   return cudaGetLastError();
 }
 
@@ -364,10 +366,11 @@ cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, cons
                                cudaStream_t s) {
   if (k > 8) return cudaErrorInvalidValue;
   if (T == 0) return cudaSuccess;
+  const int seg = row_segments(T, H * dtype_bytes(dt) / 16);
   if (dt == DType::BF16)
-    combine_p2p_kernel<true><<<(T + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y);
+    combine_p2p_kernel<true><<<(T * seg + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y, seg);
   else
-    combine_p2p_kernel<false><<<(T + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y);
+    combine_p2p_kernel<false><<<(T * seg + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y, seg);
   return cudaGetLastError();
 }
 

@@ -45,6 +45,19 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   return r;
 }
 
+// Row kernels run one warp per (token, row segment).  With few tokens (cfg1: 512) one
+// warp per token leaves most SMs idle and each warp walks its row one memory latency per
+// 512 bytes; `seg` warps per token cut that chain.  Returns this warp's token, segment
+// index and 16-byte-vector range [v0, v1) of the row.
+__device__ __forceinline__ void row_segment(int vecs, int seg, int& t, int& s, int& v0, int& v1) {
+  const int w = blockIdx.x * static_cast<int>(blockDim.x >> 5) + static_cast<int>(threadIdx.x >> 5);
+  t = w / seg;
+  s = w - t * seg;
+  const int per = ((vecs + seg - 1) / seg + 31) & ~31;
+  v0 = s * per;
+  v1 = min(vecs, v0 + per);
+}
+
 __device__ __forceinline__ void st_v4(void* p, const uint4& v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)

@@ -88,6 +88,15 @@ bool gemm_use_cta_pair();
 uint32_t gemm_schedule(int rows_per_expert, int N, int K, bool up);
 
 // fp32 SIMT grouped GEMM (gemm_f32.cu), same contract with fp32 operands.
+// Warps per row for the row kernels (permute / combine): one per token once the tokens
+// alone fill the GPU (148 SMs x 64 warps), else up to one per 512 bytes of the row.
+inline int row_segments(int T, int vecs) {
+  constexpr int kTargetWarps = 148 * 64;
+  if (T <= 0 || T >= kTargetWarps) return 1;
+  const int want = (kTargetWarps + T - 1) / T, most = (vecs + 31) / 32;
+  return want < most ? want : (most > 0 ? most : 1);
+}
+
 // K-extent (fp32 columns) of one 3xTF32 pipeline stage; tensor maps of its operands use
 // this box width (32: 128-byte swizzle, 2 stages of 96 KB; 16: 64-byte swizzle, 4 stages
 // of 48 KB -- 3% faster on cfg1, profiles/README.md).

@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(256) gate_mma_kernel(const __nv_bfloat16* __re
     const int hc = kc * kGC;
     __nv_bfloat16* xd = xs + static_cast<size_t>(s) * kGT * kGPitch;
     __nv_bfloat16* wd = ws + static_cast<size_t>(s) * EROWS * kGPitch;
-#pragma unroll
     constexpr int kCh = kGC / 8;  // 16-byte chunks per row per stage
+#pragma unroll
     for (int i = tid; i < kGT * kCh; i += 256) {
       const int r = i / kCh, c8 = (i % kCh) * 8;
       const int t = t0 + r;
@@ -401,14 +401,43 @@ __global__ void __launch_bounds__(256) gate_f32_oneshot_kernel(const float* __re
   cp_async_wait<0>();
   __syncthreads();
   {
-    const int tok = tid >> 3, eg = tid & 7;  // experts eg, eg + 8, ... (only the real ones)
-    const float* xr = xs + tok * pitch;
-    for (int e = eg; e < E; e += 8) {
-      const float* wr = ws + e * pitch;
-      float acc = 0.f;
-#pragma unroll 8
-      for (int c = 0; c < H; ++c) acc = fmaf(xr[c], wr[c], acc);
-      logits[tok][e] = acc;
+    // Warp w: tokens 4w..4w+3 against 8 experts at a time; lane l sums the float4 columns
+    // l, l+32, ... (4 x 8 register accumulators, every shared-memory word read once per
+    // warp), then a transposing butterfly leaves the (token, expert) total l on lane l.
+    // Logits are exact for the dyadic parity inputs in any order (S3).
+    const int tb = warp * 4;
+    for (int e0 = 0; e0 < E; e0 += 8) {
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      for (int c = lane * 4; c < H; c += 128) {
+        float4 xv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xv[q] = *reinterpret_cast<const float4*>(xs + (tb + q) * pitch + c);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float4 wv = *reinterpret_cast<const float4*>(ws + (e0 + e) * pitch + c);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float a = v[q * 8 + e];
+            a = fmaf(xv[q].x, wv.x, a);
+            a = fmaf(xv[q].y, wv.y, a);
+            a = fmaf(xv[q].z, wv.z, a);
+            v[q * 8 + e] = fmaf(xv[q].w, wv.w, a);
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+          const float send = up ? v[i] : v[i + off];
+          const float keep = up ? v[i + off] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      logits[tb + (lane >> 3)][e0 + (lane & 7)] = v[0];
     }
   }
   __syncthreads();
@@ -766,9 +795,11 @@ __global__ void __launch_bounds__(256) permute_kernel(const uint8_t* __restrict_
                                                       const int* __restrict__ chunk_off,
                                                       const int* __restrict__ key_off,
                                                       int* __restrict__ pos,
-                                                      uint8_t* __restrict__ packed) {
+                                                      uint8_t* __restrict__ packed, int seg) {
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int vecs = row_bytes >> 4;
+  int t, sg, v0, v1;
+  row_segment(vecs, seg, t, sg, v0, v1);
   if (t >= T_tok) return;
   const int chunk = t / kChunk;
   int dst[kMaxK];
@@ -776,11 +807,10 @@ __global__ void __launch_bounds__(256) permute_kernel(const uint8_t* __restrict_
     const size_t o = static_cast<size_t>(t) * k + j;
     const int key = keys[o];
     dst[j] = key_off[key] + chunk_off[static_cast<size_t>(chunk) * NK + key] + ranks[o];
-    if (lane == 0) pos[o] = dst[j];
+    if (lane == 0 && sg == 0) pos[o] = dst[j];
   }
   const uint8_t* src = x + static_cast<size_t>(t) * row_bytes;
-  const int vecs = row_bytes >> 4;
-  for (int v = lane; v < vecs; v += 32) {
+  for (int v = v0 + lane; v < v1; v += 32) {
     const uint4 val = ld_nc_v4(src + 16 * v);
     for (int j = 0; j < k; ++j) st_v4(packed + static_cast<size_t>(dst[j]) * row_bytes + 16 * v, val);
   }
@@ -800,9 +830,11 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
                                                            const int* __restrict__ pos,
                                                            const float* __restrict__ w, int T_tok,
                                                            int H, int k,
-                                                           __nv_bfloat16* __restrict__ y) {
+                                                           __nv_bfloat16* __restrict__ y, int seg) {
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int vecs = H >> 3;
+  int t, sg, v0, v1;
+  row_segment(vecs, seg, t, sg, v0, v1);
   if (t >= T_tok) return;
   int p[kMaxK];
   float wt[kMaxK];
@@ -810,8 +842,7 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
     p[j] = pos[static_cast<size_t>(t) * k + j];
     wt[j] = w[static_cast<size_t>(t) * k + j];
   }
-  const int vecs = H >> 3;
-  for (int v = lane; v < vecs; v += 32) {
+  for (int v = v0 + lane; v < v1; v += 32) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = 0; j < k; ++j) {
       float f[8];
@@ -826,9 +857,11 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
 __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restrict__ out,
                                                           const int* __restrict__ pos,
                                                           const float* __restrict__ w, int T_tok,
-                                                          int H, int k, float* __restrict__ y) {
+                                                          int H, int k, float* __restrict__ y, int seg) {
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int vecs = H >> 2;
+  int t, sg, v0, v1;
+  row_segment(vecs, seg, t, sg, v0, v1);
   if (t >= T_tok) return;
   int p[kMaxK];
   float wt[kMaxK];
@@ -836,8 +869,7 @@ __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restric
     p[j] = pos[static_cast<size_t>(t) * k + j];
     wt[j] = w[static_cast<size_t>(t) * k + j];
   }
-  const int vecs = H >> 2;
-  for (int v = lane; v < vecs; v += 32) {
+  for (int v = v0 + lane; v < v1; v += 32) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int j = 0; j < k; ++j) {
       const uint4 r = ld_nc_v4(out + static_cast<size_t>(p[j]) * H + 4 * v);
@@ -981,10 +1013,11 @@ cudaError_t launch_permute(DType dt, const void* x, int T, int H, int k, int NK,
   const int row_bytes = H * dtype_bytes(dt);
   if (row_bytes % 16) return cudaErrorInvalidValue;
   if (T == 0) return cudaSuccess;
-  const int blocks = (T + 7) / 8;
+  const int seg = row_segments(T, row_bytes >> 4);
+  const int blocks = (T * seg + 7) / 8;
   permute_kernel<<<blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(x), T, row_bytes, k, NK,
                                              keys, ranks, chunk_off, key_off, pos,
-                                             static_cast<uint8_t*>(packed));
+                                             static_cast<uint8_t*>(packed), seg);
   return cudaGetLastError();
 }
 
@@ -997,16 +1030,17 @@ cudaError_t launch_positions(int T, int k, int NK, const int* keys, const int* r
 cudaError_t launch_combine(DType dt, const void* out, const int* pos, const float* topk_w, int T,
                            int H, int k, void* y, cudaStream_t stream) {
   if (T == 0) return cudaSuccess;
-  const int blocks = (T + 7) / 8;
+  const int seg = row_segments(T, H * dtype_bytes(dt) / 16);
+  const int blocks = (T * seg + 7) / 8;
   if (dt == DType::BF16) {
     if (H % 8) return cudaErrorInvalidValue;
     combine_bf16_kernel<<<blocks, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(out), pos,
                                                     topk_w, T, H, k,
-                                                    static_cast<__nv_bfloat16*>(y));
+                                                    static_cast<__nv_bfloat16*>(y), seg);
   } else {
     if (H % 4) return cudaErrorInvalidValue;
     combine_f32_kernel<<<blocks, 256, 0, stream>>>(static_cast<const float*>(out), pos, topk_w, T,
-                                                   H, k, static_cast<float*>(y));
+                                                   H, k, static_cast<float*>(y), seg);
   }
   return cudaGetLastError();
 }

@@ -94,10 +94,15 @@ def report(cfg_name, path):
         rec = {"kernel": l["name"].split("(")[0].split("::")[-1], "kind": kd, "ms": ms, "dram_bytes": dram}
         if kd == "K8 grouped GEMM":
             flops = 2.0 * rows * H * F
+            # fp32 layers run 3xTF32: tf32 is half the bf16 rate and takes three passes, so
+            # the fp32 peak is bf16/6; the hi/lo operand pairs it streams are 2x the fp32 bytes
+            peak = peaks["bf16_tflops"] / (1 if b == 2 else 6)
             rec.update(which="up" if gemm_i == 0 else "down", tflops=flops / ms / 1e9,
-                       frac_burst=flops / ms / 1e9 / peaks["bf16_tflops"] if b == 2 else None,
+                       frac_burst=flops / ms / 1e9 / peak,
                        alg_bytes=(rows * H * b + E * H * F * b + rows * F * b) if gemm_i == 0 else
                        (rows * F * b + E * H * F * b + rows * H * b))
+            if b == 4:
+                rec.update(operand_bytes=2 * rec["alg_bytes"], operand_frac=2 * rec["alg_bytes"] / ms / 1e6 / hbm)
             gemm_i += 1
         elif kd in alg:
             rec.update(alg_bytes=alg[kd], gbs=alg[kd] / ms / 1e6, frac=alg[kd] / ms / 1e6 / hbm)
@@ -107,8 +112,10 @@ def report(cfg_name, path):
     print("|---|---|---|---|---|---|")
     for r in out:
         if "tflops" in r:
+            extra = (f" (3xTF32 peak = bf16/6); hi/lo operands {r['operand_bytes'] / 1e6:.0f} MB at "
+                     f"{r['operand_frac']:.2f} of HBM" if "operand_bytes" in r else " of burst")
             print(f"| {r['kind']} {r['which']} | {r['ms']:.3f} | {2.0 * rows * H * F / 1e12:.2f} TFLOP | "
-                  f"{r['tflops']:.0f} TF/s | {r['frac_burst']:.2f} of burst | {r['dram_bytes'] / r['alg_bytes']:.1f}x |")
+                  f"{r['tflops']:.0f} TF/s | {r['frac_burst']:.2f}{extra} | {r['dram_bytes'] / r['alg_bytes']:.1f}x |")
         elif "gbs" in r:
             print(f"| {r['kind']} | {r['ms']:.3f} | {r['alg_bytes'] / 1e6:.0f} MB | {r['gbs']:.0f} GB/s | "
                   f"{r['frac']:.2f} of HBM | {r['dram_bytes'] / r['alg_bytes']:.2f}x |")
