@@ -425,7 +425,10 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
         int mt, nt;
         decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
         const int a_row = s.row_start[g] + mt * P_BM + 128 * static_cast<int>(cta);
-        const int b_row = s.slot[g] * N + nt * P_BN + 128 * static_cast<int>(cta);
+        // a tail n-tile of <= 128 columns runs as an N=128 MMA: each CTA supplies 64 B rows
+        // (the first 64 of its 128-row box)
+        const int b_half = N - nt * P_BN <= P_BN / 2 ? 64 : 128;
+        const int b_row = s.slot[g] * N + nt * P_BN + b_half * static_cast<int>(cta);
         if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
@@ -439,12 +442,18 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
   } else if (warp == 1) {
     // ================= MMA issuer (leader CTA only) =================
     if (cta == 0 && lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(P_BM, P_BN);
+      constexpr uint32_t idesc_full = umma_idesc_bf16(P_BM, P_BN);
+      constexpr uint32_t idesc_half = umma_idesc_bf16(P_BM, P_BN / 2);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = cluster; tile < total; tile += nclusters) {
+        const int g = find_group2(s, ng, tile);
+        const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
+        int mt, nt;
+        decode_tile(tile - s.tile_start[g], m_tiles, n_tiles, sched, mt, nt);
+        const uint32_t idesc = N - nt * P_BN <= P_BN / 2 ? idesc_half : idesc_full;
         mbar_wait(&s.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * P_BN);

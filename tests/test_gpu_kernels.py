@@ -51,6 +51,8 @@ def _reference(A, B, N, rows, slots, relu):
     (1408, 2048, [129, 256], 0),      # cfg4 down-projection K, N multiple of 256
     (2048, 1408, [200, 513], 1),      # cfg4 up-projection: N tail (1408 = 5.5 x 256)
     (4096, 768, [1000], 0),
+    (512, 1088, [300, 40], 1),        # 64-column tail: N=128 MMA on the CTA pair
+    (256, 160, [70, 300], 0),         # N below one tile
 ])
 def test_grouped_gemm_bf16(K, N, rows, relu, pair, monkeypatch):
     monkeypatch.setenv("HEP_GEMM_2CTA", pair)
