@@ -388,10 +388,15 @@ def main():
     value = world * T * args.steps / (ms_max / 1000.0)
 
     # Rows this GPU's expert GEMMs processed in one step (local + received), all layers.
+    # key_counts[d*E + e] = this GPU's rows for expert e computed on GPU d; summed over the
+    # sources, the slice d = rank is every row this GPU's GEMMs ran (local, received and
+    # rows for gathered experts)
     rows = 0
     for layer in layers:
-        kc = layer.debug(T)["key_counts"]
-        rows += int(kc.sum().item()) if world == 1 else T * k
+        kc = layer.debug(T)["key_counts"].to(dev).long()
+        if world > 1:
+            dist.all_reduce(kc)
+        rows += int(kc[rank * E:(rank + 1) * E].sum().item())
     gemm_ms = sum(v for kname, v in phases.items() if kname.startswith("gemm_"))
     pk = peaks()
     flops = 4.0 * H * F * rows

@@ -372,6 +372,10 @@ __global__ void __launch_bounds__(256) gate_mma_kernel(const __nv_bfloat16* __re
 // rows and W_g^T land in shared memory through cp.async in one shot (no per-column
 // round trips), logits on the CUDA cores (exact for the dyadic parity inputs), top-k by
 // eight threads per token, ranking by match.any as in the bf16 kernel.
+// CS > 1: a cluster of CS CTAs per chunk, CTA r staging columns [r H/CS, (r+1) H/CS) --
+// CS times the SMs pulling the chunk in when there are few chunks (cfg1: 16).  CTA 0 sums
+// the partial logits over DSMEM in rank order, then ranks the chunk alone.
+template <int CS>
 __global__ void __launch_bounds__(256) gate_f32_oneshot_kernel(const float* __restrict__ x,
                                                                const float* __restrict__ wg_t, int T_tok, int H,
                                                                int E, int k, const int* __restrict__ dest_of_owner,
@@ -380,22 +384,24 @@ __global__ void __launch_bounds__(256) gate_f32_oneshot_kernel(const float* __re
                                                                int* __restrict__ ranks,
                                                                int* __restrict__ chunk_counts) {
   extern __shared__ __align__(16) float fsm[];
-  const int pitch = H + 4;  // floats; rows stay 16-byte aligned
+  const int Hc = H / CS;     // this CTA's columns
+  const int pitch = Hc + 4;  // floats; rows stay 16-byte aligned
   float* xs = fsm;                   // [kChunk][pitch]
   float* ws = fsm + kChunk * pitch;  // [E][pitch]
   __shared__ float logits[kChunk][kMaxE + 1];
   __shared__ int skey[kChunk][kMaxK];
   __shared__ int kcount[kMaxNK];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int chunk = blockIdx.x, t0 = chunk * kChunk;
-  const int c4 = H / 4;
+  const int crank = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int chunk = blockIdx.x / CS, t0 = chunk * kChunk, col0 = crank * Hc;
+  const int c4 = Hc / 4;
   for (int i = tid; i < kChunk * c4; i += blockDim.x) {
     const int r = i / c4, c = (i % c4) * 4, t = t0 + r;
-    cp_async16(xs + r * pitch + c, x + static_cast<size_t>(t < T_tok ? t : 0) * H + c, t < T_tok);
+    cp_async16(xs + r * pitch + c, x + static_cast<size_t>(t < T_tok ? t : 0) * H + col0 + c, t < T_tok);
   }
   for (int i = tid; i < E * c4; i += blockDim.x) {
     const int r = i / c4, c = (i % c4) * 4;
-    cp_async16(ws + r * pitch + c, wg_t + static_cast<size_t>(r) * H + c, true);
+    cp_async16(ws + r * pitch + c, wg_t + static_cast<size_t>(r) * H + col0 + c, true);
   }
   cp_async_commit();
   cp_async_wait<0>();
@@ -410,7 +416,7 @@ __global__ void __launch_bounds__(256) gate_f32_oneshot_kernel(const float* __re
       float v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      for (int c = lane * 4; c < H; c += 128) {
+      for (int c = lane * 4; c < Hc; c += 128) {
         float4 xv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) xv[q] = *reinterpret_cast<const float4*>(xs + (tb + q) * pitch + c);
@@ -439,6 +445,22 @@ __global__ void __launch_bounds__(256) gate_f32_oneshot_kernel(const float* __re
       }
       logits[tb + (lane >> 3)][e0 + (lane & 7)] = v[0];
     }
+  }
+  if constexpr (CS > 1) {
+    cluster_sync();  // every CTA's partial logits are in its shared memory
+    if (crank != 0) {
+      cluster_sync();  // CTA 0 has read them; nothing else to do
+      return;
+    }
+    auto cl = cooperative_groups::this_cluster();
+    for (int i = tid; i < kChunk * E; i += blockDim.x) {
+      const int r = i / E, e = i % E;
+      float acc = logits[r][e];
+#pragma unroll
+      for (int q = 1; q < CS; ++q) acc += cl.map_shared_rank(&logits[0][0], q)[r * (kMaxE + 1) + e];
+      logits[r][e] = acc;
+    }
+    cluster_sync();  // peers may exit
   }
   __syncthreads();
   {  // top-k: eight threads per token, each scans E/8 logits
@@ -970,18 +992,38 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
     if (e != cudaSuccess) return e;
   } else {
     const int nchunks = (T + kChunk - 1) / kChunk;
-    const size_t smem = static_cast<size_t>(kChunk + E) * (H + 4) * sizeof(float);
+    // few chunks: split each chunk's columns over a cluster of 4 (or 2) CTAs
+    int cs = 1;
+    if (nchunks * 4 <= 2 * 148 && H % 16 == 0) cs = 4;
+    else if (nchunks * 2 <= 2 * 148 && H % 8 == 0) cs = 2;
+    const size_t smem = static_cast<size_t>(kChunk + E) * (H / cs + 4) * sizeof(float);
     if (H % 4 == 0 && smem <= 200 * 1024 && NK <= kMaxNK && k <= kMaxK && E % 8 == 0) {
-      static bool attr = false;
-      if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(gate_f32_oneshot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   200 * 1024);
-        if (e != cudaSuccess) return e;
-        attr = true;
-      }
-      gate_f32_oneshot_kernel<<<nchunks, 256, smem, stream>>>(
-          static_cast<const float*>(x), static_cast<const float*>(wg_t), T, H, E, k, dest_of_owner, experts_per_gpu,
-          NK, topk_idx, topk_w, keys, ranks, chunk_counts);
+      auto go = [&](auto kern, int csz, bool& attr) {
+        if (!attr) {
+          const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          if (e != cudaSuccess) return e;
+          attr = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(nchunks * csz));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(csz);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, static_cast<const float*>(x), static_cast<const float*>(wg_t), T, H, E,
+                                  k, dest_of_owner, experts_per_gpu, NK, topk_idx, topk_w, keys, ranks, chunk_counts);
+      };
+      static bool a1 = false, a2 = false, a4 = false;
+      const cudaError_t e = cs == 4   ? go(gate_f32_oneshot_kernel<4>, 4, a4)
+                            : cs == 2 ? go(gate_f32_oneshot_kernel<2>, 2, a2)
+                                      : go(gate_f32_oneshot_kernel<1>, 1, a1);
+      if (e != cudaSuccess) return e;
     } else {
       gate_kernel<float><<<nchunks, 256, 0, stream>>>(static_cast<const float*>(x), static_cast<const float*>(wg_t),
                                                       T, H, E, k, dest_of_owner, experts_per_gpu, NK, topk_idx,
