@@ -13,7 +13,8 @@ value : tokens/s of all ranks, inputs resident in HBM, device-timed (CUDA events
 e2e   : same metric through hep_layer_forward_host (pinned host x -> H2D -> step ->
         D2H of y) -- the reference-facing call with host buffers.
 roofline : the expert grouped GEMM (K8), FLOPs per launch / mean launch time measured
-        live with CUDA events inside the timed region, vs the measured sustained bf16
+        live with CUDA events on the launching stream in a second pass of the same K steps
+        (phase events kept out of the `value` pass), vs the measured sustained bf16
         peak of MEASURED_PEAKS.json.
 cpu_baseline : the CPU oracle (oracle/moe_oracle.c, OpenMP) on a bounded token sample.
 --impl reference : times that same CPU implementation as the reference arm (the
@@ -362,9 +363,6 @@ def main():
     # ---------------------------------------------------------------- device-timed region
     for _ in range(args.warmup):
         step()
-    for layer in layers:
-        layer.set_profiling(True)
-        layer.timings()  # drop warm-up marks
     barrier()
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -375,6 +373,16 @@ def main():
     t1.record(stream)
     barrier()
     ms = t0.elapsed_time(t1)
+    # Per-phase device times (phase_ms, and the GEMM launches the roofline divides by):
+    # a second pass of the same K steps with a CUDA event at every phase boundary on the
+    # launching streams.  Kept out of the pass above, whose ten-odd extra event records per
+    # step cost ~5% on the smallest config (cfg1 at 4 GPUs).
+    for layer in layers:
+        layer.set_profiling(True)
+        layer.timings()
+    for _ in range(args.steps):
+        step()
+    barrier()
     phases = {}
     for layer in layers:
         for kname, v in layer.timings().items():
