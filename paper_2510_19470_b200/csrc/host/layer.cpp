@@ -713,7 +713,7 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
                                   static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, ksplit_down_,
                                   kpart_.as<float>(), rows_cap_),
        "gemm down");
-    launches_ += 1;
+    launches_ += 1 + (ksplit_up_ > 1) + (ksplit_down_ > 1);  // x split, split-K reduces
   } else {
     mark(up.c_str(), s);
     ck(launch_grouped_gemm_f32(xall_.as<float>(), static_cast<int>(H_), w_up_c_.as<float>(), hbuf_.as<float>(), static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_ * 2, s), "gemm up");
