@@ -100,8 +100,10 @@ def peaks():
 
 class ClockSampler:
     """SM clocks and throttle reasons sampled during the timed region: an NVML polling
-    thread (every 2 ms, so even a few-ms region of a small config gets samples; the
-    first sample is taken before __enter__ returns), nvidia-smi -lms 50 if NVML is absent."""
+    thread every 25 ms plus one sample as the region opens (in __enter__) and one as it
+    closes (in __exit__), so even a few-ms region of a small config is covered;
+    nvidia-smi -lms 50 if NVML is absent.  (Polling every 2 ms stalled cfg1's launch-bound
+    4-GPU step by up to 5x.)"""
 
     REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
                ("sw_power_cap", 0x4))
@@ -143,7 +145,7 @@ class ClockSampler:
         self.rows.append((float(sm), float(self.max_sm), [n for n, b in self.REASONS if bits & b]))
 
     def _poll(self):
-        while not self.stop.wait(0.002):
+        while not self.stop.wait(0.025):
             try:
                 self._sample()
             except Exception:
@@ -361,6 +363,21 @@ def main():
         torch.cuda.synchronize()
 
     # ---------------------------------------------------------------- device-timed region
+    # Bring the SM clocks up from idle first (200 ms of torch bf16 matmuls, none of our
+    # kernels): the W warm-up steps of a small config last ~1 ms, far shorter than the
+    # clock ramp, and a cfg1 value taken straight after setup read 40% low.
+    ramp = torch.randn(4096, 4096, device=dev, dtype=torch.bfloat16)
+    r0 = torch.cuda.Event(enable_timing=True)
+    r1 = torch.cuda.Event(enable_timing=True)
+    r0.record()
+    while True:
+        for _ in range(20):
+            ramp2 = ramp @ ramp
+        r1.record()
+        r1.synchronize()
+        if r0.elapsed_time(r1) >= 200.0:
+            break
+    del ramp, ramp2
     for _ in range(args.warmup):
         step()
     barrier()
@@ -508,6 +525,7 @@ def main():
             "config": {"workload": cfg["workload"], "tokens_per_gpu": T, "hidden": H, "ffn": F, "experts": E,
                        "top_k": k, "sf": sf, "sed": sed, "layers": cfg["layers"], "sr_migration": use_sr,
                        "e2e_host_threads": f"bound to {len(numa_cpus)} GPU-local cores (NVML affinity)" if numa_cpus else "unbound",
+                       "clock_ramp": "200 ms of torch bf16 matmul before the warm-up steps",
                        "planner_p": p_plan, "sed_source": sed_source, "comm": "nccl" if os.environ.get("HEP_COMM") == "nccl" else "nvlink-p2p",
                        "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per GPU)" %
                              (T * row_bytes / 1e6, cfg["layers"] * len(layer.owned_experts()) * 2 * H * F * (row_bytes // H) / 1e9)},
