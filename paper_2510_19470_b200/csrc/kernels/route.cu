@@ -887,13 +887,18 @@ __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restric
   if (t >= T_tok) return;
   int p[kMaxK];
   float wt[kMaxK];
-  for (int j = 0; j < k; ++j) {
-    p[j] = pos[static_cast<size_t>(t) * k + j];
-    wt[j] = w[static_cast<size_t>(t) * k + j];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) {  // fully unrolled + guarded: p and wt stay in registers
+    if (j < k) {
+      p[j] = pos[static_cast<size_t>(t) * k + j];
+      wt[j] = w[static_cast<size_t>(t) * k + j];
+    }
   }
   for (int v = v0 + lane; v < v1; v += 32) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j = 0; j < k; ++j) {
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+      if (j >= k) break;
       const uint4 r = ld_nc_v4(out + static_cast<size_t>(p[j]) * H + 4 * v);
       acc.x = fmaf(wt[j], __uint_as_float(r.x), acc.x);
       acc.y = fmaf(wt[j], __uint_as_float(r.y), acc.y);
