@@ -435,12 +435,15 @@ def main():
         peak = peak / 6.0
         peak_source = "derived: MEASURED_PEAKS.json bf16_tflops_sustained / 2 (tf32 rate) / 3 (3xTF32 MMAs per product)"
         gemm_kernel = "grouped expert GEMM (up+down, tcgen05 kind::tf32, 3xTF32)"
+    # DRAM bytes of one up+down GEMM pair from an ncu capture of the same N=1 workload
+    # (profiles/ncu_summary.json); the N>1 step splits the GEMM into more launches
     traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof.get(args.config, {}).get("gemm_dram_bytes_per_launch")
-    except Exception:
-        pass
+    if world == 1:
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+            traffic = prof.get(args.config, {}).get("gemm_dram_bytes_per_launch")
+        except Exception:
+            pass
 
     # ---------------------------------------------------------------- e2e through host buffers
     xh = x.cpu().pin_memory()
@@ -534,8 +537,9 @@ def main():
             "roofline": {"bound": "tensor", "kernel": gemm_kernel,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per up+down launch pair (ncu, profiles/ncu_summary.json)",
                          "peak_source": peak_source,
-                         "flops_per_launch_pair": flops},
+                         "flops_per_launch_pair": flops / cfg["layers"]},
             "phase_ms": phases,
             "gpu_launches": launches,
             "comm": comm_stats,
