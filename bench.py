@@ -529,7 +529,7 @@ def main():
                        "top_k": k, "sf": sf, "sed": sed, "layers": cfg["layers"], "sr_migration": use_sr,
                        "e2e_host_threads": f"bound to {len(numa_cpus)} GPU-local cores (NVML affinity)" if numa_cpus else "unbound",
                        "clock_ramp": "200 ms of torch bf16 matmul before the warm-up steps",
-                       "planner_p": p_plan, "sed_source": sed_source, "comm": "nccl" if os.environ.get("HEP_COMM") == "nccl" else "nvlink-p2p",
+                       "planner_p": p_plan, "sed_source": sed_source, "comm": "none (one GPU)" if world == 1 else ("nccl" if os.environ.get("HEP_COMM") == "nccl" else "nvlink-p2p"),
                        "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per GPU)" %
                              (T * row_bytes / 1e6, cfg["layers"] * len(layer.owned_experts()) * 2 * H * F * (row_bytes // H) / 1e9)},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": T * row_bytes,
