@@ -1,0 +1,52 @@
+"""bench.py output contract (CPU): the reference arm runs here and prints one JSON line
+with the keys the driver reads; the committed round-end bench lines (profiles/r1_final/)
+carry every key of the contract (value, e2e with copy bytes, roofline with its peak and
+fraction, cpu_baseline, clocks sampled in the timed region, gpu_launches)."""
+import glob
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _json_lines(path):
+    return [json.loads(ln) for ln in open(path) if ln.startswith("{")]
+
+
+def test_reference_arm_prints_contract_line():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "cfg1",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["metric"] == "MoE-layer tokens/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"] == {"value": line["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    assert line["higher_is_better"] is True
+
+
+FINAL = sorted(glob.glob(os.path.join(ROOT, "profiles", "r1_final", "cfg*_n*.log")))
+
+
+@pytest.mark.parametrize("path", FINAL, ids=[os.path.basename(p) for p in FINAL])
+def test_committed_bench_line_has_contract_keys(path):
+    lines = [d for d in _json_lines(path) if d.get("metric")]
+    assert len(lines) == 1
+    d = lines[0]
+    for key in ("value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "clocks", "gpu_launches"):
+        assert key in d, key
+    assert d["warmup"] >= 3 and d["scaling"] == "weak" and d["unit"] == "tokens/s"
+    assert d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    roof = d["roofline"]
+    assert roof["bound"] == "tensor" and roof["unit"] == "TFLOP/s"
+    assert abs(roof["frac"] - roof["achieved"] / roof["peak"]) < 1e-9
+    assert d["clocks"]["samples"] > 0
+    assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(d["clocks"]["reasons"])
+    if d["n_gpus"] == 1:
+        assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
