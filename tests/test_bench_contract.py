@@ -50,3 +50,21 @@ def test_committed_bench_line_has_contract_keys(path):
     assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(d["clocks"]["reasons"])
     if d["n_gpus"] == 1:
         assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg3", "cfg4"])
+def test_kernel_roofline_report_from_committed_launch_list(cfg):
+    """The per-kernel roofline tables in profiles/ are reproducible from the committed ncu
+    launch lists: every HBM-bound kernel of the forward at a fraction in (0, 1.05]."""
+    csv = os.path.join(ROOT, "profiles", f"r1_kernel_launches_{cfg}.csv")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "kernel_roofline.py"), "report", "--config", cfg,
+                        "--csv", csv], capture_output=True, text=True, timeout=120, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rep = json.loads(r.stdout.splitlines()[0])
+    kinds = {k["kind"] for k in rep["kernels"]}
+    assert {"K1 gate", "K2 permute", "K8 grouped GEMM", "K9 combine"} <= kinds
+    for k in rep["kernels"]:
+        if "frac" in k:
+            assert 0 < k["frac"] <= 1.05, k
+        if k["kind"] == "K8 grouped GEMM":
+            assert k["tflops"] > 0
