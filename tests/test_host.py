@@ -107,6 +107,29 @@ def test_route_table_matches_oracle_restatement():
         assert np.array_equal(ours, oracle.route_table(sf, sed)), (sf, sed)
 
 
+def test_route_table_matches_oracle_random_hierarchies():
+    """S2 on random multilevel hierarchies beyond 8 GPUs (up to 3 levels, 64 GPUs): our
+    host library and the C restatement agree on every (source, owner) destination, or
+    both report a hole (an owner no A2A peer reaches)."""
+    rng = np.random.default_rng(31)
+    checked = holes = 0
+    for _ in range(60):
+        L = int(rng.integers(1, 4))
+        sf = [int(rng.choice([1, 2, 3, 4])) for _ in range(L)]
+        sed = [int(rng.choice([d for d in range(1, v + 1) if v % d == 0])) for v in sf]
+        try:
+            want = oracle.route_table(sf, sed)
+        except ValueError:
+            holes += 1
+            with pytest.raises(Exception):
+                topo.route_table(topo.ClusterSpec.of(sf, sed))
+            continue
+        got = topo.route_table(topo.ClusterSpec.of(sf, sed))
+        assert np.array_equal(got, want), (sf, sed)
+        checked += 1
+    assert checked > 30
+
+
 def test_route_table_semantics_cfg1():
     # SF=[2,4], S_ED=[1,4]: Algorithm 1 classifies every pair whose level-1 digits
     # differ as AG (SURVEY Appendix A: m=0 row ". G1 G1 G1 A0 G1 G1 G1"), so after the
