@@ -146,6 +146,15 @@ typedef struct hep_comm_s* hep_comm_t;
 /* 128-byte NCCL unique id, to be broadcast by the caller (e.g. torch.distributed). */
 int hep_comm_unique_id(void* id128);
 int hep_comm_init(const void* id128, int rank, int nranks, hep_comm_t* comm);
+/* Virtual ranks: `nranks` communicators for nranks ranks driven by ONE process on ONE
+ * device (comms[r] is rank r).  The peer-memory step runs unchanged -- count exchange,
+ * NVLink-path dispatch stores, GEMM peer-store epilogue, epoch flags, expert All-Gather
+ * pulls, the shared-expert chain -- with peers' buffers exchanged as device pointers
+ * instead of CUDA IPC handles.  Every rank needs its own stream; rank r's k-th layer
+ * pairs with every other rank's k-th layer.  No NCCL (HEP_COMM=nccl is rejected).
+ * Replaces nothing in the reference (its "GPUs" are integer indices in one process,
+ * simcore.cpp:268-367): it is how a one-GPU box runs the multi-GPU data path. */
+int hep_comm_init_virtual(int nranks, hep_comm_t* comms);
 int hep_comm_destroy(hep_comm_t comm);
 
 /* ------------------------------------------------------------- MoE layer step */
@@ -200,6 +209,12 @@ int hep_layer_forward(hep_layer_t layer, const void* x, int64_t tokens, void* y,
 int hep_layer_forward_host(hep_layer_t layer, const void* host_x, int64_t tokens, void* host_y,
                            void* stream);
 int hep_layer_host_fence(hep_layer_t layer, void* stream);
+/* Synchronises `stream` and the layer's pending All-Gather and reports a migrated expert
+ * whose SR wire failed to decode (RUNTIME: bad magic, truncation, out-of-order or
+ * out-of-range indices -- the errors sr_decode throws, sparsecomp.cpp:36, 236-238).
+ * forward / gather_experts also raise it, without synchronising, once the failed decode
+ * has completed. */
+int hep_layer_check(hep_layer_t layer, void* stream);
 /* Communication microbenchmark of this layer's exchanges (A2A dispatch over NVLink peer
  * memory; expert All-Gather): out6 = {a2a_ms, a2a_bytes_sent, 0, ag_ms, ag_bytes_received,
  * 0}, per GPU, averaged over `iters`.  Collective: every rank must call it. */
@@ -218,6 +233,12 @@ int hep_layer_timings(hep_layer_t layer, char* names, size_t names_cap, float* m
                       int* count);
 /* Number of kernels the last forward launched (this library's own kernels). */
 int hep_layer_launch_count(hep_layer_t layer, int* count);
+/* Test hook: the next SR All-Gather overwrites the magic of the first gathered wire after
+ * the pull and before decode (exercises the rejection path above). */
+int hep_layer_debug_corrupt_next_gather(hep_layer_t layer);
+/* The L2-policy/raster words the layer's bf16 expert GEMMs run with (up, down); see
+ * hep_grouped_gemm's `sched`. */
+int hep_layer_gemm_schedule(hep_layer_t layer, uint32_t* up, uint32_t* down);
 
 /* ------------------------------------------------------------- kernel-level entry points */
 /* Routing of one GPU's tokens without moving them (gate + top-k + S2 destination +
@@ -229,11 +250,16 @@ int hep_layer_launch_count(hep_layer_t layer, int* count);
 int hep_route_plan(const hep_level* levels, int num_levels, int rank, hep_dtype dtype, const void* x,
                    int64_t tokens, int64_t hidden, const void* w_gate, int64_t experts, int64_t top_k,
                    int32_t* topk_idx, float* topk_w, int32_t* pos, int32_t* key_counts, void* stream);
-/* Exposed for parity tests and for frameworks that own their buffers. */
+/* Exposed for parity tests and for frameworks that own their buffers.
+ * C[r, n] = act(sum_k A[r, k] B[slot(g) N + n, k]) for the rows r of group g.
+ * bf16: the tcgen05 grouped GEMM the layer runs; sched = 0 picks the layer's schedule for
+ * this shape (gemm_schedule), any other value is the raw L2-policy/raster word (bits 0-1
+ * L2 policy of A, 2-3 of B, 4-5 raster, 8-15 super-row height; e.g. 0x822 = super-rows
+ * of 8 m-tiles, A evict_last).  fp32: the layer's 3xTF32 tcgen05 path (sched ignored). */
 int hep_grouped_gemm(hep_dtype dtype, const void* A, int64_t a_rows, const void* B,
                      int64_t b_slots, void* C, int64_t N, int64_t K, const int32_t* g_row_start,
                      const int32_t* g_rows, const int32_t* g_slot, int num_groups, int relu,
-                     void* stream);
+                     uint32_t sched, void* stream);
 /* Reference layout [rows, cols] -> compute layout [cols, rows] (K-major weight copy). */
 int hep_transpose_convert(hep_dtype in_dtype, const void* in, int64_t rows, int64_t cols,
                           hep_dtype out_dtype, void* out, void* stream);

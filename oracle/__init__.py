@@ -178,8 +178,10 @@ def gate(x, wg, k):
     return idx, w
 
 
-def moe_layer(x, wg, w_up, w_down, k, sf, sed, bf16, stride=1):
+def moe_layer(x, wg, w_up, w_down, k, sf, sed, bf16, stride=1, exact=False):
     """x: [G, T, H]; wg: [H, E]; w_up: [E, H, F]; w_down: [E, F, H] (fp32 values).
+    bf16=True mirrors the device's bf16 rounding points; with exact=True a bf16 layer is
+    instead evaluated as the fp32 reference (same bf16 routing, h and y unrounded).
     Returns dict(y [G,T,H], topk_idx, topk_w, pos [G,T,k], key_counts [G, G*E])."""
     x = np.ascontiguousarray(x, np.float32)
     wg = np.ascontiguousarray(wg, np.float32)
@@ -193,7 +195,8 @@ def moe_layer(x, wg, w_up, w_down, k, sf, sed, bf16, stride=1):
     tw = np.zeros((G, T, k), np.float32)
     pos = np.zeros((G, T, k), np.int32)
     kc = np.zeros((G, G * E), np.int32)
-    rc = orc.orc_moe_layer(int(bf16), _p(x), _p(wg), _p(w_up), _p(w_down), G, T, H, F, E, k, _p(sf_), _p(sed_),
+    mode = (2 if exact else 1) if bf16 else 0
+    rc = orc.orc_moe_layer(mode, _p(x), _p(wg), _p(w_up), _p(w_down), G, T, H, F, E, k, _p(sf_), _p(sed_),
                            len(sf_), stride, _p(y), _p(ti), _p(tw), _p(pos), _p(kc))
     if rc:
         raise ValueError(f"oracle layer failed ({rc})")

@@ -358,6 +358,11 @@ static void ffn_row(const float* x, const float* w_up, const float* w_down, int6
 }
 
 /* One MoE layer over G simulated GPUs (S1-S7).
+ *   bf16:   0 = fp32 layer; 1 = bf16 layer mirroring the device rounding points (bf16
+ *           W_g for routing, h, y_expert and y rounded to bf16); 2 = the fp32 reference
+ *           of a bf16 layer: the same bf16 routing (bf16 W_g, so the experts match), but
+ *           h, y_expert and y kept unrounded (fp64 accumulate, fp32 results) -- the
+ *           reference a bf16 layer's accuracy is stated against (north_star).
  *   x:      G*T*H (fp32 values; bf16-representable when bf16 != 0)
  *   wg:     H*E
  *   w_up:   E*H*F, w_down: E*F*H (reference layout per expert)
@@ -378,6 +383,7 @@ int orc_moe_layer(int bf16, const float* x, const float* wg, const float* w_up, 
   /* bf16 layers route with bf16 gate weights (the device keeps W_g in the layer dtype). */
   float* wgr = (float*)malloc(sizeof(float) * H * E);
   for (int64_t i = 0; i < H * E; ++i) wgr[i] = bf16 ? bf16_round(wg[i]) : wg[i];
+  const int rnd = bf16 == 1; /* mode 2: bf16 routing, unrounded arithmetic */
   for (int64_t g = 0; g < G; ++g)
     orc_gate(x + g * T * H, wgr, T, H, E, k, topk_idx + g * T * k, topk_w + g * T * k);
   free(wgr);
@@ -414,11 +420,11 @@ int orc_moe_layer(int bf16, const float* x, const float* wg, const float* w_up, 
       for (int64_t c = 0; c < H; ++c) acc[c] = 0.f;
       for (int64_t j = 0; j < k; ++j) {
         const int64_t e = topk_idx[r * k + j];
-        ffn_row(xr, w_up + e * H * F, w_down + e * F * H, H, F, bf16, hacc, yacc, out);
+        ffn_row(xr, w_up + e * H * F, w_down + e * F * H, H, F, rnd, hacc, yacc, out);
         const float wt = topk_w[r * k + j];
         for (int64_t c = 0; c < H; ++c) acc[c] = fmaf(wt, out[c], acc[c]);
       }
-      for (int64_t c = 0; c < H; ++c) y[r * H + c] = bf16 ? bf16_round(acc[c]) : acc[c];
+      for (int64_t c = 0; c < H; ++c) y[r * H + c] = rnd ? bf16_round(acc[c]) : acc[c];
     }
     free(hacc); free(yacc); free(out); free(acc);
   }

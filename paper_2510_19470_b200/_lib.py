@@ -129,6 +129,7 @@ SIGNATURES = {
     "hep_shared_mean": [P(VP), I32, I32, I64, VP, VP],
     "hep_comm_unique_id": [VP],
     "hep_comm_init": [VP, I32, I32, P(VP)],
+    "hep_comm_init_virtual": [I32, P(VP)],
     "hep_comm_destroy": [VP],
     "hep_layer_create": [P(LayerParams), VP, P(VP)],
     "hep_layer_destroy": [VP],
@@ -141,13 +142,16 @@ SIGNATURES = {
     "hep_layer_forward": [VP, VP, I64, VP, VP],
     "hep_layer_forward_host": [VP, VP, I64, VP, VP],
     "hep_layer_host_fence": [VP, VP],
+    "hep_layer_check": [VP, VP],
+    "hep_layer_debug_corrupt_next_gather": [VP],
     "hep_layer_comm_bench": [VP, VP, I64, I32, P(C.c_double), VP],
     "hep_layer_debug": [VP, P(VP), P(VP), P(VP), P(VP), P(VP)],
     "hep_layer_set_profiling": [VP, I32],
     "hep_layer_timings": [VP, C.c_char_p, SZ, P(C.c_float), I32, P(I32)],
     "hep_layer_launch_count": [VP, P(I32)],
+    "hep_layer_gemm_schedule": [VP, P(C.c_uint32), P(C.c_uint32)],
     "hep_route_plan": [P(Level), I32, I32, I32, VP, I64, I64, VP, I64, I64, VP, VP, VP, VP, VP],
-    "hep_grouped_gemm": [I32, VP, I64, VP, I64, VP, I64, I64, VP, VP, VP, I32, I32, VP],
+    "hep_grouped_gemm": [I32, VP, I64, VP, I64, VP, I64, I64, VP, VP, VP, I32, I32, C.c_uint32, VP],
     "hep_transpose_convert": [I32, VP, I64, I64, I32, VP, VP],
 }
 _RESTYPE = {"hep_last_error": C.c_char_p, "hep_version": C.c_char_p}

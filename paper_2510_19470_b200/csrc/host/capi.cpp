@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -383,6 +385,24 @@ int hep_comm_init(const void* id128, int rank, int nranks, hep_comm_t* comm) {
   });
 }
 
+int hep_comm_init_virtual(int nranks, hep_comm_t* comms) {
+  return guarded([&] {
+    if (nranks < 1 || nranks > 8) throw std::invalid_argument("virtual ranks: 1 <= nranks <= 8");
+    if (!comms) throw std::invalid_argument("null argument");
+    auto group = std::make_shared<hep::VirtualGroup>();
+    group->nranks = nranks;
+    std::vector<std::unique_ptr<hep_comm_s>> made;
+    for (int r = 0; r < nranks; ++r) {
+      auto c = std::make_unique<hep_comm_s>();
+      c->c.rank = r;
+      c->c.nranks = nranks;
+      c->c.vgroup = group;
+      made.push_back(std::move(c));
+    }
+    for (int r = 0; r < nranks; ++r) comms[r] = made[static_cast<size_t>(r)].release();
+  });
+}
+
 int hep_comm_destroy(hep_comm_t comm) {
   return guarded([&] {
     if (!comm) return;
@@ -472,6 +492,21 @@ int hep_layer_launch_count(hep_layer_t layer, int* count) {
   return guarded([&] { *count = layer->impl->launch_count(); });
 }
 
+int hep_layer_check(hep_layer_t layer, void* stream) {
+  return guarded([&] {
+    cuda_ok(cudaStreamSynchronize(st(stream)), "sync");
+    layer->impl->check_migration(true);
+  });
+}
+
+int hep_layer_debug_corrupt_next_gather(hep_layer_t layer) {
+  return guarded([&] { layer->impl->corrupt_next_gather(); });
+}
+
+int hep_layer_gemm_schedule(hep_layer_t layer, uint32_t* up, uint32_t* down) {
+  return guarded([&] { layer->impl->gemm_schedules(up, down); });
+}
+
 int hep_route_plan(const hep_level* levels, int num_levels, int rank, hep_dtype dtype, const void* x,
                    int64_t tokens, int64_t hidden, const void* w_gate, int64_t experts, int64_t top_k,
                    int32_t* topk_idx, float* topk_w, int32_t* pos, int32_t* key_counts, void* stream) {
@@ -520,26 +555,56 @@ int hep_route_plan(const hep_level* levels, int num_levels, int rank, hep_dtype 
 
 int hep_grouped_gemm(hep_dtype dtype, const void* A, int64_t a_rows, const void* B, int64_t b_slots, void* C,
                      int64_t N, int64_t K, const int32_t* g_row_start, const int32_t* g_rows,
-                     const int32_t* g_slot, int num_groups, int relu, void* stream) {
+                     const int32_t* g_slot, int num_groups, int relu, uint32_t sched, void* stream) {
   return guarded([&] {
     int dev = 0, sms = 148;
     cuda_ok(cudaGetDevice(&dev), "device");
     cuda_ok(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+    if (num_groups <= 0 || a_rows < 0 || b_slots <= 0 || N <= 0 || K <= 0)
+      throw std::invalid_argument("grouped GEMM needs groups, rows >= 0 and positive N, K");
     hep::GroupTable gt{g_row_start, g_rows, g_slot, num_groups};
+    cudaStream_t s = st(stream);
     if (dt_of(dtype) == hep::DType::BF16) {
       CUtensorMap ma, mb;
       const bool pair = hep::gemm_use_cta_pair();
-      cuda_ok(hep::make_tmap_bf16_2d(&ma, A, static_cast<uint64_t>(a_rows), static_cast<uint64_t>(K), 128, 64), "tmap A");
+      // sched 0: the schedule the layer would pick for this shape (rows per group ~ a_rows / groups)
+      if (sched == 0)
+        sched = hep::gemm_schedule(static_cast<int>(a_rows / num_groups), static_cast<int>(N), static_cast<int>(K),
+                                   N > K);
+      cuda_ok(hep::make_tmap_bf16_2d(&ma, A, static_cast<uint64_t>(std::max<int64_t>(a_rows, 1)),
+                                     static_cast<uint64_t>(K), 128, 64), "tmap A");
       cuda_ok(hep::make_tmap_bf16_2d(&mb, B, static_cast<uint64_t>(b_slots * N), static_cast<uint64_t>(K), pair ? 128 : 256, 64), "tmap B");
       if (pair)
-        cuda_ok(hep::launch_grouped_gemm_bf16_2cta(ma, mb, C, static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt, relu, sms, st(stream)), "gemm bf16 2cta");
+        cuda_ok(hep::launch_grouped_gemm_bf16_2cta(ma, mb, C, static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt, relu, sms, s, sched), "gemm bf16 2cta");
       else
-        cuda_ok(hep::launch_grouped_gemm_bf16(ma, mb, C, static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt, relu, sms, st(stream)), "gemm bf16");
-    } else {
+        cuda_ok(hep::launch_grouped_gemm_bf16(ma, mb, C, static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt, relu, sms, s, sched), "gemm bf16");
+      return;
+    }
+    const char* f32 = std::getenv("HEP_F32_GEMM");
+    if ((f32 && std::string(f32) == "simt") || N % 32 || K % hep::kTf32BK) {
       cuda_ok(hep::launch_grouped_gemm_f32(static_cast<const float*>(A), static_cast<int>(K), static_cast<const float*>(B),
                                            static_cast<float*>(C), static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt,
-                                           relu, sms * 2, st(stream)), "gemm f32");
+                                           relu, sms * 2, s), "gemm f32");
+      return;
     }
+    // The fp32 product path the layer runs: 3xTF32 on tcgen05 over hi/lo operand splits
+    // (scratch allocated stream-ordered for this call).
+    const size_t a_n = static_cast<size_t>(std::max<int64_t>(a_rows, 1) * K), b_n = static_cast<size_t>(b_slots * N * K);
+    float* buf = nullptr;
+    cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(float) * 2 * (a_n + b_n), s), "gemm scratch");
+    float *ahi = buf, *alo = buf + a_n, *bhi = alo + a_n, *blo = bhi + b_n;
+    cuda_ok(hep::launch_split_tf32(static_cast<const float*>(A), ahi, alo, static_cast<int64_t>(a_n), s), "split A");
+    cuda_ok(hep::launch_split_tf32(static_cast<const float*>(B), bhi, blo, static_cast<int64_t>(b_n), s), "split B");
+    CUtensorMap t_ahi, t_alo, t_bhi, t_blo;
+    const uint64_t ar = static_cast<uint64_t>(std::max<int64_t>(a_rows, 1)), br = static_cast<uint64_t>(b_slots * N);
+    cuda_ok(hep::make_tmap_f32_2d(&t_ahi, ahi, ar, static_cast<uint64_t>(K), 128, hep::kTf32BK), "tmap");
+    cuda_ok(hep::make_tmap_f32_2d(&t_alo, alo, ar, static_cast<uint64_t>(K), 128, hep::kTf32BK), "tmap");
+    cuda_ok(hep::make_tmap_f32_2d(&t_bhi, bhi, br, static_cast<uint64_t>(K), 256, hep::kTf32BK), "tmap");
+    cuda_ok(hep::make_tmap_f32_2d(&t_blo, blo, br, static_cast<uint64_t>(K), 256, hep::kTf32BK), "tmap");
+    cuda_ok(hep::launch_grouped_gemm_tf32x3(t_ahi, t_alo, t_bhi, t_blo, static_cast<float*>(C), nullptr, static_cast<int>(N),
+                                            static_cast<int>(N), static_cast<int>(K), gt, relu, sms, s),
+            "gemm tf32x3");
+    cuda_ok(cudaFreeAsync(buf, s), "gemm scratch free");
   });
 }
 

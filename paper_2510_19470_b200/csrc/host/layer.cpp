@@ -14,6 +14,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <numeric>
 #include <stdexcept>
 
@@ -33,6 +35,49 @@ void nck(ncclResult_t r, const char* what) {
 }
 
 ncclDataType_t nccl_type(DType dt) { return dt == DType::BF16 ? ncclBfloat16 : ncclFloat32; }
+
+// Side (remote dispatch) and All-Gather streams, shared by every layer of one rank on one
+// device: an 8-layer stack then needs 2 streams per rank, not 2 per layer, which keeps
+// every stream of the step on its own hardware queue (CUDA_DEVICE_MAX_CONNECTIONS <= 32,
+// DESIGN.md §7) even with 8 virtual ranks on one device.
+struct SharedStreams {
+  cudaStream_t side = nullptr, ag = nullptr;
+  int refs = 0;
+};
+std::mutex g_streams_mu;
+std::map<std::pair<int, int>, SharedStreams> g_streams;
+
+SharedStreams acquire_streams(int dev, int rank) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  SharedStreams& st = g_streams[{dev, rank}];
+  if (st.refs++ == 0) {
+    ck(cudaStreamCreateWithFlags(&st.side, cudaStreamNonBlocking), "side stream");
+    ck(cudaStreamCreateWithFlags(&st.ag, cudaStreamNonBlocking), "ag stream");
+  }
+  return st;
+}
+
+void release_streams(int dev, int rank) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  auto it = g_streams.find({dev, rank});
+  if (it == g_streams.end()) return;
+  if (--it->second.refs == 0) {
+    cudaStreamSynchronize(it->second.side);
+    cudaStreamSynchronize(it->second.ag);
+    cudaStreamDestroy(it->second.side);
+    cudaStreamDestroy(it->second.ag);
+    g_streams.erase(it);
+  }
+}
+
+uint64_t p2p_timeout_ns() {
+  // HEP_P2P_TIMEOUT_S: seconds a cross-GPU flag wait may take before it traps with a
+  // diagnostic (0 or unset: wait forever, like NCCL -- ranks may skew by minutes).
+  const char* e = std::getenv("HEP_P2P_TIMEOUT_S");
+  if (!e || !*e) return 0;
+  const double sec = std::strtod(e, nullptr);
+  return sec > 0 ? static_cast<uint64_t>(sec * 1e9) : 0;
+}
 
 }  // namespace
 
@@ -74,6 +119,8 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
   if (rank_ < 0 || rank_ >= G_) throw std::domain_error("rank out of range");
   if (G_ > 1 && (!comm_ || comm_->nranks != G_ || comm_->rank != rank_))
     throw std::invalid_argument("a communicator of G ranks matching this rank is required when G > 1");
+  if (comm_) seq_ = comm_->layers_created++;
+  if (cluster_.levels.size() > 16) throw std::invalid_argument("at most 16 levels");
   n_ = E_ / G_;
   NK_ = G_ * E_;
   if (use_sr_) {
@@ -87,6 +134,7 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
   int dev = 0;
   ck(cudaGetDevice(&dev), "cudaGetDevice");
   ck(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  ck(preload_kernels(), "kernel preload");
 
   // Placement and routing from the topology table.
   const std::vector<int32_t> route = hybridep::moe::route_table(cluster_);
@@ -204,15 +252,11 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
     shared_c_.alloc(static_cast<size_t>(dtype_bytes(dt_)) * P);
     if (G_ > 1) partial_.alloc(sizeof(double) * P);  // shared-expert refresh chain
   }
-  for (int b = 0; b < 2; ++b) {
-    x_dev_[b].alloc(eb * Tmax_ * H_);
-    y_dev_[b].alloc(eb * Tmax_ * H_);
-    ck(cudaEventCreateWithFlags(&ev_h2d_[b], cudaEventDisableTiming), "event");
-    ck(cudaEventCreateWithFlags(&ev_comp_[b], cudaEventDisableTiming), "event");
-    ck(cudaEventCreateWithFlags(&ev_d2h_[b], cudaEventDisableTiming), "event");
+  if (use_sr_) {
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&mig_err_host_), sizeof(int32_t), cudaHostAllocMapped), "mapped flag");
+    *mig_err_host_ = 0;
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mig_err_dev_), mig_err_host_, 0), "mapped flag");
   }
-  ck(cudaStreamCreateWithFlags(&h2d_s_, cudaStreamNonBlocking), "stream");
-  ck(cudaStreamCreateWithFlags(&d2h_s_, cudaStreamNonBlocking), "stream");
   send_off_.resize(a2a_peers_.size());
   send_rows_.resize(a2a_peers_.size());
   recv_off_.resize(a2a_peers_.size());
@@ -221,11 +265,91 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
   if (G_ > 1) {
     const char* mode = std::getenv("HEP_COMM");
     p2p_ = !(mode && std::string(mode) == "nccl");
-    if (p2p_) setup_p2p();
+    if (comm_->vgroup && !p2p_)
+      throw std::invalid_argument("virtual ranks share one device: only the peer-memory path applies (unset HEP_COMM)");
+    timeout_ns_ = p2p_timeout_ns();
+    if (p2p_) {
+      setup_p2p();
+    } else {
+      // NCCL baseline: agree on the layer shape before any row is received
+      const LayerSig mine = signature();
+      DevBuf d_mine, d_all;
+      d_mine.alloc(sizeof(LayerSig));
+      d_all.alloc(sizeof(LayerSig) * G_);
+      ck(cudaMemcpy(d_mine.p, &mine, sizeof(LayerSig), cudaMemcpyHostToDevice), "sig h2d");
+      nck(ncclAllGather(d_mine.p, d_all.p, sizeof(LayerSig), ncclUint8, comm_->nccl, 0), "sig allgather");
+      ck(cudaStreamSynchronize(0), "sig sync");
+      std::vector<LayerSig> all(static_cast<size_t>(G_));
+      ck(cudaMemcpy(all.data(), d_all.p, sizeof(LayerSig) * G_, cudaMemcpyDeviceToHost), "sig d2h");
+      check_signatures(all);
+    }
   }
   const int rows_per_expert = static_cast<int>(Tmax_ * k_ / E_);
   sched_up_ = gemm_schedule(rows_per_expert, static_cast<int>(F_), static_cast<int>(H_), true);
   sched_down_ = gemm_schedule(rows_per_expert, static_cast<int>(H_), static_cast<int>(F_), false);
+}
+
+LayerSig Layer::signature() const {
+  LayerSig g;
+  std::memset(&g, 0, sizeof(g));
+  g.H = H_;
+  g.F = F_;
+  g.E = E_;
+  g.k = k_;
+  g.Tmax = Tmax_;
+  g.dtype = static_cast<int32_t>(dt_);
+  g.use_sr = use_sr_ ? 1 : 0;
+  if (use_sr_) {
+    g.sr_k = sr_cfg_.k.value_or(-1);
+    g.sr_ratio = sr_cfg_.ratio_CR.value_or(0.0);
+    g.per_matrix = sr_cfg_.per_matrix_budget ? 1 : 0;
+    g.iw = sr_cfg_.index_width_bits;
+    g.vw = sr_cfg_.value_width_bits;
+  }
+  g.nlev = static_cast<int32_t>(cluster_.levels.size());
+  for (size_t i = 0; i < cluster_.levels.size(); ++i) {
+    g.sf[i] = cluster_.levels[i].scaling_factor;
+    g.sed[i] = cluster_.levels[i].domain_size;
+  }
+  g.p2p = p2p_ ? 1 : 0;
+  return g;
+}
+
+void Layer::check_signatures(const std::vector<LayerSig>& all) const {
+  const LayerSig mine = signature();
+  for (size_t r = 0; r < all.size(); ++r)
+    if (std::memcmp(&all[r], &mine, sizeof(LayerSig)) != 0)
+      throw std::invalid_argument("rank " + std::to_string(r) + " created this layer with a different shape, " +
+                                  "max_tokens, dtype, SR configuration, cluster or comm path than rank " +
+                                  std::to_string(rank_));
+}
+
+PeerBufs Layer::my_bufs() const {
+  return PeerBufs{xall_.p,  oall_.p,    sync_.p,        w_up_c_.p, w_down_c_.p,
+                  wires_.p, partial_.p, chain_flags_.p, shared_.p};
+}
+
+void Layer::setup_streams() {
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "device");
+  const SharedStreams st = acquire_streams(dev, rank_);
+  side_s_ = st.side;
+  ag_s_ = st.ag;
+  // Every stream a rank's step uses needs its own hardware queue: the
+  // caller's stream plus the shared side and All-Gather streams, per rank of this process.
+  const int ranks_here = comm_->vgroup ? static_cast<int>(G_) : 1;
+  const int need = 3 * ranks_here + 1;
+  const char* env = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+  const int have = env ? std::atoi(env) : 8;
+  static bool warned = false;
+  if (have < need && !warned) {
+    warned = true;
+    std::fprintf(stderr,
+                 "hep: CUDA_DEVICE_MAX_CONNECTIONS=%s but the peer-memory step needs >= %d hardware queues; set it "
+                 "(<= 32) before the CUDA context is created, or aliased queues may serialise a spin-wait ahead of "
+                 "the work it waits for\n",
+                 env ? env : "unset (8)", need);
+  }
 }
 
 void Layer::setup_p2p() {
@@ -233,88 +357,129 @@ void Layer::setup_p2p() {
   sync_.alloc(p2p_sync_bytes(static_cast<int>(G_), static_cast<int>(E_)));
   ck(cudaMemset(sync_.p, 0, sync_.bytes), "sync memset");
   send_base_.alloc(sizeof(int) * NK_);
-  // Exchange CUDA IPC handles of xall / oall / sync (token path) and of the expert
-  // compute copies and SR wires (expert All-Gather pulls) through NCCL.
-  constexpr int kBufs = 9;
-  cudaIpcMemHandle_t mine[kBufs] = {};
-  ck(cudaIpcGetMemHandle(&mine[0], xall_.p), "ipc handle");
-  ck(cudaIpcGetMemHandle(&mine[1], oall_.p), "ipc handle");
-  ck(cudaIpcGetMemHandle(&mine[2], sync_.p), "ipc handle");
-  ck(cudaIpcGetMemHandle(&mine[3], w_up_c_.p), "ipc handle");
-  ck(cudaIpcGetMemHandle(&mine[4], w_down_c_.p), "ipc handle");
   if (use_sr_) {
-    // + the shared-expert refresh chain: fp64 partials, chunk flags, the fp32 mean
+    // the shared-expert refresh chain: chunk flags (+ barrier flags)
     const int64_t P = 2 * H_ * F_;
     chain_flags_.alloc(sizeof(uint32_t) * ((P + kChainChunk - 1) / kChainChunk + kMaxG));
     ck(cudaMemset(chain_flags_.p, 0, chain_flags_.bytes), "chain flags");
-    ck(cudaIpcGetMemHandle(&mine[5], wires_.p), "ipc handle");
-    ck(cudaIpcGetMemHandle(&mine[6], partial_.p), "ipc handle");
-    ck(cudaIpcGetMemHandle(&mine[7], chain_flags_.p), "ipc handle");
-    ck(cudaIpcGetMemHandle(&mine[8], shared_.p), "ipc handle");
   }
-  DevBuf dmine, dall;
-  dmine.alloc(sizeof(mine));
-  dall.alloc(sizeof(mine) * G_);
-  ck(cudaMemcpy(dmine.p, mine, sizeof(mine), cudaMemcpyHostToDevice), "ipc h2d");
-  nck(ncclAllGather(dmine.p, dall.p, sizeof(mine), ncclUint8, comm_->nccl, 0), "ipc allgather");
-  ck(cudaStreamSynchronize(0), "ipc sync");
-  std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(kBufs * G_));
-  ck(cudaMemcpy(all.data(), dall.p, sizeof(mine) * G_, cudaMemcpyDeviceToHost), "ipc d2h");
-  P2PArgs& a = p2p_args_;
-  a.G = static_cast<int>(G_);
-  a.E = static_cast<int>(E_);
-  a.rank = rank_;
-  a.recv_start = static_cast<int>(Tmax_ * k_);
-  a.row_bytes = static_cast<int>(H_ * dtype_bytes(dt_));
   g_out_down_.alloc(sizeof(unsigned long long) * slots_ * (1 + static_cast<int64_t>(a2a_peers_.size())));
   g_wait_.alloc(sizeof(int) * slots_ * (1 + static_cast<int64_t>(a2a_peers_.size())));
-  ck(cudaStreamCreateWithFlags(&side_s_, cudaStreamNonBlocking), "side stream");
+  setup_streams();
   ck(cudaEventCreateWithFlags(&ev_counts_, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&ev_remote_, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&ev_arrived_, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&ev_ag_start_, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&ev_ag_done_, cudaEventDisableTiming), "event");
   {
     const char* spin = std::getenv("HEP_GEMM_SPIN");  // 1: GEMM producers wait on dispatch flags (old)
     spin_ = spin && spin[0] == '1';
   }
+  if (comm_->vgroup) {
+    // Virtual ranks: register; peers resolve on first use, once every rank's layer exists.
+    std::lock_guard<std::mutex> lk(comm_->vgroup->mu);
+    auto& slot = comm_->vgroup->layers[{seq_, rank_}];
+    if (slot) throw std::invalid_argument("virtual rank already has a layer with this sequence number");
+    slot = this;
+    connected_ = false;
+    return;
+  }
+  // Processes: exchange the layer signature and CUDA IPC handles of xall / oall / sync
+  // (token path), the expert compute copies and SR wires (All-Gather pulls) and the
+  // shared-expert chain buffers through NCCL.
+  constexpr int kBufs = 9;
+  struct Hello {
+    LayerSig sig;
+    cudaIpcMemHandle_t h[kBufs];
+  } mine;
+  std::memset(&mine, 0, sizeof(mine));
+  mine.sig = signature();
+  const PeerBufs b = my_bufs();
+  void* const ptrs[kBufs] = {b.xall, b.oall, b.sync, b.w_up, b.w_down, b.wires, b.partial, b.chain_flags, b.shared};
+  const int nb = use_sr_ ? kBufs : 5;
+  for (int i = 0; i < nb; ++i) ck(cudaIpcGetMemHandle(&mine.h[i], ptrs[i]), "ipc handle");
+  DevBuf dmine, dall;
+  dmine.alloc(sizeof(Hello));
+  dall.alloc(sizeof(Hello) * G_);
+  ck(cudaMemcpy(dmine.p, &mine, sizeof(Hello), cudaMemcpyHostToDevice), "ipc h2d");
+  nck(ncclAllGather(dmine.p, dall.p, sizeof(Hello), ncclUint8, comm_->nccl, 0), "ipc allgather");
+  ck(cudaStreamSynchronize(0), "ipc sync");
+  std::vector<Hello> all(static_cast<size_t>(G_));
+  ck(cudaMemcpy(all.data(), dall.p, sizeof(Hello) * G_, cudaMemcpyDeviceToHost), "ipc d2h");
+  std::vector<LayerSig> sigs;
+  for (const Hello& h : all) sigs.push_back(h.sig);
+  check_signatures(sigs);
+  std::vector<PeerBufs> bufs(static_cast<size_t>(G_));
+  for (int r = 0; r < G_; ++r) {
+    if (r == rank_) {
+      bufs[static_cast<size_t>(r)] = b;
+      continue;
+    }
+    void* p[kBufs] = {};
+    for (int i = 0; i < nb; ++i) {
+      ck(cudaIpcOpenMemHandle(&p[i], all[static_cast<size_t>(r)].h[i], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+      ipc_opened_.push_back(p[i]);
+    }
+    bufs[static_cast<size_t>(r)] = PeerBufs{p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7], p[8]};
+  }
+  connect(bufs);
+}
+
+void Layer::ensure_connected() {
+  if (connected_) return;
+  VirtualGroup& vg = *comm_->vgroup;
+  std::vector<PeerBufs> bufs(static_cast<size_t>(G_));
+  std::vector<LayerSig> sigs(static_cast<size_t>(G_));
+  {
+    std::lock_guard<std::mutex> lk(vg.mu);
+    for (int r = 0; r < G_; ++r) {
+      auto it = vg.layers.find({seq_, r});
+      if (it == vg.layers.end())
+        throw std::runtime_error("virtual rank " + std::to_string(r) + " has not created layer #" +
+                                 std::to_string(seq_) + " yet (create every rank's layer before the first step)");
+      bufs[static_cast<size_t>(r)] = it->second->my_bufs();
+      sigs[static_cast<size_t>(r)] = it->second->signature();
+    }
+  }
+  check_signatures(sigs);
+  connect(bufs);
+  connected_ = true;
+}
+
+void Layer::connect(const std::vector<PeerBufs>& bufs) {
+  P2PArgs& a = p2p_args_;
+  a.G = static_cast<int>(G_);
+  a.E = static_cast<int>(E_);
+  a.rank = rank_;
+  a.recv_start = static_cast<int>(Tmax_ * k_);  // equal on every rank: signatures matched
+  a.row_bytes = static_cast<int>(H_ * dtype_bytes(dt_));
+  a.timeout_ns = timeout_ns_;
   peer_w_up_.assign(static_cast<size_t>(G_), nullptr);
   peer_w_down_.assign(static_cast<size_t>(G_), nullptr);
   peer_wires_.assign(static_cast<size_t>(G_), nullptr);
   peer_chain_flags_.assign(static_cast<size_t>(G_), nullptr);
-  if (use_sr_) peer_chain_flags_[static_cast<size_t>(rank_)] = chain_flags_.as<uint32_t>();
   for (int r = 0; r < G_; ++r) {
-    if (r == rank_) {
-      a.xall[r] = xall_.p;
-      a.oall[r] = oall_.p;
-      a.sync[r] = sync_.p;
-      continue;
+    const PeerBufs& b = bufs[static_cast<size_t>(r)];
+    a.xall[r] = b.xall;
+    a.oall[r] = b.oall;
+    a.sync[r] = b.sync;
+    if (r == rank_) continue;
+    peer_w_up_[static_cast<size_t>(r)] = b.w_up;
+    peer_w_down_[static_cast<size_t>(r)] = b.w_down;
+    peer_wires_[static_cast<size_t>(r)] = b.wires;
+  }
+  if (use_sr_) {
+    for (int r = 0; r < G_; ++r)
+      peer_chain_flags_[static_cast<size_t>(r)] = static_cast<uint32_t*>(bufs[static_cast<size_t>(r)].chain_flags);
+    if (rank_ > 0) {
+      peer_partial_prev_ = static_cast<const double*>(bufs[static_cast<size_t>(rank_ - 1)].partial);
+      peer_flags_prev_ = static_cast<const uint32_t*>(bufs[static_cast<size_t>(rank_ - 1)].chain_flags);
     }
-    void* ptrs[kBufs] = {};
-    const int nb = use_sr_ ? kBufs : 5;
-    for (int b = 0; b < nb; ++b) {
-      ck(cudaIpcOpenMemHandle(&ptrs[b], all[static_cast<size_t>(kBufs * r + b)], cudaIpcMemLazyEnablePeerAccess), "ipc open");
-      ipc_opened_.push_back(ptrs[b]);
-    }
-    a.xall[r] = ptrs[0];
-    a.oall[r] = ptrs[1];
-    a.sync[r] = ptrs[2];
-    peer_w_up_[static_cast<size_t>(r)] = ptrs[3];
-    peer_w_down_[static_cast<size_t>(r)] = ptrs[4];
-    peer_wires_[static_cast<size_t>(r)] = ptrs[5];
-    if (use_sr_) peer_chain_flags_[static_cast<size_t>(r)] = static_cast<uint32_t*>(ptrs[7]);
-    if (use_sr_ && r == rank_ - 1) {
-      peer_partial_prev_ = static_cast<const double*>(ptrs[6]);
-      peer_flags_prev_ = static_cast<const uint32_t*>(ptrs[7]);
-    }
-    if (use_sr_ && r == G_ - 1) {
-      peer_shared_last_ = static_cast<const float*>(ptrs[8]);
-      peer_flags_last_ = static_cast<const uint32_t*>(ptrs[7]);
-    }
+    peer_shared_last_ = static_cast<const float*>(bufs[static_cast<size_t>(G_ - 1)].shared);
+    peer_flags_last_ = static_cast<const uint32_t*>(bufs[static_cast<size_t>(G_ - 1)].chain_flags);
   }
   a.n_ag = 0;
   for (int64_t p : ag_peers_) a.ag_list[a.n_ag++] = static_cast<int>(p);
-  ck(cudaStreamCreateWithFlags(&ag_s_, cudaStreamNonBlocking), "ag stream");
-  ck(cudaEventCreateWithFlags(&ev_ag_start_, cudaEventDisableTiming), "event");
-  ck(cudaEventCreateWithFlags(&ev_ag_done_, cudaEventDisableTiming), "event");
   const std::vector<hybridep::sim::PeerLists> peers = hybridep::sim::peer_lists(cluster_);
   for (int d = 0; d < G_; ++d) {
     int n = 0;
@@ -325,13 +490,25 @@ void Layer::setup_p2p() {
 }
 
 Layer::~Layer() {
-  if (side_s_) {
-    cudaStreamSynchronize(side_s_);
-    cudaStreamDestroy(side_s_);
+  if (p2p_ && connected_ && ag_epoch_ > 0 && !ag_peers_.empty() && side_s_) {
+    // Peers pull this rank's owned experts (or wires) on their All-Gather streams: wait
+    // until every AG peer has signalled that it finished the last epoch's pulls before
+    // the memory is freed.
+    P2PArgs prev = p2p_args_;
+    prev.epoch = ag_epoch_;
+    if (launch_signal_wait(prev, 4, side_s_, true, true, false) == cudaSuccess) cudaStreamSynchronize(side_s_);
   }
-  if (ag_s_) {
-    cudaStreamSynchronize(ag_s_);
-    cudaStreamDestroy(ag_s_);
+  if (side_s_) cudaStreamSynchronize(side_s_);
+  if (ag_s_) cudaStreamSynchronize(ag_s_);
+  if (comm_ && comm_->vgroup) {
+    std::lock_guard<std::mutex> lk(comm_->vgroup->mu);
+    auto it = comm_->vgroup->layers.find({seq_, rank_});
+    if (it != comm_->vgroup->layers.end() && it->second == this) comm_->vgroup->layers.erase(it);
+  }
+  if (side_s_) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    release_streams(dev, rank_);
   }
   if (ev_ag_start_) cudaEventDestroy(ev_ag_start_);
   if (ev_ag_done_) cudaEventDestroy(ev_ag_done_);
@@ -349,6 +526,23 @@ Layer::~Layer() {
   }
   if (h2d_s_) cudaStreamDestroy(h2d_s_);
   if (d2h_s_) cudaStreamDestroy(d2h_s_);
+  if (mig_err_host_) cudaFreeHost(mig_err_host_);
+}
+
+void Layer::init_host_staging() {
+  if (h2d_s_) return;
+  // forward_host's staging buffers and copy streams, created on first use (an 8-layer
+  // stack driven through device buffers never pays for them)
+  const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
+  for (int b = 0; b < 2; ++b) {
+    x_dev_[b].alloc(eb * Tmax_ * H_);
+    y_dev_[b].alloc(eb * Tmax_ * H_);
+    ck(cudaEventCreateWithFlags(&ev_h2d_[b], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_comp_[b], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_d2h_[b], cudaEventDisableTiming), "event");
+  }
+  ck(cudaStreamCreateWithFlags(&h2d_s_, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&d2h_s_, cudaStreamNonBlocking), "stream");
 }
 
 void Layer::set_gate(const void* w_gate, DType dt, cudaStream_t s) {
@@ -359,6 +553,14 @@ void Layer::set_gate(const void* w_gate, DType dt, cudaStream_t s) {
 void Layer::set_expert(int64_t e, const void* w_up, const void* w_down, DType dt, cudaStream_t s) {
   if (e < 0 || e >= E_) throw std::domain_error("expert id out of range");
   if (e / n_ != rank_) throw std::invalid_argument("expert is not owned by this rank");
+  if (ag_pending_) ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");  // the encode reads the masters
+  if (p2p_ && !use_sr_ && ag_epoch_ > 0 && !ag_peers_.empty()) {
+    // AG peers pull the owned compute copies on their own streams: rewrite them only once
+    // every peer has signalled that it finished the previous epoch's pulls (slot 4)
+    P2PArgs prev = p2p_args_;
+    prev.epoch = ag_epoch_;
+    ck(launch_signal_wait(prev, 4, s, true, true, false), "ag pulled");
+  }
   const int64_t slot = slot_of_expert_[static_cast<size_t>(e)];
   const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
   uint8_t* up = w_up_c_.as<uint8_t>() + eb * slot * F_ * H_;
@@ -396,6 +598,7 @@ void Layer::get_shared(float* out, cudaStream_t s) const {
 
 void Layer::refresh_shared(cudaStream_t s) {
   if (!use_sr_) throw std::invalid_argument("shared expert is only used with SR migration");
+  if (p2p_) ensure_connected();
   const int64_t P = 2 * H_ * F_;
   if (G_ == 1) {  // every expert is local: the plain kernel over the list
     std::vector<const void*> ex(static_cast<size_t>(n_));
@@ -425,6 +628,7 @@ void Layer::refresh_shared(cudaStream_t s) {
     const int64_t nchunks = (P + kChainChunk - 1) / kChainChunk;
     for (int r = 0; r < G_; ++r) c.bar[r] = peer_chain_flags_[static_cast<size_t>(r)] + nchunks;
     c.epoch = ++chain_epoch_;
+    c.timeout_ns = timeout_ns_;
     ck(launch_shared_chain(c, s), "shared chain");
   } else {
     // NCCL: the same chain with whole-vector hops, then a broadcast from the last rank
@@ -472,6 +676,8 @@ void Layer::split_dirty_slots(cudaStream_t s) {
 
 void Layer::gather_experts(cudaStream_t s) {
   if (G_ == 1 || ag_peers_.empty()) return;
+  if (p2p_) ensure_connected();
+  check_migration(false);
   mark_gathered_dirty();  // the gathered slots' compute copies are rewritten below
   const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
   const size_t per_slot_up = static_cast<size_t>(F_ * H_), per_slot_down = static_cast<size_t>(H_ * F_);
@@ -522,10 +728,9 @@ void Layer::gather_experts(cudaStream_t s) {
                            eb * n_ * per_slot_down, cudaMemcpyDeviceToDevice, ag_s_), "pull down");
       }
     }
-    if (use_sr_) {
-      ck(launch_signal_wait(ag, 4, ag_s_, false, true, true), "wires pulled");
-      decode_gathered(wb, stride, ag_s_);
-    }
+    // "I have pulled your experts / wires of this epoch": owners may rewrite them now
+    ck(launch_signal_wait(ag, 4, ag_s_, false, true, true), "pulled");
+    if (use_sr_) decode_gathered(wb, stride, ag_s_);
     ck(cudaEventRecord(ev_ag_done_, ag_s_), "record");
     ag_pending_ = true;
     return;
@@ -581,6 +786,10 @@ void Layer::decode_gathered(size_t wb, size_t stride, cudaStream_t s) {
   std::vector<int64_t> gathered;
   for (int64_t p : ag_peers_)
     for (int64_t i = 0; i < n_; ++i) gathered.push_back(first_slot_of(p) + i);
+  if (corrupt_next_ && !gathered.empty()) {  // test hook: break the first gathered wire's magic
+    ck(cudaMemsetAsync(wires + stride * gathered[0], 0x58, 1, s), "corrupt");
+    corrupt_next_ = false;
+  }
   for (size_t b0 = 0; b0 < gathered.size(); b0 += kMaxSrBatch) {
     const size_t nb = std::min(gathered.size() - b0, static_cast<size_t>(kMaxSrBatch));
     std::vector<const uint8_t*> wi;
@@ -594,7 +803,33 @@ void Layer::decode_gathered(size_t wb, size_t stride, cudaStream_t s) {
     ck(launch_sr_decode_layout_batch(wi.data(), static_cast<int>(nb), wb, shared_.as<float>(), shared_c_.p, dt_, H_,
                                      F_, up.data(), down.data(), sr_status_.as<int32_t>(), s),
        "decode");
+    // a rejected wire (sparsecomp.cpp:36, 236-238) must not pass silently: fold the batch
+    // status into the host-mapped error word that the next call (or check_migration) raises
+    ck(launch_sr_status_fold(sr_status_.as<int32_t>(), static_cast<int>(nb), mig_err_dev_, s), "decode status");
   }
+}
+
+void Layer::check_migration(bool sync) {
+  if (!use_sr_ || !mig_err_host_) return;
+  if (sync) {
+    if (ag_pending_) ck(cudaEventSynchronize(ev_ag_done_), "ag sync");
+    ck(cudaDeviceSynchronize(), "sync");
+  }
+  const int32_t v = *reinterpret_cast<volatile int32_t*>(mig_err_host_);
+  if (v == 0) return;
+  *reinterpret_cast<volatile int32_t*>(mig_err_host_) = 0;
+  const int code = v & 0xff, entry = v >> 8;
+  std::string why;
+  switch (code) {
+    case 1: why = "bad residual magic"; break;
+    case 2: why = "compressed residual truncated"; break;
+    case 3: why = "unsupported residual widths"; break;
+    case 4: why = "residual shape tag does not match the shared expert"; break;
+    case 5: why = "corrupt residual: index out of bounds (entry " + std::to_string(entry) + ")"; break;
+    case 6: why = "corrupt residual: indices not strictly increasing (entry " + std::to_string(entry) + ")"; break;
+    default: why = "decode status " + std::to_string(code);
+  }
+  throw std::runtime_error("migrated expert rejected: " + why);
 }
 
 void Layer::mark(const char* name, cudaStream_t s) {
@@ -656,6 +891,7 @@ void Layer::build_comm_plan_and_groups(int T, cudaStream_t s) {
     }
     recv_rows_[i] = rr;
     recv_at += rr;
+    if (recv_at > rows_cap_) throw std::runtime_error("received rows exceed the receive area (max_tokens mismatch)");
   }
   num_groups_ = static_cast<int>(grs.size());
   ck(cudaMemcpyAsync(g_row_start_.p, grs.data(), sizeof(int32_t) * grs.size(), cudaMemcpyHostToDevice, s), "groups");
@@ -692,6 +928,7 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     gt.wait_src = wait_src + g0;
     gt.wait_flags = p2p_dispatch_flags(p2p_args_);
     gt.epoch = p2p_args_.epoch;
+    gt.timeout_ns = timeout_ns_;
   }
   const std::string up = std::string("gemm_up") + tag, down = std::string("gemm_down") + tag;
   if (dt_ == DType::BF16) {
@@ -727,6 +964,8 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
   // T = 0 is legal: a rank with an empty batch still takes part in the exchange (it
   // sends no rows, receives its peers' rows and runs their experts).
   if (T < 0 || T > Tmax_) throw std::invalid_argument("token count must be in [0, max_tokens]");
+  if (p2p_) ensure_connected();
+  check_migration(false);
   launches_ = 0;
   const int Ti = static_cast<int>(T);
   const int nchunks = (Ti + 31) / 32;
@@ -851,6 +1090,8 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
 void Layer::comm_bench(const void* x, int64_t T, int iters, double* out, cudaStream_t s) {
   for (int i = 0; i < 6; ++i) out[i] = 0.0;
   if (G_ == 1) return;
+  if (p2p_) ensure_connected();
+  init_host_staging();
   cudaEvent_t e0, e1;
   ck(cudaEventCreate(&e0), "event");
   ck(cudaEventCreate(&e1), "event");
@@ -942,6 +1183,7 @@ void Layer::collect_timings(char* names, size_t names_cap, float* ms, int cap, i
 void Layer::forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s) {
   const size_t bytes = static_cast<size_t>(T * H_ * dtype_bytes(dt_));
   if (T < 0 || T > Tmax_) throw std::invalid_argument("token count must be in [0, max_tokens]");
+  init_host_staging();
   const int b = hslot_;
   hslot_ ^= 1;
   // H2D on its own stream once the step that last used this slot stopped reading it.
@@ -960,6 +1202,7 @@ void Layer::forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s) {
 }
 
 void Layer::host_fence(cudaStream_t s) {
+  if (!h2d_s_) return;
   ck(cudaStreamWaitEvent(s, ev_d2h_[0], 0), "wait");
   ck(cudaStreamWaitEvent(s, ev_d2h_[1], 0), "wait");
 }

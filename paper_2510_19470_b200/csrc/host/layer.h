@@ -6,7 +6,11 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../kernels/comm_p2p.h"
@@ -17,10 +21,47 @@
 
 namespace hep {
 
+class Layer;
+
+// Several ranks of one process on ONE device ("virtual ranks", hep_comm_init_virtual):
+// the NVLink peer-memory path with the buffers exchanged as plain device pointers
+// instead of CUDA IPC handles, so the fused dispatch / GEMM peer-store / combine
+// kernels, the epoch flags and the shared-expert chain run unchanged on a one-GPU box.
+struct VirtualGroup {
+  std::mutex mu;
+  int nranks = 0;
+  std::map<std::pair<int, int>, Layer*> layers;  // (layer sequence number on its rank, rank)
+};
+
 struct Comm {
   ncclComm_t nccl = nullptr;
   int rank = 0;
   int nranks = 1;
+  std::shared_ptr<VirtualGroup> vgroup;  // set: virtual ranks (no NCCL)
+  int layers_created = 0;                // pairs the k-th layer of every rank (virtual ranks)
+};
+
+// What every rank must agree on before any peer-memory store lands in its buffers
+// (ranks with different max_tokens would place rows at different receive offsets).
+struct LayerSig {
+  int64_t H, F, E, k, Tmax, sr_k;
+  double sr_ratio;
+  int32_t dtype, use_sr, per_matrix, nlev, p2p, pad;
+  uint32_t iw, vw;
+  int64_t sf[16], sed[16];
+};
+
+// A rank's buffers as seen from this process (IPC-mapped, or local for virtual ranks).
+struct PeerBufs {
+  void* xall;
+  void* oall;
+  void* sync;
+  void* w_up;
+  void* w_down;
+  void* wires;
+  void* partial;
+  void* chain_flags;
+  void* shared;
 };
 
 // Device buffer with RAII.
@@ -67,6 +108,17 @@ class Layer {
   // Mean device time per named phase over every profiled forward since the last call.
   void collect_timings(char* names, size_t names_cap, float* ms, int cap, int* count);
   int launch_count() const { return launches_; }
+  // Raises RuntimeFailure (std::runtime_error) if a gathered SR wire failed to decode
+  // (bad magic, truncation, out-of-order indices: sparsecomp.cpp:36, 236-238).  With
+  // sync, waits for the pending All-Gather first; otherwise reads what has completed.
+  void check_migration(bool sync);
+  // Test hook (hep_layer_debug_corrupt_next_gather): the next gather corrupts the magic
+  // of the first gathered wire after the pull, before decode.
+  void corrupt_next_gather() { corrupt_next_ = true; }
+  void gemm_schedules(uint32_t* up, uint32_t* down) const {
+    *up = sched_up_;
+    *down = sched_down_;
+  }
   bool p2p() const { return p2p_; }
 
  private:
@@ -140,6 +192,19 @@ class Layer {
   std::vector<void*> ipc_opened_;
   uint32_t epoch_ = 0;
   void setup_p2p();
+  void setup_streams();
+  LayerSig signature() const;
+  PeerBufs my_bufs() const;
+  void connect(const std::vector<PeerBufs>& bufs);
+  void ensure_connected();  // virtual ranks: resolve peers on first use
+  void check_signatures(const std::vector<LayerSig>& all) const;
+  void init_host_staging();
+  int seq_ = 0;
+  bool connected_ = true;
+  uint64_t timeout_ns_ = 0;
+  bool corrupt_next_ = false;
+  int32_t* mig_err_host_ = nullptr;  // mapped pinned flag: a gathered wire failed to decode
+  int32_t* mig_err_dev_ = nullptr;
 
   // per-forward plan
   int num_groups_;

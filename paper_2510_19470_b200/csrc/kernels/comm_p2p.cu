@@ -40,11 +40,13 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 // who: (rank << 16) | (site << 8) | peer, printed if the wait times out.  Sites: 0 counts,
 // 11..14 signal slots 1..4, 20 refresh barrier, 21 refresh chain, 22 refresh fetch.
-__device__ void wait_flag(const uint32_t* f, uint32_t epoch, uint32_t who = 0) {
+// timeout_ns = 0 waits forever (ranks may legitimately skew by minutes: checkpointing,
+// evaluation); a finite HEP_P2P_TIMEOUT_S turns a lost peer into a diagnosed trap.
+__device__ void wait_flag(const uint32_t* f, uint32_t epoch, uint32_t who, uint64_t timeout_ns) {
   const uint64_t t0 = globaltimer();
   // Epochs only grow; a peer that already moved on to a later epoch also satisfies us.
   while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
-    if (globaltimer() - t0 > 60ull * 1000000000ull) {  // peer never arrived
+    if (timeout_ns && globaltimer() - t0 > timeout_ns) {  // peer never arrived
       printf("hep: flag wait timed out: rank %u site %u peer %u epoch %u flag %u\n", who >> 16, (who >> 8) & 0xffu,
              who & 0xffu, epoch, ld_acquire_sys(f));
       __trap();
@@ -91,7 +93,8 @@ __global__ void __launch_bounds__(256) count_exchange_kernel(P2PArgs a, const in
   // 2) wait for everyone's counts.
   const SyncView mine = view(a.sync[me], NK);
   if (threadIdx.x < G && static_cast<int>(threadIdx.x) != me)
-    wait_flag(mine.flags + 0 * kMaxG + threadIdx.x, a.epoch, (static_cast<uint32_t>(me) << 16) | threadIdx.x);
+    wait_flag(mine.flags + 0 * kMaxG + threadIdx.x, a.epoch, (static_cast<uint32_t>(me) << 16) | threadIdx.x,
+              a.timeout_ns);
   __syncthreads();
   for (int i = threadIdx.x; i < G * NK; i += blockDim.x) {
     const int s = i / NK, key = i % NK;
@@ -213,7 +216,7 @@ __global__ void signal_wait_kernel(P2PArgs a, int slot, int wait, int ag, int si
   __syncthreads();
   if (i < n)
     wait_flag(view(a.sync[a.rank], NK).flags + slot * kMaxG + list[i], a.epoch,
-              (static_cast<uint32_t>(a.rank) << 16) | ((10u + slot) << 8) | static_cast<uint32_t>(list[i]));
+              (static_cast<uint32_t>(a.rank) << 16) | ((10u + slot) << 8) | static_cast<uint32_t>(list[i]), a.timeout_ns);
 }
 
 template <bool BF16>
@@ -272,14 +275,15 @@ __global__ void chain_barrier_kernel(ChainArgs c) {
   const int r = threadIdx.x;
   if (r < c.G) st_release_sys(c.bar[r] + c.rank, c.epoch);
   __syncthreads();
-  if (r < c.G) wait_flag(c.bar[c.rank] + r, c.epoch, (static_cast<uint32_t>(c.rank) << 16) | (20u << 8) | r);
+  if (r < c.G) wait_flag(c.bar[c.rank] + r, c.epoch, (static_cast<uint32_t>(c.rank) << 16) | (20u << 8) | r, c.timeout_ns);
 }
 
 __global__ void __launch_bounds__(256) shared_chain_kernel(ChainArgs c) {
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * c.chunk;
   const int64_t i1 = min(c.P, i0 + c.chunk);
   if (c.rank > 0 && c.epoch) {
-    if (threadIdx.x == 0) wait_flag(c.pred_flags + blockIdx.x, c.epoch, (static_cast<uint32_t>(c.rank) << 16) | (21u << 8));
+    if (threadIdx.x == 0)
+      wait_flag(c.pred_flags + blockIdx.x, c.epoch, (static_cast<uint32_t>(c.rank) << 16) | (21u << 8), c.timeout_ns);
     __syncthreads();
   }
   const bool last = c.rank == c.G - 1;
@@ -302,7 +306,8 @@ __global__ void __launch_bounds__(256) shared_chain_kernel(ChainArgs c) {
 __global__ void __launch_bounds__(256) shared_fetch_kernel(ChainArgs c) {
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * c.chunk;
   const int64_t i1 = min(c.P, i0 + c.chunk);
-  if (threadIdx.x == 0) wait_flag(c.last_flags + blockIdx.x, c.epoch, (static_cast<uint32_t>(c.rank) << 16) | (22u << 8));
+  if (threadIdx.x == 0)
+    wait_flag(c.last_flags + blockIdx.x, c.epoch, (static_cast<uint32_t>(c.rank) << 16) | (22u << 8), c.timeout_ns);
   __syncthreads();
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) c.shared[i] = __ldcv(c.last_shared + i);
 }
@@ -333,14 +338,14 @@ cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T,
   const int row_bytes = H * dtype_bytes(dt);
   if (row_bytes % 16 || k > 8) return cudaErrorInvalidValue;
   if (T == 0) return cudaSuccess;  // empty batch: nothing to send
-  static bool carveout = false;
-  if (!carveout) {
+  static DeviceOnce carveout;
+  if (!carveout.done()) {
     // Same L1/shared split as the persistent GEMM, so remote-row blocks can run on SMs
     // next to GEMM CTAs that wait for peers' rows (overlapped dispatch).
     const cudaError_t e = cudaFuncSetAttribute(permute_p2p_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                                cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
-    carveout = true;
+    carveout.set();
   }
   const int seg = row_segments(T, row_bytes >> 4);
   permute_p2p_kernel<<<(T * seg + 7) / 8, 256, 0, s>>>(a, static_cast<const uint8_t*>(x), T, row_bytes, k, keys,
@@ -372,6 +377,24 @@ cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, cons
   else
     combine_p2p_kernel<false><<<(T * seg + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y, seg);
   return cudaGetLastError();
+}
+
+
+// Loads every kernel of this file now (see preload_kernels in kernels.h).
+cudaError_t preload_comm_p2p_kernels() {
+  auto load = [](const void* fn) {
+    cudaFuncAttributes attr;
+    return cudaFuncGetAttributes(&attr, fn);
+  };
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(count_exchange_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(permute_p2p_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(signal_wait_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(combine_p2p_kernel<true>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(combine_p2p_kernel<false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(chain_barrier_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(shared_chain_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(shared_fetch_kernel))) return e;
+  return cudaSuccess;
 }
 
 }  // namespace hep

@@ -23,9 +23,10 @@ struct P2PArgs {
   int ag_list[kMaxG];           // this rank's All-Gather peers (ring order)
   int n_ag;
   int G, E, rank;
-  int recv_start;               // first receive row (Tmax * k), same on every rank
+  int recv_start;               // first receive row (Tmax * k), same on every rank (checked at setup)
   int row_bytes;                // H * element bytes of xall / oall rows
   uint32_t epoch;
+  uint64_t timeout_ns;          // flag waits trap after this long (0: wait forever); HEP_P2P_TIMEOUT_S
 };
 
 size_t p2p_sync_bytes(int G, int E);
@@ -67,6 +68,7 @@ struct ChainArgs {
   int n, rank, G;
   double inv;                   // 1 / E
   uint32_t epoch;               // 0: no flags (the NCCL path moves the partials)
+  uint64_t timeout_ns;          // as P2PArgs::timeout_ns
 };
 constexpr int64_t kChainChunk = 65536;  // elements per pipelined chunk
 cudaError_t launch_shared_chain(const ChainArgs& c, cudaStream_t s);

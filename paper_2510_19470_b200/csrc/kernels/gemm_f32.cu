@@ -130,4 +130,15 @@ cudaError_t launch_grouped_gemm_f32(const float* A, int lda, const float* B, flo
   return cudaGetLastError();
 }
 
+
+// Loads every kernel of this file now (see preload_kernels in kernels.h).
+cudaError_t preload_gemm_f32_kernels() {
+  auto load = [](const void* fn) {
+    cudaFuncAttributes attr;
+    return cudaFuncGetAttributes(&attr, fn);
+  };
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_f32_kernel))) return e;
+  return cudaSuccess;
+}
+
 }  // namespace hep

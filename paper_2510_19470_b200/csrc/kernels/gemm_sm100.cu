@@ -84,7 +84,7 @@ __device__ __forceinline__ void decode_tile(int local, int m_tiles, int n_tiles,
 
 // Spin (producer thread) until a peer's dispatch flag reaches `epoch`, then order the
 // TMA (async proxy) reads of the rows that peer stored after its release.
-__device__ __forceinline__ void wait_dispatch(const uint32_t* flag, uint32_t epoch) {
+__device__ __forceinline__ void wait_dispatch(const uint32_t* flag, uint32_t epoch, uint64_t timeout_ns) {
   uint32_t v;
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -93,7 +93,7 @@ __device__ __forceinline__ void wait_dispatch(const uint32_t* flag, uint32_t epo
     if (static_cast<int32_t>(v - epoch) >= 0) break;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 60ull * 1000000000ull) {
+    if (timeout_ns && t - t0 > timeout_ns) {
       printf("hep: GEMM dispatch wait timed out: epoch %u flag %u\n", epoch, v);
       __trap();
     }
@@ -118,7 +118,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                          const int* __restrict__ g_rows, const int* __restrict__ g_slot,
                          const unsigned long long* __restrict__ g_out, const int* __restrict__ g_wait,
                          const uint32_t* __restrict__ wait_flags, uint32_t epoch, int ng, int relu,
-                         uint32_t sched) {
+                         uint32_t sched, uint64_t timeout_ns) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -197,7 +197,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
         const int a_row = s.row_start[g] + mt * BM;
         const int b_row = s.slot[g] * N + nt * BN;
-        if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch);
+        if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch, timeout_ns);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&s.full[stage], STAGE_BYTES);
@@ -345,7 +345,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
                               const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
                               const int* __restrict__ g_slot, const unsigned long long* __restrict__ g_out,
                               const int* __restrict__ g_wait, const uint32_t* __restrict__ wait_flags,
-                              uint32_t epoch, int ng, int relu, uint32_t sched) {
+                              uint32_t epoch, int ng, int relu, uint32_t sched, uint64_t timeout_ns) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -429,7 +429,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
         // (the first 64 of its 128-row box)
         const int b_half = N - nt * P_BN <= P_BN / 2 ? 64 : 128;
         const int b_row = s.slot[g] * N + nt * P_BN + b_half * static_cast<int>(cta);
-        if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch);
+        if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch, timeout_ns);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
           if (cta == 0) mbar_arrive_expect_tx(&s.full[stage], 2 * P_STAGE_BYTES);
@@ -939,12 +939,12 @@ cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMa
   if (ksplit < 1 || K % (T_BK * ksplit) || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
     return cudaErrorInvalidValue;
   if (ksplit > 1 && !partial) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceOnce attr_set;
+  if (!attr_set.done()) {
     const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(kSmemBytesT));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.set();
   }
   const size_t stride = static_cast<size_t>(rows_total) * ldc;
   grouped_gemm_tf32x3_kernel<<<num_sms, kThreads, kSmemBytesT, stream>>>(
@@ -971,16 +971,16 @@ cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap
                                      int num_sms, cudaStream_t stream, uint32_t sched) {
   if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
     return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceOnce attr_set;
+  if (!attr_set.done()) {
     const cudaError_t e = cudaFuncSetAttribute(
         grouped_gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.set();
   }
   grouped_gemm_bf16_kernel<<<num_sms, kThreads, kSmemBytes, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
-      groups.slot, groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched);
+      groups.slot, groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns);
   return cudaGetLastError();
 }
 
@@ -988,19 +988,34 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
                                           int N, int K, const GroupTable& groups, int relu, int num_sms,
                                           cudaStream_t stream, uint32_t sched) {
   if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceOnce attr_set;
+  if (!attr_set.done()) {
     const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(kSmemBytes2));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.set();
   }
   const int grid = (num_sms / 2) * 2;
   grouped_gemm_bf16_2cta_kernel<<<grid, kThreads, kSmemBytes2, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
-      groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched);
+      groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns);
   return cudaGetLastError();
+}
+
+
+// Loads every kernel of this file now (see preload_kernels in kernels.h).
+cudaError_t preload_gemm_sm100_kernels() {
+  auto load = [](const void* fn) {
+    cudaFuncAttributes attr;
+    return cudaFuncGetAttributes(&attr, fn);
+  };
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(ksplit_reduce_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(split_tf32_kernel))) return e;
+  return cudaSuccess;
 }
 
 }  // namespace hep

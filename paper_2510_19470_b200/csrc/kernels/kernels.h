@@ -11,7 +11,33 @@ namespace hep {
 
 enum class DType : int { F32 = 0, BF16 = 1 };
 
+// One-time per-device setup (kernel attributes such as the dynamic shared memory limit
+// are per device, and one process may drive several devices): done() / set() refer to
+// the calling thread's current device.
+struct DeviceOnce {
+  unsigned long long mask = 0;
+  static int device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+  }
+  bool done() const { return (__atomic_load_n(&mask, __ATOMIC_ACQUIRE) >> device()) & 1ull; }
+  void set() { __atomic_fetch_or(&mask, 1ull << device(), __ATOMIC_RELEASE); }
+};
+
 inline int dtype_bytes(DType t) { return t == DType::F32 ? 4 : 2; }
+
+// Lazy module loading (CUDA 12's default) loads a kernel at its first launch and may
+// synchronise the context to do so.  The peer-memory step has kernels that spin until
+// another rank's kernel runs; with several ranks in one context (virtual ranks) a first
+// launch behind such a spin would wait for it forever.  preload_kernels() loads every
+// kernel of the library up front (once per device, at layer creation).
+cudaError_t preload_kernels();
+cudaError_t preload_comm_p2p_kernels();
+cudaError_t preload_gemm_f32_kernels();
+cudaError_t preload_gemm_sm100_kernels();
+cudaError_t preload_route_kernels();
+cudaError_t preload_sr_codec_kernels();
 
 // ----------------------------------------------------------------- routing (route.cu)
 // Gate + top-k + per-32-token-chunk stable ranking.  x:[T,H] (dtype).  Outputs per (t, j): expert, weight, key =
@@ -65,6 +91,7 @@ struct GroupTable {
   const int* wait_src = nullptr;
   const uint32_t* wait_flags = nullptr;
   uint32_t epoch = 0;
+  uint64_t timeout_ns = 0;  // dispatch waits trap after this long (0: wait forever)
 };
 
 // bf16 tcgen05 grouped GEMM (gemm_sm100.cu): C[r, n] = act(sum_k A[r,k] B[slot*N+n, k]).
@@ -143,6 +170,8 @@ cudaError_t launch_sr_decode_layout_batch(const uint8_t* const* wires, int batch
                                           const float* shared, const void* shared_c, DType out_dt, int64_t h,
                                           int64_t m, void* const* up, void* const* down, int32_t* status,
                                           cudaStream_t stream);
+// err := (code | entry << 8) of the first failed wire of a decode batch, if err is still 0.
+cudaError_t launch_sr_status_fold(const int32_t* status, int n, int32_t* err, cudaStream_t stream);
 // out = mean over experts (fp64 accumulate in list order, times 1/n, round to fp32).
 cudaError_t launch_shared_mean(DType dt, const void* const* experts, int n, int64_t P, float* out,
                                cudaStream_t stream);

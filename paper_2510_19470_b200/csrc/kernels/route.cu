@@ -944,10 +944,10 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
       // Measured no faster for cfg3 and slower for cfg4 (profiles/README.md), so off.
       const char* split_env = std::getenv("HEP_GATE_SPLIT");
       const bool split = split_env && split_env[0] == '1' && (H / kUGK) % 2 == 0;
-      auto launch = [&](auto kern, size_t smem, int ks, bool& attr) {
-        if (!attr) {
+      auto launch = [&](auto kern, size_t smem, int ks, DeviceOnce& attr) {
+        if (!attr.done()) {
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-          attr = true;
+          attr.set();
         }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(tiles * ks));
@@ -964,7 +964,7 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
         return cudaLaunchKernelEx(&cfg, kern, *mx, *mw, T, H, E, k, dest_of_owner, experts_per_gpu, NK, topk_idx,
                                   topk_w, keys, ranks, chunk_counts);
       };
-      static bool a[4] = {false, false, false, false};
+      static DeviceOnce a[4];
       cudaError_t err;
       if (NE == 16)
         err = split ? launch(gate_umma_kernel<16, 2>, gate_umma_smem<16, 2>(), 2, a[0])
@@ -976,19 +976,19 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
       return cudaGetLastError();
     }
     const int blocks = (T + kGT - 1) / kGT;
-    auto go = [&](auto kern, size_t smem, bool& attr) {
-      if (!attr) {  // once per instantiation
+    auto go = [&](auto kern, size_t smem, DeviceOnce& attr) {
+      if (!attr.done()) {  // once per instantiation
         const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr.set();
       }
       kern<<<blocks, 256, smem, stream>>>(static_cast<const __nv_bfloat16*>(x),
                                           static_cast<const __nv_bfloat16*>(wg_t), T, H, E, k, dest_of_owner,
                                           experts_per_gpu, NK, topk_idx, topk_w, keys, ranks, chunk_counts);
       return cudaSuccess;
     };
-    static bool a8 = false, a8w = false, a16 = false, a64 = false;
+    static DeviceOnce a8, a8w, a16, a64;
     cudaError_t e;
     if (E <= 8 && H % 128 == 0) e = go(gate_mma_kernel<4, 8, 128>, gate_smem<4, 8, 128>(), a8w);
     else if (E <= 8) e = go(gate_mma_kernel<8, 8, 64>, gate_smem<8, 8, 64>(), a8);
@@ -1003,11 +1003,11 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
     else if (nchunks * 2 <= 2 * 148 && H % 8 == 0) cs = 2;
     const size_t smem = static_cast<size_t>(kChunk + E) * (H / cs + 4) * sizeof(float);
     if (H % 4 == 0 && smem <= 200 * 1024 && NK <= kMaxNK && k <= kMaxK && E % 8 == 0) {
-      auto go = [&](auto kern, int csz, bool& attr) {
-        if (!attr) {
+      auto go = [&](auto kern, int csz, DeviceOnce& attr) {
+        if (!attr.done()) {
           const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
           if (e != cudaSuccess) return e;
-          attr = true;
+          attr.set();
         }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(nchunks * csz));
@@ -1024,7 +1024,7 @@ cudaError_t launch_gate(DType dt, const void* x, const void* wg_t, int T, int H,
         return cudaLaunchKernelEx(&cfg, kern, static_cast<const float*>(x), static_cast<const float*>(wg_t), T, H, E,
                                   k, dest_of_owner, experts_per_gpu, NK, topk_idx, topk_w, keys, ranks, chunk_counts);
       };
-      static bool a1 = false, a2 = false, a4 = false;
+      static DeviceOnce a1, a2, a4;
       const cudaError_t e = cs == 4   ? go(gate_f32_oneshot_kernel<4>, 4, a4)
                             : cs == 2 ? go(gate_f32_oneshot_kernel<2>, 2, a2)
                                       : go(gate_f32_oneshot_kernel<1>, 1, a1);
@@ -1090,6 +1090,44 @@ cudaError_t launch_combine(DType dt, const void* out, const int* pos, const floa
                                                    H, k, static_cast<float*>(y), seg);
   }
   return cudaGetLastError();
+}
+
+
+// Loads every kernel of this file now (see preload_kernels in kernels.h).
+cudaError_t preload_route_kernels() {
+  auto load = [](const void* fn) {
+    cudaFuncAttributes attr;
+    return cudaFuncGetAttributes(&attr, fn);
+  };
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_kernel<float>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_mma_kernel<4, 8, 128>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_mma_kernel<8, 8, 64>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_mma_kernel<8, 16, 64>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_mma_kernel<4, kMaxE, 64>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_f32_oneshot_kernel<1>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_f32_oneshot_kernel<2>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_f32_oneshot_kernel<4>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_umma_kernel<16, 1>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_umma_kernel<16, 2>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_umma_kernel<64, 1>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(gate_umma_kernel<64, 2>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(chunk_scan_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(key_scan_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(permute_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(positions_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(combine_bf16_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(combine_f32_kernel))) return e;
+  return cudaSuccess;
+}
+
+cudaError_t preload_kernels() {
+  static DeviceOnce once;
+  if (once.done()) return cudaSuccess;
+  for (cudaError_t (*f)() : {preload_route_kernels, preload_gemm_sm100_kernels, preload_gemm_f32_kernels,
+                             preload_sr_codec_kernels, preload_comm_p2p_kernels})
+    if (const cudaError_t e = f()) return e;
+  once.set();
+  return cudaSuccess;
 }
 
 }  // namespace hep

@@ -1642,13 +1642,13 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
   sr_init_kernel<<<dim3(16, batch), 256, 0, stream>>>(ws, eb, bf16, shared, ra, plan.h, plan.m, plan.k,
                                                       plan.index_bits, plan.value_bits);
   if (any_list) {
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (!attr.done()) {
       cudaFuncSetAttribute(sr_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSampleSmem);
       cudaFuncSetAttribute(sr_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 8);
       cudaFuncSetAttribute(sr_split_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 8);
       cudaFuncSetAttribute(sr_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFinSmem);
-      attr = true;
+      attr.set();
     }
     sr_sample_kernel<<<dim3(ra.nr, batch), kSampleThreads, kSampleSmem, stream>>>(ra, ws);
     const bool bulk = ((ra.lo[0] | (ra.nr > 1 ? ra.lo[1] : 0)) & 7) == 0;
@@ -1692,6 +1692,20 @@ cudaError_t launch_sr_decode_batch(const uint8_t* const* wires, int batch, size_
   const int vblocks = static_cast<int>(std::max<int64_t>(1, (kmax + 255) / 256));
   sr_decode_scatter_kernel<<<dim3(vblocks, batch), 256, 0, stream>>>(db, wire_bytes, shared, h, m, status);
   sr_status_finalize_kernel<<<1, kMaxSrBatch, 0, stream>>>(status, batch);
+  return cudaGetLastError();
+}
+
+namespace {
+// First failing decode code of a batch -> a (host-mapped) error word, kept until read.
+__global__ void sr_status_fold_kernel(const int32_t* __restrict__ status, int n, int32_t* __restrict__ err) {
+  const int i = threadIdx.x;
+  if (i < n && status[4 * i] != 0) atomicCAS(err, 0, (status[4 * i] & 0xff) | (min(status[4 * i + 1], 0xffffff) << 8));
+}
+}  // namespace
+
+cudaError_t launch_sr_status_fold(const int32_t* status, int n, int32_t* err, cudaStream_t stream) {
+  if (n <= 0 || n > kMaxSrBatch) return cudaErrorInvalidValue;
+  sr_status_fold_kernel<<<1, 64, 0, stream>>>(status, n, err);
   return cudaGetLastError();
 }
 
@@ -1748,6 +1762,37 @@ cudaError_t launch_transpose_convert(DType in_dt, const void* in, int64_t rows, 
   else
     transpose_convert_kernel<__nv_bfloat16, float><<<grid, block, 0, stream>>>(static_cast<const __nv_bfloat16*>(in), rows, cols, static_cast<float*>(out));
   return cudaGetLastError();
+}
+
+
+// Loads every kernel of this file now (see preload_kernels in kernels.h).
+cudaError_t preload_sr_codec_kernels() {
+  auto load = [](const void* fn) {
+    cudaFuncAttributes attr;
+    return cudaFuncGetAttributes(&attr, fn);
+  };
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_init_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_sample_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_split_kernel<true>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_split_kernel<false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_finish_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_scan_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_pack_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_select_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_emit_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_decode_copy_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_decode_scatter_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_decode_scatter_layout_kernel<true>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_decode_scatter_layout_kernel<false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_status_init_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_status_finalize_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(shared_mean_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(transpose_convert_kernel<float, float>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(transpose_convert_kernel<float, __nv_bfloat16>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(transpose_convert_kernel<__nv_bfloat16, __nv_bfloat16>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(transpose_convert_kernel<__nv_bfloat16, float>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_status_fold_kernel))) return e;
+  return cudaSuccess;
 }
 
 }  // namespace hep

@@ -50,6 +50,14 @@ class Communicator:
         check(lib.hep_comm_init(uid, rank, world, C.byref(h)))
         return Communicator(h, rank, world)
 
+    @staticmethod
+    def virtual(nranks: int) -> list:
+        """`nranks` virtual ranks on the current device (hep_comm_init_virtual): one
+        process drives every rank's layer, each on its own stream."""
+        hs = (C.c_void_p * nranks)()
+        check(lib.hep_comm_init_virtual(nranks, hs))
+        return [Communicator(C.c_void_p(hs[r]), r, nranks) for r in range(nranks)]
+
     def close(self):
         if self.handle:
             check(lib.hep_comm_destroy(self.handle))
@@ -126,6 +134,13 @@ class MoELayer:
     def host_fence(self, stream=None):
         check(lib.hep_layer_host_fence(self.handle, _stream(stream)))
 
+    def check(self, stream=None):
+        """Synchronise and raise RuntimeFailure if a migrated expert's wire was rejected."""
+        check(lib.hep_layer_check(self.handle, _stream(stream)))
+
+    def debug_corrupt_next_gather(self):
+        check(lib.hep_layer_debug_corrupt_next_gather(self.handle))
+
     def comm_bench(self, x: torch.Tensor, iters: int = 10, stream=None) -> dict:
         """Per-GPU exchange microbenchmark (collective): NVLink A2A dispatch and expert
         All-Gather bytes and times; bus GB/s = bytes / time."""
@@ -170,6 +185,12 @@ class MoELayer:
         check(lib.hep_layer_timings(self.handle, names, 1024, ms, 32, C.byref(cnt)))
         keys = names.value.decode().split(";") if cnt.value else []
         return dict(zip(keys, list(ms)[: cnt.value]))
+
+    def gemm_schedule(self) -> tuple:
+        """(up, down) L2-policy/raster words of the bf16 expert GEMMs (hep_grouped_gemm sched)."""
+        u, d = C.c_uint32(), C.c_uint32()
+        check(lib.hep_layer_gemm_schedule(self.handle, C.byref(u), C.byref(d)))
+        return u.value, d.value
 
     def launch_count(self) -> int:
         c = C.c_int()

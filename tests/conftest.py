@@ -34,3 +34,19 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture
+def record_accuracy(request):
+    """record_accuracy(**errors): appends the observed errors of a parity test to the JSON
+    lines file named by HEP_ACCURACY_LOG (if set) -- the data the stated tolerances
+    (tests/tolerances.py) are set from."""
+    import json
+
+    def rec(**vals):
+        path = os.environ.get("HEP_ACCURACY_LOG")
+        if path:
+            with open(path, "a") as f:
+                f.write(json.dumps({"test": request.node.nodeid, **vals}) + "\n")
+
+    return rec

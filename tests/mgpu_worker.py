@@ -26,6 +26,7 @@ from paper_2510_19470_b200 import synthetic  # noqa: E402
 from paper_2510_19470_b200 import topology as topo  # noqa: E402
 from paper_2510_19470_b200.moe import Communicator, MoELayer  # noqa: E402
 from paper_2510_19470_b200.sr import CompressionConfig  # noqa: E402
+from tests import tolerances as tol  # noqa: E402
 
 
 def main():
@@ -103,6 +104,13 @@ def check(a, layer, x_all, wg, w_up, w_down, flat, shared, rank, G, bf16, report
     T = x_all.shape[1]
     y = layer.forward(x_all[rank].cuda())
     torch.cuda.synchronize()
+    verify(a, layer, y, x_all, wg, w_up, w_down, flat, shared, rank, G, bf16, report)
+
+
+def verify(a, layer, y, x_all, wg, w_up, w_down, flat, shared, rank, G, bf16, report):
+    """This rank's finished forward (y on the device) against the oracle over G
+    simulated GPUs (also used by tests/vrank_worker.py for virtual ranks)."""
+    T = x_all.shape[1]
     if T == 0:
         assert tuple(y.shape) == (0, a.H)
         return
@@ -141,9 +149,9 @@ def check(a, layer, x_all, wg, w_up, w_down, flat, shared, rank, G, bf16, report
     d = np.abs(y - want)
     report.update(max_rel=float(d.max() / scale), mean_rel=float(d.mean() / scale))
     if bf16:
-        assert d.max() <= 2e-2 * scale and d.mean() <= 2e-3 * scale, report
+        assert d.max() <= tol.BF16_VS_MIRROR_MAX * scale and d.mean() <= tol.BF16_VS_MIRROR_MEAN * scale, report
     else:
-        assert d.max() <= 1e-4 * scale, report
+        assert d.max() <= tol.F32_MAX * scale, report
 
 
 if __name__ == "__main__":

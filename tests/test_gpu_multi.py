@@ -56,6 +56,6 @@ def test_multi_gpu_layer(sf, sed, extra, comm):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(HERE, "mgpu_worker.py"),
            "--sf", *map(str, sf), "--sed", *map(str, sed), *extra]
-    env = dict(os.environ, HEP_COMM=comm)
+    env = dict(os.environ, HEP_COMM=comm, HEP_P2P_TIMEOUT_S="60")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]

@@ -1,0 +1,62 @@
+"""The multi-GPU data path on ONE GPU: every rank of the hierarchy as a virtual rank of one
+process (hep_comm_init_virtual), so the driver's one-GPU box runs the fused peer-memory
+step -- count exchange, dispatch stores into peers' receive areas, the down-projection's
+peer-store epilogue, epoch flags, expert All-Gather pulls, SR migration and the
+shared-expert chain -- against the oracle.  One subprocess per case (tests/vrank_worker.py)
+under a timeout, with HEP_P2P_TIMEOUT_S so a lost flag traps with a diagnostic instead of
+hanging."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+CASES = [
+    # (sf, sed, extra args)
+    ([2], [1], []),                    # pure A2A (standard EP)
+    ([2], [2], []),                    # pure All-Gather
+    ([2], [2], ["--sr"]),              # All-Gather of SR-migrated experts
+    ([2], [1], ["--dtype", "f32", "--H", "1024", "--F", "4096", "--T", "512"]),  # cfg1/2 shape, fp32
+    ([4], [2], []),
+    ([2, 2], [1, 2], []),
+    ([2, 2], [2, 1], ["--sr"]),
+    ([2, 2], [1, 1], ["--E", "64", "--k", "6", "--H", "512", "--F", "256"]),   # fine-grained experts
+    ([2, 4], [1, 4], []),              # cfg1 / cfg3 hierarchy
+    ([2, 4], [1, 2], []),              # ambiguous relay (S2 tie-break)
+    ([2, 4], [2, 2], []),
+    ([2, 4], [1, 1], []),              # pure A2A over 8 ranks
+    ([2, 4], [2, 4], []),              # pure All-Gather over 8 ranks
+    ([2, 4], [1, 4], ["--dtype", "f32", "--H", "1024", "--F", "4096", "--T", "512"]),  # cfg1 itself
+    ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr"]),  # cfg4 hierarchy with migration
+    ([2, 2, 2], [2, 1, 2], ["--E", "64", "--k", "6"]),
+    # ragged: a different token count on every rank, rotated, then rank 0 empty
+    ([2], [1], ["--ragged"]),
+    ([2, 2], [1, 2], ["--ragged"]),
+    ([2, 2], [2, 1], ["--ragged", "--sr"]),
+    ([2, 4], [1, 2], ["--ragged"]),
+    ([2, 2], [1, 1], ["--ragged", "--dtype", "f32", "--E", "16", "--k", "4"]),
+    # weights rewritten between steps while peers pull them (dense and SR All-Gather)
+    ([2, 4], [1, 4], ["--update"]),
+    ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr", "--update"]),
+    # a corrupted migrated expert is rejected (RuntimeFailure), not consumed silently
+    ([2, 2], [1, 2], ["--sr", "--corrupt"]),
+    # ranks that disagree on the layer shape are rejected before any peer store
+    ([2], [1], ["--mismatch"]),
+]
+
+
+@pytest.mark.parametrize("sf,sed,extra", CASES, ids=lambda v: str(v))
+def test_virtual_ranks_layer(sf, sed, extra):
+    cmd = [sys.executable, os.path.join(HERE, "vrank_worker.py"), "--sf", *map(str, sf), "--sed", *map(str, sed),
+           *extra]
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", HEP_P2P_TIMEOUT_S="60")
+    env.pop("HEP_COMM", None)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=420, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    if "--mismatch" in extra:
+        assert "mismatch rejected" in r.stdout, r.stdout[-2000:]
+    else:
+        assert r.stdout.count(" ok ") >= 2, r.stdout[-2000:]
