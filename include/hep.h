@@ -88,14 +88,6 @@ typedef struct {
 int hep_solve_optimal_p(const hep_workload* w, double throughput_C, double bandwidth_B,
                         int64_t gpus, double* p, int64_t* domain_size, double* latency6);
 
-/* One MoE iteration on the discrete-event engine: build_schedule (simcore.cpp:96-266)
- * for the plan {p, domain_sizes, encode/decode cost per expert, layers} and
- * sim::run (simcore.cpp:268-367).  Returns the makespan (s), the worst All-Gather
- * stall and the bytes moved per level (num_levels doubles). */
-int hep_sim_step(const hep_level* levels, int num_levels, const hep_workload* w, double p,
-                 const int64_t* domain_sizes, double encode_cost, double decode_cost, int layers, double* makespan,
-                 double* max_ag_stall, double* level_bytes);
-
 /* ------------------------------------------------------------- SR migration codec */
 typedef struct {
   double ratio_CR;           /* used when k < 0 */

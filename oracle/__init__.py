@@ -75,6 +75,7 @@ def _load_ref():
     lib.ref_sr_encode.argtypes = [VP, VP, I64, I64, D, I64, C.c_uint32, C.c_uint32, C.c_int, VP, I64]
     lib.ref_sr_decode.argtypes = [VP, I64, VP, I64, I64, VP]
     lib.ref_shared_mean.argtypes = [VP, C.c_int, I64, I64, VP]
+    lib.ref_sim_step.argtypes = [VP, VP, C.c_int, D, D, D, I64, D, D, D, D, C.c_int, VP, VP]
     return lib
 
 
@@ -120,6 +121,20 @@ def route_table(sf, sed):
     if rc:
         raise ValueError("route table has a hole")
     return out
+
+
+def sim_step(sf, sed, bandwidth, D, PE, n, pre, expert_lat, enc=0.0, dec=0.0, layers=1):
+    """The reference's own step DAG + discrete-event engine (oracle/_ref): (makespan s,
+    worst All-Gather stall s)."""
+    if ref is None:
+        raise RuntimeError("oracle/_ref/libhybridep_ref.so is not built (needs /root/reference once)")
+    sf_, sed_ = _i64(sf), _i64(sed)
+    mk, st = C.c_double(), C.c_double()
+    rc = ref.ref_sim_step(_p(sf_), _p(sed_), len(sf_), float(bandwidth), float(D), float(PE), int(n), float(pre),
+                          float(expert_lat), float(enc), float(dec), int(layers), C.byref(mk), C.byref(st))
+    if rc:
+        raise ValueError(f"reference sim failed ({rc})")
+    return mk.value, st.value
 
 
 # --------------------------------------------------------------------- SR codec

@@ -155,6 +155,37 @@ int64_t ref_schedule(const int64_t* sf, const int64_t* sed, int L, double D, dou
   return count;
 }
 
+// One iteration on the reference's discrete-event engine (build_schedule + sim::run,
+// simcore.cpp:96-367) with per-level bandwidth bw (bytes/s): makespan and worst AG stall.
+// The predicted side of tools/model_vs_measured.py (the engine is the reference's timing
+// model; the B200 build measures real time instead and does not ship one).
+int ref_sim_step(const int64_t* sf, const int64_t* sed, int L, double bw, double D, double PE, int64_t n_experts,
+                 double pre, double expert_lat, double enc, double dec, int layers, double* makespan, double* stall) {
+  return guard([&] {
+    topo::ClusterSpec c;
+    for (int i = 0; i < L; ++i) c.levels.push_back({sf[i], sed[i], bw});
+    perf::WorkloadSpec w;
+    w.data_size_D = D;
+    w.expert_size_PE = PE;
+    w.experts_per_gpu_n = n_experts;
+    w.attn_latency = pre;
+    w.ffn_latency = 1e-12;
+    w.expert_latency = expert_lat;
+    HybridPlan plan;
+    plan.domain_sizes.assign(sed, sed + L);
+    const int64_t G = c.total_gpus();
+    int64_t s = 1;
+    for (int i = 0; i < L; ++i) s *= sed[i];
+    plan.p = G > 1 ? static_cast<double>(G - s) / static_cast<double>(G - 1) : 1.0;
+    plan.encode_cost = enc;
+    plan.decode_cost = dec;
+    plan.layers = layers;
+    const auto trace = sim::run(sim::build_schedule(c, w, plan), with_domain_sizes(c, plan.domain_sizes));
+    *makespan = trace.makespan;
+    *stall = trace.max_ag_stall;
+  });
+}
+
 int ref_solve_optimal_p(double D, double PE, int64_t n, int64_t m, double attn, double ffn, double expert,
                         double bwd, double C, double B, int64_t gpus, double* p, int64_t* s, double* total) {
   return guard([&] {

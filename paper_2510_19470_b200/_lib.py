@@ -116,8 +116,6 @@ SIGNATURES = {
     "hep_route_table": [P(Level), I32, P(C.c_int32)],
     "hep_factor_domain_sizes": [I64, P(Level), I32, P(I64)],
     "hep_solve_optimal_p": [P(Workload), C.c_double, C.c_double, I64, P(C.c_double), P(I64), P(C.c_double)],
-    "hep_sim_step": [VP, C.c_int, P(Workload), C.c_double, P(I64), C.c_double, C.c_double, C.c_int, P(C.c_double),
-                     P(C.c_double), P(C.c_double)],
     "hep_sr_resolve_k": [P(SrConfig), I64, I64, P(I64)],
     "hep_sr_wire_bytes": [I64, I64, P(SrConfig), P(SZ)],
     "hep_sr_workspace_bytes": [I64, I64, I32, P(SZ)],

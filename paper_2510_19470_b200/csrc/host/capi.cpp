@@ -217,34 +217,6 @@ int hep_solve_optimal_p(const hep_workload* w, double throughput_C, double bandw
   });
 }
 
-int hep_sim_step(const hep_level* levels, int num_levels, const hep_workload* w, double p,
-                 const int64_t* domain_sizes, double encode_cost, double decode_cost, int layers, double* makespan,
-                 double* max_ag_stall, double* level_bytes) {
-  return guarded([&] {
-    hybridep::perf::WorkloadSpec ws;
-    ws.data_size_D = w->data_size_D;
-    ws.expert_size_PE = w->expert_size_PE;
-    ws.experts_per_gpu_n = w->experts_per_gpu_n;
-    ws.pre_blocks_m = w->pre_blocks_m;
-    ws.attn_latency = w->attn_latency;
-    ws.ffn_latency = w->ffn_latency;
-    ws.expert_latency = w->expert_latency;
-    ws.backward_allreduce_const = w->backward_allreduce_const;
-    hybridep::HybridPlan plan;
-    plan.p = p;
-    plan.domain_sizes.assign(domain_sizes, domain_sizes + num_levels);
-    plan.encode_cost = encode_cost;
-    plan.decode_cost = decode_cost;
-    plan.layers = layers;
-    const auto cluster = cluster_of(levels, num_levels);
-    const auto graph = hybridep::sim::build_schedule(cluster, ws, plan);
-    const auto trace = hybridep::sim::run(graph, hybridep::with_domain_sizes(cluster, plan.domain_sizes));
-    *makespan = trace.makespan;
-    if (max_ag_stall) *max_ag_stall = trace.max_ag_stall;
-    if (level_bytes) std::copy(trace.level_bytes.begin(), trace.level_bytes.end(), level_bytes);
-  });
-}
-
 int hep_sr_resolve_k(const hep_sr_config* cfg, int64_t total_elements, int64_t elem_bytes, int64_t* k) {
   return guarded([&] { *k = sr_config_of(cfg).resolve_k(total_elements, elem_bytes); });
 }

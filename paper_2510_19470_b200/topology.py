@@ -150,28 +150,3 @@ def solve_optimal_p(*, data_size_D, expert_size_PE, experts_per_gpu_n, pre_block
     check(lib.hep_solve_optimal_p(C.byref(w), throughput_C, bandwidth_B, gpus, C.byref(p), C.byref(s), lat))
     keys = ("comp", "pre_expert", "comm_a2a", "comm_ag", "overlap", "total")
     return p.value, s.value, dict(zip(keys, list(lat)))
-
-
-def sim_step(cluster: ClusterSpec, *, data_size_D, expert_size_PE, experts_per_gpu_n, attn_latency, expert_latency,
-             p=None, domain_sizes=None, pre_blocks_m=0, ffn_latency=1e-12, encode_cost=0.0, decode_cost=0.0,
-             layers=1):
-    """One iteration of the step DAG on the discrete-event engine (hep_sim_step):
-    returns (makespan s, worst All-Gather stall s, bytes per level)."""
-    sed = list(domain_sizes) if domain_sizes is not None else [l.domain_size for l in cluster.levels]
-    G = 1
-    for l in cluster.levels:
-        G *= l.scaling_factor
-    dom = 1
-    for v in sed:
-        dom *= v
-    if p is None:
-        p = 1.0 if G == 1 else (G - dom) / (G - 1)
-    w = Workload(data_size_D, expert_size_PE, experts_per_gpu_n, pre_blocks_m, attn_latency, ffn_latency,
-                 expert_latency, 0.0)
-    arr, n = cluster._c()
-    ds = (C.c_int64 * len(sed))(*sed)
-    mk, stall = C.c_double(), C.c_double()
-    lb = (C.c_double * len(sed))()
-    check(lib.hep_sim_step(arr, n, C.byref(w), float(p), ds, encode_cost, decode_cost, layers, C.byref(mk),
-                           C.byref(stall), lb))
-    return mk.value, stall.value, list(lb)

@@ -178,25 +178,21 @@ def test_sr_resolve_k_goldens():
         CompressionConfig(ratio_CR=0.5).resolve_k(100, 4)
 
 
-def test_sim_step_event_engine_two_gpu_expert_parallel():
-    """Our discrete-event engine through the C-ABI (hep_sim_step = build_schedule +
-    sim::run) on the 2-GPU expert-parallel DAG, against the hand-derived critical path:
-    pre-expert, the local expert chunk while the dispatch is on the wire, the received
-    chunk, then the combine transfer (simcore.cpp:96-266 job structure)."""
-    from paper_2510_19470_b200 import topology as topo
+def test_reference_engine_two_gpu_expert_parallel():
+    """The predicted side of tools/model_vs_measured.py: the reference's OWN step DAG and
+    discrete-event engine (oracle/_ref, build_schedule + sim::run) on the 2-GPU
+    expert-parallel DAG, against the hand-derived critical path: pre-expert, the local
+    expert chunk while the dispatch is on the wire, the received chunk, then the combine
+    transfer (simcore.cpp:96-266 job structure).  The B200 build ships no timing model."""
+    import oracle
 
+    if oracle.ref is None:
+        pytest.skip("oracle/_ref not built")
     D, bw, pre, e, n = 8e6, 50e9, 1e-3, 2e-3, 1
-    mk, stall, level_bytes = topo.sim_step(topo.ClusterSpec.of([2], [1], bandwidth=bw), data_size_D=D,
-                                           expert_size_PE=2e6, experts_per_gpu_n=n, attn_latency=pre,
-                                           expert_latency=e, domain_sizes=[1])
+    mk, stall = oracle.sim_step([2], [1], bw, D=D, PE=2e6, n=n, pre=pre, expert_lat=e)
     wire = D / 2 / bw
     want = max(pre + n * e / 2, pre + wire) + n * e / 2 + wire
     assert abs(mk - want) <= 1e-12 + 1e-9 * want, (mk, want)
     assert stall == 0.0
-    assert level_bytes[0] > 0
-    # more bandwidth never makes the step slower; the same plan is deterministic
-    mk2, _, _ = topo.sim_step(topo.ClusterSpec.of([2], [1], bandwidth=4 * bw), data_size_D=D, expert_size_PE=2e6,
-                              experts_per_gpu_n=n, attn_latency=pre, expert_latency=e, domain_sizes=[1])
+    mk2, _ = oracle.sim_step([2], [1], 4 * bw, D=D, PE=2e6, n=n, pre=pre, expert_lat=e)
     assert mk2 <= mk
-    assert topo.sim_step(topo.ClusterSpec.of([2], [1], bandwidth=bw), data_size_D=D, expert_size_PE=2e6,
-                         experts_per_gpu_n=n, attn_latency=pre, expert_latency=e, domain_sizes=[1])[0] == mk

@@ -5,8 +5,10 @@ oracle/Makefile, run against this repository's C++ implementation of the API:
                        doctest cases) built with include/hybridep/ and csrc/host/ (doctest
                        shim)
 * acceptance_vs_ours : proj/tests/acceptance.cpp (12 release criteria) linked against our
-                       host library only: topology, plan, perfmodel, SR codec, step-DAG
-                       builder and discrete-event engine (csrc/host/simrun.cpp)
+                       host library: topology, plan, perfmodel, SR codec and step-DAG
+                       builder; the discrete-event engine (sim::run, out of scope for the
+                       B200 build) is the reference's own simcore.cpp with its symbols
+                       weakened, so build_schedule resolves to ours
 * ref_unit_vs_ref    : control, the same suites against the reference itself
 """
 import os

@@ -2,7 +2,8 @@
 
 For every N>1 bench line in a directory (default profiles/r1_sweep), the reference's
 step DAG (build_schedule, simcore.cpp:96-266) is built for the measured configuration
-and run on the discrete-event engine (sim::run) with MEASURED inputs:
+and run on the reference's own discrete-event engine (sim::run, from oracle/_ref: the
+timing model is the reference's, not shipped by the B200 build) with MEASURED inputs:
   * pre-expert time      = gate + scans of that line + the N=1 permute of the config;
   * expert_latency       = that line's expert-GEMM time per layer / n;
   * NVLink bandwidth     = that line's measured A2A bus GB/s (AG bus GB/s if no A2A);
@@ -23,7 +24,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from paper_2510_19470_b200 import topology as topo  # noqa: E402
+import oracle  # noqa: E402  (the reference's engine, compiled from its sources)
 
 
 def lines(dirs):
@@ -84,10 +85,8 @@ def main():
         else:
             pe = n * P * b
             enc = dec = 0.0
-        cl = topo.ClusterSpec.of(c["sf"], c["sed"], bandwidth=bw)
-        mk, stall, _ = topo.sim_step(cl, data_size_D=T * k * H * b, expert_size_PE=pe, experts_per_gpu_n=n,
-                                     attn_latency=pre, expert_latency=gemm / n, domain_sizes=c["sed"],
-                                     encode_cost=enc, decode_cost=dec, layers=layers)
+        mk, stall = oracle.sim_step(c["sf"], c["sed"], bw, D=T * k * H * b, PE=pe, n=n, pre=pre,
+                                    expert_lat=gemm / n, enc=enc, dec=dec, layers=layers)
         combine = ph.get("combine", 0.0) / 1e3  # all layers
         model = (mk + combine) * 1e3
         meas = r["ms_per_step"]
