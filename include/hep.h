@@ -88,6 +88,16 @@ typedef struct {
 int hep_solve_optimal_p(const hep_workload* w, double throughput_C, double bandwidth_B,
                         int64_t gpus, double* p, int64_t* domain_size, double* latency6);
 
+/* The planner with its reports, as the reference's `plan` + `topo` commands produce them
+ * (resolve_plan, cli_app.cpp:132-168; plan.json / freq.json / topo.csv, :183-243) but fed
+ * measured device numbers instead of a JSON config: the solver's S_ED, or
+ * pinned_domain_sizes[num_levels] when not NULL.  Writes the three files into out_dir
+ * (NULL or "": no files); returns p, the per-level S_ED (num_levels entries) and the
+ * modelled latency terms {comp, pre_expert, comm_a2a, comm_ag, overlap, total}. */
+int hep_plan_reports(const hep_level* levels, int num_levels, const hep_workload* w, double throughput_C,
+                     double bandwidth_B, const int64_t* pinned_domain_sizes, const char* out_dir, double* p,
+                     int64_t* domain_sizes, double* latency6);
+
 /* ------------------------------------------------------------- SR migration codec */
 typedef struct {
   double ratio_CR;           /* used when k < 0 */

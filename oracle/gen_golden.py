@@ -85,7 +85,31 @@ def main():
         cases[f"c{i}_spec"] = np.array([h, m, -1 if ratio is None else ratio, -1 if k is None else k, iw, vw, pm],
                                        np.float64)
     np.savez_compressed(os.path.join(ROOT, "tests", "golden", "sr_cases.npz"), **cases)
-    print("wrote tests/golden/topology_g8.json and sr_cases.npz")
+
+    # Planner reports: the reference's own run_plan + run_topo (oracle/_ref/ref_reports)
+    # on B200-like measured inputs (D, P_E, n, pre-expert s, expert s, C FLOP/s, B bytes/s).
+    import subprocess
+    import tempfile
+    reports = []
+    for sf, pin, D, PE, n, pre, ex, Cc, B in [
+            ([2], None, 2.68e8, 9.4e8, 4, 1.7e-4, 6.9e-4, 1.4e15, 7.4e11),
+            ([2, 2], None, 2.68e8, 4.7e8, 2, 1.7e-4, 1.4e-3, 1.4e15, 7.4e11),
+            ([2, 4], None, 2.68e8, 2.35e8, 1, 1.7e-4, 2.7e-3, 1.4e15, 7.4e11),
+            ([2, 4], [1, 4], 2.68e8, 2.35e8, 1, 1.7e-4, 2.7e-3, 1.4e15, 7.4e11),
+            ([2, 4], None, 4.0e6, 2.35e8, 1, 2.0e-3, 2.0e-5, 1.4e15, 7.4e11),   # tiny token volume: AG wins
+            ([2, 2, 2], None, 2.0e8, 1.8e6, 8, 1.0e-4, 5.0e-5, 1.4e15, 7.4e11),
+            ([2, 2, 2], [1, 2, 2], 2.0e8, 1.8e6, 8, 1.0e-4, 5.0e-5, 1.4e15, 7.4e11)]:
+        with tempfile.TemporaryDirectory() as d:
+            args = [os.path.join(HERE, "_ref", "ref_reports"), d] + [repr(v) for v in (D, PE, n, pre, ex, Cc, B)] + \
+                   [",".join(map(str, sf))] + ([",".join(map(str, pin))] if pin else [])
+            subprocess.run(args, check=True, capture_output=True)
+            reports.append({"sf": sf, "pinned_sed": pin, "D": D, "PE": PE, "n": n, "pre": pre, "expert": ex, "C": Cc,
+                            "B": B, "plan": json.load(open(os.path.join(d, "plan.json"))),
+                            "freq": json.load(open(os.path.join(d, "freq.json"))),
+                            "topo_csv": open(os.path.join(d, "topo.csv")).read()})
+    with open(os.path.join(ROOT, "tests", "golden", "plan_reports.json"), "w") as f:
+        json.dump(reports, f, indent=1)
+    print("wrote tests/golden/topology_g8.json, sr_cases.npz and plan_reports.json")
 
 
 if __name__ == "__main__":

@@ -116,6 +116,8 @@ SIGNATURES = {
     "hep_route_table": [P(Level), I32, P(C.c_int32)],
     "hep_factor_domain_sizes": [I64, P(Level), I32, P(I64)],
     "hep_solve_optimal_p": [P(Workload), C.c_double, C.c_double, I64, P(C.c_double), P(I64), P(C.c_double)],
+    "hep_plan_reports": [P(Level), I32, P(Workload), C.c_double, C.c_double, VP, C.c_char_p, P(C.c_double), P(I64),
+                         P(C.c_double)],
     "hep_sr_resolve_k": [P(SrConfig), I64, I64, P(I64)],
     "hep_sr_wire_bytes": [I64, I64, P(SrConfig), P(SZ)],
     "hep_sr_workspace_bytes": [I64, I64, I32, P(SZ)],

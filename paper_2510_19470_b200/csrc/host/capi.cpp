@@ -217,6 +217,36 @@ int hep_solve_optimal_p(const hep_workload* w, double throughput_C, double bandw
   });
 }
 
+int hep_plan_reports(const hep_level* levels, int num_levels, const hep_workload* w, double throughput_C,
+                     double bandwidth_B, const int64_t* pinned_domain_sizes, const char* out_dir, double* p,
+                     int64_t* domain_sizes, double* latency6) {
+  return guarded([&] {
+    if (!w) throw std::invalid_argument("null workload");
+    hybridep::perf::WorkloadSpec ws;
+    ws.data_size_D = w->data_size_D;
+    ws.expert_size_PE = w->expert_size_PE;
+    ws.experts_per_gpu_n = w->experts_per_gpu_n;
+    ws.pre_blocks_m = w->pre_blocks_m;
+    ws.attn_latency = w->attn_latency;
+    ws.ffn_latency = w->ffn_latency;
+    ws.expert_latency = w->expert_latency;
+    ws.backward_allreduce_const = w->backward_allreduce_const;
+    const auto cluster = cluster_of(levels, num_levels);
+    std::vector<int64_t> pinned;
+    if (pinned_domain_sizes) pinned.assign(pinned_domain_sizes, pinned_domain_sizes + num_levels);
+    const auto plan = hybridep::moe::resolve_plan(cluster, ws, hybridep::perf::DeviceSpec{throughput_C, bandwidth_B},
+                                                  pinned_domain_sizes ? &pinned : nullptr);
+    if (out_dir && *out_dir) hybridep::moe::write_plan_reports(cluster, ws, plan, out_dir);
+    if (p) *p = plan.point.p;
+    if (domain_sizes) std::copy(plan.domain_sizes.begin(), plan.domain_sizes.end(), domain_sizes);
+    if (latency6) {
+      const auto& L = plan.point.latency;
+      const double v[6] = {L.comp, L.pre_expert, L.comm_a2a, L.comm_ag, L.overlap, L.total};
+      std::copy(v, v + 6, latency6);
+    }
+  });
+}
+
 int hep_sr_resolve_k(const hep_sr_config* cfg, int64_t total_elements, int64_t elem_bytes, int64_t* k) {
   return guarded([&] { *k = sr_config_of(cfg).resolve_k(total_elements, elem_bytes); });
 }

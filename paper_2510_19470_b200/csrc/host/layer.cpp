@@ -677,12 +677,16 @@ void Layer::split_dirty_slots(cudaStream_t s) {
 void Layer::gather_experts(cudaStream_t s) {
   if (G_ == 1 || ag_peers_.empty()) return;
   if (p2p_) ensure_connected();
-  check_migration(false);
+  gather(s);
+  check_migration(false);  // after the collective is enqueued (see forward)
+}
+
+void Layer::gather(cudaStream_t s) {
   mark_gathered_dirty();  // the gathered slots' compute copies are rewritten below
   const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
   const size_t per_slot_up = static_cast<size_t>(F_ * H_), per_slot_down = static_cast<size_t>(H_ * F_);
   auto first_slot_of = [&](int64_t owner) { return slot_of_expert_[static_cast<size_t>(owner * n_)]; };
-  if (p2p_ && dt_ == DType::BF16) {
+  if (p2p_) {
     // "AgTransfer eligible from t=0" (simcore.cpp:155-156): the All-Gather runs on its own
     // stream with the copy engines pulling peers' experts over NVLink, while the step
     // starts; forward() waits for it only before the GEMMs of gathered experts.
@@ -961,11 +965,18 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
 }
 
 void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
+  step(x, T, y, s);
+  // A gathered expert whose wire failed to decode (found once that decode has completed)
+  // is reported after this rank's share of the collective step is enqueued, so its peers
+  // never wait for a rank that bailed out.
+  check_migration(false);
+}
+
+void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s) {
   // T = 0 is legal: a rank with an empty batch still takes part in the exchange (it
   // sends no rows, receives its peers' rows and runs their experts).
   if (T < 0 || T > Tmax_) throw std::invalid_argument("token count must be in [0, max_tokens]");
   if (p2p_) ensure_connected();
-  check_migration(false);
   launches_ = 0;
   const int Ti = static_cast<int>(T);
   const int nchunks = (Ti + 31) / 32;
@@ -1057,6 +1068,11 @@ void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
                             pos_.as<int>(), s), "permute p2p");
       ck(launch_signal_wait(p2p_args_, 1, s), "dispatch flags");
       launches_ += 3;
+      if (ag_pending_) {  // the All-Gather pulled on the copy engines while gate + dispatch ran
+        mark("ag_wait", s);
+        ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");
+        ag_pending_ = false;
+      }
       run_expert_gemms(s);
       mark("combine", s);
       ck(launch_signal_wait(p2p_args_, 2, s), "combine flags");

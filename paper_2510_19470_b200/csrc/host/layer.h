@@ -128,6 +128,8 @@ class Layer {
   void run_expert_gemms(cudaStream_t s, const unsigned long long* out_down = nullptr, const int* wait_src = nullptr,
                         int g0 = 0, int ng = -1, const char* tag = "");
   void decode_gathered(size_t wire_bytes, size_t stride, cudaStream_t s);
+  void step(const void* x, int64_t T, void* y, cudaStream_t s);  // forward's enqueue
+  void gather(cudaStream_t s);                                     // gather_experts' enqueue
 
   // shape
   int64_t H_, F_, E_, k_, Tmax_, G_, n_, NK_;

@@ -150,3 +150,21 @@ def solve_optimal_p(*, data_size_D, expert_size_PE, experts_per_gpu_n, pre_block
     check(lib.hep_solve_optimal_p(C.byref(w), throughput_C, bandwidth_B, gpus, C.byref(p), C.byref(s), lat))
     keys = ("comp", "pre_expert", "comm_a2a", "comm_ag", "overlap", "total")
     return p.value, s.value, dict(zip(keys, list(lat)))
+
+
+def plan_reports(cluster: ClusterSpec, *, data_size_D, expert_size_PE, experts_per_gpu_n, attn_latency,
+                 expert_latency, throughput_C, bandwidth_B, pre_blocks_m=0, ffn_latency=1e-12, pinned_sed=None,
+                 out_dir=None):
+    """The reference's plan + topo reports (plan.json, freq.json, topo.csv) for measured
+    inputs (hep_plan_reports): returns (p, per-level S_ED, latency terms)."""
+    w = Workload(data_size_D, expert_size_PE, experts_per_gpu_n, pre_blocks_m, attn_latency, ffn_latency,
+                 expert_latency, 0.0)
+    arr, n = cluster._c()
+    pin = (C.c_int64 * n)(*pinned_sed) if pinned_sed is not None else None
+    p = C.c_double()
+    sed = (C.c_int64 * n)()
+    lat = (C.c_double * 6)()
+    check(lib.hep_plan_reports(arr, n, C.byref(w), throughput_C, bandwidth_B, pin, (out_dir or "").encode(),
+                               C.byref(p), sed, lat))
+    keys = ("comp", "pre_expert", "comm_a2a", "comm_ag", "overlap", "total")
+    return p.value, list(sed), dict(zip(keys, list(lat)))

@@ -8,6 +8,7 @@ import torch
 import oracle
 from paper_2510_19470_b200 import sr as srmod
 from paper_2510_19470_b200._lib import HEP_BF16, HEP_F32, check, lib
+from tests import sr_golden
 from tests.tolerances import F32_GEMM_MAX
 
 pytestmark = pytest.mark.gpu
@@ -175,6 +176,35 @@ def test_sr_encode_decode_bitexact(h, m, ratio, k, iw, vw, per_matrix, quant, se
     rc, want_dec = oracle.sr_decode(want, s, h, m, use_ref=oracle.ref is not None)
     assert rc == 0
     assert dec.tobytes() == want_dec.tobytes(), "decoded expert differs from the reference"
+
+
+@pytest.mark.parametrize("select", ["auto", "full", "fallback", "multiblock"])
+def test_sr_gpu_reference_golden_wire(select, monkeypatch):
+    """The device encoder against the reference's own golden bytes
+    (test_sparsecomp.cpp:258-279) -- no oracle involved."""
+    monkeypatch.setenv("HEP_SR_SELECT", select)
+    e = torch.from_numpy(sr_golden.REF_TEST_EXPERT).cuda()
+    s = torch.from_numpy(sr_golden.REF_TEST_SHARED).cuda()
+    wire = srmod.sr_encode(e, s, 1, 2, srmod.CompressionConfig(k=2))
+    assert wire.cpu().numpy().tobytes() == sr_golden.REF_TEST_WIRE
+    dec = srmod.sr_decode(wire, s, 1, 2).cpu().numpy()
+    assert dec.tobytes() == np.array([0.0, -1.25, 0.0, 2.0], np.float32).tobytes()
+
+
+@pytest.mark.parametrize("name,c", sr_golden.cases(), ids=[n for n, _ in sr_golden.cases()])
+@pytest.mark.parametrize("select", ["auto", "full", "fallback", "multiblock"])
+def test_sr_gpu_reference_fixtures(name, c, select, monkeypatch):
+    """The device codec against the committed reference fixtures (tests/golden/sr_cases.npz,
+    written from the unmodified reference by oracle/gen_golden.py): byte-identical wires and
+    bit-identical decoded experts on the GPU box, where /root/reference does not exist."""
+    monkeypatch.setenv("HEP_SR_SELECT", select)
+    cfg = srmod.CompressionConfig(ratio_CR=c["ratio"], k=c["k"], index_width_bits=c["iw"], value_width_bits=c["vw"],
+                                  per_matrix_budget=c["per_matrix"])
+    e, s = torch.from_numpy(c["expert"]).cuda(), torch.from_numpy(c["shared"]).cuda()
+    wire = srmod.sr_encode(e, s, c["h"], c["m"], cfg)
+    assert wire.cpu().numpy().tobytes() == c["wire"].tobytes()
+    dec = srmod.sr_decode(torch.from_numpy(c["wire"]).cuda(), s, c["h"], c["m"]).cpu().numpy()
+    assert dec.tobytes() == c["decoded"].tobytes()
 
 
 def test_sr_bf16_expert_upcast():

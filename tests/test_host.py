@@ -196,3 +196,28 @@ def test_reference_engine_two_gpu_expert_parallel():
     assert stall == 0.0
     mk2, _ = oracle.sim_step([2], [1], 4 * bw, D=D, PE=2e6, n=n, pre=pre, expert_lat=e)
     assert mk2 <= mk
+
+
+def _plan_golden():
+    return json.load(open(os.path.join(GOLDEN, "plan_reports.json")))
+
+
+@pytest.mark.parametrize("case", _plan_golden(), ids=lambda c: f"sf{c['sf']}-pin{c['pinned_sed']}-D{c['D']:.0e}")
+def test_plan_reports_match_reference(case, tmp_path):
+    """hep_plan_reports vs the reference's own run_plan + run_topo (cli_app.cpp:183-243,
+    recorded by oracle/gen_golden.py through oracle/_ref/ref_reports): plan.json and
+    freq.json equal as JSON (every double bit-equal), topo.csv byte-equal."""
+    from paper_2510_19470_b200 import topology as topo
+
+    cl = topo.ClusterSpec.of(case["sf"], [1] * len(case["sf"]), bandwidth=case["B"])
+    p, sed, lat = topo.plan_reports(cl, data_size_D=case["D"], expert_size_PE=case["PE"],
+                                    experts_per_gpu_n=case["n"], attn_latency=case["pre"],
+                                    expert_latency=case["expert"], throughput_C=case["C"], bandwidth_B=case["B"],
+                                    pinned_sed=case["pinned_sed"], out_dir=str(tmp_path))
+    got_plan = json.load(open(tmp_path / "plan.json"))
+    got_freq = json.load(open(tmp_path / "freq.json"))
+    assert got_plan == case["plan"]
+    assert got_freq == case["freq"]
+    assert (tmp_path / "topo.csv").read_text() == case["topo_csv"]
+    assert p == case["plan"]["p"] and sed == case["plan"]["domain_sizes_per_level"]
+    assert lat["total"] == case["plan"]["latency"]["total_s"]
