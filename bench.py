@@ -12,13 +12,19 @@ value : tokens/s of all ranks, inputs resident in HBM, device-timed (CUDA events
         the launching stream), max over ranks.
 e2e   : same metric through hep_layer_forward_host (pinned host x -> H2D -> step ->
         D2H of y) -- the reference-facing call with host buffers.
-roofline : the expert grouped GEMM (K8), FLOPs per launch / mean launch time measured
-        live with CUDA events on the launching stream in a second pass of the same K steps
-        (phase events kept out of the `value` pass), vs the measured sustained bf16
-        peak of MEASURED_PEAKS.json.
+roofline : the expert grouped GEMM (K8), FLOPs / its launch time measured live with
+        CUDA events on the launching stream IN the timed `value` pass (phase events at
+        every kernel boundary of every step), vs the measured sustained bf16 peak of
+        MEASURED_PEAKS.json (burst fraction beside it); `kernels` gives the same pass's
+        gate / permute / combine times as fractions of measured HBM bandwidth.
+planner : at N > 1 the S_ED of cfg3/cfg5 comes from the reference's solver fed numbers
+        measured in this run (calibration: pre-expert time and expert-GEMM rate of a
+        one-GPU layer of the same shape, NVLink bytes/s of an NCCL all-gather); the
+        plan.json / freq.json / topo.csv reports are written in the reference's formats.
 cpu_baseline : the CPU oracle (oracle/moe_oracle.c, OpenMP) on a bounded token sample.
 --impl reference : times that same CPU implementation as the reference arm (the
-        reference has no GPU path and no gate/FFN/combine of its own).
+        reference has no GPU path and no gate/FFN/combine of its own),
+        with inputs generated on the CPU: that arm never loads libhep.so or touches a GPU.
 """
 from __future__ import annotations
 
@@ -58,24 +64,72 @@ CONFIGS = {
                  topo={1: ([1], [1]), 2: ([2], [1]), 4: ([2, 2], [1, 1]), 8: ([2, 4], [1, 4])}),
 }
 
-# Measured on B200 (profiles/): used only to let the reference planner pick S_ED (cfg5).
-PLANNER_INPUTS = dict(pre_expert_s=0.17e-3,        # gate + scans + permute, cfg3 shape (profiles/r1_bench_*)
-                      expert_s_per_token_row=6.0e-3 / 32768,  # up+down GEMM time per routed row
-                      nvlink_Bps=770e9)             # peer-copy bandwidth (B200_PROFILING.md)
+def calibrate(cfg, dev, dtype, world, MoELayer):
+    """Planner inputs measured on this GPU: a one-GPU layer of the
+    config's shape (all E experts local) times gate + scans + permute (the pre-expert
+    stream) and the expert GEMM pair (C = 4HF FLOPs per routed row / GEMM time); an NCCL
+    all-gather of 64 MB per rank gives the NVLink bytes/s each GPU receives (B)."""
+    import torch
+    import torch.distributed as dist
+
+    H, F, E, k, T = cfg["H"], cfg["F"], cfg["E"], cfg["k"], cfg["T"]
+    x, wg = make_inputs(cfg, 0, dev, dtype)
+    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype)
+    layer.set_gate(wg)
+    for e in range(E):
+        u, d = expert_weights(cfg, e, dev, dtype)
+        layer.set_expert(e, u, d)
+        del u, d
+    y = torch.empty_like(x)
+    for _ in range(3):
+        layer.forward(x, out=y)
+    layer.set_profiling(True)
+    layer.timings()
+    for _ in range(5):
+        layer.forward(x, out=y)
+    ph = layer.timings()
+    layer.close()
+    del layer, y
+    torch.cuda.empty_cache()
+    pre = (ph.get("gate", 0.0) + ph.get("scan", 0.0) + ph.get("permute", 0.0)) / 1e3
+    gemm = sum(v for n, v in ph.items() if n.startswith("gemm_")) / 1e3
+    rows = T * k
+    out = {"pre_expert_s": pre, "expert_s_per_routed_row": gemm / rows, "gemm_flops_per_s": 4.0 * H * F * rows / gemm,
+           "source": "measured in this run: one-GPU layer of this shape, 5 profiled forwards"}
+    if world > 1:
+        n = 64 << 20
+        buf = torch.empty(n, dtype=torch.uint8, device=dev)
+        gat = torch.empty(world * n, dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(gat, buf)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            dist.all_gather_into_tensor(gat, buf)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / 5 / 1e3], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out["nvlink_bytes_per_s"] = (world - 1) * n / float(t.item())
+        del buf, gat
+    return out
 
 
-def planned_sed(cfg, sf, world):
-    """cfg5: the reference solver (hep_solve_optimal_p, perfmodel.cpp:200-217) on measured
-    numbers, then the innermost-first split (plan.cpp:41-58)."""
+def planned_sed(cfg, sf, world, cal, report_dir):
+    """cfg3/cfg5 at N > 1: the reference solver (perfmodel.cpp:200-217, via
+    hep_plan_reports) on this run's measured numbers, the innermost-first split
+    (plan.cpp:41-58), and the reference's plan.json / freq.json / topo.csv."""
     from paper_2510_19470_b200 import topology as topo
     n = cfg["E"] // world
     rows = cfg["T"] * cfg["k"]
-    p, s, _ = topo.solve_optimal_p(
-        data_size_D=float(rows * cfg["H"] * 2), expert_size_PE=float(n * 2 * cfg["H"] * cfg["F"] * 2),
-        experts_per_gpu_n=n, pre_blocks_m=0, attn_latency=PLANNER_INPUTS["pre_expert_s"], ffn_latency=1e-9,
-        expert_latency=PLANNER_INPUTS["expert_s_per_token_row"] * rows / n, throughput_C=1.3e15,
-        bandwidth_B=PLANNER_INPUTS["nvlink_Bps"], gpus=world)
-    return topo.factor_domain_sizes(s, topo.ClusterSpec.of(sf)), p
+    b = 2 if cfg["dtype"] == "bf16" else 4
+    p, sed, lat = topo.plan_reports(
+        topo.ClusterSpec.of(sf, [1] * len(sf), bandwidth=cal["nvlink_bytes_per_s"]),
+        data_size_D=float(rows * cfg["H"] * b), expert_size_PE=float(n * 2 * cfg["H"] * cfg["F"] * b),
+        experts_per_gpu_n=n, attn_latency=cal["pre_expert_s"],
+        expert_latency=cal["expert_s_per_routed_row"] * rows / n, throughput_C=cal["gemm_flops_per_s"],
+        bandwidth_B=cal["nvlink_bytes_per_s"], out_dir=report_dir)
+    return sed, p, lat
 
 
 def parse():
@@ -88,6 +142,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--cpu-stride", type=int, default=64)
     p.add_argument("--sed", default="", help="override S_ED per level, e.g. 1,4")
+    p.add_argument("--report-dir", default="", help="where the planner reports go (default gpurun_out/plan_reports)")
     return p.parse_args()
 
 
@@ -243,12 +298,38 @@ def cpu_oracle_time(cfg, inputs, stride):
     return sampled / (secs * cfg.get("layers", 1)), secs, sampled, oracle.num_threads()
 
 
+def cpu_inputs(cfg):
+    """The same synthetic workload, generated on the CPU for the reference arm (which must
+    not load libhep.so or touch a GPU): dyadic tokens and gate, the reference demo expert
+    population (cli_app.cpp:89-118) at the config's shape and dtype.  Distribution and
+    shapes equal the GPU arm's; the CPU oracle's cost does not depend on the draw."""
+    import numpy as np
+    import torch
+
+    H, F, E, T = cfg["H"], cfg["F"], cfg["E"], cfg["T"]
+    dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    g = torch.Generator().manual_seed(1000)
+    x = (torch.randint(-8, 9, (T, H), generator=g).float() / 16.0)
+    wg = (torch.randint(-8, 9, (H, E), generator=g).float() / 16.0)
+    scale = 2.0 ** -5 if H <= 1024 else 2.0 ** -6
+    ups = np.empty((E, H, F), np.float32)
+    downs = np.empty((E, F, H), np.float32)
+    gb = torch.Generator().manual_seed(11)
+    base_u = (0.05 + 0.95 * torch.rand((H, F), generator=gb)) * (torch.randint(0, 2, (H, F), generator=gb) * 2 - 1)
+    base_d = (0.05 + 0.95 * torch.rand((F, H), generator=gb)) * (torch.randint(0, 2, (F, H), generator=gb) * 2 - 1)
+    for e in range(E):
+        ge = torch.Generator().manual_seed(100 + e)
+        ups[e] = ((base_u + (torch.rand((H, F), generator=ge) * 2 - 1) * 0.05) * scale).to(dt).float().numpy()
+        downs[e] = ((base_d + (torch.rand((F, H), generator=ge) * 2 - 1) * 0.05) * scale).to(dt).float().numpy()
+    return x.to(dt).float().numpy()[None], wg.numpy(), ups, downs
+
+
 def run_reference(args, cfg):
-    """Reference arm: the CPU implementation of the path, rank 0 only."""
+    """Reference arm: the CPU implementation of the path, rank 0 only, CPU inputs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    inputs = cpu_oracle_inputs(cfg)
+    inputs = cpu_inputs(cfg)
     vals = []
     for i in range(args.warmup + args.steps):
         tps, secs, sampled, cores = cpu_oracle_time(cfg, inputs, args.cpu_stride)
@@ -259,7 +340,7 @@ def run_reference(args, cfg):
     line = {"impl": "reference", "metric": "MoE-layer tokens/s", "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sampled / v,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
-            "data": "synthetic", "config": {"workload": cfg["workload"], "tokens_per_gpu": cfg["T"]},
+            "data": "synthetic (generated on the CPU)", "config": {"workload": cfg["workload"], "tokens_per_gpu": cfg["T"]},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -297,7 +378,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2510_19470_b200.moe import Communicator, MoELayer
+    from paper_2510_19470_b200.moe import Communicator, MoELayer, gather_all
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -311,13 +392,17 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         comm = Communicator.from_torch()
     sf, sed = cfg["topo"][world]
-    p_plan = None
+    dtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    p_plan = planner = None
     if args.sed:
         sed = [int(v) for v in args.sed.split(",")]
     elif sed is None:
-        sed, p_plan = planned_sed(cfg, sf, world)
+        cal = calibrate(cfg, dev, dtype, world, MoELayer)
+        report_dir = args.report_dir or os.path.join(ROOT, "gpurun_out", "plan_reports", f"{args.config}_n{world}")
+        sed, p_plan, lat = planned_sed(cfg, sf, world, cal, report_dir if rank == 0 else None)
+        planner = {"measured_inputs": cal, "p": p_plan, "sed": sed, "modelled_latency_s": lat,
+                   "reports": os.path.relpath(report_dir, ROOT) + "/{plan.json,freq.json,topo.csv}"}
     sed_source = "override" if args.sed else ("planner" if p_plan is not None else "pinned")
-    dtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     H, F, E, k, T = cfg["H"], cfg["F"], cfg["E"], cfg["k"], cfg["T"]
     use_sr = cfg["sr"] and world > 1
     srcfg = None
@@ -351,9 +436,11 @@ def main():
     acts = [x] + [torch.empty_like(x) for _ in range(cfg["layers"])]
 
     def step():
+        if world > 1:
+            # every layer's expert All-Gather queued at t=0 (simcore.cpp:155-174); the
+            # pulls run on the copy engines under the layers' compute
+            gather_all(layers)
         for li, layer in enumerate(layers):
-            if world > 1:
-                layer.gather_experts()
             layer.forward(acts[li], out=acts[li + 1])
 
     def barrier():
@@ -378,9 +465,16 @@ def main():
         if r0.elapsed_time(r1) >= 200.0:
             break
     del ramp, ramp2
+    # The timed pass carries a CUDA event at every phase boundary of every step (on the
+    # launching streams), so the GEMM time the roofline divides by and the per-kernel
+    # HBM fractions come from the same K steps as `value`.
+    for layer in layers:
+        layer.set_profiling(True)
     for _ in range(args.warmup):
         step()
     barrier()
+    for layer in layers:
+        layer.timings()  # drop the warm-up marks
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local).__enter__()
@@ -390,17 +484,7 @@ def main():
     t1.record(stream)
     barrier()
     ms = t0.elapsed_time(t1)
-    # Per-phase device times (phase_ms, and the GEMM launches the roofline divides by):
-    # a second pass of the same K steps with a CUDA event at every phase boundary on the
-    # launching streams.  Kept out of the pass above, whose ten-odd extra event records per
-    # step cost ~5% on the smallest config (cfg1 at 4 GPUs).
-    for layer in layers:
-        layer.set_profiling(True)
-        layer.timings()
-    for _ in range(args.steps):
-        step()
-    barrier()
-    phases = {}
+    phases = {}  # mean ms per step, summed over the layers of the stack
     for layer in layers:
         for kname, v in layer.timings().items():
             phases[kname] = phases.get(kname, 0.0) + v
@@ -423,18 +507,46 @@ def main():
             dist.all_reduce(kc)
         rows += int(kc[rank * E:(rank + 1) * E].sum().item())
     gemm_ms = sum(v for kname, v in phases.items() if kname.startswith("gemm_"))
+    step_ms_local = ms / args.steps
+    assert gemm_ms <= step_ms_local * 1.001, f"GEMM time {gemm_ms:.4f} ms exceeds the step {step_ms_local:.4f} ms"
     pk = peaks()
     flops = 4.0 * H * F * rows
     achieved = flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
     peak = pk.get("bf16_tflops_sustained", 1400.0)
-    peak_source = "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside the step loop)"
+    peak_burst = pk.get("bf16_tflops", 1590.0)
+    peak_source = ("MEASURED_PEAKS.json bf16_tflops_sustained (the GEMM is timed inside a back-to-back step loop "
+                   "under sw_power_cap, the regime of the sustained figure; see clocks)")
     gemm_kernel = "grouped expert GEMM (up+down, tcgen05 kind::f16)"
     if cfg["dtype"] == "f32":
         # fp32 layers run 3xTF32 on the tensor cores: TF32 is half the bf16 rate and every
         # fp32 product costs three TF32 MMAs, so the fp32-equivalent ceiling is bf16 / 6
         peak = peak / 6.0
+        peak_burst = peak_burst / 6.0
         peak_source = "derived: MEASURED_PEAKS.json bf16_tflops_sustained / 2 (tf32 rate) / 3 (3xTF32 MMAs per product)"
         gemm_kernel = "grouped expert GEMM (up+down, tcgen05 kind::tf32, 3xTF32)"
+    # HBM-bound kernels of the same pass (SURVEY §8(d) algorithmic bytes, b = element bytes)
+    b = 2 if dtype == torch.bfloat16 else 4
+    L = cfg["layers"]
+    hbm = pk.get("hbm_gbs", 6650.0)
+    algo = {"gate": L * (T * H * b + E * H * b + T * k * 16),
+            "permute": L * (T * H * b + T * k * H * b + T * k * 4),
+            "combine": L * (T * k * H * b + T * k * 8 + T * H * b)}
+    kernels = {}
+    for kname, nbytes in algo.items():
+        if phases.get(kname):
+            gbs = nbytes / (phases[kname] / 1e3) / 1e9
+            kernels[kname] = {"ms_per_step": phases[kname], "algorithmic_bytes": nbytes, "achieved_gbs": gbs,
+                              "hbm_frac": gbs / hbm}
+    for kname in ("gemm_up", "gemm_down"):
+        # every launch of that projection (own, received and gathered groups at N > 1)
+        t_ms = sum(v for n_, v in phases.items() if n_.startswith(kname))
+        if t_ms:
+            f = flops / 2.0  # up and down are 2HF FLOPs per row each
+            kernels[kname] = {"ms_per_step": t_ms, "tflops": f / (t_ms / 1e3) / 1e12,
+                              "frac_sustained": f / (t_ms / 1e3) / 1e12 / peak,
+                              "frac_burst": f / (t_ms / 1e3) / 1e12 / peak_burst}
+    kernels["hbm_peak_gbs"] = hbm
+    kernels["source"] = "CUDA events at every phase boundary of the timed pass (launching stream)"
     # DRAM bytes of one up+down GEMM pair from an ncu capture of the same N=1 workload
     # (profiles/ncu_summary.json); the N>1 step splits the GEMM into more launches
     traffic = None
@@ -508,9 +620,19 @@ def main():
             del payload, gathered
         stats = torch.tensor([cb["a2a_bus_gbs"] or 0.0, cb["ag_bus_gbs"] or 0.0], device=dev, dtype=torch.float64)
         dist.all_reduce(stats, op=dist.ReduceOp.MIN)
+        # The reference's per-level stripe-model bytes of this plan (traffic_report,
+        # topology.cpp:249-281) beside the physical bytes this GPU moved (SURVEY §7 hard
+        # part 2: the two differ for multi-level clusters)
+        from paper_2510_19470_b200 import topology as topo
+        n_e = E // world
+        stripe = topo.traffic_report(topo.ClusterSpec.of(sf, sed), data_size_D=float(T * k * H * b),
+                                     expert_size_PE=float(n_e * 2 * H * F * b))
         comm_stats = dict(cb, a2a_bus_gbs_min_over_ranks=float(stats[0]), ag_bus_gbs_min_over_ranks=float(stats[1]),
                           nvlink_peak_gbs=770.0, peak_source="B200_PROFILING.md measured peer copy per direction",
-                          a2a_frac=float(stats[0]) / 770.0, ag_frac=float(stats[1]) / 770.0)
+                          a2a_frac=float(stats[0]) / 770.0, ag_frac=float(stats[1]) / 770.0,
+                          physical_bytes_per_gpu={"a2a_dispatch_sent": cb["a2a_bytes"], "ag_received": cb["ag_bytes"]},
+                          stripe_model_bytes_cluster={"per_level": stripe, "unit": "bytes per layer pass, "
+                                                      "all GPUs (traffic_report, topology.cpp:249-281)"})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -538,8 +660,12 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "traffic_unit": "DRAM bytes per up+down launch pair (ncu, profiles/ncu_summary.json)",
-                         "peak_source": peak_source,
+                         "peak_source": peak_source, "peak_burst": peak_burst,
+                         "frac_burst": (achieved / peak_burst) if achieved else None,
+                         "gemm_ms_per_step": gemm_ms, "timed_in": "the value pass (same K steps)",
                          "flops_per_launch_pair": flops / cfg["layers"]},
+            "kernels": kernels,
+            "planner": planner,
             "phase_ms": phases,
             "gpu_launches": launches,
             "comm": comm_stats,

@@ -200,6 +200,12 @@ int hep_layer_get_shared(hep_layer_t layer, float* out, void* stream);
 /* Expert-domain All-Gather of the owned experts (dense or SR-migrated), so that every
  * held expert is resident.  Issued on `stream`. */
 int hep_layer_gather_experts(hep_layer_t layer, void* stream);
+/* The All-Gather queue of a layer stack (the paper's per-layer send/recv queues,
+ * PAPER.md:258-266; "AgTransfer for all layers eligible from t=0", simcore.cpp:155-174):
+ * issues every layer's expert All-Gather at once at the start of an iteration.  On the
+ * peer-memory path the pulls run in layer order on the rank's All-Gather stream (copy
+ * engines) while the layers compute; each layer's forward waits only for its own. */
+int hep_layers_gather(hep_layer_t* layers, int n, void* stream);
 /* The step: gate -> permute -> dispatch -> expert FFN -> combine.  x, y: device
  * [tokens, H] in the layer dtype, 0 <= tokens <= max_tokens (tokens may differ between
  * GPUs; a GPU with tokens = 0 still takes part and serves its peers' rows). */

@@ -139,6 +139,7 @@ SIGNATURES = {
     "hep_layer_refresh_shared": [VP, VP],
     "hep_layer_get_shared": [VP, VP, VP],
     "hep_layer_gather_experts": [VP, VP],
+    "hep_layers_gather": [P(VP), I32, VP],
     "hep_layer_forward": [VP, VP, I64, VP, VP],
     "hep_layer_forward_host": [VP, VP, I64, VP, VP],
     "hep_layer_host_fence": [VP, VP],

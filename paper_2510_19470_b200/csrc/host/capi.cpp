@@ -451,6 +451,13 @@ int hep_layer_gather_experts(hep_layer_t layer, void* stream) {
   return guarded([&] { layer->impl->gather_experts(st(stream)); });
 }
 
+int hep_layers_gather(hep_layer_t* layers, int n, void* stream) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && !layers)) throw std::invalid_argument("need an array of n layers");
+    for (int i = 0; i < n; ++i) layers[i]->impl->gather_experts(st(stream));
+  });
+}
+
 int hep_layer_forward(hep_layer_t layer, const void* x, int64_t tokens, void* y, void* stream) {
   return guarded([&] { layer->impl->forward(x, tokens, y, st(stream)); });
 }

@@ -64,6 +64,14 @@ class Communicator:
             self.handle = None
 
 
+def gather_all(layers, stream=None):
+    """Queue the expert All-Gather of every layer of a stack at the start of an iteration
+    (hep_layers_gather): pulls run in layer order under the compute, each forward waits
+    only for its own layer's experts."""
+    arr = (C.c_void_p * len(layers))(*[layer.handle.value for layer in layers])
+    check(lib.hep_layers_gather(arr, len(layers), _stream(stream)))
+
+
 class MoELayer:
     def __init__(self, *, hidden, ffn, experts, top_k, max_tokens, dtype=torch.bfloat16, sf=(1,), sed=None,
                  rank=0, comm: Optional[Communicator] = None, sr: Optional[CompressionConfig] = None):

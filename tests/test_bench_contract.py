@@ -18,10 +18,17 @@ def _json_lines(path):
 
 
 def test_reference_arm_prints_contract_line():
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "cfg1",
-                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    """The reference arm prints the contract line without loading libhep.so or
+    initialising CUDA (its inputs are generated on the CPU)."""
+    probe = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--config', 'cfg1', '--steps', '1', "
+             "'--warmup', '0']; runpy.run_path('bench.py', run_name='__main__'); import torch; "
+             "maps = open('/proc/self/maps').read(); "
+             "print('LOADED_LIBHEP' if 'libhep.so' in maps else 'NO_LIBHEP', "
+             "'CUDA_INIT' if torch.cuda.is_initialized() else 'NO_CUDA_INIT')")
+    r = subprocess.run([sys.executable, "-c", probe], capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
-    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert r.stdout.strip().splitlines()[-1] == "NO_LIBHEP NO_CUDA_INIT", r.stdout[-500:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["impl"] == "reference" and line["metric"] == "MoE-layer tokens/s" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"] == {"value": line["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
