@@ -126,6 +126,18 @@ int hep_sr_encode(const void* expert, hep_dtype expert_dtype, const float* share
 int hep_sr_encode_batch(const void* const* experts, int n, hep_dtype expert_dtype, const float* shared,
                         int64_t h, int64_t m, const hep_sr_config* cfg, void* const* wires,
                         size_t wire_capacity, void* workspace, size_t workspace_bytes, void* stream);
+/* The paper's SREncode fused with the optimizer step (-30% claimed at
+ * :1185; the Optimizer job that carries the encode, simcore.cpp:126): masters[b] (fp32 flat
+ * P, device) <- fmaf(-lr, grads[b], masters[b]), and wires[b] = the SRC1 encode of the
+ * stepped master against `shared` -- byte-identical to hep_sgd_step_batch followed by
+ * hep_sr_encode_batch.  The encode's one full read applies and writes back the step
+ * (when every range is list-selected; otherwise the step runs as its own pass first). */
+int hep_sr_encode_update_batch(float* const* masters, const float* const* grads, int n, float lr, const float* shared,
+                               int64_t h, int64_t m, const hep_sr_config* cfg, void* const* wires, size_t wire_capacity,
+                               void* workspace, size_t workspace_bytes, void* stream);
+/* The unfused step: masters[b][i] = fmaf(-lr, grads[b][i], masters[b][i]), i < elements. */
+int hep_sgd_step_batch(float* const* masters, const float* const* grads, int n, int64_t elements, float lr,
+                       void* stream);
 /* Device decode = deserialize + sr_decode (sparsecomp.cpp:99-131, :226-246).
  * out: fp32 flat P.  status: device int32[4] (16 bytes); status[0] after the stream
  * reaches this point: 0 ok, 1 bad magic, 2 truncated, 3 bad widths, 4 shape tag
@@ -195,6 +207,11 @@ int hep_layer_set_shared(hep_layer_t layer, const float* shared, void* stream);
  * order), pipelined in chunks over NVLink peer memory (NCCL send/recv + broadcast on the
  * HEP_COMM=nccl path).  Collective: every rank calls it on its stream. */
 int hep_layer_refresh_shared(hep_layer_t layer, void* stream);
+/* SR mode: the optimizer step of this rank's owned experts fused with their migration
+ * encode: grads[i] (fp32 flat P, reference layout, device) for owned expert rank*n + i,
+ * i < n.  Updates the fp32 masters and the compute copies and leaves the wires encoded for
+ * the next hep_layer_gather_experts, which then skips its own encode. */
+int hep_layer_sgd_step(hep_layer_t layer, const float* const* grads, int n, float lr, void* stream);
 /* SR mode: copy of the current fp32 shared expert (flat P) into `out` (device). */
 int hep_layer_get_shared(hep_layer_t layer, float* out, void* stream);
 /* Expert-domain All-Gather of the owned experts (dense or SR-migrated), so that every

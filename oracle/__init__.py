@@ -48,6 +48,8 @@ def _load_orc():
     lib.orc_moe_layer.argtypes = [C.c_int, VP, VP, VP, VP, I64, I64, I64, I64, I64, I64, VP, VP, C.c_int, I64,
                                   VP, VP, VP, VP, VP]
     lib.orc_num_threads.restype = C.c_int
+    lib.orc_sgd_step.argtypes = [VP, VP, C.c_float, I64]
+    lib.orc_sgd_step.restype = None
     return lib
 
 
@@ -167,6 +169,14 @@ def sr_decode(wire, shared, h, m, use_ref=False):
     fn = ref.ref_sr_decode if use_ref else orc.orc_sr_decode
     rc = fn(_p(wire), wire.size, _p(shared), h, m, _p(out))
     return rc, out
+
+
+def sgd_step(master, grad, lr):
+    """m - lr g with one rounding (fmaf), as the fused encode applies it."""
+    m = np.ascontiguousarray(master, np.float32).copy()
+    g = np.ascontiguousarray(grad, np.float32)
+    orc.orc_sgd_step(_p(m), _p(g), float(lr), m.size)
+    return m
 
 
 def shared_mean(experts, use_ref=False, h=None, m=None):

@@ -290,6 +290,13 @@ int orc_sr_decode(const uint8_t* wire, int64_t bytes, const float* shared, int64
   return 0;
 }
 
+/* The optimizer step the fused SR encode applies (hep_sr_encode_update_batch): plain SGD
+ * with one rounding, m = fmaf(-lr, g, m).  The reference has no optimizer; its Optimizer
+ * job only carries the encode cost (simcore.cpp:126). */
+void orc_sgd_step(float* m, const float* g, float lr, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) m[i] = fmaf(-lr, g[i], m[i]);
+}
+
 /* ------------------------------------------------------------------ MoE layer */
 
 static float bf16_round(float f) {

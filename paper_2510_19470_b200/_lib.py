@@ -123,6 +123,9 @@ SIGNATURES = {
     "hep_sr_workspace_bytes": [I64, I64, I32, P(SZ)],
     "hep_sr_encode": [VP, I32, VP, I64, I64, P(SrConfig), VP, SZ, VP, SZ, VP],
     "hep_sr_encode_batch": [P(VP), I32, I32, VP, I64, I64, P(SrConfig), P(VP), SZ, VP, SZ, VP],
+    "hep_sr_encode_update_batch": [P(VP), P(VP), I32, C.c_float, VP, I64, I64, P(SrConfig), P(VP), SZ, VP, SZ, VP],
+    "hep_sgd_step_batch": [P(VP), P(VP), I32, I64, C.c_float, VP],
+    "hep_layer_sgd_step": [VP, P(VP), I32, C.c_float, VP],
     "hep_sr_decode": [VP, SZ, VP, I64, I64, VP, VP, VP],
     "hep_sr_decode_batch": [P(VP), I32, SZ, VP, I64, I64, P(VP), VP, VP],
     "hep_sr_check_status": [VP, VP],

@@ -311,6 +311,35 @@ int hep_sr_encode_batch(const void* const* experts, int n, hep_dtype expert_dtyp
   });
 }
 
+int hep_sr_encode_update_batch(float* const* masters, const float* const* grads, int n, float lr, const float* shared,
+                               int64_t h, int64_t m, const hep_sr_config* cfg, void* const* wires, size_t wire_capacity,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    if (n <= 0 || n > hep::kMaxSrBatch) throw std::invalid_argument("batch must be in [1, 64]");
+    if (!grads) throw std::invalid_argument("null gradient array");
+    const hep::SrPlan plan = make_sr_plan(h, m, cfg);
+    if (wire_capacity < plan.wire_bytes) throw std::invalid_argument("wire buffer too small");
+    if (workspace_bytes < hep::sr_workspace_bytes(h, m, n)) throw std::invalid_argument("workspace too small");
+    std::vector<const void*> ex(masters, masters + n);
+    cuda_ok(hep::launch_sr_encode_batch(hep::DType::F32, ex.data(), n, shared, plan,
+                                        reinterpret_cast<uint8_t* const*>(wires), workspace, st(stream), grads, lr),
+            "sr encode update");
+  });
+}
+
+int hep_sgd_step_batch(float* const* masters, const float* const* grads, int n, int64_t elements, float lr,
+                       void* stream) {
+  return guarded([&] {
+    if (n <= 0 || n > hep::kMaxSrBatch) throw std::invalid_argument("batch must be in [1, 64]");
+    if (elements <= 0) throw std::invalid_argument("empty expert");
+    cuda_ok(hep::launch_sgd_step_batch(masters, grads, n, elements, lr, st(stream)), "sgd step");
+  });
+}
+
+int hep_layer_sgd_step(hep_layer_t layer, const float* const* grads, int n, float lr, void* stream) {
+  return guarded([&] { layer->impl->sgd_step(grads, n, lr, st(stream)); });
+}
+
 int hep_sr_encode(const void* expert, hep_dtype expert_dtype, const float* shared, int64_t h, int64_t m,
                   const hep_sr_config* cfg, void* wire, size_t wire_capacity, void* workspace,
                   size_t workspace_bytes, void* stream) {

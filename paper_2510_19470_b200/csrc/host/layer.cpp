@@ -701,7 +701,7 @@ void Layer::gather(cudaStream_t s) {
     if (use_sr_) {
       if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
       stride = (wb + 15) / 16 * 16;
-      if (ag.epoch > 1) {  // every AG peer has pulled last epoch's wires before they are rewritten
+      if (ag.epoch > 1 && !wires_fresh_) {  // every AG peer has pulled last epoch's wires before they are rewritten
         P2PArgs prev = ag;
         prev.epoch = ag.epoch - 1;
         ck(launch_signal_wait(prev, 4, ag_s_, true, true, false), "wires pulled");
@@ -712,9 +712,11 @@ void Layer::gather(cudaStream_t s) {
         ex.push_back(master_.as<float>() + i * P);
         wo.push_back(wires_.as<uint8_t>() + stride * (first_slot_of(rank_) + i));
       }
-      if (hep_sr_encode_batch(ex.data(), static_cast<int>(n_), HEP_F32, shared_.as<float>(), H_, F_, &c, wo.data(),
+      if (!wires_fresh_ &&
+          hep_sr_encode_batch(ex.data(), static_cast<int>(n_), HEP_F32, shared_.as<float>(), H_, F_, &c, wo.data(),
                               wb, sr_ws_.p, sr_ws_.bytes, ag_s_) != HEP_OK)
         throw std::runtime_error(hep_last_error());
+      wires_fresh_ = false;
     }
     // Every AG peer's experts (or wires) for this epoch are final -> pull.
     ck(launch_signal_wait(ag, 3, ag_s_, true, true), "ag flags");
@@ -760,7 +762,7 @@ void Layer::gather(cudaStream_t s) {
   if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
   const size_t stride = (wb + 15) / 16 * 16;
   uint8_t* wires = wires_.as<uint8_t>();
-  {
+  if (!wires_fresh_) {
     std::vector<const void*> ex;
     std::vector<void*> wo;
     for (int64_t i = 0; i < n_; ++i) {
@@ -771,6 +773,7 @@ void Layer::gather(cudaStream_t s) {
                             sr_ws_.p, sr_ws_.bytes, s) != HEP_OK)
       throw std::runtime_error(hep_last_error());
   }
+  wires_fresh_ = false;
   nck(ncclGroupStart(), "group start");
   for (int64_t p : ag_peers_) {
     nck(ncclSend(wires + stride * first_slot_of(rank_), stride * n_, ncclUint8, static_cast<int>(p), comm_->nccl, s), "send wire");
@@ -778,6 +781,51 @@ void Layer::gather(cudaStream_t s) {
   }
   nck(ncclGroupEnd(), "group end");
   decode_gathered(wb, stride, s);
+}
+
+void Layer::sgd_step(const float* const* grads, int n, float lr, cudaStream_t s) {
+  if (!use_sr_) throw std::invalid_argument("the fused optimizer step updates the fp32 masters of SR-migrated layers");
+  if (n != n_ || !grads) throw std::invalid_argument("one gradient per owned expert is required");
+  if (p2p_) ensure_connected();
+  if (ag_pending_) ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");  // the last encode read the masters
+  if (p2p_ && ag_epoch_ > 0 && !ag_peers_.empty()) {
+    // the wires are rewritten below: every AG peer has pulled the last epoch's (slot 4)
+    P2PArgs prev = p2p_args_;
+    prev.epoch = ag_epoch_;
+    ck(launch_signal_wait(prev, 4, s, true, true, false), "wires pulled");
+  }
+  const int64_t P = 2 * H_ * F_;
+  size_t wb = 0;
+  hep_sr_config c{sr_cfg_.ratio_CR.value_or(1.0), sr_cfg_.k.value_or(-1), sr_cfg_.index_width_bits,
+                  sr_cfg_.value_width_bits, sr_cfg_.per_matrix_budget ? 1 : 0};
+  if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
+  const size_t stride = (wb + 15) / 16 * 16;
+  const int32_t first = slot_of_expert_[static_cast<size_t>(rank_ * n_)];
+  std::vector<float*> ms;
+  std::vector<void*> wo;
+  for (int64_t i = 0; i < n_; ++i) {
+    ms.push_back(master_.as<float>() + i * P);
+    wo.push_back(wires_.as<uint8_t>() + stride * (first + i));
+  }
+  if (ag_peers_.empty()) {  // nothing migrates: the plain step
+    if (hep_sgd_step_batch(ms.data(), grads, static_cast<int>(n_), P, lr, s) != HEP_OK)
+      throw std::runtime_error(hep_last_error());
+  } else {
+    if (hep_sr_encode_update_batch(ms.data(), grads, static_cast<int>(n_), lr, shared_.as<float>(), H_, F_, &c,
+                                   wo.data(), wb, sr_ws_.p, sr_ws_.bytes, s) != HEP_OK)
+      throw std::runtime_error(hep_last_error());
+    wires_fresh_ = true;
+  }
+  // the owned compute copies (GEMM layout, layer dtype) from the stepped masters
+  const size_t eb = static_cast<size_t>(dtype_bytes(dt_));
+  for (int64_t i = 0; i < n_; ++i) {
+    const int64_t slot = first + i;
+    ck(launch_transpose_convert(DType::F32, ms[static_cast<size_t>(i)], H_, F_, dt_,
+                                w_up_c_.as<uint8_t>() + eb * slot * F_ * H_, s), "w_up layout");
+    ck(launch_transpose_convert(DType::F32, ms[static_cast<size_t>(i)] + H_ * F_, F_, H_, dt_,
+                                w_down_c_.as<uint8_t>() + eb * slot * H_ * F_, s), "w_down layout");
+    slot_dirty_[static_cast<size_t>(slot)] = 1;
+  }
 }
 
 void Layer::decode_gathered(size_t wb, size_t stride, cudaStream_t s) {

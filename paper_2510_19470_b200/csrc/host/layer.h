@@ -92,6 +92,9 @@ class Layer {
   void refresh_shared(cudaStream_t s);
   void get_shared(float* out, cudaStream_t s) const;  // SR mode: copy of the fp32 shared expert
   void gather_experts(cudaStream_t s);
+  // SR mode: SGD step of the owned fp32 masters fused with their encode (wires ready for
+  // the next gather); grads[i] flat P fp32 for owned expert rank*n + i.
+  void sgd_step(const float* const* grads, int n, float lr, cudaStream_t s);
   void forward(const void* x, int64_t T, void* y, cudaStream_t s);
   void forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s);
   void host_fence(cudaStream_t s);
@@ -205,6 +208,7 @@ class Layer {
   bool connected_ = true;
   uint64_t timeout_ns_ = 0;
   bool corrupt_next_ = false;
+  bool wires_fresh_ = false;  // sgd_step encoded the owned wires; the next gather reuses them
   int32_t* mig_err_host_ = nullptr;  // mapped pinned flag: a gathered wire failed to decode
   int32_t* mig_err_dev_ = nullptr;
 

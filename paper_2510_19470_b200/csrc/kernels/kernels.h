@@ -157,9 +157,16 @@ struct SrPlan {
 constexpr int kMaxSrBatch = 64;
 size_t sr_workspace_bytes(int64_t h, int64_t m, int batch);
 // Encodes `batch` experts (same shape, same shared expert) in one launch sequence.
+// grads != nullptr: the optimizer step fused with the encode (fp32 masters only): every
+// master becomes fmaf(-lr, grad, master) and the wire encodes that stepped value; the
+// split pass (the encode's one full read) applies and writes back the step when every
+// range is list-selected, else a separate step kernel runs first.
 cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, int batch, const float* shared,
                                    const SrPlan& plan, uint8_t* const* wires, void* workspace,
-                                   cudaStream_t stream);
+                                   cudaStream_t stream, const float* const* grads = nullptr, float lr = 0.f);
+// The unfused optimizer step: masters[b] = fmaf(-lr, grads[b], masters[b]) over P elements.
+cudaError_t launch_sgd_step_batch(float* const* masters, const float* const* grads, int batch, int64_t P, float lr,
+                                  cudaStream_t stream);
 // Validates each wire (status int32[4] per wire: code, failing entry, scratch) and writes
 // out_b = shared + residual_b (fp32).
 cudaError_t launch_sr_decode_batch(const uint8_t* const* wires, int batch, size_t wire_bytes, const float* shared,

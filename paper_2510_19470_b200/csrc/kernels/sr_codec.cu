@@ -31,9 +31,11 @@
 // All fp64 arithmetic uses explicit _rn intrinsics so no FMA contraction can
 // change a rounding.
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include <cooperative_groups.h>
 
@@ -113,6 +115,12 @@ struct WsView {
 struct EncBatch {
   const void* expert[kMaxSrBatch];
   uint8_t* wire[kMaxSrBatch];
+  // Optimizer step fused with the encode (update = 1, fp32 experts only): expert b is the
+  // fp32 master; the value encoded is fmaf(-lr, grad, master), and the split pass -- the
+  // encode's one full read -- writes it back as the new master.
+  const float* grad[kMaxSrBatch];
+  float lr;
+  int update;
 };
 
 struct DecBatch {
@@ -342,8 +350,9 @@ __global__ void sr_init_kernel(WsView ws, EncBatch batch, int bf16, const float*
     uint32_t* keys = ws.skeys(b, r);
     for (int j = blockIdx.x * blockDim.x + t; j < S; j += static_cast<int>(stride)) {
       const int64_t i = lo + static_cast<int64_t>(j) * step;
-      const float e = bf16 ? __uint_as_float(static_cast<uint32_t>(__ldcs(static_cast<const unsigned short*>(batch.expert[b]) + i)) << 16)
-                           : __ldcs(static_cast<const float*>(batch.expert[b]) + i);
+      float e = bf16 ? __uint_as_float(static_cast<uint32_t>(__ldcs(static_cast<const unsigned short*>(batch.expert[b]) + i)) << 16)
+                     : __ldcs(static_cast<const float*>(batch.expert[b]) + i);
+      if (batch.update) e = fmaf(-batch.lr, __ldcs(batch.grad[b] + i), e);  // the stepped master
       keys[j] = key32_of(__dsub_rn(static_cast<double>(e), static_cast<double>(__ldcs(shared + i))));
     }
   }
@@ -484,6 +493,8 @@ __global__ void __launch_bounds__(kTileThreads) sr_split_kernel(EncBatch batch, 
   const int count = static_cast<int>(hi - t_lo < kSplitTile ? hi - t_lo : kSplitTile);
   const void* expert = batch.expert[b];
   const int eb = bf16 ? 2 : 4;
+  float* s_gr = reinterpret_cast<float*>(s_ex + kSplitTile * 4);  // update mode: the gradient tile
+  const float* grad = batch.update ? batch.grad[b] : nullptr;
   // bulk part: the first count8 elements (multiple of 8 = 16 B of bf16, 32 B of f32)
   const int count8 = BULK ? (count & ~7) : 0;
   if (BULK) {
@@ -494,16 +505,18 @@ __global__ void __launch_bounds__(kTileThreads) sr_split_kernel(EncBatch batch, 
     __syncthreads();
     if (threadIdx.x == 0 && count8) {
       const uint64_t pol = l2_policy_evict_first();
-      mbar_arrive_expect_tx(&full_bar, static_cast<uint32_t>(count8 * (4 + eb)));
+      mbar_arrive_expect_tx(&full_bar, static_cast<uint32_t>(count8 * (4 + eb + (grad ? 4 : 0))));
       bulk_load(s_sh, shared + t_lo, static_cast<uint32_t>(count8 * 4), &full_bar, pol);
       bulk_load(s_ex, static_cast<const uint8_t*>(expert) + t_lo * eb, static_cast<uint32_t>(count8 * eb), &full_bar,
                 pol);
+      if (grad) bulk_load(s_gr, grad + t_lo, static_cast<uint32_t>(count8 * 4), &full_bar, pol);
     }
   }
   for (int p = count8 + threadIdx.x; p < count; p += blockDim.x) {  // plain-load part
     s_sh[p] = shared[t_lo + p];
     if (bf16) reinterpret_cast<uint16_t*>(s_ex)[p] = static_cast<const uint16_t*>(expert)[t_lo + p];
     else reinterpret_cast<float*>(s_ex)[p] = static_cast<const float*>(expert)[t_lo + p];
+    if (grad) s_gr[p] = grad[t_lo + p];
   }
   const uint32_t lo32 = s.lo32, hi32 = s.hi32;
   // fp32 "surely below B0" threshold; outside [2^-100, 2^126] every element is exact
@@ -511,6 +524,29 @@ __global__ void __launch_bounds__(kTileThreads) sr_split_kernel(EncBatch batch, 
   const float t_below = (b0 >= 0x1p-100 && b0 <= 0x1p126) ? __double2float_rd(b0 * (1.0 - 0x1p-22)) : -1.0f;
   if (BULK && count8) mbar_wait(&full_bar, 0);
   __syncthreads();
+  if (grad) {
+    // the optimizer step fused into the encode's one full read: master' = master - lr g
+    // (one rounding), written back as the new master and classified below
+    float* s_m = reinterpret_cast<float*>(s_ex);
+    float* master = const_cast<float*>(static_cast<const float*>(expert)) + t_lo;
+    const bool vec = ((reinterpret_cast<uintptr_t>(master) & 15) == 0);
+    const int count4 = vec ? (count & ~3) : 0;
+    for (int p = 4 * threadIdx.x; p < count4; p += 4 * blockDim.x) {
+      float4 m4 = *reinterpret_cast<const float4*>(s_m + p);
+      const float4 g4 = *reinterpret_cast<const float4*>(s_gr + p);
+      m4.x = fmaf(-batch.lr, g4.x, m4.x);
+      m4.y = fmaf(-batch.lr, g4.y, m4.y);
+      m4.z = fmaf(-batch.lr, g4.z, m4.z);
+      m4.w = fmaf(-batch.lr, g4.w, m4.w);
+      *reinterpret_cast<float4*>(s_m + p) = m4;
+      __stcs(reinterpret_cast<float4*>(master + p), m4);
+    }
+    for (int p = count4 + threadIdx.x; p < count; p += blockDim.x) {
+      s_m[p] = fmaf(-batch.lr, s_gr[p], s_m[p]);
+      master[p] = s_m[p];
+    }
+    __syncthreads();
+  }
 
   // element p = 1024 it + 4 tid + q  ->  bit 4 it + q
   constexpr int kSteps = kSplitTile / (kTileThreads * 4);  // 8
@@ -1588,15 +1624,55 @@ size_t sr_workspace_bytes(int64_t h, int64_t m, int batch) {
   return static_cast<size_t>(batch) * 2 * make_ws(nullptr, 2 * h * m).per + 256;
 }
 
+namespace {
+// The unfused optimizer step (and the fallback of the fused one): m = fmaf(-lr, g, m).
+__global__ void sgd_step_kernel(EncBatch eb, int64_t P) {
+  const int b = blockIdx.y;
+  float* m = const_cast<float*>(static_cast<const float*>(eb.expert[b]));
+  const float* g = eb.grad[b];
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(g)) & 15) == 0;
+  const int64_t P4 = vec ? P / 4 : 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P4; i += stride) {
+    float4 v = reinterpret_cast<const float4*>(m)[i];
+    const float4 d = __ldcs(reinterpret_cast<const float4*>(g) + i);
+    v.x = fmaf(-eb.lr, d.x, v.x);
+    v.y = fmaf(-eb.lr, d.y, v.y);
+    v.z = fmaf(-eb.lr, d.z, v.z);
+    v.w = fmaf(-eb.lr, d.w, v.w);
+    reinterpret_cast<float4*>(m)[i] = v;
+  }
+  for (int64_t i = 4 * P4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P; i += stride)
+    m[i] = fmaf(-eb.lr, g[i], m[i]);
+}
+}  // namespace
+
+cudaError_t launch_sgd_step_batch(float* const* masters, const float* const* grads, int batch, int64_t P, float lr,
+                                  cudaStream_t stream) {
+  if (batch <= 0 || batch > kMaxSrBatch) return cudaErrorInvalidValue;
+  EncBatch eb{};
+  for (int i = 0; i < batch; ++i) {
+    eb.expert[i] = masters[i];
+    eb.grad[i] = grads[i];
+  }
+  eb.lr = lr;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 8 / batch, (P / 4 + 255) / 256)));
+  sgd_step_kernel<<<dim3(blocks, batch), 256, 0, stream>>>(eb, P);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, int batch, const float* shared,
                                    const SrPlan& plan, uint8_t* const* wires, void* workspace,
-                                   cudaStream_t stream) {
+                                   cudaStream_t stream, const float* const* grads, float lr) {
   if (batch <= 0 || batch > kMaxSrBatch) return cudaErrorInvalidValue;
+  if (grads && expert_dt != DType::F32) return cudaErrorInvalidValue;  // the fused step updates fp32 masters
   EncBatch eb{};
   for (int i = 0; i < batch; ++i) {
     eb.expert[i] = experts[i];
     eb.wire[i] = wires[i];
+    if (grads) eb.grad[i] = grads[i];
   }
+  eb.lr = lr;
   const int64_t P = plan.total, up = plan.h * plan.m;
   // 256-byte align the slots (the workspace pointer itself may be any cudaMalloc offset)
   uint8_t* wbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
@@ -1639,20 +1715,37 @@ cudaError_t launch_sr_encode_batch(DType expert_dt, const void* const* experts, 
   const bool cluster = expect_max <= kFinMaxList && ovr != 3 && ovr != 4;
 
   ra.lookback = (any_full || (any_list && !cluster)) ? 1 : 0;
+  if (grads) {
+    // Fused only when every range is list-selected: then the split pass reads every
+    // element once and writes the stepped master back.  Otherwise step first, then encode.
+    bool all_list = true;
+    for (int r = 0; r < ra.nr; ++r) {
+      const int64_t n = ra.hi[r] - ra.lo[r], k = ra.k[r];
+      all_list &= !ra.full[r] && k > 0 && k < n;
+    }
+    if (all_list) {
+      eb.update = 1;
+    } else {
+      std::vector<float*> ms(static_cast<size_t>(batch));
+      for (int i = 0; i < batch; ++i) ms[static_cast<size_t>(i)] = const_cast<float*>(static_cast<const float*>(experts[i]));
+      const cudaError_t e = launch_sgd_step_batch(ms.data(), grads, batch, P, lr, stream);
+      if (e != cudaSuccess) return e;
+    }
+  }
   sr_init_kernel<<<dim3(16, batch), 256, 0, stream>>>(ws, eb, bf16, shared, ra, plan.h, plan.m, plan.k,
                                                       plan.index_bits, plan.value_bits);
   if (any_list) {
     static DeviceOnce attr;
     if (!attr.done()) {
       cudaFuncSetAttribute(sr_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSampleSmem);
-      cudaFuncSetAttribute(sr_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 8);
-      cudaFuncSetAttribute(sr_split_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 8);
+      cudaFuncSetAttribute(sr_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 12);
+      cudaFuncSetAttribute(sr_split_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSplitTile * 12);
       cudaFuncSetAttribute(sr_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFinSmem);
       attr.set();
     }
     sr_sample_kernel<<<dim3(ra.nr, batch), kSampleThreads, kSampleSmem, stream>>>(ra, ws);
     const bool bulk = ((ra.lo[0] | (ra.nr > 1 ? ra.lo[1] : 0)) & 7) == 0;
-    const int smem = kSplitTile * (4 + (bf16 ? 2 : 4));
+    const int smem = kSplitTile * (4 + (bf16 ? 2 : 4) + (eb.update ? 4 : 0));
     const dim3 sgrid(static_cast<unsigned>(tiles_max), slots);
     if (bulk) sr_split_kernel<true><<<sgrid, kTileThreads, smem, stream>>>(eb, bf16, shared, ra, ws);
     else sr_split_kernel<false><<<sgrid, kTileThreads, smem, stream>>>(eb, bf16, shared, ra, ws);
@@ -1792,6 +1885,7 @@ cudaError_t preload_sr_codec_kernels() {
   if (const cudaError_t e = load(reinterpret_cast<const void*>(transpose_convert_kernel<__nv_bfloat16, __nv_bfloat16>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(transpose_convert_kernel<__nv_bfloat16, float>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_status_fold_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sgd_step_kernel))) return e;
   return cudaSuccess;
 }
 

@@ -116,6 +116,14 @@ class MoELayer:
         with the reference's init_shared / update_shared, sparsecomp.cpp:147-173)."""
         check(lib.hep_layer_refresh_shared(self.handle, _stream(stream)))
 
+    def sgd_step(self, grads, lr: float, stream=None):
+        """SR mode: SGD step of the owned fp32 masters fused with their migration encode
+        (hep_layer_sgd_step); grads: one flat fp32 [2HF] device tensor per owned expert."""
+        grads = [g.contiguous() for g in grads]
+        arr = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
+        check(lib.hep_layer_sgd_step(self.handle, arr, len(grads), float(lr), _stream(stream)))
+        self._keep = grads  # alive until the stream reaches the step
+
     def get_shared(self, stream=None) -> torch.Tensor:
         out = torch.empty(2 * self.H * self.F, dtype=torch.float32, device="cuda")
         check(lib.hep_layer_get_shared(self.handle, out.data_ptr(), _stream(stream)))

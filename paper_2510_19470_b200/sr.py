@@ -126,3 +126,27 @@ def shared_mean(experts: list) -> torch.Tensor:
     ptrs = (C.c_void_p * len(experts))(*[e.data_ptr() for e in experts])
     check(lib.hep_shared_mean(ptrs, len(experts), _dt(experts[0]), P, out.data_ptr(), _stream()))
     return out
+
+
+def sr_encode_update_batch(masters: list, grads: list, lr: float, shared: torch.Tensor, h: int, m: int,
+                           cfg: CompressionConfig) -> list:
+    """The optimizer step fused with the encode (hep_sr_encode_update_batch): every fp32
+    master (flat P, device) becomes fmaf(-lr, grad, master) IN PLACE and is encoded."""
+    n = len(masters)
+    nbytes = wire_bytes(h, m, cfg)
+    wires = [torch.empty(nbytes, dtype=torch.uint8, device=shared.device) for _ in range(n)]
+    ws = _workspace(shared.device, h, m, n)
+    mps = (C.c_void_p * n)(*[t.data_ptr() for t in masters])
+    gps = (C.c_void_p * n)(*[t.data_ptr() for t in grads])
+    wps = (C.c_void_p * n)(*[w.data_ptr() for w in wires])
+    check(lib.hep_sr_encode_update_batch(mps, gps, n, lr, shared.data_ptr(), h, m, C.byref(cfg._c()), wps, nbytes,
+                                         ws.data_ptr(), ws.numel(), _stream()))
+    return wires
+
+
+def sgd_step_batch(masters: list, grads: list, lr: float):
+    """The unfused step: masters[b] = fmaf(-lr, grads[b], masters[b]) in place."""
+    n = len(masters)
+    mps = (C.c_void_p * n)(*[t.data_ptr() for t in masters])
+    gps = (C.c_void_p * n)(*[t.data_ptr() for t in grads])
+    check(lib.hep_sgd_step_batch(mps, gps, n, masters[0].numel(), lr, _stream()))

@@ -207,6 +207,45 @@ def test_sr_gpu_reference_fixtures(name, c, select, monkeypatch):
     assert dec.tobytes() == c["decoded"].tobytes()
 
 
+@pytest.mark.parametrize("h,m,ratio,k,per_matrix,batch", [
+    (64, 96, 50.0, None, False, 3),     # fused: the split pass applies and writes back the step
+    (64, 96, 50.0, None, True, 2),      # fused, per-matrix budgets (two list ranges)
+    (333, 77, 7.0, None, False, 1),     # unaligned tile starts
+    (8, 8, None, 0, False, 2),          # k = 0: no list range -> the step runs as its own pass
+    (8, 8, None, 10 ** 9, False, 1),    # k >= P: full range -> unfused fallback
+    (2048, 1408, 50.0, None, False, 4),  # cfg4 experts
+])
+@pytest.mark.parametrize("select", ["auto", "fallback", "multiblock"])
+def test_sr_encode_fused_with_optimizer_step(h, m, ratio, k, per_matrix, batch, select, monkeypatch):
+    """hep_sr_encode_update_batch == SGD step (fmaf, one rounding) then encode: masters
+    bit-identical to the oracle's step, wires byte-identical to the reference encode of
+    the stepped masters, and identical to the unfused GPU step + encode."""
+    monkeypatch.setenv("HEP_SR_SELECT", select)
+    lr = 0.0078125 * 0.75
+    masters, grads, s = [], [], None
+    for i in range(batch):
+        e, s = _demo_expert_pair(h, m, seed=h + m + i)
+        masters.append(e)
+        grads.append(np.random.default_rng(i).standard_normal(2 * h * m).astype(np.float32))
+    cfg = srmod.CompressionConfig(ratio_CR=ratio, k=k, per_matrix_budget=per_matrix)
+    st = torch.from_numpy(s).cuda()
+    dm = [torch.from_numpy(e).cuda() for e in masters]
+    dg = [torch.from_numpy(g).cuda() for g in grads]
+    wires = srmod.sr_encode_update_batch(dm, dg, lr, st, h, m, cfg)
+    um = [torch.from_numpy(e).cuda() for e in masters]  # unfused: step, then encode
+    srmod.sgd_step_batch(um, dg, lr)
+    uw = srmod.sr_encode_batch(um, st, h, m, cfg)
+    torch.cuda.synchronize()
+    for i in range(batch):
+        want_m = oracle.sgd_step(masters[i], grads[i], lr)
+        assert dm[i].cpu().numpy().tobytes() == want_m.tobytes(), "stepped master differs"
+        assert um[i].cpu().numpy().tobytes() == want_m.tobytes()
+        want = oracle.sr_encode(want_m, s, h, m, ratio=ratio, k=k, per_matrix=per_matrix,
+                                use_ref=oracle.ref is not None)
+        assert wires[i].cpu().numpy().tobytes() == want.tobytes(), "fused wire differs from the reference"
+        assert uw[i].cpu().numpy().tobytes() == want.tobytes()
+
+
 def test_sr_bf16_expert_upcast():
     h, m = 48, 40
     e, s = _demo_expert_pair(h, m, seed=5)

@@ -41,6 +41,9 @@ CASES = [
     # weights rewritten between steps while peers pull them (dense and SR All-Gather)
     ([2, 4], [1, 4], ["--update"]),
     ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr", "--update"]),
+    # the optimizer step fused with the migration encode, then a step on the new experts
+    ([2, 2], [2, 1], ["--sr", "--sgd"]),
+    ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr", "--sgd"]),
     # a corrupted migrated expert is rejected (RuntimeFailure), not consumed silently
     ([2, 2], [1, 2], ["--sr", "--corrupt"]),
     # ranks that disagree on the layer shape are rejected before any peer store

@@ -12,6 +12,8 @@ shared-expert refresh bit-exact with the reference mean.  Options:
   --update   new expert weights between two steps (the All-Gather slot-4 guard)
   --corrupt  SR: corrupt one gathered wire; the layer must raise RuntimeFailure
   --mismatch rank 1 with a different max_tokens: the first step must raise InvalidArgument
+  --sgd      SR: an SGD step fused with the migration encode (hep_layer_sgd_step) between
+             two steps; the second must match the oracle on the stepped experts
 """
 import argparse
 import os
@@ -50,6 +52,7 @@ def main():
     ap.add_argument("--update", action="store_true")
     ap.add_argument("--corrupt", action="store_true")
     ap.add_argument("--mismatch", action="store_true")
+    ap.add_argument("--sgd", action="store_true")
     a = ap.parse_args()
 
     torch.cuda.set_device(0)
@@ -158,6 +161,23 @@ def main():
 
     for counts in plan:
         step(counts, w_up, w_down, flat, shared)
+    if a.sgd:
+        assert a.sr
+        lr = 2.0 ** -7
+        rng = np.random.default_rng(7)
+        grads = [rng.standard_normal(2 * a.H * a.F).astype(np.float32) * 2.0 ** -6 for _ in range(a.E)]
+        for r in range(G):
+            with torch.cuda.stream(streams[r]):
+                layers[r].sgd_step([torch.from_numpy(grads[e]).cuda() for e in layers[r].owned_experts()], lr,
+                                   stream=streams[r])
+        each(lambda r, L: L.gather_experts(stream=streams[r]))
+        flat2 = [oracle.sgd_step(flat[e], grads[e], lr) for e in range(a.E)]
+        HF = a.H * a.F
+        # what an owner computes with: its stepped master in the layer dtype
+        w_up2 = torch.stack([torch.from_numpy(f[:HF].reshape(a.H, a.F)) for f in flat2]).to(dt)
+        w_down2 = torch.stack([torch.from_numpy(f[HF:].reshape(a.F, a.H)) for f in flat2]).to(dt)
+        step(plan[0], w_up2, w_down2, flat2, shared)
+        print("sgd ok", flush=True)
     if a.update:
         # new weights on every owner between steps: peers must not pull torn experts
         g2 = torch.Generator().manual_seed(4242)
