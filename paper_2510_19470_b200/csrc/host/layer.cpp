@@ -248,7 +248,7 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
     wires_.alloc(((wb + 15) / 16 * 16) * slots_);
     sr_ws_.alloc(sr_workspace_bytes(H_, F_, static_cast<int>(n_)));
     sr_tmp_.alloc(sizeof(float) * P);
-    sr_status_.alloc(16 * kMaxSrBatch);
+    sr_status_.alloc(16 * std::max<int64_t>(kMaxSrBatch, slots_));  // fused decode: one status per slot
     shared_c_.alloc(static_cast<size_t>(dtype_bytes(dt_)) * P);
     if (G_ > 1) partial_.alloc(sizeof(double) * P);  // shared-expert refresh chain
   }
@@ -270,6 +270,27 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
     timeout_ns_ = p2p_timeout_ns();
     if (p2p_) {
       setup_p2p();
+      const char* fused = std::getenv("HEP_SR_FUSED");  // 0: dense decode of gathered experts
+      sr_fused_ = use_sr_ && dt_ == DType::BF16 && !(fused && fused[0] == '0') && H_ < 65536 && F_ < 65536;
+      if (sr_fused_) {
+        size_t wb = 0;
+        hep_sr_config c{sr_cfg_.ratio_CR.value_or(1.0), sr_cfg_.k.value_or(-1), sr_cfg_.index_width_bits,
+                        sr_cfg_.value_width_bits, sr_cfg_.per_matrix_budget ? 1 : 0};
+        if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
+        patch_kmax_ = std::max<size_t>(1, (wb - 28) / 8);
+        const size_t rp = static_cast<size_t>(H_ + F_ + 1);
+        patch_words_.alloc(sizeof(uint32_t) * patch_kmax_ * slots_);
+        patch_rowptr_.alloc(sizeof(int) * rp * slots_);
+        std::vector<PatchRef> refs(static_cast<size_t>(slots_));
+        for (int64_t sl = 0; sl < slots_; ++sl)
+          refs[static_cast<size_t>(sl)] = PatchRef{patch_words_.as<uint32_t>() + sl * patch_kmax_,
+                                                   patch_rowptr_.as<int>() + sl * rp, sr_status_.as<int32_t>() + 4 * sl};
+        patch_refs_.alloc(sizeof(PatchRef) * slots_);
+        ck(cudaMemcpy(patch_refs_.p, refs.data(), sizeof(PatchRef) * slots_, cudaMemcpyHostToDevice), "patch refs");
+        ck(make_tmap_bf16_2d(&map_shared_up_, shared_c_.p, F_, H_, 256, 64), "tmap shared up");
+        ck(make_tmap_bf16_2d(&map_shared_down_, shared_c_.as<uint8_t>() + 2 * H_ * F_, H_, F_, 256, 64),
+           "tmap shared down");
+      }
     } else {
       // NCCL baseline: agree on the layer shape before any row is received
       const LayerSig mine = signature();
@@ -736,7 +757,10 @@ void Layer::gather(cudaStream_t s) {
     }
     // "I have pulled your experts / wires of this epoch": owners may rewrite them now
     ck(launch_signal_wait(ag, 4, ag_s_, false, true, true), "pulled");
-    if (use_sr_) decode_gathered(wb, stride, ag_s_);
+    if (use_sr_) {
+      if (sr_fused_) index_gathered(wb, stride, ag_s_);
+      else decode_gathered(wb, stride, ag_s_);
+    }
     ck(cudaEventRecord(ev_ag_done_, ag_s_), "record");
     ag_pending_ = true;
     return;
@@ -825,6 +849,36 @@ void Layer::sgd_step(const float* const* grads, int n, float lr, cudaStream_t s)
     ck(launch_transpose_convert(DType::F32, ms[static_cast<size_t>(i)] + H_ * F_, F_, H_, dt_,
                                 w_down_c_.as<uint8_t>() + eb * slot * H_ * F_, s), "w_down layout");
     slot_dirty_[static_cast<size_t>(slot)] = 1;
+  }
+}
+
+void Layer::index_gathered(size_t wb, size_t stride, cudaStream_t s) {
+  // Fused decode: each gathered wire -> its slot's patch list (validated like the decode);
+  // the gathered experts' GEMMs read the shared expert and apply the patches in-kernel.
+  uint8_t* wires = wires_.as<uint8_t>();
+  const size_t rp = static_cast<size_t>(H_ + F_ + 1);
+  auto first_slot_of = [&](int64_t owner) { return slot_of_expert_[static_cast<size_t>(owner * n_)]; };
+  bool corrupt = corrupt_next_;
+  corrupt_next_ = false;
+  for (int64_t p : ag_peers_) {
+    const int64_t first = first_slot_of(p);
+    if (corrupt) {  // test hook: break the first gathered wire's magic
+      ck(cudaMemsetAsync(wires + stride * first, 0x58, 1, s), "corrupt");
+      corrupt = false;
+    }
+    std::vector<const uint8_t*> wi;
+    std::vector<uint32_t*> words;
+    std::vector<int*> rows;
+    for (int64_t i = 0; i < n_; ++i) {
+      const int64_t sl = first + i;
+      wi.push_back(wires + stride * sl);
+      words.push_back(patch_words_.as<uint32_t>() + sl * patch_kmax_);
+      rows.push_back(patch_rowptr_.as<int>() + sl * rp);
+    }
+    int32_t* st = sr_status_.as<int32_t>() + 4 * first;
+    ck(launch_sr_patch_index(wi.data(), static_cast<int>(n_), wb, shared_.as<float>(), H_, F_, words.data(),
+                             rows.data(), st, s), "patch index");
+    ck(launch_sr_status_fold(st, static_cast<int>(n_), mig_err_dev_, s), "decode status");
   }
 }
 
@@ -970,7 +1024,7 @@ void Layer::exchange(bool dispatch, cudaStream_t s) {
 }
 
 void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down, const int* wait_src, int g0,
-                             int ng, const char* tag) {
+                             int ng, const char* tag, bool patched) {
   if (ng < 0) ng = num_groups_ - g0;
   if (ng <= 0) return;
   GroupTable gt{g_row_start_.as<int>() + g0, g_rows_.as<int>() + g0, g_slot_.as<int>() + g0, ng};
@@ -983,7 +1037,18 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     gt.timeout_ns = timeout_ns_;
   }
   const std::string up = std::string("gemm_up") + tag, down = std::string("gemm_down") + tag;
-  if (dt_ == DType::BF16) {
+  if (dt_ == DType::BF16 && patched) {
+    // gathered SR experts: decode fused into the B-operand load (shared expert + patches)
+    const PatchRef* refs = patch_refs_.as<PatchRef>();
+    mark(up.c_str(), s);
+    ck(launch_grouped_gemm_bf16_patched(map_a1_, map_shared_up_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_),
+                                        static_cast<int>(H_), gt, refs, 0, 1, num_sms_, s),
+       "gemm up (fused decode)");
+    mark(down.c_str(), s);
+    ck(launch_grouped_gemm_bf16_patched(map_a2_, map_shared_down_, oall_.p, static_cast<int>(H_), static_cast<int>(H_),
+                                        static_cast<int>(F_), gt_down, refs, static_cast<int>(H_), 0, num_sms_, s),
+       "gemm down (fused decode)");
+  } else if (dt_ == DType::BF16) {
     mark(up.c_str(), s);
     auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta : launch_grouped_gemm_bf16;
     ck(gemm(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_), "gemm up");
@@ -1093,7 +1158,7 @@ void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s) {
             mark("ag_wait", s);
             ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");
           }
-          run_expert_gemms(s, out_down, nullptr, own, num_groups_ - own, "_gathered");
+          run_expert_gemms(s, out_down, nullptr, own, num_groups_ - own, "_gathered", sr_fused_);
         }
         ag_pending_ = false;
       } else if (ag_pending_) {
@@ -1102,7 +1167,7 @@ void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s) {
         mark("ag_wait", s);
         ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");
         ag_pending_ = false;
-        run_expert_gemms(s, out_down, g_wait_.as<int>(), own, num_groups_ - own, "_gathered");
+        run_expert_gemms(s, out_down, g_wait_.as<int>(), own, num_groups_ - own, "_gathered", sr_fused_);
       } else {
         run_expert_gemms(s, out_down, g_wait_.as<int>());
       }

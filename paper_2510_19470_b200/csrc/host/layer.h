@@ -129,7 +129,14 @@ class Layer {
   void build_comm_plan_and_groups(int T, cudaStream_t s);
   void exchange(bool dispatch, cudaStream_t s);
   void run_expert_gemms(cudaStream_t s, const unsigned long long* out_down = nullptr, const int* wait_src = nullptr,
-                        int g0 = 0, int ng = -1, const char* tag = "");
+                        int g0 = 0, int ng = -1, const char* tag = "", bool patched = false);
+  // Fused SR decode (bf16, peer-memory path): gathered wires become per-slot patch lists
+  // applied inside the GEMM's B-operand load instead of dense decoded compute copies.
+  void index_gathered(size_t wire_bytes, size_t stride, cudaStream_t s);
+  bool sr_fused_ = false;
+  DevBuf patch_words_, patch_rowptr_, patch_refs_;
+  size_t patch_kmax_ = 0;
+  CUtensorMap map_shared_up_, map_shared_down_;
   void decode_gathered(size_t wire_bytes, size_t stride, cudaStream_t s);
   void step(const void* x, int64_t T, void* y, cudaStream_t s);  // forward's enqueue
   void gather(cudaStream_t s);                                     // gather_experts' enqueue

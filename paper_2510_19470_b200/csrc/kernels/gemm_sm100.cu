@@ -39,6 +39,7 @@ constexpr int kThreads = 192;
 struct SmemCtl {
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
+  uint64_t patched[STAGES];  // PATCH variant: the converter warp finished this stage
   uint64_t tfull[ACC];
   uint64_t tempty[ACC];
   uint32_t tmem_base;
@@ -111,14 +112,21 @@ __device__ __forceinline__ int find_group(const SmemCtl& s, int ng, int tile) {
   return lo;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+// PATCH = true: SR migration decode fused into the B-operand load (gathered experts).
+// B is the SHARED expert's compute copy (one slot, map_b); a converter warp (warp 6) waits
+// for each stage's TMA, writes the expert's residual-patched bf16 values into the
+// 128-byte-swizzled B tile (precomputed by sr_patch_index: bf16((float)((double)shared +
+// r)), the dense decode's exact values), fences them into the async proxy and releases
+// the stage to the MMA issuer -- so the decode never materialises a dense expert copy.
+template <bool PATCH>
+__global__ void __launch_bounds__(kThreads + (PATCH ? 32 : 0), 1)
 grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_b, __nv_bfloat16* __restrict__ C,
                          int ldc, int N, int K, const int* __restrict__ g_row_start,
                          const int* __restrict__ g_rows, const int* __restrict__ g_slot,
                          const unsigned long long* __restrict__ g_out, const int* __restrict__ g_wait,
                          const uint32_t* __restrict__ wait_flags, uint32_t epoch, int ng, int relu,
-                         uint32_t sched, uint64_t timeout_ns) {
+                         uint32_t sched, uint64_t timeout_ns, const PatchRef* __restrict__ patches, int row_base) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -166,6 +174,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
+      mbar_init(&s.patched[i], 1);
     }
     for (int i = 0; i < ACC; ++i) {
       mbar_init(&s.tfull[i], 1);
@@ -182,6 +191,51 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
   const int total = s.num_tiles;
   const uint32_t tmem_base = s.tmem_base;
 
+  if (PATCH && warp == 6) {
+    // ================= converter (fused SR decode) =================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int g = find_group(s, ng, tile);
+      const int local = tile - s.tile_start[g];
+      const int m_tiles = (s.rows[g] + BM - 1) / BM;
+      int mt, nt;
+      decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
+      const PatchRef pr = patches[s.slot[g]];
+      const bool ok = *pr.status == 0;  // a rejected wire is reported by the layer, never applied
+      const int c0 = nt * BN, c1 = min(c0 + BN, N);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&s.full[stage], phase);
+        if (ok) {
+          uint8_t* bst = stage_b + stage * B_BYTES;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int rr = lane + 32 * half;  // K column of the tile = reference row
+            const int row = row_base + kb * BK + rr;
+            int lo = __ldg(pr.row_ptr + row), hi = __ldg(pr.row_ptr + row + 1);
+            while (lo < hi) {  // first entry of the row with column >= c0
+              const int mid = (lo + hi) >> 1;
+              if (static_cast<int>(__ldg(pr.words + mid) >> 16) < c0) lo = mid + 1; else hi = mid;
+            }
+            const int end = __ldg(pr.row_ptr + row + 1);
+            for (int j = lo; j < end; ++j) {
+              const uint32_t w = __ldg(pr.words + j);
+              const int r = static_cast<int>(w >> 16) - c0;
+              if (r >= c1 - c0) break;
+              // SW128: 16-byte chunk (rr / 8) of row r sits at chunk (rr / 8) ^ (r % 8)
+              const int byte = r * 128 + ((((rr >> 3) ^ (r & 7))) << 4) + ((rr & 7) << 1);
+              *reinterpret_cast<uint16_t*>(bst + byte) = static_cast<uint16_t>(w & 0xffffu);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s.patched[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  }
+
   if (warp == 0) {
     // ================= TMA producer =================
     if (lane == 0) {
@@ -196,7 +250,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         int mt, nt;
         decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
         const int a_row = s.row_start[g] + mt * BM;
-        const int b_row = s.slot[g] * N + nt * BN;
+        const int b_row = (PATCH ? 0 : s.slot[g] * N) + nt * BN;  // PATCH: the shared expert
         if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch, timeout_ns);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
@@ -220,7 +274,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&s.full[stage], phase);
+          mbar_wait(PATCH ? &s.patched[stage] : &s.full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_addr(stage_a + stage * A_BYTES);
           const uint32_t b_addr = smem_addr(stage_b + stage * B_BYTES);
@@ -236,7 +290,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else {
+  } else if (warp >= 2 && warp <= 5) {
     // ================= epilogue (warps 2..5) =================
     const uint32_t quarter = warp & 3u;  // TMEM lane quarter this warp may access
     const int row_in_tile = static_cast<int>(quarter * 32 + lane);
@@ -974,13 +1028,33 @@ cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap
   static DeviceOnce attr_set;
   if (!attr_set.done()) {
     const cudaError_t e = cudaFuncSetAttribute(
-        grouped_gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+        grouped_gemm_bf16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     if (e != cudaSuccess) return e;
     attr_set.set();
   }
-  grouped_gemm_bf16_kernel<<<num_sms, kThreads, kSmemBytes, stream>>>(
+  grouped_gemm_bf16_kernel<false><<<num_sms, kThreads, kSmemBytes, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
-      groups.slot, groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns);
+      groups.slot, groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched,
+      groups.timeout_ns, nullptr, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grouped_gemm_bf16_patched(const CUtensorMap& map_a, const CUtensorMap& map_shared_b, void* C,
+                                             int ldc, int N, int K, const GroupTable& groups, const PatchRef* patches,
+                                             int row_base, int relu, int num_sms, cudaStream_t stream, uint32_t sched) {
+  if (K % BK || N % 32 || N > 65535 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
+    return cudaErrorInvalidValue;
+  static DeviceOnce attr_set;
+  if (!attr_set.done()) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        grouped_gemm_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    if (e != cudaSuccess) return e;
+    attr_set.set();
+  }
+  grouped_gemm_bf16_kernel<true><<<num_sms, kThreads + 32, kSmemBytes, stream>>>(
+      map_a, map_shared_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
+      groups.slot, groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched,
+      groups.timeout_ns, patches, row_base);
   return cudaGetLastError();
 }
 
@@ -1010,7 +1084,8 @@ cudaError_t preload_gemm_sm100_kernels() {
     cudaFuncAttributes attr;
     return cudaFuncGetAttributes(&attr, fn);
   };
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel<false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel<true>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(ksplit_reduce_kernel))) return e;

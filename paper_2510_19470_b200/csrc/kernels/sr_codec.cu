@@ -1789,6 +1789,87 @@ cudaError_t launch_sr_decode_batch(const uint8_t* const* wires, int batch, size_
 }
 
 namespace {
+struct PatchBatch {
+  const uint8_t* wire[kMaxSrBatch];
+  uint32_t* words[kMaxSrBatch];
+  int* row_ptr[kMaxSrBatch];
+};
+
+// grid (blocks, batch): thread j < k validates entry j like the decode (first failing entry
+// wins: status word 2-3 as in sr_decode_scatter) and writes its patch word
+// (column << 16) | bf16((float)((double)shared[i] + v)); thread r <= h + m writes row_ptr[r]
+// = first entry of reference row r (binary search over the sorted indices).
+__global__ void __launch_bounds__(256) sr_patch_index_kernel(PatchBatch pb, size_t bytes,
+                                                             const float* __restrict__ shared, int64_t h,
+                                                             int64_t m, int32_t* status) {
+  const int b = blockIdx.y;
+  const uint8_t* wire = pb.wire[b];
+  int code;
+  const WireView v = read_header(wire, bytes, h, m, &code);
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t up = h * m, P = 2 * up, rows = h + m;
+  if (!v.ok_header) {
+    if (t == 0) status[4 * b] = code;
+    if (t <= rows) pb.row_ptr[b][t] = 0;  // nothing to apply
+    return;
+  }
+  if (t < v.k) {
+    const uint64_t idx = entry_index(wire, v, t);
+    int c = 0;
+    if (idx >= static_cast<uint64_t>(P)) c = 5;
+    else if (t > 0 && idx <= entry_index(wire, v, t - 1)) c = 6;
+    if (c) {
+      atomicMin(reinterpret_cast<unsigned long long*>(status + 4 * b + 2),
+                static_cast<unsigned long long>(t) * 8ull + static_cast<unsigned long long>(c));
+    } else {
+      const int64_t i = static_cast<int64_t>(idx);
+      const int64_t col = i < up ? i % m : (i - up) % h;
+      const float val = __double2float_rn(__dadd_rn(static_cast<double>(shared[i]), entry_value(wire, v, t)));
+      const uint32_t bf = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(val)));
+      pb.words[b][t] = (static_cast<uint32_t>(col) << 16) | bf;
+    }
+  }
+  if (t <= rows) {
+    const int64_t start = t < h ? t * m : (t < rows ? up + (t - h) * h : P);
+    int64_t lo = 0, hi = v.k;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (static_cast<int64_t>(entry_index(wire, v, mid)) < start) lo = mid + 1; else hi = mid;
+    }
+    pb.row_ptr[b][t] = static_cast<int>(lo);
+  }
+}
+
+__global__ void sr_patch_status_init_kernel(int32_t* status, int n) {
+  const int b = threadIdx.x;
+  if (b < n) {
+    status[4 * b] = 0;
+    status[4 * b + 1] = 0;
+    *reinterpret_cast<unsigned long long*>(status + 4 * b + 2) = ~0ull;
+  }
+}
+}  // namespace
+
+cudaError_t launch_sr_patch_index(const uint8_t* const* wires, int batch, size_t wire_bytes, const float* shared,
+                                  int64_t h, int64_t m, uint32_t* const* words, int* const* row_ptr, int32_t* status,
+                                  cudaStream_t stream) {
+  if (batch <= 0 || batch > kMaxSrBatch || h > 65535 || m > 65535) return cudaErrorInvalidValue;
+  PatchBatch pb{};
+  for (int i = 0; i < batch; ++i) {
+    pb.wire[i] = wires[i];
+    pb.words[i] = words[i];
+    pb.row_ptr[i] = row_ptr[i];
+  }
+  const int64_t kmax = wire_bytes > 28 ? static_cast<int64_t>((wire_bytes - 28) / 8) : 0;
+  const int64_t n = std::max<int64_t>(kmax, h + m + 1);
+  const int blocks = static_cast<int>(std::max<int64_t>(1, (n + 255) / 256));
+  sr_patch_status_init_kernel<<<1, kMaxSrBatch, 0, stream>>>(status, batch);
+  sr_patch_index_kernel<<<dim3(blocks, batch), 256, 0, stream>>>(pb, wire_bytes, shared, h, m, status);
+  sr_status_finalize_kernel<<<1, kMaxSrBatch, 0, stream>>>(status, batch);
+  return cudaGetLastError();
+}
+
+namespace {
 // First failing decode code of a batch -> a (host-mapped) error word, kept until read.
 __global__ void sr_status_fold_kernel(const int32_t* __restrict__ status, int n, int32_t* __restrict__ err) {
   const int i = threadIdx.x;
@@ -1886,6 +1967,8 @@ cudaError_t preload_sr_codec_kernels() {
   if (const cudaError_t e = load(reinterpret_cast<const void*>(transpose_convert_kernel<__nv_bfloat16, float>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_status_fold_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(sgd_step_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_patch_index_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_patch_status_init_kernel))) return e;
   return cudaSuccess;
 }
 

@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--corrupt", action="store_true")
     ap.add_argument("--mismatch", action="store_true")
     ap.add_argument("--sgd", action="store_true")
+    ap.add_argument("--dump", default="", help="save every rank's first-step output (bf16 bits) to this .npy")
     a = ap.parse_args()
 
     torch.cuda.set_device(0)
@@ -153,6 +154,10 @@ def main():
             with torch.cuda.stream(streams[r]):
                 ys[r] = layers[r].forward(x_all[r, :counts[r]].cuda(), stream=streams[r])
         torch.cuda.synchronize()
+        if a.dump and not getattr(step, "dumped", False):
+            np.save(a.dump, np.stack([y.view(torch.int16).cpu().numpy() if y.dtype == torch.bfloat16
+                                      else y.view(torch.int32).cpu().numpy() for y in ys]))
+            step.dumped = True
         for r in range(G):
             report = {"rank": r, "T": counts[r]}
             xr = x_all[:, :counts[r]] if xs is None else xs
