@@ -278,17 +278,23 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
                         sr_cfg_.value_width_bits, sr_cfg_.per_matrix_budget ? 1 : 0};
         if (hep_sr_wire_bytes(H_, F_, &c, &wb) != HEP_OK) throw std::invalid_argument(hep_last_error());
         patch_kmax_ = std::max<size_t>(1, (wb - 28) / 8);
-        const size_t rp = static_cast<size_t>(H_ + F_ + 1);
-        patch_words_.alloc(sizeof(uint32_t) * patch_kmax_ * slots_);
-        patch_rowptr_.alloc(sizeof(int) * rp * slots_);
+        patch_slot_bytes_ = static_cast<size_t>(patch_blocks(F_, H_) + patch_blocks(H_, F_)) * kPatchBlockBytes;
+        patch_blocks_.alloc(patch_slot_bytes_ * slots_);
+        patch_ovf_.alloc(sizeof(uint2) * patch_kmax_ * slots_);
+        patch_ovf_n_.alloc(sizeof(int) * slots_);
         std::vector<PatchRef> refs(static_cast<size_t>(slots_));
-        for (int64_t sl = 0; sl < slots_; ++sl)
-          refs[static_cast<size_t>(sl)] = PatchRef{patch_words_.as<uint32_t>() + sl * patch_kmax_,
-                                                   patch_rowptr_.as<int>() + sl * rp, sr_status_.as<int32_t>() + 4 * sl};
+        for (int64_t sl = 0; sl < slots_; ++sl) {
+          const uint8_t* base = patch_blocks_.as<uint8_t>() + sl * patch_slot_bytes_;
+          refs[static_cast<size_t>(sl)] =
+              PatchRef{{base, base + static_cast<size_t>(patch_blocks(F_, H_)) * kPatchBlockBytes},
+                       patch_ovf_.as<uint2>() + sl * patch_kmax_, patch_ovf_n_.as<int>() + sl,
+                       sr_status_.as<int32_t>() + 4 * sl};
+        }
         patch_refs_.alloc(sizeof(PatchRef) * slots_);
         ck(cudaMemcpy(patch_refs_.p, refs.data(), sizeof(PatchRef) * slots_, cudaMemcpyHostToDevice), "patch refs");
-        ck(make_tmap_bf16_2d(&map_shared_up_, shared_c_.p, F_, H_, 256, 64), "tmap shared up");
-        ck(make_tmap_bf16_2d(&map_shared_down_, shared_c_.as<uint8_t>() + 2 * H_ * F_, H_, F_, 256, 64),
+        const uint32_t box = cta_pair_ ? 128 : 256;
+        ck(make_tmap_bf16_2d(&map_shared_up_, shared_c_.p, F_, H_, box, 64), "tmap shared up");
+        ck(make_tmap_bf16_2d(&map_shared_down_, shared_c_.as<uint8_t>() + 2 * H_ * F_, H_, F_, box, 64),
            "tmap shared down");
       }
     } else {
@@ -853,10 +859,10 @@ void Layer::sgd_step(const float* const* grads, int n, float lr, cudaStream_t s)
 }
 
 void Layer::index_gathered(size_t wb, size_t stride, cudaStream_t s) {
-  // Fused decode: each gathered wire -> its slot's patch list (validated like the decode);
-  // the gathered experts' GEMMs read the shared expert and apply the patches in-kernel.
+  // Fused decode: each gathered wire -> its slot's per-stage patch blocks (validated like
+  // the decode); the gathered experts' GEMMs read the shared expert and apply the patches
+  // in-kernel.
   uint8_t* wires = wires_.as<uint8_t>();
-  const size_t rp = static_cast<size_t>(H_ + F_ + 1);
   auto first_slot_of = [&](int64_t owner) { return slot_of_expert_[static_cast<size_t>(owner * n_)]; };
   bool corrupt = corrupt_next_;
   corrupt_next_ = false;
@@ -867,17 +873,19 @@ void Layer::index_gathered(size_t wb, size_t stride, cudaStream_t s) {
       corrupt = false;
     }
     std::vector<const uint8_t*> wi;
-    std::vector<uint32_t*> words;
-    std::vector<int*> rows;
+    std::vector<uint8_t*> blocks;
+    std::vector<uint2*> ovf;
+    std::vector<int*> ovf_n;
     for (int64_t i = 0; i < n_; ++i) {
       const int64_t sl = first + i;
       wi.push_back(wires + stride * sl);
-      words.push_back(patch_words_.as<uint32_t>() + sl * patch_kmax_);
-      rows.push_back(patch_rowptr_.as<int>() + sl * rp);
+      blocks.push_back(patch_blocks_.as<uint8_t>() + sl * patch_slot_bytes_);
+      ovf.push_back(patch_ovf_.as<uint2>() + sl * patch_kmax_);
+      ovf_n.push_back(patch_ovf_n_.as<int>() + sl);
     }
     int32_t* st = sr_status_.as<int32_t>() + 4 * first;
-    ck(launch_sr_patch_index(wi.data(), static_cast<int>(n_), wb, shared_.as<float>(), H_, F_, words.data(),
-                             rows.data(), st, s), "patch index");
+    ck(launch_sr_patch_index(wi.data(), static_cast<int>(n_), wb, shared_.as<float>(), H_, F_, blocks.data(),
+                             ovf.data(), ovf_n.data(), st, s), "patch index");
     ck(launch_sr_status_fold(st, static_cast<int>(n_), mig_err_dev_, s), "decode status");
   }
 }
@@ -1040,13 +1048,15 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
   if (dt_ == DType::BF16 && patched) {
     // gathered SR experts: decode fused into the B-operand load (shared expert + patches)
     const PatchRef* refs = patch_refs_.as<PatchRef>();
+    auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta_patched : launch_grouped_gemm_bf16_patched;
+    const uint32_t sched = cta_pair_ ? 0x2u : 0x8u;  // the shared B is re-read by every group: keep A resident
     mark(up.c_str(), s);
-    ck(launch_grouped_gemm_bf16_patched(map_a1_, map_shared_up_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_),
-                                        static_cast<int>(H_), gt, refs, 0, 1, num_sms_, s),
+    ck(gemm(map_a1_, map_shared_up_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt,
+            refs, 0, 1, num_sms_, s, sched),
        "gemm up (fused decode)");
     mark(down.c_str(), s);
-    ck(launch_grouped_gemm_bf16_patched(map_a2_, map_shared_down_, oall_.p, static_cast<int>(H_), static_cast<int>(H_),
-                                        static_cast<int>(F_), gt_down, refs, static_cast<int>(H_), 0, num_sms_, s),
+    ck(gemm(map_a2_, map_shared_down_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_),
+            gt_down, refs, 1, 0, num_sms_, s, sched),
        "gemm down (fused decode)");
   } else if (dt_ == DType::BF16) {
     mark(up.c_str(), s);

@@ -134,8 +134,8 @@ class Layer {
   // applied inside the GEMM's B-operand load instead of dense decoded compute copies.
   void index_gathered(size_t wire_bytes, size_t stride, cudaStream_t s);
   bool sr_fused_ = false;
-  DevBuf patch_words_, patch_rowptr_, patch_refs_;
-  size_t patch_kmax_ = 0;
+  DevBuf patch_blocks_, patch_ovf_, patch_ovf_n_, patch_refs_;
+  size_t patch_kmax_ = 0, patch_slot_bytes_ = 0;
   CUtensorMap map_shared_up_, map_shared_down_;
   void decode_gathered(size_t wire_bytes, size_t stride, cudaStream_t s);
   void step(const void* x, int64_t T, void* y, cudaStream_t s);  // forward's enqueue

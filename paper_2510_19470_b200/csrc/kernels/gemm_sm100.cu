@@ -53,6 +53,7 @@ struct SmemCtl {
 };
 
 constexpr size_t kSmemBytes = 1024 + STAGES * STAGE_BYTES + sizeof(SmemCtl);
+constexpr size_t kSmemBytesPatch = kSmemBytes + STAGES * kPatchBlockBytes;  // + the staged patch blocks
 
 __device__ __forceinline__ uint64_t make_policy(uint32_t p) {
   uint64_t pol;
@@ -126,13 +127,14 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                          const int* __restrict__ g_rows, const int* __restrict__ g_slot,
                          const unsigned long long* __restrict__ g_out, const int* __restrict__ g_wait,
                          const uint32_t* __restrict__ wait_flags, uint32_t epoch, int ng, int relu,
-                         uint32_t sched, uint64_t timeout_ns, const PatchRef* __restrict__ patches, int row_base) {
+                         uint32_t sched, uint64_t timeout_ns, const PatchRef* __restrict__ patches, int half) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* stage_a = smem;
   uint8_t* stage_b = smem + STAGES * A_BYTES;
-  SmemCtl& s = *reinterpret_cast<SmemCtl*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* stage_p = smem + STAGES * STAGE_BYTES;  // PATCH: one patch block per stage
+  SmemCtl& s = *reinterpret_cast<SmemCtl*>(smem + STAGES * STAGE_BYTES + (PATCH ? STAGES * kPatchBlockBytes : 0));
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -201,30 +203,25 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
       const int m_tiles = (s.rows[g] + BM - 1) / BM;
       int mt, nt;
       decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
-      const PatchRef pr = patches[s.slot[g]];
+      const PatchRef& pr = patches[s.slot[g]];
       const bool ok = *pr.status == 0;  // a rejected wire is reported by the layer, never applied
-      const int c0 = nt * BN, c1 = min(c0 + BN, N);
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&s.full[stage], phase);
         if (ok) {
           uint8_t* bst = stage_b + stage * B_BYTES;
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            const int rr = lane + 32 * half;  // K column of the tile = reference row
-            const int row = row_base + kb * BK + rr;
-            int lo = __ldg(pr.row_ptr + row), hi = __ldg(pr.row_ptr + row + 1);
-            while (lo < hi) {  // first entry of the row with column >= c0
-              const int mid = (lo + hi) >> 1;
-              if (static_cast<int>(__ldg(pr.words + mid) >> 16) < c0) lo = mid + 1; else hi = mid;
-            }
-            const int end = __ldg(pr.row_ptr + row + 1);
-            for (int j = lo; j < end; ++j) {
-              const uint32_t w = __ldg(pr.words + j);
-              const int r = static_cast<int>(w >> 16) - c0;
-              if (r >= c1 - c0) break;
-              // SW128: 16-byte chunk (rr / 8) of row r sits at chunk (rr / 8) ^ (r % 8)
-              const int byte = r * 128 + ((((rr >> 3) ^ (r & 7))) << 4) + ((rr & 7) << 1);
-              *reinterpret_cast<uint16_t*>(bst + byte) = static_cast<uint16_t>(w & 0xffffu);
+          const uint32_t* blk = reinterpret_cast<const uint32_t*>(stage_p + stage * kPatchBlockBytes);
+          const int cnt = static_cast<int>(blk[0]);
+          const int n = min(cnt, kPatchBlockCap);
+          for (int j = lane; j < n; j += 32) {
+            const uint32_t w = blk[4 + j];
+            *reinterpret_cast<uint16_t*>(bst + ((w >> 16) << 1)) = static_cast<uint16_t>(w & 0xffffu);
+          }
+          if (cnt > kPatchBlockCap) {  // overflowed block: the rest from the global list (rare)
+            const uint32_t id = static_cast<uint32_t>(nt * num_kb + kb) | (static_cast<uint32_t>(half) << 31);
+            const int no = *pr.ovf_count;
+            for (int q = lane; q < no; q += 32) {
+              const uint2 e = pr.ovf[q];
+              if (e.x == id) *reinterpret_cast<uint16_t*>(bst + ((e.y >> 16) << 1)) = static_cast<uint16_t>(e.y & 0xffffu);
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -251,12 +248,17 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
         const int a_row = s.row_start[g] + mt * BM;
         const int b_row = (PATCH ? 0 : s.slot[g] * N) + nt * BN;  // PATCH: the shared expert
+        const uint8_t* pblk = PATCH ? patches[s.slot[g]].blocks[half] +
+                                          static_cast<size_t>(nt) * num_kb * kPatchBlockBytes : nullptr;
         if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch, timeout_ns);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&s.full[stage], STAGE_BYTES);
+          mbar_arrive_expect_tx(&s.full[stage], STAGE_BYTES + (PATCH ? kPatchBlockBytes : 0));
           tma_load_2d(stage_a + stage * A_BYTES, &map_a, &s.full[stage], kb * BK, a_row, pol_a);
           tma_load_2d(stage_b + stage * B_BYTES, &map_b, &s.full[stage], kb * BK, b_row, pol_b);
+          if (PATCH)
+            bulk_load(stage_p + stage * kPatchBlockBytes, pblk + static_cast<size_t>(kb) * kPatchBlockBytes,
+                      kPatchBlockBytes, &s.full[stage], pol_b);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -370,6 +372,8 @@ constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 struct SmemCtl2 {
   uint64_t full[P_STAGES];
   uint64_t empty[P_STAGES];
+  uint64_t bfull[P_STAGES];    // PATCH: this CTA's B half + patch block landed (local)
+  uint64_t patched[P_STAGES];  // PATCH (leader): both CTAs' B halves patched
   uint64_t tfull[ACC];
   uint64_t tempty[ACC];
   uint32_t tmem_base;
@@ -383,6 +387,13 @@ struct SmemCtl2 {
 };
 
 constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + P_STG_BYTES + sizeof(SmemCtl2);
+constexpr size_t kSmemBytes2Patch = kSmemBytes2 + P_STAGES * kPatchBlockBytes;
+
+// Release-arrive at cluster scope on the leader CTA's copy of `bar`: orders this thread's
+// (fenced) shared-memory writes before the leader's acquire of the barrier.
+__device__ __forceinline__ void mbar_arrive_leader_cluster(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_smem_addr(bar)) : "memory");
+}
 
 __device__ __forceinline__ int find_group2(const SmemCtl2& s, int ng, int tile) {
   int lo = 0, hi = ng - 1;
@@ -393,20 +404,29 @@ __device__ __forceinline__ int find_group2(const SmemCtl2& s, int ng, int tile) 
   return lo;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// PATCH = true: the fused SR decode on the CTA pair.  B is the shared expert; each CTA's
+// B half and the stage's patch block land on a LOCAL barrier (bfull), the CTA's converter
+// warp (warp 6) writes the entries that fall in its half, fences them into the async
+// proxy and release-arrives on the leader's `patched` barrier (count 2); the leader's MMA
+// waits for the A halves (full) and for both patched halves.
+template <bool PATCH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (PATCH ? 32 : 0), 1)
 grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                               __nv_bfloat16* __restrict__ C, int ldc, int N, int K,
                               const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
                               const int* __restrict__ g_slot, const unsigned long long* __restrict__ g_out,
                               const int* __restrict__ g_wait, const uint32_t* __restrict__ wait_flags,
-                              uint32_t epoch, int ng, int relu, uint32_t sched, uint64_t timeout_ns) {
+                              uint32_t epoch, int ng, int relu, uint32_t sched, uint64_t timeout_ns,
+                              const PatchRef* __restrict__ patches, int half) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* stage_a = smem;
   uint8_t* stage_b = smem + P_STAGES * P_A_BYTES;
   uint8_t* stage_out = smem + P_STAGES * P_STAGE_BYTES;
-  SmemCtl2& s = *reinterpret_cast<SmemCtl2*>(smem + P_STAGES * P_STAGE_BYTES + P_STG_BYTES);
+  uint8_t* stage_p = stage_out + P_STG_BYTES;  // PATCH: one patch block per stage
+  SmemCtl2& s = *reinterpret_cast<SmemCtl2*>(smem + P_STAGES * P_STAGE_BYTES + P_STG_BYTES +
+                                             (PATCH ? P_STAGES * kPatchBlockBytes : 0));
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -449,6 +469,8 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
     for (int i = 0; i < P_STAGES; ++i) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
+      mbar_init(&s.bfull[i], 1);
+      mbar_init(&s.patched[i], 2);  // one converter per CTA
     }
     for (int i = 0; i < ACC; ++i) {
       mbar_init(&s.tfull[i], 1);
@@ -464,6 +486,52 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
 
   const int total = s.num_tiles;
   const uint32_t tmem_base = s.tmem_base;
+
+  if (PATCH && warp == 6) {
+    // ================= converter (fused SR decode), both CTAs =================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = cluster; tile < total; tile += nclusters) {
+      const int g = find_group2(s, ng, tile);
+      const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
+      int mt, nt;
+      decode_tile(tile - s.tile_start[g], m_tiles, n_tiles, sched, mt, nt);
+      const PatchRef& pr = patches[s.slot[g]];
+      const bool ok = *pr.status == 0;
+      // rows of the 256-row B tile held here: [split * cta, split * cta + split)
+      const int split = N - nt * P_BN <= P_BN / 2 ? 64 : 128;
+      const uint32_t lo_byte = static_cast<uint32_t>(split * 128) * cta, hi_byte = lo_byte + split * 128;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&s.bfull[stage], phase);
+        if (ok) {
+          uint8_t* bst = stage_b + stage * P_B_BYTES;
+          const uint32_t* blk = reinterpret_cast<const uint32_t*>(stage_p + stage * kPatchBlockBytes);
+          const int cnt = static_cast<int>(blk[0]);
+          const int n = min(cnt, kPatchBlockCap);
+          for (int j = lane; j < n; j += 32) {
+            const uint32_t w = blk[4 + j];
+            const uint32_t off = (w >> 16) << 1;  // byte in the 256-row swizzled tile
+            if (off >= lo_byte && off < hi_byte)
+              *reinterpret_cast<uint16_t*>(bst + (off - lo_byte)) = static_cast<uint16_t>(w & 0xffffu);
+          }
+          if (cnt > kPatchBlockCap) {  // overflowed block: the rest from the global list (rare)
+            const uint32_t id = static_cast<uint32_t>(nt * num_kb + kb) | (static_cast<uint32_t>(half) << 31);
+            const int no = *pr.ovf_count;
+            for (int q = lane; q < no; q += 32) {
+              const uint2 e = pr.ovf[q];
+              const uint32_t off = (e.y >> 16) << 1;
+              if (e.x == id && off >= lo_byte && off < hi_byte)
+                *reinterpret_cast<uint16_t*>(bst + (off - lo_byte)) = static_cast<uint16_t>(e.y & 0xffffu);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader_cluster(&s.patched[stage]);
+        if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  }
 
   if (warp == 0) {
     // ================= TMA producer (both CTAs) =================
@@ -482,13 +550,25 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
         // a tail n-tile of <= 128 columns runs as an N=128 MMA: each CTA supplies 64 B rows
         // (the first 64 of its 128-row box)
         const int b_half = N - nt * P_BN <= P_BN / 2 ? 64 : 128;
-        const int b_row = s.slot[g] * N + nt * P_BN + b_half * static_cast<int>(cta);
+        const int b_row = (PATCH ? 0 : s.slot[g] * N) + nt * P_BN + b_half * static_cast<int>(cta);
+        const uint8_t* pblk = PATCH ? patches[s.slot[g]].blocks[half] +
+                                          static_cast<size_t>(nt) * num_kb * kPatchBlockBytes : nullptr;
         if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch, timeout_ns);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
-          if (cta == 0) mbar_arrive_expect_tx(&s.full[stage], 2 * P_STAGE_BYTES);
-          tma_load_2d_2sm(stage_a + stage * P_A_BYTES, &map_a, &s.full[stage], kb * BK, a_row, pol_a);
-          tma_load_2d_2sm(stage_b + stage * P_B_BYTES, &map_b, &s.full[stage], kb * BK, b_row, pol_b);
+          if (PATCH) {
+            // A halves on the leader's barrier; this CTA's B half + patch block on its own
+            if (cta == 0) mbar_arrive_expect_tx(&s.full[stage], 2 * P_A_BYTES);
+            mbar_arrive_expect_tx(&s.bfull[stage], P_B_BYTES + kPatchBlockBytes);
+            tma_load_2d_2sm(stage_a + stage * P_A_BYTES, &map_a, &s.full[stage], kb * BK, a_row, pol_a);
+            tma_load_2d(stage_b + stage * P_B_BYTES, &map_b, &s.bfull[stage], kb * BK, b_row, pol_b);
+            bulk_load(stage_p + stage * kPatchBlockBytes, pblk + static_cast<size_t>(kb) * kPatchBlockBytes,
+                      kPatchBlockBytes, &s.bfull[stage], pol_b);
+          } else {
+            if (cta == 0) mbar_arrive_expect_tx(&s.full[stage], 2 * P_STAGE_BYTES);
+            tma_load_2d_2sm(stage_a + stage * P_A_BYTES, &map_a, &s.full[stage], kb * BK, a_row, pol_a);
+            tma_load_2d_2sm(stage_b + stage * P_B_BYTES, &map_b, &s.full[stage], kb * BK, b_row, pol_b);
+          }
           if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -513,6 +593,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * P_BN);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.full[stage], phase);
+          if (PATCH) mbar_wait(&s.patched[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_addr(stage_a + stage * P_A_BYTES);
           const uint32_t b_addr = smem_addr(stage_b + stage * P_B_BYTES);
@@ -527,7 +608,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
         if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else {
+  } else if (warp >= 2 && warp <= 5) {
     // ================= epilogue (warps 2..5, both CTAs) =================
     const uint32_t quarter = warp & 3u;
     uint8_t* stg = stage_out + quarter * 32 * P_STG_PITCH;  // this warp's 32 staged rows
@@ -1041,20 +1122,20 @@ cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap
 
 cudaError_t launch_grouped_gemm_bf16_patched(const CUtensorMap& map_a, const CUtensorMap& map_shared_b, void* C,
                                              int ldc, int N, int K, const GroupTable& groups, const PatchRef* patches,
-                                             int row_base, int relu, int num_sms, cudaStream_t stream, uint32_t sched) {
+                                             int half, int relu, int num_sms, cudaStream_t stream, uint32_t sched) {
   if (K % BK || N % 32 || N > 65535 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
     return cudaErrorInvalidValue;
   static DeviceOnce attr_set;
   if (!attr_set.done()) {
     const cudaError_t e = cudaFuncSetAttribute(
-        grouped_gemm_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+        grouped_gemm_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytesPatch));
     if (e != cudaSuccess) return e;
     attr_set.set();
   }
-  grouped_gemm_bf16_kernel<true><<<num_sms, kThreads + 32, kSmemBytes, stream>>>(
+  grouped_gemm_bf16_kernel<true><<<num_sms, kThreads + 32, kSmemBytesPatch, stream>>>(
       map_a, map_shared_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
       groups.slot, groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched,
-      groups.timeout_ns, patches, row_base);
+      groups.timeout_ns, patches, half);
   return cudaGetLastError();
 }
 
@@ -1064,16 +1145,39 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
   if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0) return cudaErrorInvalidValue;
   static DeviceOnce attr_set;
   if (!attr_set.done()) {
-    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel,
+    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(kSmemBytes2));
     if (e != cudaSuccess) return e;
     attr_set.set();
   }
   const int grid = (num_sms / 2) * 2;
-  grouped_gemm_bf16_2cta_kernel<<<grid, kThreads, kSmemBytes2, stream>>>(
+  grouped_gemm_bf16_2cta_kernel<false><<<grid, kThreads, kSmemBytes2, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
-      groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns);
+      groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
+      nullptr, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, const CUtensorMap& map_shared_b, void* C,
+                                                  int ldc, int N, int K, const GroupTable& groups,
+                                                  const PatchRef* patches, int half, int relu, int num_sms,
+                                                  cudaStream_t stream, uint32_t sched) {
+  if (K % BK || N % 32 || N > 65535 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
+    return cudaErrorInvalidValue;
+  static DeviceOnce attr_set;
+  if (!attr_set.done()) {
+    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(kSmemBytes2Patch));
+    if (e != cudaSuccess) return e;
+    attr_set.set();
+  }
+  const int grid = (num_sms / 2) * 2;
+  grouped_gemm_bf16_2cta_kernel<true><<<grid, kThreads + 32, kSmemBytes2Patch, stream>>>(
+      map_a, map_shared_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
+      groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
+      patches, half);
   return cudaGetLastError();
 }
 
@@ -1086,7 +1190,8 @@ cudaError_t preload_gemm_sm100_kernels() {
   };
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel<false>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel<true>))) return e;
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<true>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(ksplit_reduce_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(split_tf32_kernel))) return e;

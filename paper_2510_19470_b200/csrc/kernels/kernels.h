@@ -103,21 +103,35 @@ cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows,
 cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C,
                                      int ldc, int N, int K, const GroupTable& groups, int relu,
                                      int num_sms, cudaStream_t stream, uint32_t sched = 0x8u);
-// SR decode fused into the B-operand load (1-CTA kernel + converter warp): per weight slot,
-// the migrated expert's residual patch list in the GEMM layout (sr_patch_index).  Rows are
-// the reference-layout rows of w_up (0 .. h-1, columns 0 .. m-1) then of w_down (h .. h+m-1,
-// columns 0 .. h-1); words = (column << 16) | bf16 patched value, sorted by column in a row.
+// SR decode fused into the B-operand load (1-CTA kernel + converter warp).  A migrated
+// expert's residuals are pre-sorted (sr_patch_index) into one 2 KB block per B stage of the
+// GEMM -- (n-tile, k-block) of the up [m x h] or down [h x m] compute layout -- holding the
+// patched bf16 values and their byte offsets inside the 128-byte-swizzled B tile.  The
+// TMA producer stages the block with the tile; the converter warp applies it from shared
+// memory.  Entries beyond a block's capacity go to an overflow list (rare; read from global).
+constexpr int kPatchBlockBytes = 2048;
+constexpr int kPatchBlockCap = kPatchBlockBytes / 4 - 4;  // words after a 16-byte header
 struct PatchRef {
-  const uint32_t* words;
-  const int* row_ptr;   // [h + m + 1]
-  const int32_t* status;  // the wire's decode status (non-zero: leave the shared values)
+  const uint8_t* blocks[2];   // up, down: [n_tiles][num_kb] blocks of kPatchBlockBytes
+  const uint2* ovf;           // (block id | half << 31, word) pairs
+  const int* ovf_count;
+  const int32_t* status;      // the wire's decode status (non-zero: leave the shared values)
 };
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int64_t patch_blocks(int64_t N, int64_t K) { return ((N + 255) / 256) * (K / 64); }
 // B = the shared expert's compute copy (map_shared_b: the up [m x h] or down [h x m] half,
-// box 256 x 64); row_base = 0 for the up-projection, h for the down-projection.
+// box 256 x 64); half = 0 for the up-projection, 1 for the down-projection.
 cudaError_t launch_grouped_gemm_bf16_patched(const CUtensorMap& map_a, const CUtensorMap& map_shared_b, void* C,
                                              int ldc, int N, int K, const GroupTable& groups, const PatchRef* patches,
-                                             int row_base, int relu, int num_sms, cudaStream_t stream,
+                                             int half, int relu, int num_sms, cudaStream_t stream,
                                              uint32_t sched = 0x8u);
+// The same on the CTA pair (map_shared_b box 128 x 64).
+cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, const CUtensorMap& map_shared_b, void* C,
+                                                  int ldc, int N, int K, const GroupTable& groups,
+                                                  const PatchRef* patches, int half, int relu, int num_sms,
+                                                  cudaStream_t stream, uint32_t sched = 0x6u);
 // CTA-pair variant (cta_group::2, 256x256 cluster tiles); B's tensor map box is 128 rows.
 cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C, int ldc,
                                           int N, int K, const GroupTable& groups, int relu, int num_sms,
@@ -193,11 +207,12 @@ cudaError_t launch_sr_decode_layout_batch(const uint8_t* const* wires, int batch
                                           int64_t m, void* const* up, void* const* down, int32_t* status,
                                           cudaStream_t stream);
 // The fused decode's index pass over `batch` gathered wires: validates each wire like the
-// decode (status int32[4] per wire) and writes its patch list (PatchRef layout: words[k],
-// row_ptr[h + m + 1]) with the final bf16 values bf16((float)((double)shared[i] + v)).
+// decode (status int32[4] per wire) and sorts its entries into the per-stage patch blocks
+// (PatchRef layout; blocks[b] = up blocks then down blocks, ovf[b] / ovf_count[b] the
+// overflow) with the final bf16 values bf16((float)((double)shared[i] + v)).
 cudaError_t launch_sr_patch_index(const uint8_t* const* wires, int batch, size_t wire_bytes, const float* shared,
-                                  int64_t h, int64_t m, uint32_t* const* words, int* const* row_ptr, int32_t* status,
-                                  cudaStream_t stream);
+                                  int64_t h, int64_t m, uint8_t* const* blocks, uint2* const* ovf,
+                                  int* const* ovf_count, int32_t* status, cudaStream_t stream);
 // err := (code | entry << 8) of the first failed wire of a decode batch, if err is still 0.
 cudaError_t launch_sr_status_fold(const int32_t* status, int n, int32_t* err, cudaStream_t stream);
 // out = mean over experts (fp64 accumulate in list order, times 1/n, round to fp32).

@@ -1791,14 +1791,31 @@ cudaError_t launch_sr_decode_batch(const uint8_t* const* wires, int batch, size_
 namespace {
 struct PatchBatch {
   const uint8_t* wire[kMaxSrBatch];
-  uint32_t* words[kMaxSrBatch];
-  int* row_ptr[kMaxSrBatch];
+  uint8_t* blocks[kMaxSrBatch];
+  uint2* ovf[kMaxSrBatch];
+  int* ovf_count[kMaxSrBatch];
 };
 
-// grid (blocks, batch): thread j < k validates entry j like the decode (first failing entry
-// wins: status word 2-3 as in sr_decode_scatter) and writes its patch word
-// (column << 16) | bf16((float)((double)shared[i] + v)); thread r <= h + m writes row_ptr[r]
-// = first entry of reference row r (binary search over the sorted indices).
+__global__ void sr_patch_reset_kernel(PatchBatch pb, int64_t nblocks, int32_t* status, int n) {
+  const int b = blockIdx.y;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nblocks;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    *reinterpret_cast<uint32_t*>(pb.blocks[b] + i * kPatchBlockBytes) = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *pb.ovf_count[b] = 0;
+    if (b < n) {
+      status[4 * b] = 0;
+      status[4 * b + 1] = 0;
+      *reinterpret_cast<unsigned long long*>(status + 4 * b + 2) = ~0ull;
+    }
+  }
+}
+
+// grid (blocks, batch): thread j < k validates entry j like the decode (first failing
+// entry wins, as in sr_decode_scatter) and files it into the patch block of the GEMM stage
+// that loads its B element: up entry (row r < h, column c < m) is B[c][r] of the up
+// projection (n = c, k = r), down entry (f, c) is B[c][f] of the down projection.  The
+// value is the dense decode's: bf16((float)((double)shared[i] + v)).
 __global__ void __launch_bounds__(256) sr_patch_index_kernel(PatchBatch pb, size_t bytes,
                                                              const float* __restrict__ shared, int64_t h,
                                                              int64_t m, int32_t* status) {
@@ -1806,65 +1823,63 @@ __global__ void __launch_bounds__(256) sr_patch_index_kernel(PatchBatch pb, size
   const uint8_t* wire = pb.wire[b];
   int code;
   const WireView v = read_header(wire, bytes, h, m, &code);
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t up = h * m, P = 2 * up, rows = h + m;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (!v.ok_header) {
-    if (t == 0) status[4 * b] = code;
-    if (t <= rows) pb.row_ptr[b][t] = 0;  // nothing to apply
+    if (j == 0) status[4 * b] = code;
     return;
   }
-  if (t < v.k) {
-    const uint64_t idx = entry_index(wire, v, t);
-    int c = 0;
-    if (idx >= static_cast<uint64_t>(P)) c = 5;
-    else if (t > 0 && idx <= entry_index(wire, v, t - 1)) c = 6;
-    if (c) {
-      atomicMin(reinterpret_cast<unsigned long long*>(status + 4 * b + 2),
-                static_cast<unsigned long long>(t) * 8ull + static_cast<unsigned long long>(c));
-    } else {
-      const int64_t i = static_cast<int64_t>(idx);
-      const int64_t col = i < up ? i % m : (i - up) % h;
-      const float val = __double2float_rn(__dadd_rn(static_cast<double>(shared[i]), entry_value(wire, v, t)));
-      const uint32_t bf = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(val)));
-      pb.words[b][t] = (static_cast<uint32_t>(col) << 16) | bf;
-    }
+  if (j >= v.k) return;
+  const int64_t up = h * m, P = 2 * up;
+  const uint64_t idx = entry_index(wire, v, j);
+  int c = 0;
+  if (idx >= static_cast<uint64_t>(P)) c = 5;
+  else if (j > 0 && idx <= entry_index(wire, v, j - 1)) c = 6;
+  if (c) {
+    atomicMin(reinterpret_cast<unsigned long long*>(status + 4 * b + 2),
+              static_cast<unsigned long long>(j) * 8ull + static_cast<unsigned long long>(c));
+    return;
   }
-  if (t <= rows) {
-    const int64_t start = t < h ? t * m : (t < rows ? up + (t - h) * h : P);
-    int64_t lo = 0, hi = v.k;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (static_cast<int64_t>(entry_index(wire, v, mid)) < start) lo = mid + 1; else hi = mid;
-    }
-    pb.row_ptr[b][t] = static_cast<int>(lo);
-  }
-}
-
-__global__ void sr_patch_status_init_kernel(int32_t* status, int n) {
-  const int b = threadIdx.x;
-  if (b < n) {
-    status[4 * b] = 0;
-    status[4 * b + 1] = 0;
-    *reinterpret_cast<unsigned long long*>(status + 4 * b + 2) = ~0ull;
+  const int64_t i = static_cast<int64_t>(idx);
+  const int half = i < up ? 0 : 1;
+  const int64_t N = half ? h : m, K = half ? m : h;    // B is N x K for this projection
+  const int64_t row = half ? (i - up) / h : i / m;      // reference row = k
+  const int64_t col = half ? (i - up) % h : i % m;      // reference column = n
+  const int64_t nt = col / 256, kb = row / 64;
+  const int r = static_cast<int>(col % 256), rr = static_cast<int>(row % 64);
+  const uint32_t byte = static_cast<uint32_t>(r * 128 + ((((rr >> 3) ^ (r & 7))) << 4) + ((rr & 7) << 1));
+  const float val = __double2float_rn(__dadd_rn(static_cast<double>(shared[i]), entry_value(wire, v, j)));
+  const uint32_t word = ((byte >> 1) << 16) | static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(val)));
+  const int64_t blk = (half ? patch_blocks(m, h) : 0) + nt * (K / 64) + kb;
+  (void)N;
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(pb.blocks[b] + blk * kPatchBlockBytes);
+  const uint32_t pos = atomicAdd(hdr, 1u);
+  if (pos < static_cast<uint32_t>(kPatchBlockCap)) {
+    hdr[4 + pos] = word;
+  } else {
+    const int q = atomicAdd(pb.ovf_count[b], 1);
+    pb.ovf[b][q] = make_uint2(static_cast<uint32_t>(blk - (half ? patch_blocks(m, h) : 0)) |
+                                  (static_cast<uint32_t>(half) << 31), word);
   }
 }
 }  // namespace
 
 cudaError_t launch_sr_patch_index(const uint8_t* const* wires, int batch, size_t wire_bytes, const float* shared,
-                                  int64_t h, int64_t m, uint32_t* const* words, int* const* row_ptr, int32_t* status,
-                                  cudaStream_t stream) {
-  if (batch <= 0 || batch > kMaxSrBatch || h > 65535 || m > 65535) return cudaErrorInvalidValue;
+                                  int64_t h, int64_t m, uint8_t* const* blocks, uint2* const* ovf,
+                                  int* const* ovf_count, int32_t* status, cudaStream_t stream) {
+  if (batch <= 0 || batch > kMaxSrBatch || h % 64 || m % 64) return cudaErrorInvalidValue;
   PatchBatch pb{};
   for (int i = 0; i < batch; ++i) {
     pb.wire[i] = wires[i];
-    pb.words[i] = words[i];
-    pb.row_ptr[i] = row_ptr[i];
+    pb.blocks[i] = blocks[i];
+    pb.ovf[i] = ovf[i];
+    pb.ovf_count[i] = ovf_count[i];
   }
+  const int64_t nblocks = patch_blocks(m, h) + patch_blocks(h, m);
+  sr_patch_reset_kernel<<<dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, (nblocks + 255) / 256))),
+                             batch), 256, 0, stream>>>(pb, nblocks, status, batch);
   const int64_t kmax = wire_bytes > 28 ? static_cast<int64_t>((wire_bytes - 28) / 8) : 0;
-  const int64_t n = std::max<int64_t>(kmax, h + m + 1);
-  const int blocks = static_cast<int>(std::max<int64_t>(1, (n + 255) / 256));
-  sr_patch_status_init_kernel<<<1, kMaxSrBatch, 0, stream>>>(status, batch);
-  sr_patch_index_kernel<<<dim3(blocks, batch), 256, 0, stream>>>(pb, wire_bytes, shared, h, m, status);
+  const int blocks_k = static_cast<int>(std::max<int64_t>(1, (kmax + 255) / 256));
+  sr_patch_index_kernel<<<dim3(blocks_k, batch), 256, 0, stream>>>(pb, wire_bytes, shared, h, m, status);
   sr_status_finalize_kernel<<<1, kMaxSrBatch, 0, stream>>>(status, batch);
   return cudaGetLastError();
 }
@@ -1968,7 +1983,7 @@ cudaError_t preload_sr_codec_kernels() {
   if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_status_fold_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(sgd_step_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_patch_index_kernel))) return e;
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_patch_status_init_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(sr_patch_reset_kernel))) return e;
   return cudaSuccess;
 }
 

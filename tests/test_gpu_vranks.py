@@ -72,17 +72,18 @@ def test_virtual_ranks_layer(sf, sed, extra):
     ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6"]),
     ([2], [2], ["--H", "2048", "--F", "1408", "--E", "8", "--T", "512"]),
 ], ids=lambda v: str(v))
-def test_fused_decode_gemm_inputs_bit_identical(sf, sed, extra, tmp_path):
+@pytest.mark.parametrize("pair", ["1", "0"], ids=["cta_pair", "single_cta"])
+def test_fused_decode_gemm_inputs_bit_identical(sf, sed, extra, pair, tmp_path):
     """SR decode fused into the GEMM's B-operand load vs the dense decode into compute
-    copies: with the same (1-CTA) GEMM for both, every rank's output is bit-identical, so
-    the patched B tiles equal the dense-decoded expert exactly."""
+    copies: with the same GEMM (CTA pair, or 1-CTA) for both, every rank's output is
+    bit-identical, so the patched B tiles equal the dense-decoded expert exactly."""
     outs = []
     for fused in ("1", "0"):
         dump = str(tmp_path / f"y_{fused}.npy")
         cmd = [sys.executable, os.path.join(HERE, "vrank_worker.py"), "--sf", *map(str, sf), "--sed", *map(str, sed),
                "--sr", "--dump", dump, *extra]
         env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", HEP_P2P_TIMEOUT_S="60", HEP_SR_FUSED=fused,
-                   HEP_GEMM_2CTA="0")
+                   HEP_GEMM_2CTA=pair)
         env.pop("HEP_COMM", None)
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=420, env=env)
         assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
