@@ -1047,7 +1047,9 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
   const std::string up = std::string("gemm_up") + tag, down = std::string("gemm_down") + tag;
   if (dt_ == DType::BF16 && patched) {
     // gathered SR experts: decode fused into the B-operand load (shared expert + patches)
-    const PatchRef* refs = patch_refs_.as<PatchRef>();
+    const PatchArgs refs{patch_blocks_.as<uint8_t>(), patch_slot_bytes_, 0, patch_refs_.as<PatchRef>()};
+    PatchArgs refs_down = refs;
+    refs_down.half_bytes = static_cast<size_t>(patch_blocks(F_, H_)) * kPatchBlockBytes;
     auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta_patched : launch_grouped_gemm_bf16_patched;
     const uint32_t sched = cta_pair_ ? 0x2u : 0x8u;  // the shared B is re-read by every group: keep A resident
     mark(up.c_str(), s);
@@ -1056,7 +1058,7 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
        "gemm up (fused decode)");
     mark(down.c_str(), s);
     ck(gemm(map_a2_, map_shared_down_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_),
-            gt_down, refs, 1, 0, num_sms_, s, sched),
+            gt_down, refs_down, 1, 0, num_sms_, s, sched),
        "gemm down (fused decode)");
   } else if (dt_ == DType::BF16) {
     mark(up.c_str(), s);

@@ -35,6 +35,10 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = ACC * BN;  // 512
 constexpr int kMaxGroups = 512;
 constexpr int kThreads = 192;
+// Fused SR decode: converter warps (warps 6 ..) take the B stages round-robin, so the
+// per-stage fixed latency (patch, proxy fence, barrier arrive) of one warp overlaps the
+// others' and the converters keep pace with the tensor core.
+constexpr int kConvWarps = 4;
 
 struct SmemCtl {
   uint64_t full[STAGES];
@@ -120,14 +124,14 @@ __device__ __forceinline__ int find_group(const SmemCtl& s, int ng, int tile) {
 // r)), the dense decode's exact values), fences them into the async proxy and releases
 // the stage to the MMA issuer -- so the decode never materialises a dense expert copy.
 template <bool PATCH>
-__global__ void __launch_bounds__(kThreads + (PATCH ? 32 : 0), 1)
+__global__ void __launch_bounds__(kThreads + (PATCH ? 32 * kConvWarps : 0), 1)
 grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_b, __nv_bfloat16* __restrict__ C,
                          int ldc, int N, int K, const int* __restrict__ g_row_start,
                          const int* __restrict__ g_rows, const int* __restrict__ g_slot,
                          const unsigned long long* __restrict__ g_out, const int* __restrict__ g_wait,
                          const uint32_t* __restrict__ wait_flags, uint32_t epoch, int ng, int relu,
-                         uint32_t sched, uint64_t timeout_ns, const PatchRef* __restrict__ patches, int half) {
+                         uint32_t sched, uint64_t timeout_ns, const PatchArgs patches, int half) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -193,21 +197,22 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
   const int total = s.num_tiles;
   const uint32_t tmem_base = s.tmem_base;
 
-  if (PATCH && warp == 6) {
-    // ================= converter (fused SR decode) =================
-    int stage = 0;
-    uint32_t phase = 0;
+  if (PATCH && warp >= 6) {
+    // ================= converters (fused SR decode) =================
+    const int wi = static_cast<int>(warp) - 6;
+    int c = 0;  // global stage counter: stage c % STAGES, phase (c / STAGES) & 1
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int g = find_group(s, ng, tile);
       const int local = tile - s.tile_start[g];
       const int m_tiles = (s.rows[g] + BM - 1) / BM;
       int mt, nt;
       decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
-      const PatchRef& pr = patches[s.slot[g]];
-      const bool ok = *pr.status == 0;  // a rejected wire is reported by the layer, never applied
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&s.full[stage], phase);
-        if (ok) {
+      const int slot = s.slot[g];
+      for (int kb = 0; kb < num_kb; ++kb, ++c) {
+        if (c % kConvWarps != wi) continue;
+        const int stage = c % STAGES;
+        mbar_wait(&s.full[stage], (c / STAGES) & 1);
+        {  // (a rejected wire's partial patch set is memory-safe; the layer raises the error)
           uint8_t* bst = stage_b + stage * B_BYTES;
           const uint32_t* blk = reinterpret_cast<const uint32_t*>(stage_p + stage * kPatchBlockBytes);
           const int cnt = static_cast<int>(blk[0]);
@@ -218,6 +223,7 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           }
           if (cnt > kPatchBlockCap) {  // overflowed block: the rest from the global list (rare)
             const uint32_t id = static_cast<uint32_t>(nt * num_kb + kb) | (static_cast<uint32_t>(half) << 31);
+            const PatchRef& pr = patches.patches[slot];
             const int no = *pr.ovf_count;
             for (int q = lane; q < no; q += 32) {
               const uint2 e = pr.ovf[q];
@@ -228,7 +234,6 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&s.patched[stage]);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   }
@@ -248,8 +253,9 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         decode_tile(local, m_tiles, n_tiles, sched, mt, nt);
         const int a_row = s.row_start[g] + mt * BM;
         const int b_row = (PATCH ? 0 : s.slot[g] * N) + nt * BN;  // PATCH: the shared expert
-        const uint8_t* pblk = PATCH ? patches[s.slot[g]].blocks[half] +
-                                          static_cast<size_t>(nt) * num_kb * kPatchBlockBytes : nullptr;
+        const uint8_t* pblk = PATCH ? patches.base + static_cast<size_t>(s.slot[g]) * patches.slot_bytes +
+                                          patches.half_bytes + static_cast<size_t>(nt) * num_kb * kPatchBlockBytes
+                                    : nullptr;
         if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch, timeout_ns);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
@@ -358,6 +364,8 @@ grouped_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
 constexpr int P_BM = 256;          // rows per cluster tile (128 per CTA)
 constexpr int P_BN = 256;
 constexpr int P_STAGES = 5;
+constexpr int P_STAGES_PATCH = 6;  // fused decode: the converter's latency needs one more stage in flight
+constexpr int P_STAGES_MAX = 6;
 // Epilogue staging: each epilogue warp assembles its 32 rows x 128 bf16 columns (half a
 // tile, twice per tile) in shared memory so global (and NVLink peer) stores go out as
 // whole 256-byte row segments instead of scattered 16-byte pieces; the half-width
@@ -370,10 +378,10 @@ constexpr int P_B_BYTES = 128 * BK * 2;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 
 struct SmemCtl2 {
-  uint64_t full[P_STAGES];
-  uint64_t empty[P_STAGES];
-  uint64_t bfull[P_STAGES];    // PATCH: this CTA's B half + patch block landed (local)
-  uint64_t patched[P_STAGES];  // PATCH (leader): both CTAs' B halves patched
+  uint64_t full[P_STAGES_MAX];
+  uint64_t empty[P_STAGES_MAX];
+  uint64_t bfull[P_STAGES_MAX];    // PATCH: this CTA's B half + patch block landed (local)
+  uint64_t patched[P_STAGES_MAX];  // PATCH (leader): both CTAs' B halves patched
   uint64_t tfull[ACC];
   uint64_t tempty[ACC];
   uint32_t tmem_base;
@@ -387,7 +395,9 @@ struct SmemCtl2 {
 };
 
 constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + P_STG_BYTES + sizeof(SmemCtl2);
-constexpr size_t kSmemBytes2Patch = kSmemBytes2 + P_STAGES * kPatchBlockBytes;
+// PATCH: six operand stages + patch blocks, no epilogue staging buffer (direct stores)
+constexpr size_t kSmemBytes2Patch =
+    1024 + P_STAGES_PATCH * (P_STAGE_BYTES + kPatchBlockBytes) + sizeof(SmemCtl2);
 
 // Release-arrive at cluster scope on the leader CTA's copy of `bar`: orders this thread's
 // (fenced) shared-memory writes before the leader's acquire of the barrier.
@@ -410,23 +420,24 @@ __device__ __forceinline__ int find_group2(const SmemCtl2& s, int ng, int tile) 
 // proxy and release-arrives on the leader's `patched` barrier (count 2); the leader's MMA
 // waits for the A halves (full) and for both patched halves.
 template <bool PATCH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (PATCH ? 32 : 0), 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (PATCH ? 32 * kConvWarps : 0), 1)
 grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                               __nv_bfloat16* __restrict__ C, int ldc, int N, int K,
                               const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
                               const int* __restrict__ g_slot, const unsigned long long* __restrict__ g_out,
                               const int* __restrict__ g_wait, const uint32_t* __restrict__ wait_flags,
                               uint32_t epoch, int ng, int relu, uint32_t sched, uint64_t timeout_ns,
-                              const PatchRef* __restrict__ patches, int half) {
+                              const PatchArgs patches, int half) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
+  constexpr int NST = PATCH ? P_STAGES_PATCH : P_STAGES;
   uint8_t* stage_a = smem;
-  uint8_t* stage_b = smem + P_STAGES * P_A_BYTES;
-  uint8_t* stage_out = smem + P_STAGES * P_STAGE_BYTES;
-  uint8_t* stage_p = stage_out + P_STG_BYTES;  // PATCH: one patch block per stage
-  SmemCtl2& s = *reinterpret_cast<SmemCtl2*>(smem + P_STAGES * P_STAGE_BYTES + P_STG_BYTES +
-                                             (PATCH ? P_STAGES * kPatchBlockBytes : 0));
+  uint8_t* stage_b = smem + NST * P_A_BYTES;
+  uint8_t* stage_out = smem + NST * P_STAGE_BYTES;  // !PATCH: epilogue staging
+  uint8_t* stage_p = smem + NST * P_STAGE_BYTES;    // PATCH: one patch block per stage
+  SmemCtl2& s = *reinterpret_cast<SmemCtl2*>(smem + NST * P_STAGE_BYTES +
+                                             (PATCH ? NST * kPatchBlockBytes : P_STG_BYTES));
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -466,7 +477,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
   } else if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
-    for (int i = 0; i < P_STAGES; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
       mbar_init(&s.bfull[i], 1);
@@ -487,23 +498,24 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
   const int total = s.num_tiles;
   const uint32_t tmem_base = s.tmem_base;
 
-  if (PATCH && warp == 6) {
-    // ================= converter (fused SR decode), both CTAs =================
-    int stage = 0;
-    uint32_t phase = 0;
+  if (PATCH && warp >= 6) {
+    // ================= converters (fused SR decode), both CTAs =================
+    const int wi = static_cast<int>(warp) - 6;
+    int c = 0;  // global stage counter: stage c % NST, phase (c / NST) & 1
     for (int tile = cluster; tile < total; tile += nclusters) {
       const int g = find_group2(s, ng, tile);
       const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
       int mt, nt;
       decode_tile(tile - s.tile_start[g], m_tiles, n_tiles, sched, mt, nt);
-      const PatchRef& pr = patches[s.slot[g]];
-      const bool ok = *pr.status == 0;
+      const int slot = s.slot[g];
       // rows of the 256-row B tile held here: [split * cta, split * cta + split)
       const int split = N - nt * P_BN <= P_BN / 2 ? 64 : 128;
       const uint32_t lo_byte = static_cast<uint32_t>(split * 128) * cta, hi_byte = lo_byte + split * 128;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&s.bfull[stage], phase);
-        if (ok) {
+      for (int kb = 0; kb < num_kb; ++kb, ++c) {
+        if (c % kConvWarps != wi) continue;
+        const int stage = c % NST;
+        mbar_wait(&s.bfull[stage], (c / NST) & 1);
+        {  // (a rejected wire's partial patch set is memory-safe; the layer raises the error)
           uint8_t* bst = stage_b + stage * P_B_BYTES;
           const uint32_t* blk = reinterpret_cast<const uint32_t*>(stage_p + stage * kPatchBlockBytes);
           const int cnt = static_cast<int>(blk[0]);
@@ -516,6 +528,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
           }
           if (cnt > kPatchBlockCap) {  // overflowed block: the rest from the global list (rare)
             const uint32_t id = static_cast<uint32_t>(nt * num_kb + kb) | (static_cast<uint32_t>(half) << 31);
+            const PatchRef& pr = patches.patches[slot];
             const int no = *pr.ovf_count;
             for (int q = lane; q < no; q += 32) {
               const uint2 e = pr.ovf[q];
@@ -527,8 +540,10 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive_leader_cluster(&s.patched[stage]);
-        if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        if (lane == 0) {
+          if (cta == 0) mbar_arrive(&s.patched[stage]);  // own smem: CTA-scope release suffices
+          else mbar_arrive_leader_cluster(&s.patched[stage]);
+        }
       }
     }
   }
@@ -551,8 +566,9 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
         // (the first 64 of its 128-row box)
         const int b_half = N - nt * P_BN <= P_BN / 2 ? 64 : 128;
         const int b_row = (PATCH ? 0 : s.slot[g] * N) + nt * P_BN + b_half * static_cast<int>(cta);
-        const uint8_t* pblk = PATCH ? patches[s.slot[g]].blocks[half] +
-                                          static_cast<size_t>(nt) * num_kb * kPatchBlockBytes : nullptr;
+        const uint8_t* pblk = PATCH ? patches.base + static_cast<size_t>(s.slot[g]) * patches.slot_bytes +
+                                          patches.half_bytes + static_cast<size_t>(nt) * num_kb * kPatchBlockBytes
+                                    : nullptr;
         if (s.wait[g] >= 0) wait_dispatch(wait_flags + s.wait[g], epoch, timeout_ns);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
@@ -569,7 +585,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
             tma_load_2d_2sm(stage_a + stage * P_A_BYTES, &map_a, &s.full[stage], kb * BK, a_row, pol_a);
             tma_load_2d_2sm(stage_b + stage * P_B_BYTES, &map_b, &s.full[stage], kb * BK, b_row, pol_b);
           }
-          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -602,7 +618,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
             umma_bf16_2sm(d_tmem, umma_desc_k_sw128(a_addr + 32 * k), umma_desc_k_sw128(b_addr + 32 * k), idesc,
                           (kb | k) != 0);
           umma_commit_2sm_mc(&s.empty[stage], 0x3);
-          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         umma_commit_2sm_mc(&s.tfull[acc], 0x3);
         if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
@@ -628,42 +644,66 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
       const uint32_t t_base = tmem_base + static_cast<uint32_t>(acc * P_BN) + ((quarter * 32u) << 16);
       const int rows_here = min(32, s.rows[g] - row0);
       __nv_bfloat16* out0 = s.out[g] + static_cast<size_t>(row0) * ldc + nt * P_BN;
-      // two column halves: TMEM -> registers -> (relu, bf16) -> staged row `lane` -> global
+      if constexpr (PATCH) {
+        // direct stores, one row per lane (the staging buffer's space holds a sixth stage)
 #pragma unroll 1
-      for (int h = 0; h < P_BN; h += P_STG_COLS) {
-        const int hcols = min(P_STG_COLS, ncols - h);
-        if (hcols <= 0) break;  // warp-uniform
-#pragma unroll 1
-        for (int c = 0; c < hcols; c += 32) {
+        for (int c = 0; c < ncols; c += 32) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(t_base + static_cast<uint32_t>(h + c), v);
+          tmem_ld_32x32b_x32(t_base + static_cast<uint32_t>(c), v);
           tmem_ld_wait();
-          float f[32];
+          if (static_cast<int>(lane) < rows_here) {  // signed: rows_here < 0 past a group's end
+            float f[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float x = __uint_as_float(v[i]);
-            f[i] = relu ? fmaxf(x, 0.f) : x;
+            for (int i = 0; i < 32; ++i) {
+              const float x = __uint_as_float(v[i]);
+              f[i] = relu ? fmaxf(x, 0.f) : x;
+            }
+            __nv_bfloat16* crow = out0 + static_cast<size_t>(lane) * ldc + c;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) st_v4(crow + 8 * q, pack8(f + 8 * q));
           }
-          uint4* dst = reinterpret_cast<uint4*>(stg + lane * P_STG_PITCH + c * 2);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) dst[q] = pack8(f + 8 * q);
         }
-        if (h + P_STG_COLS >= ncols) {
-          // the accumulator is free as soon as its last columns have been read
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_leader(&s.tempty[acc]);
-        }
+        tc_fence_before();
         __syncwarp();
-        // staged rows -> global, one row per instruction: lane l writes bytes [16l, 16l+16)
-        const int row_bytes = hcols * 2;
-        for (int r = 0; r < rows_here; ++r) {
-          if (lane * 16 < row_bytes) {
-            const uint4 val = *reinterpret_cast<const uint4*>(stg + r * P_STG_PITCH + lane * 16);
-            st_v4(reinterpret_cast<uint8_t*>(out0 + static_cast<size_t>(r) * ldc + h) + lane * 16, val);
+        if (lane == 0) mbar_arrive_leader(&s.tempty[acc]);
+      } else {
+        // two column halves: TMEM -> registers -> (relu, bf16) -> staged row `lane` -> global
+#pragma unroll 1
+        for (int h = 0; h < P_BN; h += P_STG_COLS) {
+          const int hcols = min(P_STG_COLS, ncols - h);
+          if (hcols <= 0) break;  // warp-uniform
+#pragma unroll 1
+          for (int c = 0; c < hcols; c += 32) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_base + static_cast<uint32_t>(h + c), v);
+            tmem_ld_wait();
+            float f[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float x = __uint_as_float(v[i]);
+              f[i] = relu ? fmaxf(x, 0.f) : x;
+            }
+            uint4* dst = reinterpret_cast<uint4*>(stg + lane * P_STG_PITCH + c * 2);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = pack8(f + 8 * q);
           }
+          if (h + P_STG_COLS >= ncols) {
+            // the accumulator is free as soon as its last columns have been read
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_leader(&s.tempty[acc]);
+          }
+          __syncwarp();
+          // staged rows -> global, one row per instruction: lane l writes bytes [16l, 16l+16)
+          const int row_bytes = hcols * 2;
+          for (int r = 0; r < rows_here; ++r) {
+            if (lane * 16 < row_bytes) {
+              const uint4 val = *reinterpret_cast<const uint4*>(stg + r * P_STG_PITCH + lane * 16);
+              st_v4(reinterpret_cast<uint8_t*>(out0 + static_cast<size_t>(r) * ldc + h) + lane * 16, val);
+            }
+          }
+          __syncwarp();  // the staging buffer is rewritten next
         }
-        __syncwarp();  // the staging buffer is rewritten next
       }
       if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
     }
@@ -1116,12 +1156,12 @@ cudaError_t launch_grouped_gemm_bf16(const CUtensorMap& map_a, const CUtensorMap
   grouped_gemm_bf16_kernel<false><<<num_sms, kThreads, kSmemBytes, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
       groups.slot, groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched,
-      groups.timeout_ns, nullptr, 0);
+      groups.timeout_ns, PatchArgs{}, 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_grouped_gemm_bf16_patched(const CUtensorMap& map_a, const CUtensorMap& map_shared_b, void* C,
-                                             int ldc, int N, int K, const GroupTable& groups, const PatchRef* patches,
+                                             int ldc, int N, int K, const GroupTable& groups, const PatchArgs& patches,
                                              int half, int relu, int num_sms, cudaStream_t stream, uint32_t sched) {
   if (K % BK || N % 32 || N > 65535 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
     return cudaErrorInvalidValue;
@@ -1132,7 +1172,7 @@ cudaError_t launch_grouped_gemm_bf16_patched(const CUtensorMap& map_a, const CUt
     if (e != cudaSuccess) return e;
     attr_set.set();
   }
-  grouped_gemm_bf16_kernel<true><<<num_sms, kThreads + 32, kSmemBytesPatch, stream>>>(
+  grouped_gemm_bf16_kernel<true><<<num_sms, kThreads + 32 * kConvWarps, kSmemBytesPatch, stream>>>(
       map_a, map_shared_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows,
       groups.slot, groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched,
       groups.timeout_ns, patches, half);
@@ -1155,13 +1195,13 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
   grouped_gemm_bf16_2cta_kernel<false><<<grid, kThreads, kSmemBytes2, stream>>>(
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
       groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
-      nullptr, 0);
+      PatchArgs{}, 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, const CUtensorMap& map_shared_b, void* C,
                                                   int ldc, int N, int K, const GroupTable& groups,
-                                                  const PatchRef* patches, int half, int relu, int num_sms,
+                                                  const PatchArgs& patches, int half, int relu, int num_sms,
                                                   cudaStream_t stream, uint32_t sched) {
   if (K % BK || N % 32 || N > 65535 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
     return cudaErrorInvalidValue;
@@ -1174,7 +1214,7 @@ cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, cons
     attr_set.set();
   }
   const int grid = (num_sms / 2) * 2;
-  grouped_gemm_bf16_2cta_kernel<true><<<grid, kThreads + 32, kSmemBytes2Patch, stream>>>(
+  grouped_gemm_bf16_2cta_kernel<true><<<grid, kThreads + 32 * kConvWarps, kSmemBytes2Patch, stream>>>(
       map_a, map_shared_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
       groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
       patches, half);

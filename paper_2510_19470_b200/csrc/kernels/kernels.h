@@ -115,7 +115,14 @@ struct PatchRef {
   const uint8_t* blocks[2];   // up, down: [n_tiles][num_kb] blocks of kPatchBlockBytes
   const uint2* ovf;           // (block id | half << 31, word) pairs
   const int* ovf_count;
-  const int32_t* status;      // the wire's decode status (non-zero: leave the shared values)
+  const int32_t* status;      // the wire's decode status (the layer raises a rejected wire)
+};
+// Where the GEMM finds slot s's blocks without a dependent load: base + s * slot_bytes +
+// half_bytes (0 for the up half); patches[s] is read only for an overflowed block.
+struct PatchArgs {
+  const uint8_t* base;
+  size_t slot_bytes, half_bytes;
+  const PatchRef* patches;
 };
 #ifdef __CUDACC__
 __host__ __device__
@@ -124,13 +131,13 @@ inline int64_t patch_blocks(int64_t N, int64_t K) { return ((N + 255) / 256) * (
 // B = the shared expert's compute copy (map_shared_b: the up [m x h] or down [h x m] half,
 // box 256 x 64); half = 0 for the up-projection, 1 for the down-projection.
 cudaError_t launch_grouped_gemm_bf16_patched(const CUtensorMap& map_a, const CUtensorMap& map_shared_b, void* C,
-                                             int ldc, int N, int K, const GroupTable& groups, const PatchRef* patches,
+                                             int ldc, int N, int K, const GroupTable& groups, const PatchArgs& patches,
                                              int half, int relu, int num_sms, cudaStream_t stream,
                                              uint32_t sched = 0x8u);
 // The same on the CTA pair (map_shared_b box 128 x 64).
 cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, const CUtensorMap& map_shared_b, void* C,
                                                   int ldc, int N, int K, const GroupTable& groups,
-                                                  const PatchRef* patches, int half, int relu, int num_sms,
+                                                  const PatchArgs& patches, int half, int relu, int num_sms,
                                                   cudaStream_t stream, uint32_t sched = 0x6u);
 // CTA-pair variant (cta_group::2, 256x256 cluster tiles); B's tensor map box is 128 rows.
 cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C, int ldc,
