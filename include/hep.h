@@ -251,8 +251,10 @@ int hep_layer_comm_bench(hep_layer_t layer, const void* x, int64_t tokens, int i
  * rows per (dest, expert) key. */
 int hep_layer_debug(hep_layer_t layer, const int32_t** topk_idx, const float** topk_w,
                     const int32_t** pos, const void** packed, const int32_t** key_counts);
-/* Per-kernel device times (ms) of the last `profile`d forward; names is a
- * ';'-separated list.  Enable with hep_layer_set_profiling(layer, 1). */
+/* Per-phase device times (ms, mean per forward since the last call); names is a
+ * ';'-separated list.  hep_layer_set_profiling(layer, level): 0 off, 1 CUDA events
+ * around the expert GEMM launches only (cheap enough for a timed pass), 2 events at every
+ * phase boundary. */
 int hep_layer_set_profiling(hep_layer_t layer, int on);
 int hep_layer_timings(hep_layer_t layer, char* names, size_t names_cap, float* ms, int cap,
                       int* count);

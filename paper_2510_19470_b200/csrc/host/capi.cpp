@@ -519,7 +519,10 @@ int hep_layer_debug(hep_layer_t layer, const int32_t** topk_idx, const float** t
 }
 
 int hep_layer_set_profiling(hep_layer_t layer, int on) {
-  return guarded([&] { layer->impl->set_profiling(on != 0); });
+  return guarded([&] {
+    if (on < 0 || on > 2) throw std::invalid_argument("profiling level must be 0, 1 (GEMM events) or 2 (all phases)");
+    layer->impl->set_profiling(on);
+  });
 }
 
 int hep_layer_timings(hep_layer_t layer, char* names, size_t names_cap, float* ms, int cap, int* count) {

@@ -270,8 +270,13 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
     timeout_ns_ = p2p_timeout_ns();
     if (p2p_) {
       setup_p2p();
-      const char* fused = std::getenv("HEP_SR_FUSED");  // 0: dense decode of gathered experts
-      sr_fused_ = use_sr_ && dt_ == DType::BF16 && !(fused && fused[0] == '0') && H_ < 65536 && F_ < 65536;
+      // HEP_SR_FUSED=1: decode fused into the expert GEMM's B-operand load.  Bit-identical
+      // to the dense decode, but its converter sits in the TMA -> MMA pipeline and the
+      // gathered-expert GEMMs run at ~0.65 of the dense path's rate (cfg4 N=2:
+      // profiles/r2_cfg4_fused.md), so the dense decode (a pass on the All-Gather stream,
+      // hidden under the own-expert GEMMs) stays the default.
+      const char* fused = std::getenv("HEP_SR_FUSED");
+      sr_fused_ = use_sr_ && dt_ == DType::BF16 && fused && fused[0] == '1' && H_ < 65536 && F_ < 65536;
       if (sr_fused_) {
         size_t wb = 0;
         hep_sr_config c{sr_cfg_.ratio_CR.value_or(1.0), sr_cfg_.k.value_or(-1), sr_cfg_.index_width_bits,
@@ -946,8 +951,8 @@ void Layer::check_migration(bool sync) {
   throw std::runtime_error("migrated expert rejected: " + why);
 }
 
-void Layer::mark(const char* name, cudaStream_t s) {
-  if (!profiling_) return;
+void Layer::mark(const char* name, cudaStream_t s, int level) {
+  if (profiling_ < level) return;
   cudaEvent_t ev;
   if (marks_.size() < event_pool_.size()) {
     ev = event_pool_[marks_.size()];
@@ -1052,41 +1057,42 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     refs_down.half_bytes = static_cast<size_t>(patch_blocks(F_, H_)) * kPatchBlockBytes;
     auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta_patched : launch_grouped_gemm_bf16_patched;
     const uint32_t sched = cta_pair_ ? 0x2u : 0x8u;  // the shared B is re-read by every group: keep A resident
-    mark(up.c_str(), s);
+    mark(up.c_str(), s, 1);
     ck(gemm(map_a1_, map_shared_up_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt,
             refs, 0, 1, num_sms_, s, sched),
        "gemm up (fused decode)");
-    mark(down.c_str(), s);
+    mark(down.c_str(), s, 1);
     ck(gemm(map_a2_, map_shared_down_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_),
             gt_down, refs_down, 1, 0, num_sms_, s, sched),
        "gemm down (fused decode)");
   } else if (dt_ == DType::BF16) {
-    mark(up.c_str(), s);
+    mark(up.c_str(), s, 1);
     auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta : launch_grouped_gemm_bf16;
     ck(gemm(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_), "gemm up");
-    mark(down.c_str(), s);
+    mark(down.c_str(), s, 1);
     ck(gemm(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_), "gemm down");
   } else if (tf32_) {
-    mark(up.c_str(), s);
+    mark(up.c_str(), s, 1);
     split_dirty_slots(s);
     ck(launch_split_tf32(xall_.as<float>(), xhi_.as<float>(), xlo_.as<float>(), rows_cap_ * H_, s), "split x");
     ck(launch_grouped_gemm_tf32x3(t_xhi_, t_xlo_, t_wuhi_, t_wulo_, hhi_.as<float>(), hlo_.as<float>(),
                                   static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s,
                                   ksplit_up_, kpart_.as<float>(), rows_cap_),
        "gemm up");
-    mark(down.c_str(), s);
+    mark(down.c_str(), s, 1);
     ck(launch_grouped_gemm_tf32x3(t_hhi_, t_hlo_, t_wdhi_, t_wdlo_, oall_.as<float>(), nullptr, static_cast<int>(H_),
                                   static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, ksplit_down_,
                                   kpart_.as<float>(), rows_cap_),
        "gemm down");
     launches_ += 1 + (ksplit_up_ > 1) + (ksplit_down_ > 1);  // x split, split-K reduces
   } else {
-    mark(up.c_str(), s);
+    mark(up.c_str(), s, 1);
     ck(launch_grouped_gemm_f32(xall_.as<float>(), static_cast<int>(H_), w_up_c_.as<float>(), hbuf_.as<float>(), static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_ * 2, s), "gemm up");
-    mark(down.c_str(), s);
+    mark(down.c_str(), s, 1);
     ck(launch_grouped_gemm_f32(hbuf_.as<float>(), static_cast<int>(F_), w_down_c_.as<float>(), oall_.as<float>(), static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_ * 2, s), "gemm down");
   }
   launches_ += 2;
+  if (profiling_ == 1) mark("end", s, 1);  // GEMM-only profiling: close the down interval
 }
 
 void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {

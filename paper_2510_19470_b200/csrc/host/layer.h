@@ -107,7 +107,9 @@ class Layer {
   const int* pos() const { return pos_.as<int>(); }
   const void* packed() const { return xall_.p; }
   const int* key_counts() const { return key_total_.as<int>(); }
-  void set_profiling(bool on) { profiling_ = on; }
+  // 0 off; 1 CUDA events around the expert GEMM launches only (cheap enough for the timed
+  // pass); 2 events at every phase boundary.
+  void set_profiling(int level) { profiling_ = level; }
   // Mean device time per named phase over every profiled forward since the last call.
   void collect_timings(char* names, size_t names_cap, float* ms, int cap, int* count);
   int launch_count() const { return launches_; }
@@ -125,7 +127,7 @@ class Layer {
   bool p2p() const { return p2p_; }
 
  private:
-  void mark(const char* name, cudaStream_t s);
+  void mark(const char* name, cudaStream_t s, int level = 2);
   void build_comm_plan_and_groups(int T, cudaStream_t s);
   void exchange(bool dispatch, cudaStream_t s);
   void run_expert_gemms(cudaStream_t s, const unsigned long long* out_down = nullptr, const int* wait_src = nullptr,
@@ -231,7 +233,7 @@ class Layer {
   cudaEvent_t ev_h2d_[2] = {}, ev_comp_[2] = {}, ev_d2h_[2] = {};
   int hslot_ = 0;
 
-  bool profiling_ = false;
+  int profiling_ = 0;
   std::vector<std::pair<std::string, cudaEvent_t>> marks_;
   std::vector<cudaEvent_t> event_pool_;
   int launches_ = 0;

@@ -191,8 +191,10 @@ class MoELayer:
             "key_counts": view(kc, self.G * self.E, torch.int32),
         }
 
-    def set_profiling(self, on: bool):
-        check(lib.hep_layer_set_profiling(self.handle, int(on)))
+    def set_profiling(self, level):
+        """0/False off, 1 events around the expert GEMMs only, 2/True every phase."""
+        level = 2 if level is True else int(level)
+        check(lib.hep_layer_set_profiling(self.handle, level))
 
     def timings(self) -> dict:
         names = C.create_string_buffer(1024)

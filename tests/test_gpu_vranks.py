@@ -67,6 +67,27 @@ def test_virtual_ranks_layer(sf, sed, extra):
         assert r.stdout.count(" ok ") >= 2, r.stdout[-2000:]
 
 
+FUSED_CASES = [
+    ([2], [2], ["--sr"]),
+    ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr", "--update"]),
+    ([2, 2], [2, 1], ["--ragged", "--sr"]),
+    ([2, 2], [2, 1], ["--sr", "--sgd"]),
+    ([2, 2], [1, 2], ["--sr", "--corrupt"]),
+]
+
+
+@pytest.mark.parametrize("sf,sed,extra", FUSED_CASES, ids=lambda v: str(v))
+def test_virtual_ranks_layer_fused_decode(sf, sed, extra):
+    """The SR cases with the decode fused into the expert GEMM (HEP_SR_FUSED=1)."""
+    cmd = [sys.executable, os.path.join(HERE, "vrank_worker.py"), "--sf", *map(str, sf), "--sed", *map(str, sed),
+           *extra]
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", HEP_P2P_TIMEOUT_S="60", HEP_SR_FUSED="1")
+    env.pop("HEP_COMM", None)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=420, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    assert r.stdout.count(" ok ") >= 2, r.stdout[-2000:]
+
+
 @pytest.mark.parametrize("sf,sed,extra", [
     ([2, 2], [2, 1], []),
     ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6"]),
