@@ -398,6 +398,7 @@ constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + P_STG_BYTES + s
 // PATCH: six operand stages + patch blocks, no epilogue staging buffer (direct stores)
 constexpr size_t kSmemBytes2Patch =
     1024 + P_STAGES_PATCH * (P_STAGE_BYTES + kPatchBlockBytes) + sizeof(SmemCtl2);
+constexpr size_t kSmemBytes2Deep = 1024 + P_STAGES_PATCH * P_STAGE_BYTES + sizeof(SmemCtl2);
 
 // Release-arrive at cluster scope on the leader CTA's copy of `bar`: orders this thread's
 // (fenced) shared-memory writes before the leader's acquire of the barrier.
@@ -419,7 +420,9 @@ __device__ __forceinline__ int find_group2(const SmemCtl2& s, int ng, int tile) 
 // warp (warp 6) writes the entries that fall in its half, fences them into the async
 // proxy and release-arrives on the leader's `patched` barrier (count 2); the leader's MMA
 // waits for the A halves (full) and for both patched halves.
-template <bool PATCH>
+// DEEP = true (no PATCH): six stages and direct-store epilogue for launches whose outputs
+// are all local (one GPU): the extra stage absorbs DRAM latency of the L2-missing operand.
+template <bool PATCH, bool DEEP = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (PATCH ? 32 * kConvWarps : 0), 1)
 grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                               __nv_bfloat16* __restrict__ C, int ldc, int N, int K,
@@ -431,13 +434,14 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  constexpr int NST = PATCH ? P_STAGES_PATCH : P_STAGES;
+  constexpr bool DIRECT = PATCH || DEEP;  // direct-store epilogue, no staging buffer
+  constexpr int NST = DIRECT ? P_STAGES_PATCH : P_STAGES;
   uint8_t* stage_a = smem;
   uint8_t* stage_b = smem + NST * P_A_BYTES;
-  uint8_t* stage_out = smem + NST * P_STAGE_BYTES;  // !PATCH: epilogue staging
+  uint8_t* stage_out = smem + NST * P_STAGE_BYTES;  // !DIRECT: epilogue staging
   uint8_t* stage_p = smem + NST * P_STAGE_BYTES;    // PATCH: one patch block per stage
   SmemCtl2& s = *reinterpret_cast<SmemCtl2*>(smem + NST * P_STAGE_BYTES +
-                                             (PATCH ? NST * kPatchBlockBytes : P_STG_BYTES));
+                                             (PATCH ? NST * kPatchBlockBytes : (DIRECT ? 0 : P_STG_BYTES)));
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -644,7 +648,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
       const uint32_t t_base = tmem_base + static_cast<uint32_t>(acc * P_BN) + ((quarter * 32u) << 16);
       const int rows_here = min(32, s.rows[g] - row0);
       __nv_bfloat16* out0 = s.out[g] + static_cast<size_t>(row0) * ldc + nt * P_BN;
-      if constexpr (PATCH) {
+      if constexpr (DIRECT) {
         // direct stores, one row per lane (the staging buffer's space holds a sixth stage)
 #pragma unroll 1
         for (int c = 0; c < ncols; c += 32) {
@@ -1183,19 +1187,32 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
                                           int N, int K, const GroupTable& groups, int relu, int num_sms,
                                           cudaStream_t stream, uint32_t sched) {
   if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0) return cudaErrorInvalidValue;
-  static DeviceOnce attr_set;
-  if (!attr_set.done()) {
-    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(kSmemBytes2));
+  // all outputs local (no per-group peer addresses): the six-stage direct-store variant,
+  // unless HEP_GEMM_DEEP=0
+  const char* deep_env = std::getenv("HEP_GEMM_DEEP");
+  const bool deep = !(deep_env && deep_env[0] == '0') && groups.out == nullptr;
+  static DeviceOnce attr_set, attr_deep;
+  DeviceOnce& once = deep ? attr_deep : attr_set;
+  if (!once.done()) {
+    const cudaError_t e =
+        deep ? cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes2Deep))
+             : cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes2));
     if (e != cudaSuccess) return e;
-    attr_set.set();
+    once.set();
   }
   const int grid = (num_sms / 2) * 2;
-  grouped_gemm_bf16_2cta_kernel<false><<<grid, kThreads, kSmemBytes2, stream>>>(
-      map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
-      groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
-      PatchArgs{}, 0);
+  if (deep)
+    grouped_gemm_bf16_2cta_kernel<false, true><<<grid, kThreads, kSmemBytes2Deep, stream>>>(
+        map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
+        groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
+        PatchArgs{}, 0);
+  else
+    grouped_gemm_bf16_2cta_kernel<false, false><<<grid, kThreads, kSmemBytes2, stream>>>(
+        map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
+        groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
+        PatchArgs{}, 0);
   return cudaGetLastError();
 }
 
@@ -1207,14 +1224,14 @@ cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, cons
     return cudaErrorInvalidValue;
   static DeviceOnce attr_set;
   if (!attr_set.done()) {
-    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<true>,
+    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<true, false>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(kSmemBytes2Patch));
     if (e != cudaSuccess) return e;
     attr_set.set();
   }
   const int grid = (num_sms / 2) * 2;
-  grouped_gemm_bf16_2cta_kernel<true><<<grid, kThreads + 32 * kConvWarps, kSmemBytes2Patch, stream>>>(
+  grouped_gemm_bf16_2cta_kernel<true, false><<<grid, kThreads + 32 * kConvWarps, kSmemBytes2Patch, stream>>>(
       map_a, map_shared_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
       groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
       patches, half);
@@ -1230,8 +1247,9 @@ cudaError_t preload_gemm_sm100_kernels() {
   };
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel<false>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel<true>))) return e;
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false>))) return e;
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<true>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, true>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<true, false>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(ksplit_reduce_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(split_tf32_kernel))) return e;
