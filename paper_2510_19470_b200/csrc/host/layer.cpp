@@ -316,6 +316,10 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
       check_signatures(all);
     }
   }
+  if (G_ == 1) {
+    const char* g = std::getenv("HEP_GRAPH");  // 0: enqueue every kernel on every forward
+    use_graphs_ = !(g && g[0] == '0');
+  }
   const int rows_per_expert = static_cast<int>(Tmax_ * k_ / E_);
   sched_up_ = gemm_schedule(rows_per_expert, static_cast<int>(F_), static_cast<int>(H_), true);
   sched_down_ = gemm_schedule(rows_per_expert, static_cast<int>(H_), static_cast<int>(F_), false);
@@ -559,6 +563,60 @@ Layer::~Layer() {
   if (h2d_s_) cudaStreamDestroy(h2d_s_);
   if (d2h_s_) cudaStreamDestroy(d2h_s_);
   if (mig_err_host_) cudaFreeHost(mig_err_host_);
+  drop_graphs();
+  if (graph_s_) {
+    cudaStreamSynchronize(graph_s_);
+    cudaStreamDestroy(graph_s_);
+  }
+  if (ev_graph_in_) cudaEventDestroy(ev_graph_in_);
+  if (ev_graph_out_) cudaEventDestroy(ev_graph_out_);
+}
+
+void Layer::drop_graphs() {
+  for (GraphEntry& e : graphs_) cudaGraphExecDestroy(e.exec);
+  graphs_.clear();
+}
+
+bool Layer::forward_graph(const void* x, int64_t T, void* y, cudaStream_t s) {
+  if (!use_graphs_ || profiling_ || T == 0) return false;
+  if (!graph_s_) {
+    ck(cudaStreamCreateWithFlags(&graph_s_, cudaStreamNonBlocking), "graph stream");
+    ck(cudaEventCreateWithFlags(&ev_graph_in_, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_graph_out_, cudaEventDisableTiming), "event");
+  }
+  if (tf32_) split_dirty_slots(s);  // weight splits stay outside the replayed graph
+  ck(cudaEventRecord(ev_graph_in_, s), "record");
+  ck(cudaStreamWaitEvent(graph_s_, ev_graph_in_, 0), "wait");
+  GraphEntry* hit = nullptr;
+  for (GraphEntry& e : graphs_)
+    if (e.x == x && e.T == T && e.y == y) hit = &e;
+  if (!hit) {
+    if (graphs_.size() >= 4) {  // keep a few (x, T, y) shapes
+      cudaGraphExecDestroy(graphs_.front().exec);
+      graphs_.erase(graphs_.begin());
+    }
+    cudaGraph_t g = nullptr;
+    ck(cudaStreamBeginCapture(graph_s_, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+      step(x, T, y, graph_s_);
+    } catch (...) {
+      cudaStreamEndCapture(graph_s_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    ck(cudaStreamEndCapture(graph_s_, &g), "end capture");
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    ck(e, "graph instantiate");
+    graphs_.push_back(GraphEntry{x, T, y, exec, launches_});
+    hit = &graphs_.back();
+  }
+  ck(cudaGraphLaunch(hit->exec, graph_s_), "graph launch");
+  launches_ = hit->launches;
+  ck(cudaEventRecord(ev_graph_out_, graph_s_), "record");
+  ck(cudaStreamWaitEvent(s, ev_graph_out_, 0), "wait");
+  return true;
 }
 
 void Layer::init_host_staging() {
@@ -578,11 +636,13 @@ void Layer::init_host_staging() {
 }
 
 void Layer::set_gate(const void* w_gate, DType dt, cudaStream_t s) {
+  drop_graphs();
   // W_g is H x E; the gate kernel wants it expert-major in the layer dtype.
   ck(launch_transpose_convert(dt, w_gate, H_, E_, dt_, wg_t_.p, s), "gate layout");
 }
 
 void Layer::set_expert(int64_t e, const void* w_up, const void* w_down, DType dt, cudaStream_t s) {
+  drop_graphs();
   if (e < 0 || e >= E_) throw std::domain_error("expert id out of range");
   if (e / n_ != rank_) throw std::invalid_argument("expert is not owned by this rank");
   if (ag_pending_) ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");  // the encode reads the masters
@@ -1096,7 +1156,8 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
 }
 
 void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
-  step(x, T, y, s);
+  if (T < 0 || T > Tmax_) throw std::invalid_argument("token count must be in [0, max_tokens]");
+  if (!forward_graph(x, T, y, s)) step(x, T, y, s);
   // A gathered expert whose wire failed to decode (found once that decode has completed)
   // is reported after this rank's share of the collective step is enqueued, so its peers
   // never wait for a rank that bailed out.

@@ -109,7 +109,7 @@ class Layer {
   const int* key_counts() const { return key_total_.as<int>(); }
   // 0 off; 1 CUDA events around the expert GEMM launches only (cheap enough for the timed
   // pass); 2 events at every phase boundary.
-  void set_profiling(int level) { profiling_ = level; }
+  void set_profiling(int level) { profiling_ = level; }  // profiled forwards run eagerly
   // Mean device time per named phase over every profiled forward since the last call.
   void collect_timings(char* names, size_t names_cap, float* ms, int cap, int* count);
   int launch_count() const { return launches_; }
@@ -141,6 +141,22 @@ class Layer {
   CUtensorMap map_shared_up_, map_shared_down_;
   void decode_gathered(size_t wire_bytes, size_t stride, cudaStream_t s);
   void step(const void* x, int64_t T, void* y, cudaStream_t s);  // forward's enqueue
+  // One-GPU layers replay the step as a CUDA graph, one per (x, T, y); any weight change
+  // drops them.  Launched on graph_s_ with event joins to the caller's stream (capture on
+  // the legacy default stream is not allowed).
+  struct GraphEntry {
+    const void* x;
+    int64_t T;
+    void* y;
+    cudaGraphExec_t exec;
+    int launches;
+  };
+  std::vector<GraphEntry> graphs_;
+  bool use_graphs_ = false;
+  cudaStream_t graph_s_ = nullptr;
+  cudaEvent_t ev_graph_in_ = nullptr, ev_graph_out_ = nullptr;
+  void drop_graphs();
+  bool forward_graph(const void* x, int64_t T, void* y, cudaStream_t s);
   void gather(cudaStream_t s);                                     // gather_experts' enqueue
 
   // shape

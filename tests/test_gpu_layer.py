@@ -163,3 +163,53 @@ def test_refresh_shared_single_gpu(dtype):
     flat = [torch.cat([w_up[e].float().reshape(-1), w_down[e].float().reshape(-1)]).numpy() for e in range(E)]
     assert got.tobytes() == oracle.shared_mean(flat).tobytes()
     layer.close()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
+def test_layer_graph_replay_matches_eager(dtype):
+    """One-GPU layers replay the step as a CUDA graph per (x, T, y).  Replays must equal the
+    eager step (profiled forwards run eagerly) bit for bit, see new data written into the
+    same x buffer, and follow weight updates."""
+    H, F, E, k, T = 256, 512, 8, 2, 100
+    g = torch.Generator().manual_seed(21)
+    wg = synthetic.dyadic((H, E), g)
+    w_up, w_down = synthetic.experts(E, H, F, g, dtype=dtype)
+    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype)
+    layer.set_gate(wg.cuda())
+    for e in range(E):
+        layer.set_expert(e, w_up[e].cuda(), w_down[e].cuda())
+    x = synthetic.dyadic((T, H), g, dtype=dtype).cuda()
+    y = torch.empty_like(x)
+    side = torch.cuda.Stream()
+    for stream in (None, side):  # the legacy default stream and a side stream
+        outs = []
+        for _ in range(3):  # capture, then replays
+            layer.forward(x, out=y, stream=stream)
+            torch.cuda.synchronize()
+            outs.append(y.clone())
+        layer.set_profiling(2)
+        layer.forward(x, out=y, stream=stream)  # eager
+        torch.cuda.synchronize()
+        layer.timings()
+        layer.set_profiling(0)
+        for o in outs:
+            assert torch.equal(o, y)
+    x2 = synthetic.dyadic((T, H), g, dtype=dtype).cuda()
+    x.copy_(x2)  # same buffer, new tokens: the replay reads them
+    layer.forward(x, out=y)
+    torch.cuda.synchronize()
+    ref = oracle.moe_layer(x2.float().cpu().numpy()[None], wg.numpy(), w_up.float().numpy(), w_down.float().numpy(), k,
+                           [1], [1], bf16=dtype == torch.bfloat16)
+    scale = np.abs(ref["y"][0]).max()
+    assert np.abs(y.float().cpu().numpy() - ref["y"][0]).max() <= (
+        tol.BF16_VS_MIRROR_MAX if dtype == torch.bfloat16 else tol.F32_MAX) * scale
+    layer.set_expert(0, (w_up[0] * 2).cuda(), w_down[0].cuda())  # weights change -> new result
+    layer.forward(x, out=y)
+    torch.cuda.synchronize()
+    w_up2 = w_up.clone()
+    w_up2[0] *= 2
+    ref2 = oracle.moe_layer(x2.float().cpu().numpy()[None], wg.numpy(), w_up2.float().numpy(), w_down.float().numpy(),
+                            k, [1], [1], bf16=dtype == torch.bfloat16)
+    assert np.abs(y.float().cpu().numpy() - ref2["y"][0]).max() <= (
+        tol.BF16_VS_MIRROR_MAX if dtype == torch.bfloat16 else tol.F32_MAX) * np.abs(ref2["y"][0]).max()
+    layer.close()
