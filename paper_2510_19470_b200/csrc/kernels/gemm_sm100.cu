@@ -399,6 +399,7 @@ constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + P_STG_BYTES + s
 constexpr size_t kSmemBytes2Patch =
     1024 + P_STAGES_PATCH * (P_STAGE_BYTES + kPatchBlockBytes) + sizeof(SmemCtl2);
 constexpr size_t kSmemBytes2Deep = 1024 + P_STAGES_PATCH * P_STAGE_BYTES + sizeof(SmemCtl2);
+constexpr size_t kSmemBytes2Four = 1024 + 4 * P_STAGE_BYTES + P_STG_BYTES + sizeof(SmemCtl2);
 
 // Release-arrive at cluster scope on the leader CTA's copy of `bar`: orders this thread's
 // (fenced) shared-memory writes before the leader's acquire of the barrier.
@@ -420,9 +421,12 @@ __device__ __forceinline__ int find_group2(const SmemCtl2& s, int ng, int tile) 
 // warp (warp 6) writes the entries that fall in its half, fences them into the async
 // proxy and release-arrives on the leader's `patched` barrier (count 2); the leader's MMA
 // waits for the A halves (full) and for both patched halves.
-// DEEP = true (no PATCH): six stages and direct-store epilogue for launches whose outputs
-// are all local (one GPU): the extra stage absorbs DRAM latency of the L2-missing operand.
-template <bool PATCH, bool DEEP = false>
+// NST operand stages; DIRECT: direct-store epilogue (no staging buffer).  The default is 5
+// stages + staged epilogue: measured under ncu on the cfg3 down-projection, a sixth stage
+// lets the CTAs drift apart, their L2 sharing drops (DRAM reads 5.1 -> 7.0 GB), the SM
+// clock falls under the power cap (1.38 -> 1.31 GHz) and the launch slows 4%
+// (profiles/r2_gemm_power.md).
+template <bool PATCH, int NST_T = P_STAGES, bool DIRECT_T = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (PATCH ? 32 * kConvWarps : 0), 1)
 grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                               __nv_bfloat16* __restrict__ C, int ldc, int N, int K,
@@ -434,8 +438,8 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  constexpr bool DIRECT = PATCH || DEEP;  // direct-store epilogue, no staging buffer
-  constexpr int NST = DIRECT ? P_STAGES_PATCH : P_STAGES;
+  constexpr bool DIRECT = PATCH || DIRECT_T;  // direct-store epilogue, no staging buffer
+  constexpr int NST = PATCH ? P_STAGES_PATCH : NST_T;
   uint8_t* stage_a = smem;
   uint8_t* stage_b = smem + NST * P_A_BYTES;
   uint8_t* stage_out = smem + NST * P_STAGE_BYTES;  // !DIRECT: epilogue staging
@@ -1187,32 +1191,36 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
                                           int N, int K, const GroupTable& groups, int relu, int num_sms,
                                           cudaStream_t stream, uint32_t sched) {
   if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0) return cudaErrorInvalidValue;
-  // all outputs local (no per-group peer addresses): the six-stage direct-store variant,
-  // unless HEP_GEMM_DEEP=0
-  const char* deep_env = std::getenv("HEP_GEMM_DEEP");
-  const bool deep = !(deep_env && deep_env[0] == '0') && groups.out == nullptr;
-  static DeviceOnce attr_set, attr_deep;
-  DeviceOnce& once = deep ? attr_deep : attr_set;
+  // HEP_GEMM_STAGES = 4 | 5 (default) | 6 (six stages, direct-store epilogue; local outputs only)
+  const char* st_env = std::getenv("HEP_GEMM_STAGES");
+  int stages = st_env ? std::atoi(st_env) : 5;
+  if (stages == 6 && groups.out != nullptr) stages = 5;
+  if (stages != 4 && stages != 6) stages = 5;
+  static DeviceOnce attr4, attr5, attr6;
+  DeviceOnce& once = stages == 4 ? attr4 : (stages == 6 ? attr6 : attr5);
   if (!once.done()) {
-    const cudaError_t e =
-        deep ? cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes2Deep))
-             : cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes2));
+    cudaError_t e;
+    if (stages == 4)
+      e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, 4, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes2Four));
+    else if (stages == 6)
+      e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, 6, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes2Deep));
+    else
+      e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, 5, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes2));
     if (e != cudaSuccess) return e;
     once.set();
   }
   const int grid = (num_sms / 2) * 2;
-  if (deep)
-    grouped_gemm_bf16_2cta_kernel<false, true><<<grid, kThreads, kSmemBytes2Deep, stream>>>(
-        map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
-        groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
-        PatchArgs{}, 0);
-  else
-    grouped_gemm_bf16_2cta_kernel<false, false><<<grid, kThreads, kSmemBytes2, stream>>>(
-        map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
-        groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
-        PatchArgs{}, 0);
+#define HEP_LAUNCH_2CTA(ST, DIR, SMEM)                                                                               \
+  grouped_gemm_bf16_2cta_kernel<false, ST, DIR><<<grid, kThreads, SMEM, stream>>>(                                  \
+      map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot, groups.out, \
+      groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns, PatchArgs{}, 0)
+  if (stages == 4) HEP_LAUNCH_2CTA(4, false, kSmemBytes2Four);
+  else if (stages == 6) HEP_LAUNCH_2CTA(6, true, kSmemBytes2Deep);
+  else HEP_LAUNCH_2CTA(5, false, kSmemBytes2);
+#undef HEP_LAUNCH_2CTA
   return cudaGetLastError();
 }
 
@@ -1224,14 +1232,14 @@ cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, cons
     return cudaErrorInvalidValue;
   static DeviceOnce attr_set;
   if (!attr_set.done()) {
-    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<true, false>,
+    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<true>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(kSmemBytes2Patch));
     if (e != cudaSuccess) return e;
     attr_set.set();
   }
   const int grid = (num_sms / 2) * 2;
-  grouped_gemm_bf16_2cta_kernel<true, false><<<grid, kThreads + 32 * kConvWarps, kSmemBytes2Patch, stream>>>(
+  grouped_gemm_bf16_2cta_kernel<true><<<grid, kThreads + 32 * kConvWarps, kSmemBytes2Patch, stream>>>(
       map_a, map_shared_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
       groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
       patches, half);
@@ -1247,9 +1255,10 @@ cudaError_t preload_gemm_sm100_kernels() {
   };
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel<false>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_kernel<true>))) return e;
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, false>))) return e;
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, true>))) return e;
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<true, false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 4, false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 5, false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 6, true>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<true>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(ksplit_reduce_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(split_tf32_kernel))) return e;
