@@ -1,9 +1,9 @@
 """Interleaved A/B timing of cfg3 down-/up-projection GEMM variants (schedule word x
-HEP_GEMM_DEEP), so clock drift under the power cap does not bias the comparison: every
+HEP_GEMM_STAGES), so clock drift under the power cap does not bias the comparison: every
 round runs every variant (3 launches, median), rounds repeat; reports the median over
 rounds per variant.
 
-    python tools/gemm_ab.py --proj down --variants 822:0,822:1,422:0,422:1 --rounds 6
+    python tools/gemm_ab.py --proj down --variants 822:5,822:6,422:5,822:4 --rounds 6
 """
 import argparse
 import ctypes as C
@@ -22,7 +22,7 @@ from paper_2510_19470_b200._lib import HEP_BF16, check, lib  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--proj", default="down")
-    ap.add_argument("--variants", default="822:0,822:1,422:0,422:1")
+    ap.add_argument("--variants", default="822:5,822:6,422:5,822:4")
     ap.add_argument("--rounds", type=int, default=6)
     ap.add_argument("--data", default="layer", help="layer: dyadic tokens + demo experts (the bench's); randn")
     a = ap.parse_args()
@@ -60,7 +60,7 @@ def main():
     res = {v: [] for v in variants}
     for _ in range(a.rounds):
         for v in variants:
-            os.environ["HEP_GEMM_DEEP"] = v[1]
+            os.environ["HEP_GEMM_STAGES"] = v[1]
             ts = []
             for _ in range(3):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -72,7 +72,7 @@ def main():
             res[v].append(statistics.median(ts))
     for v in variants:
         ms = statistics.median(res[v])
-        print(json.dumps({"proj": a.proj, "sched": hex(v[0]), "deep": v[1], "ms": ms, "tflops": flops / ms / 1e9,
+        print(json.dumps({"proj": a.proj, "sched": hex(v[0]), "stages": v[1], "ms": ms, "tflops": flops / ms / 1e9,
                           "rounds_ms": [round(t, 3) for t in res[v]], "data": a.data}), flush=True)
 
 

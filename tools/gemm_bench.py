@@ -1,7 +1,7 @@
 """cfg3 expert-GEMM shapes through hep_grouped_gemm (8 experts x 4096 rows): up
 (K=4096 -> N=14336, ReLU) and down (K=14336 -> N=4096) under schedule words, timed with
 CUDA events (median of `--reps` after warm-up, each launch alone; plus the mean of a
-back-to-back burst of up+down pairs).  HEP_GEMM_DEEP / HEP_GEMM_2CTA select the variant.
+back-to-back burst of up+down pairs).  HEP_GEMM_STAGES / HEP_GEMM_2CTA select the variant.
 
     python tools/gemm_bench.py --sched-up 2 --sched-down 822,2,12,422
 """
@@ -58,7 +58,7 @@ def main():
                 ts.append(e0.elapsed_time(e1))
         return statistics.median(ts)
 
-    env = {k: os.environ.get(k) for k in ("HEP_GEMM_DEEP", "HEP_GEMM_2CTA")}
+    env = {k: os.environ.get(k) for k in ("HEP_GEMM_STAGES", "HEP_GEMM_2CTA")}
     for su in a.sched_up.split(","):
         s_up = int(su, 16)
         ms = t(lambda: up(s_up))
