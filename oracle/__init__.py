@@ -48,6 +48,8 @@ def _load_orc():
     lib.orc_moe_layer.argtypes = [C.c_int, VP, VP, VP, VP, I64, I64, I64, I64, I64, I64, VP, VP, C.c_int, I64,
                                   VP, VP, VP, VP, VP]
     lib.orc_num_threads.restype = C.c_int
+    lib.orc_ffn_row.argtypes = [VP, VP, VP, I64, I64, C.c_int, VP, VP, VP]
+    lib.orc_ffn_row.restype = None
     lib.orc_sgd_step.argtypes = [VP, VP, C.c_float, I64]
     lib.orc_sgd_step.restype = None
     return lib
@@ -226,6 +228,18 @@ def moe_layer(x, wg, w_up, w_down, k, sf, sed, bf16, stride=1, exact=False):
     if rc:
         raise ValueError(f"oracle layer failed ({rc})")
     return {"y": y, "topk_idx": ti, "topk_w": tw, "pos": pos, "key_counts": kc}
+
+
+def ffn_row(x, w_up, w_down, bf16):
+    """S4 for one row (the per-row definition): y = relu(x w_up) w_down, fp64 sums."""
+    x = np.ascontiguousarray(x, np.float32)
+    w_up = np.ascontiguousarray(w_up, np.float32)
+    w_down = np.ascontiguousarray(w_down, np.float32)
+    H, F = w_up.shape
+    hacc, yacc = np.zeros(F), np.zeros(H)
+    out = np.zeros(H, np.float32)
+    orc.orc_ffn_row(_p(x), _p(w_up), _p(w_down), H, F, int(bf16), _p(hacc), _p(yacc), _p(out))
+    return out
 
 
 def num_threads() -> int:

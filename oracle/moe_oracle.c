@@ -342,9 +342,10 @@ void orc_gate(const float* x, const float* wg, int64_t T, int64_t H, int64_t E, 
 }
 
 /* S4 expert FFN for one row: y = relu(x . w_up) . w_down, fp64 accumulation.
- * bf16 mode mirrors the device rounding points: h and y are rounded to bf16. */
-static void ffn_row(const float* x, const float* w_up, const float* w_down, int64_t H, int64_t F, int bf16,
-                    double* hacc, double* yacc, float* y) {
+ * bf16 mode mirrors the device rounding points: h and y are rounded to bf16.  The
+ * definition the batched layer below reproduces bit for bit (tests/test_oracle.py). */
+void orc_ffn_row(const float* x, const float* w_up, const float* w_down, int64_t H, int64_t F, int bf16,
+                 double* hacc, double* yacc, float* y) {
   for (int64_t f = 0; f < F; ++f) hacc[f] = 0.0;
   for (int64_t h = 0; h < H; ++h) {
     const double xv = (double)x[h];
@@ -410,31 +411,97 @@ int orc_moe_layer(int bf16, const float* x, const float* wg, const float* w_up, 
     free(off);
   }
   /* Expert FFN where the row is processed (the result is independent of which GPU
-   * computes it: S1 makes every holder use identical weights), then S5 combine. */
+   * computes it: S1 makes every holder use identical weights), then S5 combine.
+   * Batched per expert so each expert's weights stream once, not once per row: the
+   * sampled (row, slot) pairs are grouped by expert and the products accumulate in fp64
+   * in the same order as ffn_row (h ascending for h, f ascending for y), with the same
+   * rounding points -- the per-pair results are identical to ffn_row's. */
   memset(y, 0, sizeof(float) * G * T * H);
   const int64_t rows = G * T;
-#pragma omp parallel
-  {
-    double* hacc = (double*)malloc(sizeof(double) * F);
-    double* yacc = (double*)malloc(sizeof(double) * H);
-    float* out = (float*)malloc(sizeof(float) * H);
-    float* acc = (float*)malloc(sizeof(float) * H);
-#pragma omp for schedule(dynamic, 1)
-    for (int64_t r = 0; r < rows; ++r) {
-      const int64_t t = r % T;
-      if (t % stride) continue;
-      const float* xr = x + r * H;
-      for (int64_t c = 0; c < H; ++c) acc[c] = 0.f;
-      for (int64_t j = 0; j < k; ++j) {
-        const int64_t e = topk_idx[r * k + j];
-        ffn_row(xr, w_up + e * H * F, w_down + e * F * H, H, F, rnd, hacc, yacc, out);
-        const float wt = topk_w[r * k + j];
-        for (int64_t c = 0; c < H; ++c) acc[c] = fmaf(wt, out[c], acc[c]);
+  int64_t* cnt_e = (int64_t*)calloc((size_t)E + 1, sizeof(int64_t));
+  for (int64_t r = 0; r < rows; ++r)
+    if ((r % T) % stride == 0)
+      for (int64_t j = 0; j < k; ++j) cnt_e[topk_idx[r * k + j] + 1]++;
+  for (int64_t e = 0; e < E; ++e) cnt_e[e + 1] += cnt_e[e];
+  const int64_t npairs = cnt_e[E];
+  int64_t* pair_of = (int64_t*)malloc(sizeof(int64_t) * (npairs ? npairs : 1));  /* r * k + j, grouped by expert */
+  int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)E);
+  for (int64_t e = 0; e < E; ++e) fill[e] = cnt_e[e];
+  for (int64_t r = 0; r < rows; ++r)
+    if ((r % T) % stride == 0)
+      for (int64_t j = 0; j < k; ++j) pair_of[fill[topk_idx[r * k + j]]++] = r * k + j;
+  float* pout = (float*)malloc(sizeof(float) * (size_t)(npairs ? npairs : 1) * H);  /* expert output per pair */
+  const int64_t CB = 256;
+  for (int64_t e = 0; e < E; ++e) {
+    const int64_t p0 = cnt_e[e], ne = cnt_e[e + 1] - p0;
+    if (ne == 0) continue;
+    float* hm = (float*)malloc(sizeof(float) * ne * F);
+    const float* wu = w_up + e * H * F;
+    const float* wd = w_down + e * F * H;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t f0 = 0; f0 < F; f0 += CB) {
+      const int64_t nb = F - f0 < CB ? F - f0 : CB;
+      double* acc = (double*)calloc((size_t)(ne * nb), sizeof(double));
+      for (int64_t h = 0; h < H; ++h) {
+        const float* row = wu + h * F + f0;
+        for (int64_t q = 0; q < ne; ++q) {
+          const double xv = (double)x[(pair_of[p0 + q] / k) * H + h];
+          if (xv == 0.0) continue;
+          double* a = acc + q * nb;
+          for (int64_t f = 0; f < nb; ++f) a[f] += xv * (double)row[f];
+        }
       }
-      for (int64_t c = 0; c < H; ++c) y[r * H + c] = rnd ? bf16_round(acc[c]) : acc[c];
+      for (int64_t q = 0; q < ne; ++q)
+        for (int64_t f = 0; f < nb; ++f) {
+          float hv = (float)acc[q * nb + f];
+          hv = hv > 0.f ? hv : 0.f;
+          if (rnd) hv = bf16_round(hv);
+          hm[q * F + f0 + f] = hv;
+        }
+      free(acc);
     }
-    free(hacc); free(yacc); free(out); free(acc);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c0 = 0; c0 < H; c0 += CB) {
+      const int64_t nb = H - c0 < CB ? H - c0 : CB;
+      double* acc = (double*)calloc((size_t)(ne * nb), sizeof(double));
+      for (int64_t f = 0; f < F; ++f) {
+        const float* row = wd + f * H + c0;
+        for (int64_t q = 0; q < ne; ++q) {
+          const float hv = hm[q * F + f];
+          if (hv == 0.f) continue;
+          double* a = acc + q * nb;
+          for (int64_t c = 0; c < nb; ++c) a[c] += (double)hv * (double)row[c];
+        }
+      }
+      for (int64_t q = 0; q < ne; ++q)
+        for (int64_t c = 0; c < nb; ++c)
+          pout[(p0 + q) * H + c0 + c] = rnd ? bf16_round((float)acc[q * nb + c]) : (float)acc[q * nb + c];
+      free(acc);
+    }
+    free(hm);
   }
+  /* S5: combine in slot order (fmaf, fp32) */
+  int64_t* slot_pair = (int64_t*)malloc(sizeof(int64_t) * (size_t)(rows * k));
+  for (int64_t p = 0; p < npairs; ++p) slot_pair[pair_of[p]] = p;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r) {
+    if ((r % T) % stride) continue;
+    float acc[8192];
+    float* a = H <= 8192 ? acc : (float*)malloc(sizeof(float) * H);
+    for (int64_t c = 0; c < H; ++c) a[c] = 0.f;
+    for (int64_t j = 0; j < k; ++j) {
+      const float* out = pout + slot_pair[r * k + j] * H;
+      const float wt = topk_w[r * k + j];
+      for (int64_t c = 0; c < H; ++c) a[c] = fmaf(wt, out[c], a[c]);
+    }
+    for (int64_t c = 0; c < H; ++c) y[r * H + c] = rnd ? bf16_round(a[c]) : a[c];
+    if (a != acc) free(a);
+  }
+  free(slot_pair);
+  free(pout);
+  free(fill);
+  free(pair_of);
+  free(cnt_e);
   free(route);
   return 0;
 }

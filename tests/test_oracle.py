@@ -66,3 +66,34 @@ def test_orc_matches_reference_library_randomized(seed):
     assert ra == rb == 0 and da.tobytes() == db.tobytes()
     experts = [e, s, (e + s).astype(np.float32)]
     assert oracle.shared_mean(experts).tobytes() == oracle.shared_mean(experts, use_ref=True, h=h, m=m).tobytes()
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+def test_batched_layer_equals_per_row_definition(bf16):
+    """The oracle's layer batches the FFN per expert (weights streamed once per expert);
+    every sampled token's output must equal the per-row definition (ffn_row in slot
+    order, fmaf combine) bit for bit."""
+    import torch
+
+    from paper_2510_19470_b200 import synthetic
+
+    H, F, E, k, G, T, stride = 128, 320, 8, 2, 2, 40, 3
+    g = torch.Generator().manual_seed(31)
+    dt = torch.bfloat16 if bf16 else torch.float32
+    x = synthetic.dyadic((G, T, H), g, dtype=dt).float().numpy()
+    wg = synthetic.dyadic((H, E), g).numpy()
+    w_up, w_down = synthetic.experts(E, H, F, g, dtype=dt)
+    w_up, w_down = w_up.float().numpy(), w_down.float().numpy()
+    ref = oracle.moe_layer(x, wg, w_up, w_down, k, [2], [1], bf16=bf16, stride=stride)
+    for gg in range(G):
+        for t in range(0, T, stride):
+            acc = np.zeros(H, np.float32)
+            for j in range(k):
+                e = ref["topk_idx"][gg, t, j]
+                out = oracle.ffn_row(x[gg, t], w_up[e], w_down[e], bf16)
+                acc = (np.float32(ref["topk_w"][gg, t, j]) * out.astype(np.float64) + acc).astype(np.float32)
+            want = acc
+            got = ref["y"][gg, t]
+            if bf16:
+                want = torch.from_numpy(want).to(torch.bfloat16).float().numpy()
+            np.testing.assert_allclose(got, want, rtol=0, atol=0)
