@@ -629,7 +629,8 @@ def main():
             cb["ag_bus_gbs"] = cb["ag_bytes"] / (ag_ms * 1e6)
             cb["ag_source"] = "nccl all_gather of one GPU's expert payload (torch.distributed)"
             del payload, gathered
-        stats = torch.tensor([cb["a2a_bus_gbs"] or 0.0, cb["ag_bus_gbs"] or 0.0], device=dev, dtype=torch.float64)
+        stats = torch.tensor([cb["a2a_bus_gbs"] or 0.0, cb["ag_bus_gbs"] or 0.0, cb.get("ag_pull_bus_gbs") or 0.0],
+                             device=dev, dtype=torch.float64)
         dist.all_reduce(stats, op=dist.ReduceOp.MIN)
         # The reference's per-level stripe-model bytes of this plan (traffic_report,
         # topology.cpp:249-281) beside the physical bytes this GPU moved (SURVEY §7 hard
@@ -641,6 +642,7 @@ def main():
         comm_stats = dict(cb, a2a_bus_gbs_min_over_ranks=float(stats[0]), ag_bus_gbs_min_over_ranks=float(stats[1]),
                           nvlink_peak_gbs=770.0, peak_source="B200_PROFILING.md measured peer copy per direction",
                           a2a_frac=float(stats[0]) / 770.0, ag_frac=float(stats[1]) / 770.0,
+                          ag_pull_bus_gbs_min_over_ranks=float(stats[2]), ag_pull_frac=float(stats[2]) / 770.0,
                           physical_bytes_per_gpu={"a2a_dispatch_sent": cb["a2a_bytes"], "ag_received": cb["ag_bytes"]},
                           stripe_model_bytes_cluster={"per_level": stripe, "unit": "bytes per layer pass, "
                                                       "all GPUs (traffic_report, topology.cpp:249-281)"})

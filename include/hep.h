@@ -242,7 +242,8 @@ int hep_layer_host_fence(hep_layer_t layer, void* stream);
 int hep_layer_check(hep_layer_t layer, void* stream);
 /* Communication microbenchmark of this layer's exchanges (A2A dispatch over NVLink peer
  * memory; expert All-Gather): out6 = {a2a_ms, a2a_bytes_sent, 0, ag_ms, ag_bytes_received,
- * 0}, per GPU, averaged over `iters`.  Collective: every rank must call it. */
+ * ag_pull_ms}, per GPU, averaged over `iters`.  ag_ms is the whole gather (SR: encode, flags,
+ * pulls, decode); ag_pull_ms the same peer pulls alone.  Collective: every rank calls it. */
 int hep_layer_comm_bench(hep_layer_t layer, const void* x, int64_t tokens, int iters, double* out6,
                          void* stream);
 /* Introspection of the last forward (device pointers owned by the layer):

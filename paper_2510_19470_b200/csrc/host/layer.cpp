@@ -1353,6 +1353,31 @@ void Layer::comm_bench(const void* x, int64_t T, int iters, double* out, cudaStr
     const double per_expert = use_sr_ ? static_cast<double>(wires_.bytes) / static_cast<double>(slots_)
                                       : static_cast<double>(2 * H_ * F_ * eb);
     out[4] = static_cast<double>(ag_peers_.size()) * n_ * per_expert;
+    if (p2p_) {
+      // the NVLink transfer alone: the same peer pulls (copy engines), no encode / decode /
+      // flags, into scratch
+      const size_t wb_stride = use_sr_ ? wires_.bytes / static_cast<size_t>(slots_) : 0;
+      const size_t per_peer = use_sr_ ? wb_stride * static_cast<size_t>(n_)
+                                      : eb * static_cast<size_t>(n_) * static_cast<size_t>(F_ * H_);
+      DevBuf scratch;
+      scratch.alloc(per_peer * (use_sr_ ? 1 : 2));
+      ck(cudaEventRecord(e0, s), "record");
+      for (int it = 0; it < iters; ++it)
+        for (int64_t p : ag_peers_) {
+          const size_t pi = static_cast<size_t>(p);
+          if (use_sr_) {
+            ck(cudaMemcpyAsync(scratch.p, peer_wires_[pi], per_peer, cudaMemcpyDeviceToDevice, s), "pull");
+          } else {
+            ck(cudaMemcpyAsync(scratch.p, peer_w_up_[pi], per_peer, cudaMemcpyDeviceToDevice, s), "pull");
+            ck(cudaMemcpyAsync(scratch.as<uint8_t>() + per_peer, peer_w_down_[pi], per_peer, cudaMemcpyDeviceToDevice, s),
+               "pull");
+          }
+        }
+      ck(cudaEventRecord(e1, s), "record");
+      ck(cudaEventSynchronize(e1), "sync");
+      ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+      out[5] = ms / iters;
+    }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

@@ -162,9 +162,11 @@ class MoELayer:
         All-Gather bytes and times; bus GB/s = bytes / time."""
         out = (C.c_double * 6)()
         check(lib.hep_layer_comm_bench(self.handle, x.data_ptr(), x.shape[0], iters, out, _stream(stream)))
-        r = {"a2a_ms": out[0], "a2a_bytes": out[1], "ag_ms": out[3], "ag_bytes": out[4]}
+        r = {"a2a_ms": out[0], "a2a_bytes": out[1], "ag_ms": out[3], "ag_bytes": out[4], "ag_pull_ms": out[5]}
         r["a2a_bus_gbs"] = r["a2a_bytes"] / (r["a2a_ms"] * 1e6) if r["a2a_ms"] > 0 else None
         r["ag_bus_gbs"] = r["ag_bytes"] / (r["ag_ms"] * 1e6) if r["ag_ms"] > 0 else None
+        # the NVLink transfer of the All-Gather alone (no encode / decode / flags)
+        r["ag_pull_bus_gbs"] = r["ag_bytes"] / (r["ag_pull_ms"] * 1e6) if r["ag_pull_ms"] > 0 else None
         return r
 
     def debug(self, T: int):
