@@ -378,6 +378,7 @@ def main():
     import torch
     import torch.distributed as dist
 
+    from paper_2510_19470_b200 import synthetic
     from paper_2510_19470_b200.moe import Communicator, MoELayer, gather_all
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -415,7 +416,14 @@ def main():
     for li in range(cfg["layers"]):
         layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype, sf=sf, sed=sed, rank=rank,
                          comm=comm, sr=srcfg)
-        layer.set_gate(wg)
+        if li == 0:
+            layer.set_gate(wg)
+        else:
+            # every layer of a stack has its own gate (as the architecture does); one gate
+            # shared by all 8 layers collapses the routing of the chained activations onto a
+            # few experts
+            gl = torch.Generator(device=dev).manual_seed(7 + li)
+            layer.set_gate(synthetic.dyadic((H, E), gl, device=dev))
         if use_sr:
             # shared expert = mean of the population (the reference's init_shared); the demo
             # population shares one base, so every rank computes the same mean locally.
@@ -511,11 +519,14 @@ def main():
     # sources, the slice d = rank is every row this GPU's GEMMs ran (local, received and
     # rows for gathered experts)
     rows = 0
+    rows_per_gpu = [0] * world  # every GPU's GEMM rows per step: the load balance of the routing
     for layer in layers:
         kc = layer.debug(T)["key_counts"].to(dev).long()
         if world > 1:
             dist.all_reduce(kc)
         rows += int(kc[rank * E:(rank + 1) * E].sum().item())
+        for d in range(world):
+            rows_per_gpu[d] += int(kc[d * E:(d + 1) * E].sum().item())
     gemm_ms = sum(v for kname, v in gemm_phases.items() if kname.startswith("gemm_"))
     step_ms_local = ms / args.steps
     assert gemm_ms <= step_ms_local * 1.001, f"GEMM time {gemm_ms:.4f} ms exceeds the step {step_ms_local:.4f} ms"
@@ -679,6 +690,7 @@ def main():
                          "flops_per_launch_pair": flops / cfg["layers"]},
             "kernels": kernels,
             "planner": planner,
+            "gemm_rows_per_gpu": rows_per_gpu,
             "phase_ms": phases,
             "phase_ms_source": "second pass of the same K steps with events at every phase boundary",
             "gpu_launches": launches,
