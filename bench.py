@@ -449,7 +449,9 @@ def main():
             # pulls run on the copy engines under the layers' compute
             gather_all(layers)
         for li, layer in enumerate(layers):
-            layer.forward(acts[li], out=acts[li + 1])
+            # a stack applies each layer on the residual stream, y = x + MoE(x) (the add is
+            # fused into the combine): chained raw MoE outputs would route ever more unevenly
+            layer.forward(acts[li], out=acts[li + 1], residual=len(layers) > 1)
 
     def barrier():
         torch.cuda.synchronize()

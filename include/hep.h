@@ -227,6 +227,10 @@ int hep_layers_gather(hep_layer_t* layers, int n, void* stream);
  * [tokens, H] in the layer dtype, 0 <= tokens <= max_tokens (tokens may differ between
  * GPUs; a GPU with tokens = 0 still takes part and serves its peers' rows). */
 int hep_layer_forward(hep_layer_t layer, const void* x, int64_t tokens, void* y, void* stream);
+/* The step in residual form, y = x + MoE(x) (how a transformer stack applies the layer):
+ * the add is fused into the combine, which accumulates from x's row (one rounding).
+ * y must not alias x. */
+int hep_layer_forward_residual(hep_layer_t layer, const void* x, int64_t tokens, void* y, void* stream);
 /* Same step with host buffers (pinned recommended): H2D copy, forward, D2H copy.
  * Asynchronous and double-buffered: the H2D of the next call and the D2H of the
  * previous one run on the copy engines while this step computes on `stream`.

@@ -144,6 +144,7 @@ SIGNATURES = {
     "hep_layer_gather_experts": [VP, VP],
     "hep_layers_gather": [P(VP), I32, VP],
     "hep_layer_forward": [VP, VP, I64, VP, VP],
+    "hep_layer_forward_residual": [VP, VP, I64, VP, VP],
     "hep_layer_forward_host": [VP, VP, I64, VP, VP],
     "hep_layer_host_fence": [VP, VP],
     "hep_layer_check": [VP, VP],

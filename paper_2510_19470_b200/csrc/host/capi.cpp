@@ -487,6 +487,10 @@ int hep_layers_gather(hep_layer_t* layers, int n, void* stream) {
   });
 }
 
+int hep_layer_forward_residual(hep_layer_t layer, const void* x, int64_t tokens, void* y, void* stream) {
+  return guarded([&] { layer->impl->forward(x, tokens, y, st(stream), true); });
+}
+
 int hep_layer_forward(hep_layer_t layer, const void* x, int64_t tokens, void* y, void* stream) {
   return guarded([&] { layer->impl->forward(x, tokens, y, st(stream)); });
 }

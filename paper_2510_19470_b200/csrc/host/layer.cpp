@@ -577,7 +577,7 @@ void Layer::drop_graphs() {
   graphs_.clear();
 }
 
-bool Layer::forward_graph(const void* x, int64_t T, void* y, cudaStream_t s) {
+bool Layer::forward_graph(const void* x, int64_t T, void* y, cudaStream_t s, bool residual) {
   if (!use_graphs_ || profiling_ || T == 0) return false;
   if (!graph_s_) {
     ck(cudaStreamCreateWithFlags(&graph_s_, cudaStreamNonBlocking), "graph stream");
@@ -589,7 +589,7 @@ bool Layer::forward_graph(const void* x, int64_t T, void* y, cudaStream_t s) {
   ck(cudaStreamWaitEvent(graph_s_, ev_graph_in_, 0), "wait");
   GraphEntry* hit = nullptr;
   for (GraphEntry& e : graphs_)
-    if (e.x == x && e.T == T && e.y == y) hit = &e;
+    if (e.x == x && e.T == T && e.y == y && e.residual == residual) hit = &e;
   if (!hit) {
     if (graphs_.size() >= 4) {  // keep a few (x, T, y) shapes
       cudaGraphExecDestroy(graphs_.front().exec);
@@ -598,7 +598,7 @@ bool Layer::forward_graph(const void* x, int64_t T, void* y, cudaStream_t s) {
     cudaGraph_t g = nullptr;
     ck(cudaStreamBeginCapture(graph_s_, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
-      step(x, T, y, graph_s_);
+      step(x, T, y, graph_s_, residual);
     } catch (...) {
       cudaStreamEndCapture(graph_s_, &g);
       if (g) cudaGraphDestroy(g);
@@ -609,7 +609,7 @@ bool Layer::forward_graph(const void* x, int64_t T, void* y, cudaStream_t s) {
     const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
     cudaGraphDestroy(g);
     ck(e, "graph instantiate");
-    graphs_.push_back(GraphEntry{x, T, y, exec, launches_});
+    graphs_.push_back(GraphEntry{x, T, y, residual, exec, launches_});
     hit = &graphs_.back();
   }
   ck(cudaGraphLaunch(hit->exec, graph_s_), "graph launch");
@@ -1155,16 +1155,17 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
   if (profiling_ == 1) mark("end", s, 1);  // GEMM-only profiling: close the down interval
 }
 
-void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s) {
+void Layer::forward(const void* x, int64_t T, void* y, cudaStream_t s, bool residual) {
   if (T < 0 || T > Tmax_) throw std::invalid_argument("token count must be in [0, max_tokens]");
-  if (!forward_graph(x, T, y, s)) step(x, T, y, s);
+  if (residual && x == y) throw std::invalid_argument("the residual form needs y distinct from x");
+  if (!forward_graph(x, T, y, s, residual)) step(x, T, y, s, residual);
   // A gathered expert whose wire failed to decode (found once that decode has completed)
   // is reported after this rank's share of the collective step is enqueued, so its peers
   // never wait for a rank that bailed out.
   check_migration(false);
 }
 
-void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s) {
+void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s, bool residual) {
   // T = 0 is legal: a rank with an empty batch still takes part in the exchange (it
   // sends no rows, receives its peers' rows and runs their experts).
   if (T < 0 || T > Tmax_) throw std::invalid_argument("token count must be in [0, max_tokens]");
@@ -1253,7 +1254,8 @@ void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s) {
       ck(cudaStreamWaitEvent(s, ev_remote_, 0), "wait");
       mark("combine", s);
       ck(launch_signal_wait(p2p_args_, 2, s), "combine flags");
-      ck(launch_combine(dt_, oall_.p, pos_.as<int>(), topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine");
+      ck(launch_combine(dt_, oall_.p, pos_.as<int>(), topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s,
+                        residual ? x : nullptr), "combine");
     } else {
       ck(launch_permute_p2p(p2p_args_, dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), keys_.as<int>(),
                             ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
@@ -1269,7 +1271,7 @@ void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s) {
       mark("combine", s);
       ck(launch_signal_wait(p2p_args_, 2, s), "combine flags");
       ck(launch_combine_p2p(p2p_args_, dt_, keys_.as<int>(), pos_.as<int>(), key_off_.as<int>(), send_base_.as<int>(),
-                            topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine p2p");
+                            topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s, residual ? x : nullptr), "combine p2p");
     }
     launches_ += 2;
     mark("end", s);
@@ -1290,7 +1292,8 @@ void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s) {
     exchange(false, s);
   }
   mark("combine", s);
-  ck(launch_combine(dt_, oall_.p, pos_.as<int>(), topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s), "combine");
+  ck(launch_combine(dt_, oall_.p, pos_.as<int>(), topk_w_.as<float>(), Ti, static_cast<int>(H_), static_cast<int>(k_), y, s,
+                    residual ? x : nullptr), "combine");
   launches_ += 1;
   mark("end", s);
 }

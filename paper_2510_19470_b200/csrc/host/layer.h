@@ -95,7 +95,8 @@ class Layer {
   // SR mode: SGD step of the owned fp32 masters fused with their encode (wires ready for
   // the next gather); grads[i] flat P fp32 for owned expert rank*n + i.
   void sgd_step(const float* const* grads, int n, float lr, cudaStream_t s);
-  void forward(const void* x, int64_t T, void* y, cudaStream_t s);
+  // residual: y = x + MoE(x) (the transformer residual stream), fused into the combine
+  void forward(const void* x, int64_t T, void* y, cudaStream_t s, bool residual = false);
   void forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s);
   void host_fence(cudaStream_t s);
   // Communication microbenchmark: out = {a2a_ms, a2a_bytes_out, 0, ag_ms, ag_bytes_in, 0}.
@@ -140,7 +141,7 @@ class Layer {
   size_t patch_kmax_ = 0, patch_slot_bytes_ = 0;
   CUtensorMap map_shared_up_, map_shared_down_;
   void decode_gathered(size_t wire_bytes, size_t stride, cudaStream_t s);
-  void step(const void* x, int64_t T, void* y, cudaStream_t s);  // forward's enqueue
+  void step(const void* x, int64_t T, void* y, cudaStream_t s, bool residual);  // forward's enqueue
   // One-GPU layers replay the step as a CUDA graph, one per (x, T, y); any weight change
   // drops them.  Launched on graph_s_ with event joins to the caller's stream (capture on
   // the legacy default stream is not allowed).
@@ -148,6 +149,7 @@ class Layer {
     const void* x;
     int64_t T;
     void* y;
+    bool residual;
     cudaGraphExec_t exec;
     int launches;
   };
@@ -156,7 +158,7 @@ class Layer {
   cudaStream_t graph_s_ = nullptr;
   cudaEvent_t ev_graph_in_ = nullptr, ev_graph_out_ = nullptr;
   void drop_graphs();
-  bool forward_graph(const void* x, int64_t T, void* y, cudaStream_t s);
+  bool forward_graph(const void* x, int64_t T, void* y, cudaStream_t s, bool residual);
   void gather(cudaStream_t s);                                     // gather_experts' enqueue
 
   // shape

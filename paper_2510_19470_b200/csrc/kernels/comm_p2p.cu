@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(256) combine_p2p_kernel(P2PArgs a, const int* 
                                                           const int* __restrict__ key_off,
                                                           const int* __restrict__ send_base,
                                                           const float* __restrict__ w, int T_tok, int H, int k,
-                                                          void* __restrict__ y, int seg) {
+                                                          void* __restrict__ y, int seg,
+                                                          const void* __restrict__ residual) {
   const int lane = threadIdx.x & 31;
   const int eb = BF16 ? 2 : 4;
   int t, sg, v0, v1;
@@ -242,6 +243,16 @@ __global__ void __launch_bounds__(256) combine_p2p_kernel(P2PArgs a, const int* 
   }
   for (int v = v0 + lane; v < v1; v += 32) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (residual) {  // y = x + sum
+      const uint4 r = *reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(residual) +
+                                                      static_cast<size_t>(t) * H * eb + 16 * v);
+      if (BF16) {
+        unpack8(r, acc);
+      } else {
+        acc[0] = __uint_as_float(r.x); acc[1] = __uint_as_float(r.y);
+        acc[2] = __uint_as_float(r.z); acc[3] = __uint_as_float(r.w);
+      }
+    }
     for (int j = 0; j < k; ++j) {
       const uint4 r = *reinterpret_cast<const uint4*>(row[j] + 16 * v);
       if (BF16) {
@@ -368,14 +379,16 @@ cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool 
 
 cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, const int* pos, const int* key_off,
                                const int* send_base, const float* w, int T, int H, int k, void* y,
-                               cudaStream_t s) {
+                               cudaStream_t s, const void* residual) {
   if (k > 8) return cudaErrorInvalidValue;
   if (T == 0) return cudaSuccess;
   const int seg = row_segments(T, H * dtype_bytes(dt) / 16);
   if (dt == DType::BF16)
-    combine_p2p_kernel<true><<<(T * seg + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y, seg);
+    combine_p2p_kernel<true><<<(T * seg + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y, seg,
+                                                                residual);
   else
-    combine_p2p_kernel<false><<<(T * seg + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y, seg);
+    combine_p2p_kernel<false><<<(T * seg + 7) / 8, 256, 0, s>>>(a, keys, pos, key_off, send_base, w, T, H, k, y, seg,
+                                                                 residual);
   return cudaGetLastError();
 }
 

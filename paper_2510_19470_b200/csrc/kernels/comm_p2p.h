@@ -50,7 +50,7 @@ cudaError_t launch_signal_wait(const P2PArgs& a, int slot, cudaStream_t s, bool 
 const uint32_t* p2p_dispatch_flags(const P2PArgs& a);
 cudaError_t launch_combine_p2p(const P2PArgs& a, DType dt, const int* keys, const int* pos, const int* key_off,
                                const int* send_base, const float* w, int T, int H, int k, void* y,
-                               cudaStream_t s);
+                               cudaStream_t s, const void* residual = nullptr);
 
 // Shared-expert refresh across the ranks (comm_p2p.cu): the fp64 sum over every expert in
 // expert order as a chain over ranks 0..G-1, chunked so the ranks pipeline.

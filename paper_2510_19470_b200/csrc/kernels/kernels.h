@@ -70,9 +70,10 @@ cudaError_t launch_permute(DType dt, const void* x, int T, int H, int k, int NK,
 cudaError_t launch_positions(int T, int k, int NK, const int* keys, const int* ranks, const int* chunk_off,
                              const int* key_off, int* pos, cudaStream_t stream);
 
-// y[t] = sum_j w[t,j] * out[pos[t,j]]  (slot order, fp32 accumulate).
+// y[t] = sum_j w[t,j] * out[pos[t,j]]  (slot order, fp32 accumulate); with residual:
+// y[t] = residual[t] + that sum, accumulated from the residual (one rounding at the end).
 cudaError_t launch_combine(DType dt, const void* out, const int* pos, const float* topk_w, int T,
-                           int H, int k, void* y, cudaStream_t stream);
+                           int H, int k, void* y, cudaStream_t stream, const void* residual = nullptr);
 
 // ----------------------------------------------------------------- expert GEMM
 struct GroupTable {

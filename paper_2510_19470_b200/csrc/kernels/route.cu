@@ -852,7 +852,8 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
                                                            const int* __restrict__ pos,
                                                            const float* __restrict__ w, int T_tok,
                                                            int H, int k,
-                                                           __nv_bfloat16* __restrict__ y, int seg) {
+                                                           __nv_bfloat16* __restrict__ y, int seg,
+                                                           const __nv_bfloat16* __restrict__ residual) {
   const int lane = threadIdx.x & 31;
   const int vecs = H >> 3;
   int t, sg, v0, v1;
@@ -866,6 +867,7 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
   }
   for (int v = v0 + lane; v < v1; v += 32) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (residual) unpack8(ld_nc_v4(residual + static_cast<size_t>(t) * H + 8 * v), acc);  // y = x + sum
     for (int j = 0; j < k; ++j) {
       float f[8];
       unpack8(ld_nc_v4(out + static_cast<size_t>(p[j]) * H + 8 * v), f);
@@ -879,7 +881,8 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
 __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restrict__ out,
                                                           const int* __restrict__ pos,
                                                           const float* __restrict__ w, int T_tok,
-                                                          int H, int k, float* __restrict__ y, int seg) {
+                                                          int H, int k, float* __restrict__ y, int seg,
+                                                          const float* __restrict__ residual) {
   const int lane = threadIdx.x & 31;
   const int vecs = H >> 2;
   int t, sg, v0, v1;
@@ -895,7 +898,8 @@ __global__ void __launch_bounds__(256) combine_f32_kernel(const float* __restric
     }
   }
   for (int v = v0 + lane; v < v1; v += 32) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 acc = residual ? reinterpret_cast<const float4*>(residual + static_cast<size_t>(t) * H)[v]
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < kMaxK; ++j) {
       if (j >= k) break;
@@ -1075,7 +1079,7 @@ cudaError_t launch_positions(int T, int k, int NK, const int* keys, const int* r
 }
 
 cudaError_t launch_combine(DType dt, const void* out, const int* pos, const float* topk_w, int T,
-                           int H, int k, void* y, cudaStream_t stream) {
+                           int H, int k, void* y, cudaStream_t stream, const void* residual) {
   if (T == 0) return cudaSuccess;
   const int seg = row_segments(T, H * dtype_bytes(dt) / 16);
   const int blocks = (T * seg + 7) / 8;
@@ -1083,11 +1087,13 @@ cudaError_t launch_combine(DType dt, const void* out, const int* pos, const floa
     if (H % 8) return cudaErrorInvalidValue;
     combine_bf16_kernel<<<blocks, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(out), pos,
                                                     topk_w, T, H, k,
-                                                    static_cast<__nv_bfloat16*>(y), seg);
+                                                    static_cast<__nv_bfloat16*>(y), seg,
+                                                    static_cast<const __nv_bfloat16*>(residual));
   } else {
     if (H % 4) return cudaErrorInvalidValue;
     combine_f32_kernel<<<blocks, 256, 0, stream>>>(static_cast<const float*>(out), pos, topk_w, T,
-                                                   H, k, static_cast<float*>(y), seg);
+                                                   H, k, static_cast<float*>(y), seg,
+                                                   static_cast<const float*>(residual));
   }
   return cudaGetLastError();
 }

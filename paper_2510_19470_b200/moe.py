@@ -132,11 +132,14 @@ class MoELayer:
     def gather_experts(self, stream=None):
         check(lib.hep_layer_gather_experts(self.handle, _stream(stream)))
 
-    def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None,
+                residual: bool = False) -> torch.Tensor:
+        """y = MoE(x); with residual=True, y = x + MoE(x) (the add fused into the combine)."""
         assert x.is_cuda and x.dtype == self.dtype and x.shape[-1] == self.H and x.is_contiguous()
         T = x.shape[0]
         y = out if out is not None else torch.empty_like(x)
-        check(lib.hep_layer_forward(self.handle, x.data_ptr(), T, y.data_ptr(), _stream(stream)))
+        fn = lib.hep_layer_forward_residual if residual else lib.hep_layer_forward
+        check(fn(self.handle, x.data_ptr(), T, y.data_ptr(), _stream(stream)))
         return y
 
     __call__ = forward

@@ -213,3 +213,30 @@ def test_layer_graph_replay_matches_eager(dtype):
     assert np.abs(y.float().cpu().numpy() - ref2["y"][0]).max() <= (
         tol.BF16_VS_MIRROR_MAX if dtype == torch.bfloat16 else tol.F32_MAX) * np.abs(ref2["y"][0]).max()
     layer.close()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
+def test_layer_residual_form(dtype):
+    """hep_layer_forward_residual: y = x + MoE(x) with the add fused into the combine,
+    against the fp32 reference + x (bf16: tests/tolerances.py BF16_VS_FP32_*)."""
+    H, F, E, k, T = 512, 1024, 8, 2, 300
+    g = torch.Generator().manual_seed(23)
+    x = synthetic.dyadic((T, H), g, dtype=dtype)
+    wg = synthetic.dyadic((H, E), g)
+    w_up, w_down = synthetic.experts(E, H, F, g, dtype=dtype)
+    layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype)
+    layer.set_gate(wg.cuda())
+    for e in range(E):
+        layer.set_expert(e, w_up[e].cuda(), w_down[e].cuda())
+    y = layer.forward(x.cuda(), residual=True).float().cpu().numpy()
+    torch.cuda.synchronize()
+    layer.close()
+    bf16 = dtype == torch.bfloat16
+    ref = oracle.moe_layer(x.float().numpy()[None], wg.numpy(), w_up.float().numpy(), w_down.float().numpy(), k, [1],
+                           [1], bf16=bf16, exact=bf16)
+    want = ref["y"][0] + x.float().numpy()
+    m, mean = tol.rel_errors(y, want)
+    if bf16:
+        assert m <= tol.BF16_VS_FP32_MAX and mean <= tol.BF16_VS_FP32_MEAN, (m, mean)
+    else:
+        assert m <= tol.F32_MAX, m

@@ -40,6 +40,9 @@ CASES = [
     ([2, 2], [2, 1], ["--ragged", "--sr"]),
     ([2, 4], [1, 2], ["--ragged"]),
     ([2, 2], [1, 1], ["--ragged", "--dtype", "f32", "--E", "16", "--k", "4"]),
+    # the residual form y = x + MoE(x), fused into the combine (bf16 local combine, fp32 p2p combine)
+    ([2, 2], [1, 2], ["--residual"]),
+    ([2], [1], ["--residual", "--dtype", "f32", "--H", "1024", "--F", "4096", "--T", "512"]),
     # weights rewritten between steps while peers pull them (dense and SR All-Gather)
     ([2, 4], [1, 4], ["--update"]),
     ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr", "--update"]),

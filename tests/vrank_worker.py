@@ -53,6 +53,8 @@ def main():
     ap.add_argument("--corrupt", action="store_true")
     ap.add_argument("--mismatch", action="store_true")
     ap.add_argument("--sgd", action="store_true")
+    ap.add_argument("--residual", action="store_true",
+                    help="also run the residual form y = x + MoE(x) and check it against the plain step + x")
     ap.add_argument("--dump", default="", help="save every rank's first-step output (bf16 bits) to this .npy")
     a = ap.parse_args()
 
@@ -166,6 +168,23 @@ def main():
 
     for counts in plan:
         step(counts, w_up, w_down, flat, shared)
+    if a.residual:
+        plain, res = [None] * G, [None] * G
+        xs = [x_all[r].cuda() for r in range(G)]
+        for r in range(G):
+            with torch.cuda.stream(streams[r]):
+                plain[r] = layers[r].forward(xs[r], stream=streams[r])
+        for r in range(G):
+            with torch.cuda.stream(streams[r]):
+                res[r] = layers[r].forward(xs[r], stream=streams[r], residual=True)
+        torch.cuda.synchronize()
+        for r in range(G):
+            want = xs[r].double() + plain[r].double()
+            d = (res[r].double() - want).abs()
+            # one rounding of x + sum vs the plain step's rounding of the sum
+            bound = (2.0 ** -8 if bf16 else 2.0 ** -22) * (plain[r].double().abs() + res[r].double().abs()) + 1e-30
+            assert bool((d <= bound).all()), (r, float(d.max()))
+        print("residual ok", flush=True)
     if a.sgd:
         assert a.sr
         lr = 2.0 ** -7
