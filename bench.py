@@ -522,13 +522,16 @@ def main():
     # rows for gathered experts)
     rows = 0
     rows_per_gpu = [0] * world  # every GPU's GEMM rows per step: the load balance of the routing
+    layer_imbalance = []        # per layer: max over GPUs of its GEMM rows / the mean
     for layer in layers:
         kc = layer.debug(T)["key_counts"].to(dev).long()
         if world > 1:
             dist.all_reduce(kc)
         rows += int(kc[rank * E:(rank + 1) * E].sum().item())
+        per = [int(kc[d * E:(d + 1) * E].sum().item()) for d in range(world)]
         for d in range(world):
-            rows_per_gpu[d] += int(kc[d * E:(d + 1) * E].sum().item())
+            rows_per_gpu[d] += per[d]
+        layer_imbalance.append(max(per) * world / max(1, sum(per)))
     gemm_ms = sum(v for kname, v in gemm_phases.items() if kname.startswith("gemm_"))
     step_ms_local = ms / args.steps
     assert gemm_ms <= step_ms_local * 1.001, f"GEMM time {gemm_ms:.4f} ms exceeds the step {step_ms_local:.4f} ms"
@@ -693,6 +696,7 @@ def main():
             "kernels": kernels,
             "planner": planner,
             "gemm_rows_per_gpu": rows_per_gpu,
+            "layer_load_imbalance": layer_imbalance,
             "phase_ms": phases,
             "phase_ms_source": "second pass of the same K steps with events at every phase boundary",
             "gpu_launches": launches,
