@@ -184,6 +184,7 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
   if (dt_ == DType::BF16) {
     ck(make_tmap_bf16_2d(&map_a1_, xall_.p, rows_cap_, H_, 128, 64), "tmap a1");
     cta_pair_ = gemm_use_cta_pair();
+    tile_counters_.alloc(2 * sizeof(int));
     const uint32_t b_box = cta_pair_ ? 128 : 256;
     ck(make_tmap_bf16_2d(&map_b1_, w_up_c_.p, slots_ * F_, H_, b_box, 64), "tmap b1");
     ck(make_tmap_bf16_2d(&map_a2_, hbuf_.p, rows_cap_, F_, 128, 64), "tmap a2");
@@ -1127,10 +1128,24 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
        "gemm down (fused decode)");
   } else if (dt_ == DType::BF16) {
     mark(up.c_str(), s, 1);
-    auto gemm = cta_pair_ ? launch_grouped_gemm_bf16_2cta : launch_grouped_gemm_bf16;
-    ck(gemm(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_), "gemm up");
-    mark(down.c_str(), s, 1);
-    ck(gemm(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_), static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_), "gemm down");
+    if (cta_pair_) {
+      int* ctr = tile_counters_.as<int>();  // dynamic tile scheduler counters (zeroed in-stream per launch)
+      ck(launch_grouped_gemm_bf16_2cta(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_),
+                                       static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_, ctr),
+         "gemm up");
+      mark(down.c_str(), s, 1);
+      ck(launch_grouped_gemm_bf16_2cta(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_),
+                                       static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_, ctr + 1),
+         "gemm down");
+    } else {
+      ck(launch_grouped_gemm_bf16(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_),
+                                  static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_),
+         "gemm up");
+      mark(down.c_str(), s, 1);
+      ck(launch_grouped_gemm_bf16(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_),
+                                  static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_),
+         "gemm down");
+    }
   } else if (tf32_) {
     mark(up.c_str(), s, 1);
     split_dirty_slots(s);

@@ -196,6 +196,7 @@ class Layer {
   void split_dirty_slots(cudaStream_t s);
   void mark_gathered_dirty();
   uint32_t sched_up_ = 0, sched_down_ = 0;
+  DevBuf tile_counters_;  // dynamic tile scheduler of the CTA-pair GEMM (up, down)
   bool cta_pair_ = true;
 
   // NVLink peer-memory path (default for G > 1; HEP_COMM=nccl selects the NCCL baseline)

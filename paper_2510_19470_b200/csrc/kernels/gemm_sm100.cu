@@ -384,6 +384,9 @@ struct SmemCtl2 {
   uint64_t patched[P_STAGES_MAX];  // PATCH (leader): both CTAs' B halves patched
   uint64_t tfull[ACC];
   uint64_t tempty[ACC];
+  uint64_t tq_full[4];   // DYN: tile queue slot published (both CTAs)
+  uint64_t tq_empty[4];  // DYN (leader): every consumer of both CTAs has read the slot
+  int tile_q[4];
   uint32_t tmem_base;
   int num_tiles;
   int tile_start[kMaxGroups + 1];
@@ -393,6 +396,32 @@ struct SmemCtl2 {
   __nv_bfloat16* out[kMaxGroups];
   int wait[kMaxGroups];
 };
+constexpr int kTileQ = 4;
+constexpr int kTileQConsumers = 1 + 1 + 8;  // peer producer, MMA issuer, 4 epilogue warps x 2 CTAs
+
+// Cluster-scope tile-queue primitives (dynamic tile scheduler).
+__device__ __forceinline__ uint32_t peer_smem_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
 
 constexpr size_t kSmemBytes2 = 1024 + P_STAGES * P_STAGE_BYTES + P_STG_BYTES + sizeof(SmemCtl2);
 // PATCH: six operand stages + patch blocks, no epilogue staging buffer (direct stores)
@@ -426,7 +455,12 @@ __device__ __forceinline__ int find_group2(const SmemCtl2& s, int ng, int tile) 
 // lets the CTAs drift apart, their L2 sharing drops (DRAM reads 5.1 -> 7.0 GB), the SM
 // clock falls under the power cap (1.38 -> 1.31 GHz) and the launch slows 4%
 // (profiles/r2_gemm_power.md).
-template <bool PATCH, int NST_T = P_STAGES, bool DIRECT_T = false>
+// DYN: dynamic tile scheduler.  Instead of the static round-robin (tile = cluster +
+// i * clusters), the leader's producer takes the next tile from a global counter and
+// publishes it to a 4-slot queue in both CTAs' shared memory; every role of both CTAs
+// reads its tiles from that queue.  Clusters that run ahead take the next tiles, so the
+// tiles in flight stay a compact window of the raster and keep sharing L2 lines.
+template <bool PATCH, int NST_T = P_STAGES, bool DIRECT_T = false, bool DYN = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (PATCH ? 32 * kConvWarps : 0), 1)
 grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                               __nv_bfloat16* __restrict__ C, int ldc, int N, int K,
@@ -434,7 +468,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
                               const int* __restrict__ g_slot, const unsigned long long* __restrict__ g_out,
                               const int* __restrict__ g_wait, const uint32_t* __restrict__ wait_flags,
                               uint32_t epoch, int ng, int relu, uint32_t sched, uint64_t timeout_ns,
-                              const PatchArgs patches, int half) {
+                              const PatchArgs patches, int half, int* __restrict__ tile_counter) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -491,6 +525,10 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
       mbar_init(&s.bfull[i], 1);
       mbar_init(&s.patched[i], 2);  // one converter per CTA
     }
+    for (int i = 0; i < kTileQ; ++i) {
+      mbar_init(&s.tq_full[i], 1);
+      mbar_init(&s.tq_empty[i], kTileQConsumers);
+    }
     for (int i = 0; i < ACC; ++i) {
       mbar_init(&s.tfull[i], 1);
       mbar_init(&s.tempty[i], 8);  // 4 epilogue warps x 2 CTAs (used in the leader)
@@ -505,6 +543,39 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
 
   const int total = s.num_tiles;
   const uint32_t tmem_base = s.tmem_base;
+  // The tile sequence of this cluster: static round-robin, or (DYN) the shared queue.
+  // i counts this role's tiles; returns -1 when the cluster has no more.
+  int prefetched = -2;  // DYN publisher: the next tile id, fetched one tile ahead
+  auto next_tile = [&](int& i, bool publisher) -> int {
+    if (!DYN) {
+      const int t = cluster + i * nclusters;
+      ++i;
+      return t < total ? t : -1;
+    }
+    const int q = i % kTileQ;
+    const uint32_t ph = static_cast<uint32_t>(i / kTileQ) & 1u;
+    ++i;
+    if (publisher) {  // leader producer: take the next tile, publish it to both CTAs
+      if (prefetched == -2) prefetched = atomicAdd(tile_counter, 1);
+      int t = prefetched;
+      if (t >= total) t = -1;
+      // the following tile's id is fetched now, so the atomic's round trip overlaps this tile
+      if (t >= 0) prefetched = atomicAdd(tile_counter, 1);
+      mbar_wait(&s.tq_empty[q], ph ^ 1u);
+      s.tile_q[q] = t;
+      st_cluster_u32(peer_smem_addr(&s.tile_q[q], 1), t);
+      mbar_arrive_remote(peer_smem_addr(&s.tq_full[q], 0));
+      mbar_arrive_remote(peer_smem_addr(&s.tq_full[q], 1));
+      return t;
+    }
+    mbar_wait_cluster(&s.tq_full[q], ph);
+    const int t = *reinterpret_cast<volatile int*>(&s.tile_q[q]);
+    return t;
+  };
+  // a consumer has read slot (i - 1): release it to the publisher (one arrival per role)
+  auto release_tile = [&](int i) {
+    if (DYN) mbar_arrive_remote(peer_smem_addr(&s.tq_empty[(i - 1) % kTileQ], 0));
+  };
 
   if (PATCH && warp >= 6) {
     // ================= converters (fused SR decode), both CTAs =================
@@ -563,7 +634,9 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
       const uint64_t pol_b = make_policy((sched >> 2) & 3u);
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < total; tile += nclusters) {
+      int ti = 0;
+      for (int tile = next_tile(ti, cta == 0); tile >= 0; tile = next_tile(ti, cta == 0)) {
+        if (cta != 0) release_tile(ti);
         const int g = find_group2(s, ng, tile);
         const int local = tile - s.tile_start[g];
         const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
@@ -606,7 +679,9 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster; tile < total; tile += nclusters) {
+      int ti = 0;
+      for (int tile = next_tile(ti, false); tile >= 0; tile = next_tile(ti, false)) {
+        release_tile(ti);
         const int g = find_group2(s, ng, tile);
         const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
         int mt, nt;
@@ -638,7 +713,10 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
     uint8_t* stg = stage_out + quarter * 32 * P_STG_PITCH;  // this warp's 32 staged rows
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = cluster; tile < total; tile += nclusters) {
+    int ti = 0;
+    for (int tile = next_tile(ti, false); tile >= 0; tile = next_tile(ti, false)) {
+      __syncwarp();
+      if (lane == 0) release_tile(ti);
       const int g = find_group2(s, ng, tile);
       const int local = tile - s.tile_start[g];
       const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
@@ -1189,18 +1267,27 @@ cudaError_t launch_grouped_gemm_bf16_patched(const CUtensorMap& map_a, const CUt
 
 cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C, int ldc,
                                           int N, int K, const GroupTable& groups, int relu, int num_sms,
-                                          cudaStream_t stream, uint32_t sched) {
+                                          cudaStream_t stream, uint32_t sched, int* tile_counter) {
   if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0) return cudaErrorInvalidValue;
   // HEP_GEMM_STAGES = 4 | 5 (default) | 6 (six stages, direct-store epilogue; local outputs only)
   const char* st_env = std::getenv("HEP_GEMM_STAGES");
   int stages = st_env ? std::atoi(st_env) : 5;
   if (stages == 6 && groups.out != nullptr) stages = 5;
   if (stages != 4 && stages != 6) stages = 5;
-  static DeviceOnce attr4, attr5, attr6;
-  DeviceOnce& once = stages == 4 ? attr4 : (stages == 6 ? attr6 : attr5);
+  // HEP_GEMM_DYN=1: the dynamic tile scheduler (needs the caller's counter).  Measured
+  // (profiles/r2_gemm_power.md): on the cfg3 down-projection it cuts DRAM reads 21% and
+  // raises the power-capped clock, but the tensor pipe idles more at tile boundaries; on
+  // the up-projection it loses 4%.  Off by default.
+  const char* dyn_env = std::getenv("HEP_GEMM_DYN");
+  const bool dyn = tile_counter != nullptr && dyn_env && dyn_env[0] == '1' && stages == 5;
+  static DeviceOnce attr4, attr5, attr6, attr5d;
+  DeviceOnce& once = dyn ? attr5d : (stages == 4 ? attr4 : (stages == 6 ? attr6 : attr5));
   if (!once.done()) {
     cudaError_t e;
-    if (stages == 4)
+    if (dyn)
+      e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, 5, false, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes2));
+    else if (stages == 4)
       e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, 4, false>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes2Four));
     else if (stages == 6)
@@ -1212,14 +1299,20 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
     if (e != cudaSuccess) return e;
     once.set();
   }
+  if (dyn) {
+    const cudaError_t e = cudaMemsetAsync(tile_counter, 0, sizeof(int), stream);
+    if (e != cudaSuccess) return e;
+  }
   const int grid = (num_sms / 2) * 2;
-#define HEP_LAUNCH_2CTA(ST, DIR, SMEM)                                                                               \
-  grouped_gemm_bf16_2cta_kernel<false, ST, DIR><<<grid, kThreads, SMEM, stream>>>(                                  \
+#define HEP_LAUNCH_2CTA(ST, DIR, DY, SMEM)                                                                           \
+  grouped_gemm_bf16_2cta_kernel<false, ST, DIR, DY><<<grid, kThreads, SMEM, stream>>>(                              \
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot, groups.out, \
-      groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns, PatchArgs{}, 0)
-  if (stages == 4) HEP_LAUNCH_2CTA(4, false, kSmemBytes2Four);
-  else if (stages == 6) HEP_LAUNCH_2CTA(6, true, kSmemBytes2Deep);
-  else HEP_LAUNCH_2CTA(5, false, kSmemBytes2);
+      groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns, PatchArgs{}, \
+      0, tile_counter)
+  if (dyn) HEP_LAUNCH_2CTA(5, false, true, kSmemBytes2);
+  else if (stages == 4) HEP_LAUNCH_2CTA(4, false, false, kSmemBytes2Four);
+  else if (stages == 6) HEP_LAUNCH_2CTA(6, true, false, kSmemBytes2Deep);
+  else HEP_LAUNCH_2CTA(5, false, false, kSmemBytes2);
 #undef HEP_LAUNCH_2CTA
   return cudaGetLastError();
 }
@@ -1242,7 +1335,7 @@ cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, cons
   grouped_gemm_bf16_2cta_kernel<true><<<grid, kThreads + 32 * kConvWarps, kSmemBytes2Patch, stream>>>(
       map_a, map_shared_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
       groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
-      patches, half);
+      patches, half, nullptr);
   return cudaGetLastError();
 }
 
@@ -1258,6 +1351,8 @@ cudaError_t preload_gemm_sm100_kernels() {
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 4, false>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 5, false>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 6, true>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 5, false, true>)))
+    return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<true>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(ksplit_reduce_kernel))) return e;

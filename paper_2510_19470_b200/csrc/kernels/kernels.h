@@ -141,9 +141,11 @@ cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, cons
                                                   const PatchArgs& patches, int half, int relu, int num_sms,
                                                   cudaStream_t stream, uint32_t sched = 0x6u);
 // CTA-pair variant (cta_group::2, 256x256 cluster tiles); B's tensor map box is 128 rows.
+// tile_counter (one device int per in-flight launch, zeroed by the launcher) enables the
+// dynamic tile scheduler under HEP_GEMM_DYN=1; otherwise the static round-robin.
 cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C, int ldc,
                                           int N, int K, const GroupTable& groups, int relu, int num_sms,
-                                          cudaStream_t stream, uint32_t sched = 0x6u);
+                                          cudaStream_t stream, uint32_t sched = 0x6u, int* tile_counter = nullptr);
 // CTA-pair GEMM unless HEP_GEMM_2CTA=0 (the 1-CTA kernel stays for A/B comparisons).
 bool gemm_use_cta_pair();
 // Schedule for one expert GEMM shape: A operand reused across n-tiles is kept in L2

@@ -56,11 +56,14 @@ def main():
 
     run("up", 0x2)  # h = relu(x w_up): the down-projection's real A operand
     torch.cuda.synchronize()
-    variants = [(int(v.split(":")[0], 16), v.split(":")[1]) for v in a.variants.split(",")]
+    # sched:stages[:dyn]
+    variants = [(int(v.split(":")[0], 16), v.split(":")[1], v.split(":")[2] if v.count(":") > 1 else "1")
+                for v in a.variants.split(",")]
     res = {v: [] for v in variants}
     for _ in range(a.rounds):
         for v in variants:
             os.environ["HEP_GEMM_STAGES"] = v[1]
+            os.environ["HEP_GEMM_DYN"] = v[2]
             ts = []
             for _ in range(3):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -72,7 +75,7 @@ def main():
             res[v].append(statistics.median(ts))
     for v in variants:
         ms = statistics.median(res[v])
-        print(json.dumps({"proj": a.proj, "sched": hex(v[0]), "stages": v[1], "ms": ms, "tflops": flops / ms / 1e9,
+        print(json.dumps({"proj": a.proj, "sched": hex(v[0]), "stages": v[1], "dyn": v[2], "ms": ms, "tflops": flops / ms / 1e9,
                           "rounds_ms": [round(t, 3) for t in res[v]], "data": a.data}), flush=True)
 
 

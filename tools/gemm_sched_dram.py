@@ -14,8 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2510_19470_b200._lib import HEP_BF16, check, lib  # noqa: E402
 
-UP_VARIANTS = [(0x2, "5"), (0x2, "4"), (0x2, "6")]
-VARIANTS = [(0x822, "5"), (0x822, "4"), (0x822, "6"), (0x422, "4"), (0x1022, "4"), (0x2, "4"), (0x2, "5")]
+UP_VARIANTS = [(0x2, "5", "0"), (0x2, "5", "1")]
+VARIANTS = [(0x822, "5", "0"), (0x822, "5", "1"), (0x2, "5", "1"), (0x422, "5", "1"), (0x822, "4", "0")]
 
 
 def main():
@@ -32,18 +32,20 @@ def main():
     x = (torch.randint(-8, 9, (E * R, H), generator=g, device="cuda").float() / 16).to(torch.bfloat16)
     wu = torch.cat([((torch.rand(F, H, generator=g, device="cuda") * 2 - 1) / 64) for _ in range(E)]).to(torch.bfloat16)
     hh = torch.empty(E * R, F, dtype=torch.bfloat16, device="cuda")
-    for sched, stages in UP_VARIANTS:
+    for sched, stages, dyn in UP_VARIANTS:
         os.environ["HEP_GEMM_STAGES"] = stages
+        os.environ["HEP_GEMM_DYN"] = dyn
         check(lib.hep_grouped_gemm(HEP_BF16, x.data_ptr(), E * R, wu.data_ptr(), E, hh.data_ptr(), F, H,
                                    starts.data_ptr(), rows.data_ptr(), slots.data_ptr(), E, 1, sched, st))
         torch.cuda.synchronize()
-        print("up variant", hex(sched), "stages", stages, flush=True)
-    for sched, deep in VARIANTS:
+        print("up variant", hex(sched), "stages", stages, "dyn", dyn, flush=True)
+    for sched, deep, dyn in VARIANTS:
         os.environ["HEP_GEMM_STAGES"] = deep
+        os.environ["HEP_GEMM_DYN"] = dyn
         check(lib.hep_grouped_gemm(HEP_BF16, h.data_ptr(), E * R, wd.data_ptr(), E, y.data_ptr(), H, F,
                                    starts.data_ptr(), rows.data_ptr(), slots.data_ptr(), E, 0, sched, st))
         torch.cuda.synchronize()
-        print("variant", hex(sched), "stages", deep, flush=True)
+        print("variant", hex(sched), "stages", deep, "dyn", dyn, flush=True)
 
 
 if __name__ == "__main__":
