@@ -198,21 +198,18 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
       xlo_.alloc(fb * rows_cap_ * H_);
       hhi_.alloc(fb * rows_cap_ * F_);
       hlo_.alloc(fb * rows_cap_ * F_);
-      // weights as tf32 hi/lo in the GEMM's tiled B layout (one contiguous block per stage)
-      const int64_t up_t = tf32_tiled_elems(static_cast<int>(slots_), static_cast<int>(F_), static_cast<int>(H_));
-      const int64_t dn_t = tf32_tiled_elems(static_cast<int>(slots_), static_cast<int>(H_), static_cast<int>(F_));
-      wuhi_.alloc(fb * up_t);
-      wulo_.alloc(fb * up_t);
-      wdhi_.alloc(fb * dn_t);
-      wdlo_.alloc(fb * dn_t);
+      wuhi_.alloc(fb * slots_ * F_ * H_);
+      wulo_.alloc(fb * slots_ * F_ * H_);
+      wdhi_.alloc(fb * slots_ * H_ * F_);
+      wdlo_.alloc(fb * slots_ * H_ * F_);
       ck(make_tmap_f32_2d(&t_xhi_, xhi_.p, rows_cap_, H_, 128, kTf32BK), "tmap xhi");
       ck(make_tmap_f32_2d(&t_xlo_, xlo_.p, rows_cap_, H_, 128, kTf32BK), "tmap xlo");
       ck(make_tmap_f32_2d(&t_hhi_, hhi_.p, rows_cap_, F_, 128, kTf32BK), "tmap hhi");
       ck(make_tmap_f32_2d(&t_hlo_, hlo_.p, rows_cap_, F_, 128, kTf32BK), "tmap hlo");
-      ck(make_tmap_f32_2d(&t_wuhi_, wuhi_.p, up_t / kTf32BK, kTf32BK, 256, kTf32BK), "tmap wuhi");
-      ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, up_t / kTf32BK, kTf32BK, 256, kTf32BK), "tmap wulo");
-      ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, dn_t / kTf32BK, kTf32BK, 256, kTf32BK), "tmap wdhi");
-      ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, dn_t / kTf32BK, kTf32BK, 256, kTf32BK), "tmap wdlo");
+      ck(make_tmap_f32_2d(&t_wuhi_, wuhi_.p, slots_ * F_, H_, 256, kTf32BK), "tmap wuhi");
+      ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, slots_ * F_, H_, 256, kTf32BK), "tmap wulo");
+      ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, slots_ * H_, F_, 256, kTf32BK), "tmap wdhi");
+      ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, slots_ * H_, F_, 256, kTf32BK), "tmap wdlo");
       // split-K when (groups x m-tiles x n-tiles) of an even routing leaves SMs idle
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
@@ -757,18 +754,14 @@ void Layer::mark_gathered_dirty() {
 
 void Layer::split_dirty_slots(cudaStream_t s) {
   const int64_t per = F_ * H_;
-  const int64_t up_slot = tf32_tiled_elems(1, static_cast<int>(F_), static_cast<int>(H_));
-  const int64_t dn_slot = tf32_tiled_elems(1, static_cast<int>(H_), static_cast<int>(F_));
   for (int64_t a = 0; a < slots_;) {
     if (!slot_dirty_[static_cast<size_t>(a)]) { ++a; continue; }
     int64_t b = a;
     while (b < slots_ && slot_dirty_[static_cast<size_t>(b)]) slot_dirty_[static_cast<size_t>(b++)] = 0;
-    ck(launch_split_tf32_tiled(w_up_c_.as<float>() + a * per, wuhi_.as<float>() + a * up_slot,
-                               wulo_.as<float>() + a * up_slot, static_cast<int>(b - a), static_cast<int>(F_),
-                               static_cast<int>(H_), s), "split w_up");
-    ck(launch_split_tf32_tiled(w_down_c_.as<float>() + a * per, wdhi_.as<float>() + a * dn_slot,
-                               wdlo_.as<float>() + a * dn_slot, static_cast<int>(b - a), static_cast<int>(H_),
-                               static_cast<int>(F_), s), "split w_down");
+    ck(launch_split_tf32(w_up_c_.as<float>() + a * per, wuhi_.as<float>() + a * per, wulo_.as<float>() + a * per,
+                         (b - a) * per, s), "split w_up");
+    ck(launch_split_tf32(w_down_c_.as<float>() + a * per, wdhi_.as<float>() + a * per,
+                         wdlo_.as<float>() + a * per, (b - a) * per, s), "split w_down");
     launches_ += 2;
     a = b;
   }
@@ -1159,12 +1152,12 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     ck(launch_split_tf32(xall_.as<float>(), xhi_.as<float>(), xlo_.as<float>(), rows_cap_ * H_, s), "split x");
     ck(launch_grouped_gemm_tf32x3(t_xhi_, t_xlo_, t_wuhi_, t_wulo_, hhi_.as<float>(), hlo_.as<float>(),
                                   static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s,
-                                  ksplit_up_, kpart_.as<float>(), rows_cap_, true),
+                                  ksplit_up_, kpart_.as<float>(), rows_cap_),
        "gemm up");
     mark(down.c_str(), s, 1);
     ck(launch_grouped_gemm_tf32x3(t_hhi_, t_hlo_, t_wdhi_, t_wdlo_, oall_.as<float>(), nullptr, static_cast<int>(H_),
                                   static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, ksplit_down_,
-                                  kpart_.as<float>(), rows_cap_, true),
+                                  kpart_.as<float>(), rows_cap_),
        "gemm down");
     launches_ += 1 + (ksplit_up_ > 1) + (ksplit_down_ > 1);  // x split, split-K reduces
   } else {

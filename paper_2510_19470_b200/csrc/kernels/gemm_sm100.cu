@@ -889,8 +889,7 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
                            const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
                            float* __restrict__ C, float* __restrict__ C_lo, int ldc, int N, int K,
                            const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
-                           const int* __restrict__ g_slot, int ng, int relu, int ksplit, size_t split_stride,
-                           int b_tiled) {
+                           const int* __restrict__ g_slot, int ng, int relu, int ksplit, size_t split_stride) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -977,23 +976,13 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
         const int a_row = s.row_start[g] + mt * BM;
         const int b_row = s.slot[g] * N + nt * BN;
         const int k0 = part * num_kb * T_BK;
-        // b_tiled: B is stored as [slot][n_tile][k_block][BN rows][T_BK] (launch_split_tf32_tiled),
-        // so every stage's B box is one contiguous 16 KB block instead of 64-byte pieces of
-        // BN rows K * 4 bytes apart
-        const int kb_total = K / T_BK;
-        const int b_tile0 = ((s.slot[g] * n_tiles + nt) * kb_total + k0 / T_BK) * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&s.full[stage], T_STAGE_BYTES);
           tma_load_2d(a_hi_at(stage), &map_a_hi, &s.full[stage], k0 + kb * T_BK, a_row, pol);
           tma_load_2d(a_lo_at(stage), &map_a_lo, &s.full[stage], k0 + kb * T_BK, a_row, pol);
-          if (b_tiled) {
-            tma_load_2d(b_hi_at(stage), &map_b_hi, &s.full[stage], 0, b_tile0 + kb * BN, pol);
-            tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], 0, b_tile0 + kb * BN, pol);
-          } else {
-            tma_load_2d(b_hi_at(stage), &map_b_hi, &s.full[stage], k0 + kb * T_BK, b_row, pol);
-            tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], k0 + kb * T_BK, b_row, pol);
-          }
+          tma_load_2d(b_hi_at(stage), &map_b_hi, &s.full[stage], k0 + kb * T_BK, b_row, pol);
+          tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], k0 + kb * T_BK, b_row, pol);
           if (++stage == T_STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -1141,33 +1130,6 @@ __global__ void split_tf32_kernel(const float* __restrict__ in, float* __restric
   }
 }
 
-// Weights [slots][N][K] fp32 -> hi/lo tf32 in the tiled layout [slot][n_tile][k_block][BN][T_BK]
-// (rows past N zero-filled): one thread per 4 consecutive k of one row.
-__global__ void split_tf32_tiled_kernel(const float* __restrict__ in, float* __restrict__ hi, float* __restrict__ lo,
-                                        int slots, int N, int K) {
-  const int n_tiles = (N + BN - 1) / BN, nkb = K / T_BK;
-  const int64_t quads = static_cast<int64_t>(slots) * n_tiles * BN * (K / 4);
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < quads; q += stride) {
-    const int kq = static_cast<int>(q % (K / 4));
-    const int64_t row = q / (K / 4);  // padded row over all slots: slot * n_tiles * BN + nt * BN + r
-    const int slot = static_cast<int>(row / (static_cast<int64_t>(n_tiles) * BN));
-    const int rr = static_cast<int>(row % (static_cast<int64_t>(n_tiles) * BN));
-    const int nt = rr / BN, r = rr % BN, n = nt * BN + r;
-    const int k = 4 * kq, kb = k / T_BK, c = k % T_BK;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (n < N) v = *reinterpret_cast<const float4*>(in + (static_cast<int64_t>(slot) * N + n) * K + k);
-    float4 h, l;
-    h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
-    h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
-    h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
-    h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
-    const int64_t o = (((static_cast<int64_t>(slot) * n_tiles + nt) * nkb + kb) * BN + r) * T_BK + c;
-    *reinterpret_cast<float4*>(hi + o) = h;
-    *reinterpret_cast<float4*>(lo + o) = l;
-  }
-}
-
 }  // namespace
 
 bool gemm_use_cta_pair() {
@@ -1234,7 +1196,7 @@ cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, 
 cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
                                        const CUtensorMap& b_lo, float* C, float* C_lo, int ldc, int N, int K,
                                        const GroupTable& groups, int relu, int num_sms, cudaStream_t stream,
-                                       int ksplit, float* partial, int64_t rows_total, bool b_tiled) {
+                                       int ksplit, float* partial, int64_t rows_total) {
   if (ksplit < 1 || K % (T_BK * ksplit) || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
     return cudaErrorInvalidValue;
   if (ksplit > 1 && !partial) return cudaErrorInvalidValue;
@@ -1248,25 +1210,12 @@ cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMa
   const size_t stride = static_cast<size_t>(rows_total) * ldc;
   grouped_gemm_tf32x3_kernel<<<num_sms, kThreads, kSmemBytesT, stream>>>(
       a_hi, a_lo, b_hi, b_lo, ksplit > 1 ? partial : C, C_lo, ldc, N, K, groups.row_start, groups.rows, groups.slot,
-      groups.num_groups, relu, ksplit, stride, b_tiled ? 1 : 0);
+      groups.num_groups, relu, ksplit, stride);
   if (ksplit > 1) {
     const int64_t n4 = static_cast<int64_t>(stride) / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n4 + 255) / 256)));
     ksplit_reduce_kernel<<<blocks, 256, 0, stream>>>(partial, ksplit, stride, n4, relu, C, C_lo);
   }
-  return cudaGetLastError();
-}
-
-int64_t tf32_tiled_elems(int slots, int N, int K) {
-  return static_cast<int64_t>(slots) * ((N + BN - 1) / BN) * BN * K;
-}
-
-cudaError_t launch_split_tf32_tiled(const float* in, float* hi, float* lo, int slots, int N, int K,
-                                    cudaStream_t stream) {
-  if (K % T_BK || slots <= 0) return cudaErrorInvalidValue;
-  const int64_t quads = tf32_tiled_elems(slots, N, K) / 4;
-  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 8, (quads + 255) / 256)));
-  split_tf32_tiled_kernel<<<blocks, 256, 0, stream>>>(in, hi, lo, slots, N, K);
   return cudaGetLastError();
 }
 
@@ -1408,7 +1357,6 @@ cudaError_t preload_gemm_sm100_kernels() {
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(ksplit_reduce_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(split_tf32_kernel))) return e;
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(split_tf32_tiled_kernel))) return e;
   return cudaSuccess;
 }
 

@@ -173,18 +173,11 @@ cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, 
                              uint32_t box_cols);
 // ksplit > 1: split-K over ksplit parts into `partial` ([ksplit][rows_total][ldc]) and an
 // in-order reduce (small-M layers, where tiles alone do not fill the SMs).
-// b_tiled: B comes from launch_split_tf32_tiled (map_b over [tiles * 256 rows][kTf32BK]).
 cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
                                        const CUtensorMap& b_lo, float* C, float* C_lo, int ldc, int N, int K,
                                        const GroupTable& groups, int relu, int num_sms, cudaStream_t stream,
-                                       int ksplit = 1, float* partial = nullptr, int64_t rows_total = 0,
-                                       bool b_tiled = false);
+                                       int ksplit = 1, float* partial = nullptr, int64_t rows_total = 0);
 cudaError_t launch_split_tf32(const float* in, float* hi, float* lo, int64_t n, cudaStream_t stream);
-// Weights [slots][N][K] -> hi/lo in the GEMM's tiled B layout [slot][n_tile][k_block][256][kTf32BK]
-// (each stage's box one contiguous block); tf32_tiled_elems floats per hi / lo array.
-int64_t tf32_tiled_elems(int slots, int N, int K);
-cudaError_t launch_split_tf32_tiled(const float* in, float* hi, float* lo, int slots, int N, int K,
-                                    cudaStream_t stream);
 
 cudaError_t launch_grouped_gemm_f32(const float* A, int lda, const float* B, float* C, int ldc,
                                     int N, int K, const GroupTable& groups, int relu,
