@@ -15,6 +15,8 @@
 // the same layout the NCCL path produces, so both paths feed the same GEMM groups.
 // Flags carry a per-forward epoch; spins time out (trap) instead of hanging.
 
+#include <cstdlib>
+#include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
@@ -176,31 +178,38 @@ __global__ void __launch_bounds__(256) permute_p2p_kernel(P2PArgs a, const uint8
                                                           const int* __restrict__ send_base, int* __restrict__ pos,
                                                           int mode, int seg) {
   // mode 0: every row; 1: rows staying on this GPU (and all of pos); 2: remote rows only.
+  // Grid-stride over (token, segment) warps: the remote pass runs on a capped grid so
+  // the own-expert GEMM's CTAs find room beside it (overlapped dispatch).
   const int lane = threadIdx.x & 31;
-  int t, sg, v0, v1;
-  row_segment(row_bytes >> 4, seg, t, sg, v0, v1);
-  if (t >= T_tok) return;
   const int NK = a.G * a.E;
-  const int chunk = t / 32;
-  uint8_t* dst[8];
-  for (int j = 0; j < k; ++j) {
-    const size_t o = static_cast<size_t>(t) * k + j;
-    const int key = keys[o];
-    const int p = key_off[key] + chunk_off[static_cast<size_t>(chunk) * NK + key] + ranks[o];
-    if (lane == 0 && sg == 0 && mode != 2) pos[o] = p;
-    const int d = key / a.E;
-    const bool skip = (mode == 1 && d != a.rank) || (mode == 2 && d == a.rank);
-    const int row = d == a.rank ? p : send_base[key] + (p - key_off[key]);
-    dst[j] = skip ? nullptr : static_cast<uint8_t*>(a.xall[d]) + static_cast<size_t>(row) * row_bytes;
-  }
-  const uint8_t* src = x + static_cast<size_t>(t) * row_bytes;
-  bool any = false;
-  for (int j = 0; j < k; ++j) any |= dst[j] != nullptr;
-  if (!any) return;
-  for (int v = v0 + lane; v < v1; v += 32) {
-    const uint4 val = ld_nc_v4(src + 16 * v);
-    for (int j = 0; j < k; ++j)
-      if (dst[j]) st_v4(dst[j] + 16 * v, val);
+  const int vecs = row_bytes >> 4;
+  const int per = ((vecs + seg - 1) / seg + 31) & ~31;
+  const int nwarps = static_cast<int>(gridDim.x * (blockDim.x >> 5));
+  for (int w = blockIdx.x * static_cast<int>(blockDim.x >> 5) + static_cast<int>(threadIdx.x >> 5);
+       w < T_tok * seg; w += nwarps) {
+    const int t = w / seg, sg = w - t * seg;
+    const int v0 = sg * per, v1 = min(vecs, v0 + per);
+    const int chunk = t / 32;
+    uint8_t* dst[8];
+    bool any = false;
+    for (int j = 0; j < k; ++j) {
+      const size_t o = static_cast<size_t>(t) * k + j;
+      const int key = keys[o];
+      const int p = key_off[key] + chunk_off[static_cast<size_t>(chunk) * NK + key] + ranks[o];
+      if (lane == 0 && sg == 0 && mode != 2) pos[o] = p;
+      const int d = key / a.E;
+      const bool skip = (mode == 1 && d != a.rank) || (mode == 2 && d == a.rank);
+      const int row = d == a.rank ? p : send_base[key] + (p - key_off[key]);
+      dst[j] = skip ? nullptr : static_cast<uint8_t*>(a.xall[d]) + static_cast<size_t>(row) * row_bytes;
+      any |= !skip;
+    }
+    if (!any) continue;
+    const uint8_t* src = x + static_cast<size_t>(t) * row_bytes;
+    for (int v = v0 + lane; v < v1; v += 32) {
+      const uint4 val = ld_nc_v4(src + 16 * v);
+      for (int j = 0; j < k; ++j)
+        if (dst[j]) st_v4(dst[j] + 16 * v, val);
+    }
   }
 }
 
@@ -359,7 +368,18 @@ cudaError_t launch_permute_p2p(const P2PArgs& a, DType dt, const void* x, int T,
     carveout.set();
   }
   const int seg = row_segments(T, row_bytes >> 4);
-  permute_p2p_kernel<<<(T * seg + 7) / 8, 256, 0, s>>>(a, static_cast<const uint8_t*>(x), T, row_bytes, k, keys,
+  int blocks = (T * seg + 7) / 8;
+  if (mode == 2) {
+    // HEP_DISPATCH_CTAS=n caps the remote pass's grid so the own-expert GEMM can launch
+    // beside it.  Default uncapped: at N=4 a cap of 148 or 296 moved the dispatch time
+    // into the GEMM without changing the step (profiles/r2_dispatch/).
+    static const int cap = [] {
+      const char* e = std::getenv("HEP_DISPATCH_CTAS");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (cap > 0) blocks = std::min(blocks, cap);
+  }
+  permute_p2p_kernel<<<blocks, 256, 0, s>>>(a, static_cast<const uint8_t*>(x), T, row_bytes, k, keys,
                                                        ranks, chunk_off, key_off, send_base, pos, mode, seg);
   return cudaGetLastError();
 }
