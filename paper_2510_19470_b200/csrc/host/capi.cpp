@@ -640,20 +640,29 @@ int hep_grouped_gemm(hep_dtype dtype, const void* A, int64_t a_rows, const void*
     }
     // The fp32 product path the layer runs: 3xTF32 on tcgen05 over hi/lo operand splits
     // (scratch allocated stream-ordered for this call).
+    // B pre-split into hi/lo copies (HEP_TF32_RAWB=1: raw B split in shared memory).
+    const char* raw = std::getenv("HEP_TF32_RAWB");
+    const bool presplit = !(raw && raw[0] == '1');
     const size_t a_n = static_cast<size_t>(std::max<int64_t>(a_rows, 1) * K), b_n = static_cast<size_t>(b_slots * N * K);
     float* buf = nullptr;
-    cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(float) * 2 * (a_n + b_n), s), "gemm scratch");
-    float *ahi = buf, *alo = buf + a_n, *bhi = alo + a_n, *blo = bhi + b_n;
+    cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(float) * 2 * (a_n + (presplit ? b_n : 0)), s),
+            "gemm scratch");
+    float *ahi = buf, *alo = buf + a_n;
     cuda_ok(hep::launch_split_tf32(static_cast<const float*>(A), ahi, alo, static_cast<int64_t>(a_n), s), "split A");
-    cuda_ok(hep::launch_split_tf32(static_cast<const float*>(B), bhi, blo, static_cast<int64_t>(b_n), s), "split B");
     CUtensorMap t_ahi, t_alo, t_bhi, t_blo;
     const uint64_t ar = static_cast<uint64_t>(std::max<int64_t>(a_rows, 1)), br = static_cast<uint64_t>(b_slots * N);
     cuda_ok(hep::make_tmap_f32_2d(&t_ahi, ahi, ar, static_cast<uint64_t>(K), 128, hep::kTf32BK), "tmap");
     cuda_ok(hep::make_tmap_f32_2d(&t_alo, alo, ar, static_cast<uint64_t>(K), 128, hep::kTf32BK), "tmap");
-    cuda_ok(hep::make_tmap_f32_2d(&t_bhi, bhi, br, static_cast<uint64_t>(K), 256, hep::kTf32BK), "tmap");
-    cuda_ok(hep::make_tmap_f32_2d(&t_blo, blo, br, static_cast<uint64_t>(K), 256, hep::kTf32BK), "tmap");
-    cuda_ok(hep::launch_grouped_gemm_tf32x3(t_ahi, t_alo, t_bhi, t_blo, static_cast<float*>(C), nullptr, static_cast<int>(N),
-                                            static_cast<int>(N), static_cast<int>(K), gt, relu, sms, s),
+    if (presplit) {
+      float *bhi = alo + a_n, *blo = bhi + b_n;
+      cuda_ok(hep::launch_split_tf32(static_cast<const float*>(B), bhi, blo, static_cast<int64_t>(b_n), s), "split B");
+      cuda_ok(hep::make_tmap_f32_2d(&t_bhi, bhi, br, static_cast<uint64_t>(K), 256, hep::kTf32BK), "tmap");
+      cuda_ok(hep::make_tmap_f32_2d(&t_blo, blo, br, static_cast<uint64_t>(K), 256, hep::kTf32BK), "tmap");
+    } else {
+      cuda_ok(hep::make_tmap_f32_2d(&t_bhi, B, br, static_cast<uint64_t>(K), 256, hep::kTf32BK), "tmap");
+    }
+    cuda_ok(hep::launch_grouped_gemm_tf32x3(t_ahi, t_alo, t_bhi, presplit ? &t_blo : nullptr, static_cast<float*>(C), nullptr,
+                                            static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt, relu, sms, s),
             "gemm tf32x3");
     cuda_ok(cudaFreeAsync(buf, s), "gemm scratch free");
   });

@@ -198,18 +198,28 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
       xlo_.alloc(fb * rows_cap_ * H_);
       hhi_.alloc(fb * rows_cap_ * F_);
       hlo_.alloc(fb * rows_cap_ * F_);
-      wuhi_.alloc(fb * slots_ * F_ * H_);
-      wulo_.alloc(fb * slots_ * F_ * H_);
-      wdhi_.alloc(fb * slots_ * H_ * F_);
-      wdlo_.alloc(fb * slots_ * H_ * F_);
       ck(make_tmap_f32_2d(&t_xhi_, xhi_.p, rows_cap_, H_, 128, kTf32BK), "tmap xhi");
       ck(make_tmap_f32_2d(&t_xlo_, xlo_.p, rows_cap_, H_, 128, kTf32BK), "tmap xlo");
       ck(make_tmap_f32_2d(&t_hhi_, hhi_.p, rows_cap_, F_, 128, kTf32BK), "tmap hhi");
       ck(make_tmap_f32_2d(&t_hlo_, hlo_.p, rows_cap_, F_, 128, kTf32BK), "tmap hlo");
-      ck(make_tmap_f32_2d(&t_wuhi_, wuhi_.p, slots_ * F_, H_, 256, kTf32BK), "tmap wuhi");
-      ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, slots_ * F_, H_, 256, kTf32BK), "tmap wulo");
-      ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, slots_ * H_, F_, 256, kTf32BK), "tmap wdhi");
-      ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, slots_ * H_, F_, 256, kTf32BK), "tmap wdlo");
+      // Pre-split hi/lo weight copies (split once per weight change).  HEP_TF32_RAWB=1
+      // streams the raw fp32 weights instead and splits them in shared memory: half the
+      // DRAM reads, same time (profiles/r2_tf32_tiled.md).
+      const char* raw = std::getenv("HEP_TF32_RAWB");
+      tf32_presplit_ = !(raw && raw[0] == '1');
+      if (tf32_presplit_) {
+        wuhi_.alloc(fb * slots_ * F_ * H_);
+        wulo_.alloc(fb * slots_ * F_ * H_);
+        wdhi_.alloc(fb * slots_ * H_ * F_);
+        wdlo_.alloc(fb * slots_ * H_ * F_);
+        ck(make_tmap_f32_2d(&t_wuhi_, wuhi_.p, slots_ * F_, H_, 256, kTf32BK), "tmap wuhi");
+        ck(make_tmap_f32_2d(&t_wulo_, wulo_.p, slots_ * F_, H_, 256, kTf32BK), "tmap wulo");
+        ck(make_tmap_f32_2d(&t_wdhi_, wdhi_.p, slots_ * H_, F_, 256, kTf32BK), "tmap wdhi");
+        ck(make_tmap_f32_2d(&t_wdlo_, wdlo_.p, slots_ * H_, F_, 256, kTf32BK), "tmap wdlo");
+      } else {
+        ck(make_tmap_f32_2d(&t_wuhi_, w_up_c_.p, slots_ * F_, H_, 256, kTf32BK), "tmap w_up");
+        ck(make_tmap_f32_2d(&t_wdhi_, w_down_c_.p, slots_ * H_, F_, 256, kTf32BK), "tmap w_down");
+      }
       // split-K when (groups x m-tiles x n-tiles) of an even routing leaves SMs idle
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
@@ -411,6 +421,8 @@ void Layer::setup_p2p() {
   {
     const char* spin = std::getenv("HEP_GEMM_SPIN");  // 1: GEMM producers wait on dispatch flags (old)
     spin_ = spin && spin[0] == '1';
+    const char* merge = std::getenv("HEP_MERGE_GEMMS");
+    merge_gemms_ = merge && merge[0] == '1' && !sr_fused_;
   }
   if (comm_->vgroup) {
     // Virtual ranks: register; peers resolve on first use, once every rank's layer exists.
@@ -753,6 +765,7 @@ void Layer::mark_gathered_dirty() {
 }
 
 void Layer::split_dirty_slots(cudaStream_t s) {
+  if (!tf32_presplit_) return;  // the GEMM splits raw weights in shared memory
   const int64_t per = F_ * H_;
   for (int64_t a = 0; a < slots_;) {
     if (!slot_dirty_[static_cast<size_t>(a)]) { ++a; continue; }
@@ -1150,12 +1163,12 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     mark(up.c_str(), s, 1);
     split_dirty_slots(s);
     ck(launch_split_tf32(xall_.as<float>(), xhi_.as<float>(), xlo_.as<float>(), rows_cap_ * H_, s), "split x");
-    ck(launch_grouped_gemm_tf32x3(t_xhi_, t_xlo_, t_wuhi_, t_wulo_, hhi_.as<float>(), hlo_.as<float>(),
+    ck(launch_grouped_gemm_tf32x3(t_xhi_, t_xlo_, t_wuhi_, tf32_presplit_ ? &t_wulo_ : nullptr, hhi_.as<float>(), hlo_.as<float>(),
                                   static_cast<int>(F_), static_cast<int>(F_), static_cast<int>(H_), gt, 1, num_sms_, s,
                                   ksplit_up_, kpart_.as<float>(), rows_cap_),
        "gemm up");
     mark(down.c_str(), s, 1);
-    ck(launch_grouped_gemm_tf32x3(t_hhi_, t_hlo_, t_wdhi_, t_wdlo_, oall_.as<float>(), nullptr, static_cast<int>(H_),
+    ck(launch_grouped_gemm_tf32x3(t_hhi_, t_hlo_, t_wdhi_, tf32_presplit_ ? &t_wdlo_ : nullptr, oall_.as<float>(), nullptr, static_cast<int>(H_),
                                   static_cast<int>(H_), static_cast<int>(F_), gt, 0, num_sms_, s, ksplit_down_,
                                   kpart_.as<float>(), rows_cap_),
        "gemm down");
@@ -1242,7 +1255,17 @@ void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s, bool residua
       const int n_src = p2p_args_.n_src[rank_];
       const int own_local = static_cast<int>(n_), own = static_cast<int>(n_ * (1 + n_src));
       const unsigned long long* out_down = g_out_down_.as<unsigned long long>();
-      if (!spin_) {
+      if (!spin_ && merge_gemms_) {
+        // HEP_MERGE_GEMMS=1: one up + one down launch over every group, once the remote
+        // rows and the All-Gather have landed (fewer launch tails, no overlap).
+        ck(cudaStreamWaitEvent(s, ev_arrived_, 0), "wait dispatch");
+        if (ag_pending_ && num_groups_ > own) {
+          mark("ag_wait", s);
+          ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");
+        }
+        run_expert_gemms(s, out_down, nullptr, 0, num_groups_, "", false);
+        ag_pending_ = false;
+      } else if (!spin_) {
         // Own experts' local rows overlap the remote dispatch; received rows follow once
         // they have all landed; gathered experts once the All-Gather is resident.
         run_expert_gemms(s, out_down, nullptr, 0, own_local);

@@ -194,6 +194,8 @@ class Layer {
   int ksplit_up_ = 1, ksplit_down_ = 1;  // split-K when the tiles alone cannot fill the SMs
   DevBuf kpart_;
   void split_dirty_slots(cudaStream_t s);
+  bool tf32_presplit_ = false;
+  bool merge_gemms_ = false;  // HEP_MERGE_GEMMS=1: one launch per projection over all groups  // HEP_TF32_PRESPLIT=1: pre-split hi/lo weight copies
   void mark_gathered_dirty();
   uint32_t sched_up_ = 0, sched_down_ = 0;
   DevBuf tile_counters_;  // dynamic tile scheduler of the CTA-pair GEMM (up, down)

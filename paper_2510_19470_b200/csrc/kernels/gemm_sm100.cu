@@ -841,6 +841,7 @@ constexpr int T_STAGE_BYTES = 2 * T_A_BYTES + 2 * T_B_BYTES;
 struct SmemCtlT {
   uint64_t full[T_STAGES];
   uint64_t empty[T_STAGES];
+  uint64_t conv[T_STAGES];  // BRAW: the converter warps split this stage's B into hi/lo
   uint64_t tfull[ACC];
   uint64_t tempty[ACC];
   uint32_t tmem_base;
@@ -884,7 +885,14 @@ __device__ __forceinline__ float rna_tf32(float x) {
   return __uint_as_float(r);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+// BRAW: B arrives as raw fp32 (one TMA box per stage, half the HBM bytes of pre-split
+// hi/lo weights); converter warps 6..9 split it in shared memory, hi in place and lo
+// into the B_lo slot, with the same rna_tf32 split as split_tf32_kernel (bit-identical
+// products).  The MMA issuer waits on conv[] instead of full[].  Opt-in
+// (HEP_TF32_RAWB=1): it halves the kernel's DRAM reads but not its time, which is not
+// bound by HBM (profiles/r2_tf32_tiled.md).
+template <bool BRAW>
+__global__ void __launch_bounds__(kThreads + (BRAW ? 32 * kConvWarps : 0), 1)
 grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
                            const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
                            float* __restrict__ C, float* __restrict__ C_lo, int ldc, int N, int K,
@@ -939,6 +947,7 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
     for (int i = 0; i < T_STAGES; ++i) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
+      mbar_init(&s.conv[i], kConvWarps);
     }
     for (int i = 0; i < ACC; ++i) {
       mbar_init(&s.tfull[i], 1);
@@ -957,7 +966,34 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
   // tiles walk (group, m-tile, n-tile) with m fastest: a group's A rows stay in L2
   // across its n-tiles
 
-  if (warp == 0) {
+  if (BRAW && warp >= 6) {
+    // ================= converters: split raw B into hi (in place) / lo =================
+    const int wi = static_cast<int>(warp) - 6;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&s.full[stage], phase);
+        float4* bh = reinterpret_cast<float4*>(b_hi_at(stage));
+        float4* bl = reinterpret_cast<float4*>(b_lo_at(stage));
+#pragma unroll 4
+        for (int i = wi * 32 + static_cast<int>(lane); i < T_B_BYTES / 16; i += 32 * kConvWarps) {
+          const float4 v = bh[i];
+          float4 h, l;
+          h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
+          h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
+          h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
+          h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
+          bh[i] = h;
+          bl[i] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s.conv[stage]);
+        if (++stage == T_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {  // ================= TMA producer =================
       const uint64_t pol = make_policy(0);
       int stage = 0;
@@ -978,11 +1014,11 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
         const int k0 = part * num_kb * T_BK;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&s.full[stage], T_STAGE_BYTES);
+          mbar_arrive_expect_tx(&s.full[stage], BRAW ? T_STAGE_BYTES - T_B_BYTES : T_STAGE_BYTES);
           tma_load_2d(a_hi_at(stage), &map_a_hi, &s.full[stage], k0 + kb * T_BK, a_row, pol);
           tma_load_2d(a_lo_at(stage), &map_a_lo, &s.full[stage], k0 + kb * T_BK, a_row, pol);
           tma_load_2d(b_hi_at(stage), &map_b_hi, &s.full[stage], k0 + kb * T_BK, b_row, pol);
-          tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], k0 + kb * T_BK, b_row, pol);
+          if (!BRAW) tma_load_2d(b_lo_at(stage), &map_b_lo, &s.full[stage], k0 + kb * T_BK, b_row, pol);
           if (++stage == T_STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -999,7 +1035,7 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&s.full[stage], phase);
+          mbar_wait(BRAW ? &s.conv[stage] : &s.full[stage], phase);
           tc_fence_after();
           const uint32_t ah = smem_addr(a_hi_at(stage)), al = smem_addr(a_lo_at(stage));
           const uint32_t bh = smem_addr(b_hi_at(stage)), bl = smem_addr(b_lo_at(stage));
@@ -1017,7 +1053,7 @@ grouped_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a_hi, const _
         if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else {
+  } else if (warp < 6) {
     // ================= epilogue (warps 2..5) =================
     const uint32_t quarter = warp & 3u;
     const int row_in_tile = static_cast<int>(quarter * 32 + lane);
@@ -1194,23 +1230,30 @@ cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, 
 }
 
 cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
-                                       const CUtensorMap& b_lo, float* C, float* C_lo, int ldc, int N, int K,
+                                       const CUtensorMap* b_lo, float* C, float* C_lo, int ldc, int N, int K,
                                        const GroupTable& groups, int relu, int num_sms, cudaStream_t stream,
                                        int ksplit, float* partial, int64_t rows_total) {
   if (ksplit < 1 || K % (T_BK * ksplit) || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0)
     return cudaErrorInvalidValue;
   if (ksplit > 1 && !partial) return cudaErrorInvalidValue;
-  static DeviceOnce attr_set;
-  if (!attr_set.done()) {
-    const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(kSmemBytesT));
+  const bool b_raw = b_lo == nullptr;
+  static DeviceOnce attr_pre, attr_raw;
+  DeviceOnce& once = b_raw ? attr_raw : attr_pre;
+  if (!once.done()) {
+    const cudaError_t e = cudaFuncSetAttribute(b_raw ? grouped_gemm_tf32x3_kernel<true> : grouped_gemm_tf32x3_kernel<false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytesT));
     if (e != cudaSuccess) return e;
-    attr_set.set();
+    once.set();
   }
   const size_t stride = static_cast<size_t>(rows_total) * ldc;
-  grouped_gemm_tf32x3_kernel<<<num_sms, kThreads, kSmemBytesT, stream>>>(
-      a_hi, a_lo, b_hi, b_lo, ksplit > 1 ? partial : C, C_lo, ldc, N, K, groups.row_start, groups.rows, groups.slot,
-      groups.num_groups, relu, ksplit, stride);
+  float* out = ksplit > 1 ? partial : C;
+  const int ng = groups.num_groups;
+  if (b_raw)
+    grouped_gemm_tf32x3_kernel<true><<<num_sms, kThreads + 32 * kConvWarps, kSmemBytesT, stream>>>(
+        a_hi, a_lo, b_hi, b_hi, out, C_lo, ldc, N, K, groups.row_start, groups.rows, groups.slot, ng, relu, ksplit, stride);
+  else
+    grouped_gemm_tf32x3_kernel<false><<<num_sms, kThreads, kSmemBytesT, stream>>>(
+        a_hi, a_lo, b_hi, *b_lo, out, C_lo, ldc, N, K, groups.row_start, groups.rows, groups.slot, ng, relu, ksplit, stride);
   if (ksplit > 1) {
     const int64_t n4 = static_cast<int64_t>(stride) / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n4 + 255) / 256)));
@@ -1354,7 +1397,8 @@ cudaError_t preload_gemm_sm100_kernels() {
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 5, false, true>)))
     return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<true>))) return e;
-  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel<false>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel<true>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(ksplit_reduce_kernel))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(split_tf32_kernel))) return e;
   return cudaSuccess;

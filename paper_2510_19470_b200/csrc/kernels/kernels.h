@@ -173,8 +173,9 @@ cudaError_t make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, 
                              uint32_t box_cols);
 // ksplit > 1: split-K over ksplit parts into `partial` ([ksplit][rows_total][ldc]) and an
 // in-order reduce (small-M layers, where tiles alone do not fill the SMs).
+// b_lo == nullptr: b_hi maps the raw fp32 B, split into hi/lo in shared memory.
 cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
-                                       const CUtensorMap& b_lo, float* C, float* C_lo, int ldc, int N, int K,
+                                       const CUtensorMap* b_lo, float* C, float* C_lo, int ldc, int N, int K,
                                        const GroupTable& groups, int relu, int num_sms, cudaStream_t stream,
                                        int ksplit = 1, float* partial = nullptr, int64_t rows_total = 0);
 cudaError_t launch_split_tf32(const float* in, float* hi, float* lo, int64_t n, cudaStream_t stream);

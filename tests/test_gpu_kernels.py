@@ -133,6 +133,24 @@ def test_grouped_gemm_f32(K, N, rows, kernel, monkeypatch):
     assert rel < (1e-5 if kernel == "simt" else F32_GEMM_MAX), rel
 
 
+@pytest.mark.parametrize("K,N,rows", [(1024, 4096, [130, 0, 512]), (4096, 1024, [257, 31]), (64, 96, [5, 300])])
+def test_tf32_raw_b_split_in_smem_bitexact(K, N, rows, monkeypatch):
+    """The 3xTF32 GEMM's raw-B variant (HEP_TF32_RAWB=1) streams raw fp32 B and splits it
+    into hi/lo in shared memory; its products must be bit-identical to the default
+    pre-split hi/lo weights (the same rna_tf32 split done by a separate kernel)."""
+    monkeypatch.delenv("HEP_F32_GEMM", raising=False)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n_slots = 2
+    A = torch.randn(sum(rows), K, generator=g, device="cuda")
+    B = torch.randn(n_slots * N, K, generator=g, device="cuda") * 0.03
+    slots = [(i + 1) % n_slots for i in range(len(rows))]
+    monkeypatch.setenv("HEP_TF32_RAWB", "1")
+    raw = _gemm(HEP_F32, A, B, n_slots, N, K, rows, slots, 1)
+    monkeypatch.delenv("HEP_TF32_RAWB", raising=False)
+    pre = _gemm(HEP_F32, A, B, n_slots, N, K, rows, slots, 1)
+    assert torch.equal(raw, pre)
+
+
 def _demo_expert_pair(h, m, seed, quantize=False):
     rng = np.random.default_rng(seed)
     P = 2 * h * m
