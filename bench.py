@@ -490,12 +490,21 @@ def main():
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local).__enter__()
+    # an event at every step boundary too (K records, no syncs): the per-step spread shows
+    # a host stall inside the timed region, which the total alone cannot
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
     t0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         step()
+        if i < args.steps - 1:
+            marks[i].record(stream)
     t1.record(stream)
     barrier()
     ms = t0.elapsed_time(t1)
+    bounds = [t0] + marks + [t1]
+    per_step = sorted(bounds[i].elapsed_time(bounds[i + 1]) for i in range(args.steps))
+    step_spread = {"min": per_step[0], "median": per_step[len(per_step) // 2], "max": per_step[-1],
+                   "source": "CUDA events at every step boundary of the timed pass (rank 0)"}
     gemm_phases = {}  # mean ms per step, summed over the layers of the stack
     for layer in layers:
         for kname, v in layer.timings().items():
@@ -697,6 +706,7 @@ def main():
             "planner": planner,
             "gemm_rows_per_gpu": rows_per_gpu,
             "layer_load_imbalance": layer_imbalance,
+            "step_ms": step_spread,
             "phase_ms": phases,
             "phase_ms_source": "second pass of the same K steps with events at every phase boundary",
             "gpu_launches": launches,

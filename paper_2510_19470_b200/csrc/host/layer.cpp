@@ -52,7 +52,13 @@ SharedStreams acquire_streams(int dev, int rank) {
   SharedStreams& st = g_streams[{dev, rank}];
   if (st.refs++ == 0) {
     ck(cudaStreamCreateWithFlags(&st.side, cudaStreamNonBlocking), "side stream");
-    ck(cudaStreamCreateWithFlags(&st.ag, cudaStreamNonBlocking), "ag stream");
+    // HEP_AG_PRIORITY=1: the All-Gather stream gets the highest stream priority, so the
+    // migration chain (encode, flags, pulls, decode) is scheduled ahead of the gate and
+    // dispatch blocks it otherwise shares the SMs with.
+    const char* pr = std::getenv("HEP_AG_PRIORITY");
+    int least = 0, greatest = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+    ck(cudaStreamCreateWithPriority(&st.ag, cudaStreamNonBlocking, pr && pr[0] == '1' ? greatest : 0), "ag stream");
   }
   return st;
 }

@@ -1247,6 +1247,7 @@ cudaError_t launch_grouped_gemm_tf32x3(const CUtensorMap& a_hi, const CUtensorMa
   }
   const size_t stride = static_cast<size_t>(rows_total) * ldc;
   float* out = ksplit > 1 ? partial : C;
+
   const int ng = groups.num_groups;
   if (b_raw)
     grouped_gemm_tf32x3_kernel<true><<<num_sms, kThreads + 32 * kConvWarps, kSmemBytesT, stream>>>(

@@ -25,6 +25,9 @@ def main():
             print("  kernels", {n: round(v.get("hbm_frac", v.get("frac_burst", 0)), 3) for n, v in k.items()
                                 if isinstance(v, dict)})
             print("  phases", {n: round(v, 4) for n, v in d["phase_ms"].items()})
+            if "step_ms" in d:
+                sp = d["step_ms"]
+                print("  step ms min %.3f median %.3f max %.3f" % (sp["min"], sp["median"], sp["max"]))
             c = d.get("comm")
             if c:
                 print("  comm a2a %.1f GB/s ag %.1f GB/s (ag %.3f ms for %.1f MB)" % (
