@@ -513,7 +513,7 @@ int hep_layer_comm_bench(hep_layer_t layer, const void* x, int64_t tokens, int i
 int hep_layer_debug(hep_layer_t layer, const int32_t** topk_idx, const float** topk_w, const int32_t** pos,
                     const void** packed, const int32_t** key_counts) {
   return guarded([&] {
-    const hep::Layer& l = *layer->impl;
+    hep::Layer& l = *layer->impl;
     if (topk_idx) *topk_idx = l.topk_idx();
     if (topk_w) *topk_w = l.topk_w();
     if (pos) *pos = l.pos();

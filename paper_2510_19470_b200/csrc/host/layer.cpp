@@ -190,6 +190,15 @@ Layer::Layer(const hep_layer_params& prm, Comm* comm) : comm_(comm) {
   if (dt_ == DType::BF16) {
     ck(make_tmap_bf16_2d(&map_a1_, xall_.p, rows_cap_, H_, 128, 64), "tmap a1");
     cta_pair_ = gemm_use_cta_pair();
+    // HEP_GATHER_A=1 (one GPU): the permute fused into the up-projection's A load, x rows
+    // gathered by the inverse routing map.  Bit-identical, but 2.8x slower on the cfg3 /
+    // cfg4 up-projection: one tile's rows span the whole input (profiles/r2_gather.md).
+    const char* ga = std::getenv("HEP_GATHER_A");
+    gather_a_ = cta_pair_ && G_ == 1 && ga && ga[0] == '1';
+    if (gather_a_) {
+      row_src_.alloc(sizeof(int32_t) * (rows_cap_ + 256));  // +256: a partial m-tile reads past the last row
+      ck(cudaMemset(row_src_.p, 0, sizeof(int32_t) * (rows_cap_ + 256)), "row_src");
+    }
     tile_counters_.alloc(2 * sizeof(int));
     const uint32_t b_box = cta_pair_ ? 128 : 256;
     ck(make_tmap_bf16_2d(&map_b1_, w_up_c_.p, slots_ * F_, H_, b_box, 64), "tmap b1");
@@ -1150,7 +1159,8 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     if (cta_pair_) {
       int* ctr = tile_counters_.as<int>();  // dynamic tile scheduler counters (zeroed in-stream per launch)
       ck(launch_grouped_gemm_bf16_2cta(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_),
-                                       static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_, ctr),
+                                       static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_, ctr,
+                                       gather_now_ ? row_src_.as<int>() : nullptr, gather_now_ ? last_x_ : nullptr),
          "gemm up");
       mark(down.c_str(), s, 1);
       ck(launch_grouped_gemm_bf16_2cta(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_),
@@ -1205,6 +1215,7 @@ void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s, bool residua
   if (T < 0 || T > Tmax_) throw std::invalid_argument("token count must be in [0, max_tokens]");
   if (p2p_) ensure_connected();
   launches_ = 0;
+  gather_now_ = false;
   const int Ti = static_cast<int>(T);
   const int nchunks = (Ti + 31) / 32;
   mark("gate", s);
@@ -1322,8 +1333,20 @@ void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s, bool residua
     return;
   }
   mark("permute", s);
-  ck(launch_permute(dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), static_cast<int>(NK_), keys_.as<int>(),
-                    ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), pos_.as<int>(), xall_.p, s), "permute");
+  if (gather_a_ && Ti > 0) {
+    // positions + the inverse map only; the up-projection gathers x rows itself
+    ck(launch_positions(Ti, static_cast<int>(k_), static_cast<int>(NK_), keys_.as<int>(), ranks_.as<int>(),
+                        chunk_off_.as<int>(), key_off_.as<int>(), pos_.as<int>(), s, row_src_.as<int>()),
+       "positions");
+    gather_now_ = true;
+    packed_stale_ = true;
+    last_x_ = x;
+    last_T_ = T;
+  } else {
+    ck(launch_permute(dt_, x, Ti, static_cast<int>(H_), static_cast<int>(k_), static_cast<int>(NK_), keys_.as<int>(),
+                      ranks_.as<int>(), chunk_off_.as<int>(), key_off_.as<int>(), pos_.as<int>(), xall_.p, s), "permute");
+    packed_stale_ = false;
+  }
   launches_ += 1;
   if (G_ > 1) {
     mark("dispatch", s);
@@ -1458,6 +1481,20 @@ void Layer::collect_timings(char* names, size_t names_cap, float* ms, int cap, i
     std::strncpy(names, joined.c_str(), names_cap - 1);
     names[names_cap - 1] = 0;
   }
+}
+
+const void* Layer::packed() {
+  if (packed_stale_) {
+    // the caller's x of the last step must still be alive (debug / inspection use)
+    ck(cudaDeviceSynchronize(), "sync");
+    ck(launch_permute(dt_, last_x_, static_cast<int>(last_T_), static_cast<int>(H_), static_cast<int>(k_),
+                      static_cast<int>(NK_), keys_.as<int>(), ranks_.as<int>(), chunk_off_.as<int>(),
+                      key_off_.as<int>(), pos_.as<int>(), xall_.p, nullptr),
+       "permute (inspection)");
+    ck(cudaDeviceSynchronize(), "sync");
+    packed_stale_ = false;
+  }
+  return xall_.p;
 }
 
 void Layer::forward_host(const void* hx, int64_t T, void* hy, cudaStream_t s) {

@@ -106,7 +106,9 @@ class Layer {
   const int* topk_idx() const { return topk_idx_.as<int>(); }
   const float* topk_w() const { return topk_w_.as<float>(); }
   const int* pos() const { return pos_.as<int>(); }
-  const void* packed() const { return xall_.p; }
+  // The grouped rows of the last step (materialised on demand when the up-projection
+  // gathered them from x instead; an inspection path, not the step).
+  const void* packed();
   const int* key_counts() const { return key_total_.as<int>(); }
   // 0 off; 1 CUDA events around the expert GEMM launches only (cheap enough for the timed
   // pass); 2 events at every phase boundary.
@@ -194,8 +196,14 @@ class Layer {
   int ksplit_up_ = 1, ksplit_down_ = 1;  // split-K when the tiles alone cannot fill the SMs
   DevBuf kpart_;
   void split_dirty_slots(cudaStream_t s);
-  bool tf32_presplit_ = false;
-  bool merge_gemms_ = false;  // HEP_MERGE_GEMMS=1: one launch per projection over all groups  // HEP_TF32_PRESPLIT=1: pre-split hi/lo weight copies
+  bool tf32_presplit_ = true;  // false (HEP_TF32_RAWB=1): raw weights split in shared memory
+  bool merge_gemms_ = false;   // HEP_MERGE_GEMMS=1: one launch per projection over all groups
+  bool gather_a_ = false;     // one GPU, CTA pair: the permute fused into the up-projection's A load
+  bool gather_now_ = false;   // this step's up-projection gathers A (last_x_ rows by row_src_)
+  bool packed_stale_ = false; // xall_ not written by the last step (gathered A)
+  const void* last_x_ = nullptr;
+  int64_t last_T_ = 0;
+  DevBuf row_src_;            // grouped row -> token (inverse routing map), padded by 256
   void mark_gathered_dirty();
   uint32_t sched_up_ = 0, sched_down_ = 0;
   DevBuf tile_counters_;  // dynamic tile scheduler of the CTA-pair GEMM (up, down)

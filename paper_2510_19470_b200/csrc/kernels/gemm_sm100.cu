@@ -460,15 +460,24 @@ __device__ __forceinline__ int find_group2(const SmemCtl2& s, int ng, int tile) 
 // publishes it to a 4-slot queue in both CTAs' shared memory; every role of both CTAs
 // reads its tiles from that queue.  Clusters that run ahead take the next tiles, so the
 // tiles in flight stay a compact window of the raster and keep sharing L2 lines.
-template <bool PATCH, int NST_T = P_STAGES, bool DIRECT_T = false, bool DYN = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (PATCH ? 32 * kConvWarps : 0), 1)
+// GATHER: the permute fused into the A load.  Grouped row p of A is row a_src[p] of the
+// layer input a_x (row stride K).  Gather warps 6..9 of each CTA copy their 128 rows per
+// stage with 16-byte cp.async (8 lanes per 128-byte row segment, the SW128 swizzle
+// computed in software), keep GATHER_LAG stages in flight, and publish each landed stage
+// to the leader's full barrier after a proxy fence.  The TMA producer loads only B.
+// Opt-in: this version and a tile::gather4 TMA version both ran the cfg3 up-projection
+// 2.8x slower than the explicit permute (profiles/r2_gather.md).
+constexpr int GATHER_LAG = 3;
+template <bool PATCH, int NST_T = P_STAGES, bool DIRECT_T = false, bool DYN = false, bool GATHER = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + ((PATCH || GATHER) ? 32 * kConvWarps : 0), 1)
 grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                               __nv_bfloat16* __restrict__ C, int ldc, int N, int K,
                               const int* __restrict__ g_row_start, const int* __restrict__ g_rows,
                               const int* __restrict__ g_slot, const unsigned long long* __restrict__ g_out,
                               const int* __restrict__ g_wait, const uint32_t* __restrict__ wait_flags,
                               uint32_t epoch, int ng, int relu, uint32_t sched, uint64_t timeout_ns,
-                              const PatchArgs patches, int half, int* __restrict__ tile_counter) {
+                              const PatchArgs patches, int half, int* __restrict__ tile_counter,
+                              const int* __restrict__ a_src, const __nv_bfloat16* __restrict__ a_x) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -520,7 +529,7 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
     for (int i = 0; i < NST; ++i) {
-      mbar_init(&s.full[i], 1);
+      mbar_init(&s.full[i], GATHER ? 1 + 2 * kConvWarps : 1);  // GATHER: + every gather warp of both CTAs
       mbar_init(&s.empty[i], 1);
       mbar_init(&s.bfull[i], 1);
       mbar_init(&s.patched[i], 2);  // one converter per CTA
@@ -627,7 +636,53 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
     }
   }
 
-  if (warp == 0) {
+  if (GATHER && warp >= 6) {
+    // ================= A gather warps (both CTAs) =================
+    const int wi = static_cast<int>(warp) - 6;
+    const int sub = static_cast<int>(lane >> 3), chunk = static_cast<int>(lane & 7);
+    const size_t row_bytes = static_cast<size_t>(K) * sizeof(__nv_bfloat16);
+    const uint8_t* xb = reinterpret_cast<const uint8_t*>(a_x) + chunk * 16;
+    int stage = 0, issued = 0;
+    uint32_t phase = 0;
+    auto publish = [&](int st) {  // every cp.async of stage st has landed (wait_group)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (cta == 0) mbar_arrive(&s.full[st]);
+        else mbar_arrive_leader_cluster(&s.full[st]);
+      }
+    };
+    for (int tile = cluster; tile < total; tile += nclusters) {
+      const int g = find_group2(s, ng, tile);
+      const int m_tiles = (s.rows[g] + P_BM - 1) / P_BM;
+      int mt, nt;
+      decode_tile(tile - s.tile_start[g], m_tiles, n_tiles, sched, mt, nt);
+      // this lane's 8 rows of the CTA's 128-row half: wi*32 + i*4 + sub (a_src is padded
+      // with valid token ids past the last group, so a partial m-tile reads defined rows)
+      const int r0 = s.row_start[g] + mt * P_BM + 128 * static_cast<int>(cta) + wi * 32 + sub;
+      const uint8_t* src[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) src[i] = xb + static_cast<size_t>(a_src[r0 + 4 * i]) * row_bytes;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&s.empty[stage], phase ^ 1);
+        const uint32_t base = smem_addr(stage_a + stage * P_A_BYTES);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = wi * 32 + 4 * i + sub;
+          const uint32_t dst = base + static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src[i] + kb * 128) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (++issued > GATHER_LAG) {
+          asm volatile("cp.async.wait_group %0;" ::"n"(GATHER_LAG) : "memory");
+          publish((stage + NST - GATHER_LAG) % NST);
+        }
+        if (++stage == NST) { stage = 0; phase ^= 1; }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    for (int j = min(issued, GATHER_LAG); j > 0; --j) publish((stage + NST - j) % NST);
+  } else if (warp == 0) {
     // ================= TMA producer (both CTAs) =================
     if (lane == 0) {
       const uint64_t pol_a = make_policy(sched & 3u);
@@ -662,8 +717,8 @@ grouped_gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const _
             bulk_load(stage_p + stage * kPatchBlockBytes, pblk + static_cast<size_t>(kb) * kPatchBlockBytes,
                       kPatchBlockBytes, &s.bfull[stage], pol_b);
           } else {
-            if (cta == 0) mbar_arrive_expect_tx(&s.full[stage], 2 * P_STAGE_BYTES);
-            tma_load_2d_2sm(stage_a + stage * P_A_BYTES, &map_a, &s.full[stage], kb * BK, a_row, pol_a);
+            if (cta == 0) mbar_arrive_expect_tx(&s.full[stage], GATHER ? 2 * P_B_BYTES : 2 * P_STAGE_BYTES);
+            if (!GATHER) tma_load_2d_2sm(stage_a + stage * P_A_BYTES, &map_a, &s.full[stage], kb * BK, a_row, pol_a);
             tma_load_2d_2sm(stage_b + stage * P_B_BYTES, &map_b, &s.full[stage], kb * BK, b_row, pol_b);
           }
           if (++stage == NST) { stage = 0; phase ^= 1; }
@@ -1311,7 +1366,8 @@ cudaError_t launch_grouped_gemm_bf16_patched(const CUtensorMap& map_a, const CUt
 
 cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C, int ldc,
                                           int N, int K, const GroupTable& groups, int relu, int num_sms,
-                                          cudaStream_t stream, uint32_t sched, int* tile_counter) {
+                                          cudaStream_t stream, uint32_t sched, int* tile_counter, const int* a_src,
+                                          const void* a_x) {
   if (K % BK || N % 32 || groups.num_groups > kMaxGroups || groups.num_groups <= 0) return cudaErrorInvalidValue;
   // HEP_GEMM_STAGES = 4 | 5 (default) | 6 (six stages, direct-store epilogue; local outputs only)
   const char* st_env = std::getenv("HEP_GEMM_STAGES");
@@ -1323,7 +1379,7 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
   // raises the power-capped clock, but the tensor pipe idles more at tile boundaries; on
   // the up-projection it loses 4%.  Off by default.
   const char* dyn_env = std::getenv("HEP_GEMM_DYN");
-  const bool dyn = tile_counter != nullptr && dyn_env && dyn_env[0] == '1' && stages == 5;
+  const bool dyn = tile_counter != nullptr && dyn_env && dyn_env[0] == '1' && stages == 5 && a_src == nullptr;
   static DeviceOnce attr4, attr5, attr6, attr5d;
   DeviceOnce& once = dyn ? attr5d : (stages == 4 ? attr4 : (stages == 6 ? attr6 : attr5));
   if (!once.done()) {
@@ -1348,11 +1404,27 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
     if (e != cudaSuccess) return e;
   }
   const int grid = (num_sms / 2) * 2;
+  if (a_src) {  // gathered A: the default 5-stage static schedule only, local outputs
+    if (!a_x || groups.wait_src) return cudaErrorInvalidValue;
+    static DeviceOnce attr_g;
+    if (!attr_g.done()) {
+      const cudaError_t e = cudaFuncSetAttribute(grouped_gemm_bf16_2cta_kernel<false, 5, false, false, true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kSmemBytes2));
+      if (e != cudaSuccess) return e;
+      attr_g.set();
+    }
+    grouped_gemm_bf16_2cta_kernel<false, 5, false, false, true><<<grid, kThreads + 32 * kConvWarps, kSmemBytes2, stream>>>(
+        map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot, groups.out,
+        nullptr, nullptr, 0, groups.num_groups, relu, sched, groups.timeout_ns, PatchArgs{}, 0, nullptr, a_src,
+        static_cast<const __nv_bfloat16*>(a_x));
+    return cudaGetLastError();
+  }
 #define HEP_LAUNCH_2CTA(ST, DIR, DY, SMEM)                                                                           \
   grouped_gemm_bf16_2cta_kernel<false, ST, DIR, DY><<<grid, kThreads, SMEM, stream>>>(                              \
       map_a, map_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot, groups.out, \
       groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns, PatchArgs{}, \
-      0, tile_counter)
+      0, tile_counter, nullptr, nullptr)
   if (dyn) HEP_LAUNCH_2CTA(5, false, true, kSmemBytes2);
   else if (stages == 4) HEP_LAUNCH_2CTA(4, false, false, kSmemBytes2Four);
   else if (stages == 6) HEP_LAUNCH_2CTA(6, true, false, kSmemBytes2Deep);
@@ -1379,7 +1451,7 @@ cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, cons
   grouped_gemm_bf16_2cta_kernel<true><<<grid, kThreads + 32 * kConvWarps, kSmemBytes2Patch, stream>>>(
       map_a, map_shared_b, static_cast<__nv_bfloat16*>(C), ldc, N, K, groups.row_start, groups.rows, groups.slot,
       groups.out, groups.wait_src, groups.wait_flags, groups.epoch, groups.num_groups, relu, sched, groups.timeout_ns,
-      patches, half, nullptr);
+      patches, half, nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -1398,6 +1470,8 @@ cudaError_t preload_gemm_sm100_kernels() {
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 5, false, true>)))
     return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<true>))) return e;
+  if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_bf16_2cta_kernel<false, 5, false, false, true>)))
+    return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel<false>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(grouped_gemm_tf32x3_kernel<true>))) return e;
   if (const cudaError_t e = load(reinterpret_cast<const void*>(ksplit_reduce_kernel))) return e;

@@ -66,9 +66,10 @@ cudaError_t launch_permute(DType dt, const void* x, int T, int H, int k, int NK,
                            const int* ranks, const int* chunk_off, const int* key_off, int* pos,
                            void* packed, cudaStream_t stream);
 
-// pos only (no row movement): the routing-plan entry point.
+// pos only (no row movement): the routing-plan entry point.  With src: also the inverse
+// map src[pos[t, j]] = t, for the GEMM's gathered A load (permute fused into the GEMM).
 cudaError_t launch_positions(int T, int k, int NK, const int* keys, const int* ranks, const int* chunk_off,
-                             const int* key_off, int* pos, cudaStream_t stream);
+                             const int* key_off, int* pos, cudaStream_t stream, int* src = nullptr);
 
 // y[t] = sum_j w[t,j] * out[pos[t,j]]  (slot order, fp32 accumulate); with residual:
 // y[t] = residual[t] + that sum, accumulated from the residual (one rounding at the end).
@@ -143,9 +144,14 @@ cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, cons
 // CTA-pair variant (cta_group::2, 256x256 cluster tiles); B's tensor map box is 128 rows.
 // tile_counter (one device int per in-flight launch, zeroed by the launcher) enables the
 // dynamic tile scheduler under HEP_GEMM_DYN=1; otherwise the static round-robin.
+// a_src != nullptr: A rows are gathered from a_x (the layer input, row stride K; map_a
+// unused): grouped row p is a_x row a_src[p], the permute fused into the A load.  a_src
+// must hold 256 valid row ids past the last group's rows.  Local outputs, no dispatch
+// waits.
 cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtensorMap& map_b, void* C, int ldc,
                                           int N, int K, const GroupTable& groups, int relu, int num_sms,
-                                          cudaStream_t stream, uint32_t sched = 0x6u, int* tile_counter = nullptr);
+                                          cudaStream_t stream, uint32_t sched = 0x6u, int* tile_counter = nullptr,
+                                          const int* a_src = nullptr, const void* a_x = nullptr);
 // CTA-pair GEMM unless HEP_GEMM_2CTA=0 (the 1-CTA kernel stays for A/B comparisons).
 bool gemm_use_cta_pair();
 // Schedule for one expert GEMM shape: A operand reused across n-tiles is kept in L2

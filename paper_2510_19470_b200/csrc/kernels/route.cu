@@ -840,11 +840,18 @@ __global__ void __launch_bounds__(256) permute_kernel(const uint8_t* __restrict_
 
 __global__ void positions_kernel(int T_tok, int k, int NK, const int* __restrict__ keys,
                                  const int* __restrict__ ranks, const int* __restrict__ chunk_off,
-                                 const int* __restrict__ key_off, int* __restrict__ pos) {
+                                 const int* __restrict__ key_off, int* __restrict__ pos, int* __restrict__ src) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= T_tok * k) return;
+  if (i >= T_tok * k) {
+    // the 256 rows past the last group: a partial m-tile of the gathered A load reads
+    // them, so they must name valid tokens of this step
+    if (src && i < T_tok * k + 256) src[i] = 0;
+    return;
+  }
   const int t = i / k, key = keys[i];
-  pos[i] = key_off[key] + chunk_off[static_cast<size_t>(t / kChunk) * NK + key] + ranks[i];
+  const int p = key_off[key] + chunk_off[static_cast<size_t>(t / kChunk) * NK + key] + ranks[i];
+  pos[i] = p;
+  if (src) src[p] = t;  // the inverse map: grouped row p is token t (gathered A load)
 }
 
 // One warp per token.  bf16 rows: 8 elements per 16-byte vector.
@@ -1073,8 +1080,10 @@ cudaError_t launch_permute(DType dt, const void* x, int T, int H, int k, int NK,
 }
 
 cudaError_t launch_positions(int T, int k, int NK, const int* keys, const int* ranks, const int* chunk_off,
-                             const int* key_off, int* pos, cudaStream_t stream) {
-  positions_kernel<<<(T * k + 255) / 256, 256, 0, stream>>>(T, k, NK, keys, ranks, chunk_off, key_off, pos);
+                             const int* key_off, int* pos, cudaStream_t stream, int* src) {
+  if (T == 0) return cudaSuccess;
+  const int n = T * k + (src ? 256 : 0);
+  positions_kernel<<<(n + 255) / 256, 256, 0, stream>>>(T, k, NK, keys, ranks, chunk_off, key_off, pos, src);
   return cudaGetLastError();
 }
 
