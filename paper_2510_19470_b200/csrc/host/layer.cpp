@@ -437,7 +437,8 @@ void Layer::setup_p2p() {
     const char* spin = std::getenv("HEP_GEMM_SPIN");  // 1: GEMM producers wait on dispatch flags (old)
     spin_ = spin && spin[0] == '1';
     const char* merge = std::getenv("HEP_MERGE_GEMMS");
-    merge_gemms_ = merge && merge[0] == '1' && !sr_fused_;
+    merge_mode_ = merge ? std::atoi(merge) : 0;
+    merge_gemms_ = merge_mode_ == 1 && !sr_fused_;
   }
   if (comm_->vgroup) {
     // Virtual ranks: register; peers resolve on first use, once every rank's layer exists.
@@ -1272,7 +1273,20 @@ void Layer::step(const void* x, int64_t T, void* y, cudaStream_t s, bool residua
       const int n_src = p2p_args_.n_src[rank_];
       const int own_local = static_cast<int>(n_), own = static_cast<int>(n_ * (1 + n_src));
       const unsigned long long* out_down = g_out_down_.as<unsigned long long>();
-      if (!spin_ && merge_gemms_) {
+      if (!spin_ && merge_mode_ == 2) {
+        // HEP_MERGE_GEMMS=2: own and received rows in one launch per projection once the
+        // dispatch has landed; gathered experts after the All-Gather, as in the default.
+        ck(cudaStreamWaitEvent(s, ev_arrived_, 0), "wait dispatch");
+        run_expert_gemms(s, out_down, nullptr, 0, own);
+        if (num_groups_ > own) {
+          if (ag_pending_) {
+            mark("ag_wait", s);
+            ck(cudaStreamWaitEvent(s, ev_ag_done_, 0), "wait ag");
+          }
+          run_expert_gemms(s, out_down, nullptr, own, num_groups_ - own, "_gathered", sr_fused_);
+        }
+        ag_pending_ = false;
+      } else if (!spin_ && merge_gemms_) {
         // HEP_MERGE_GEMMS=1: one up + one down launch over every group, once the remote
         // rows and the All-Gather have landed (fewer launch tails, no overlap).
         ck(cudaStreamWaitEvent(s, ev_arrived_, 0), "wait dispatch");

@@ -198,6 +198,7 @@ class Layer {
   void split_dirty_slots(cudaStream_t s);
   bool tf32_presplit_ = true;  // false (HEP_TF32_RAWB=1): raw weights split in shared memory
   bool merge_gemms_ = false;   // HEP_MERGE_GEMMS=1: one launch per projection over all groups
+  int merge_mode_ = 0;         // HEP_MERGE_GEMMS=2: own + received rows merged, gathered apart
   bool gather_a_ = false;     // one GPU, CTA pair: the permute fused into the up-projection's A load
   bool gather_now_ = false;   // this step's up-projection gathers A (last_x_ rows by row_src_)
   bool packed_stale_ = false; // xall_ not written by the last step (gathered A)
