@@ -484,15 +484,18 @@ def main():
         layer.set_profiling(1)
     for _ in range(args.warmup):
         step()
-    barrier()
+    # The clock sampler starts before the last barrier: its NVML initialisation takes a
+    # different time on every rank, and a rank that opens the timed region early counts
+    # its peers' lateness in its first step (40-100 ms outliers at N=4 before this).
+    clocks = ClockSampler(local).__enter__()
     for layer in layers:
         layer.timings()  # drop the warm-up marks
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local).__enter__()
     # an event at every step boundary too (K records, no syncs): the per-step spread shows
     # a host stall inside the timed region, which the total alone cannot
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
+    barrier()
     t0.record(stream)
     for i in range(args.steps):
         step()
