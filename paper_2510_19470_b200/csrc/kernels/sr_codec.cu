@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kSampleThreads) sr_sample_kernel(RangeArgs ra,
   }
 }
 
-// grid (tiles, batch * nr), 256 threads: one full read of the range.  A tile (8192
+// grid (tiles, batch * nr), 256 threads: one full read of the range.  A tile (kSplitTile
 // elements) is staged into shared memory by two bulk async copies (TMA engine, no
 // registers held in flight; plain loads for an unaligned range start and the last
 // < 8 elements), then classified from shared memory:
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kTileThreads) sr_split_kernel(EncBatch batch, 
   }
 
   // element p = 1024 it + 4 tid + q  ->  bit 4 it + q
-  constexpr int kSteps = kSplitTile / (kTileThreads * 4);  // 8
+  constexpr int kSteps = kSplitTile / (kTileThreads * 4);  // 8 (<= 8: two words of 8-bit step fields)
   auto ex_at = [&](int p) {
     return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(s_ex)[p]) : reinterpret_cast<const float*>(s_ex)[p];
   };
