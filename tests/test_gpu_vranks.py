@@ -70,6 +70,31 @@ def test_virtual_ranks_layer(sf, sed, extra):
         assert r.stdout.count(" ok ") >= 2, r.stdout[-2000:]
 
 
+# The step's opt-in schedules must compute the same thing: one GEMM launch per projection
+# over every group (HEP_MERGE_GEMMS=1), own + received merged (=2), a capped grid-stride
+# remote dispatch (HEP_DISPATCH_CTAS: several rows per warp), the All-Gather stream at
+# top priority (HEP_AG_PRIORITY=1).
+SCHEDULE_CASES = [
+    ({"HEP_MERGE_GEMMS": "1"}, [2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr"]),
+    ({"HEP_MERGE_GEMMS": "1"}, [2, 4], [1, 2], ["--ragged"]),
+    ({"HEP_MERGE_GEMMS": "2"}, [2, 2], [2, 1], ["--sr", "--ragged"]),
+    ({"HEP_MERGE_GEMMS": "2"}, [2, 4], [1, 4], []),
+    ({"HEP_DISPATCH_CTAS": "3"}, [2, 4], [1, 1], ["--ragged"]),
+    ({"HEP_DISPATCH_CTAS": "16", "HEP_AG_PRIORITY": "1"}, [2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr"]),
+]
+
+
+@pytest.mark.parametrize("envs,sf,sed,extra", SCHEDULE_CASES, ids=lambda v: str(v))
+def test_virtual_ranks_schedules(envs, sf, sed, extra):
+    cmd = [sys.executable, os.path.join(HERE, "vrank_worker.py"), "--sf", *map(str, sf), "--sed", *map(str, sed),
+           *extra]
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", HEP_P2P_TIMEOUT_S="60", **envs)
+    env.pop("HEP_COMM", None)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=420, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    assert r.stdout.count(" ok ") >= 2, r.stdout[-2000:]
+
+
 FUSED_CASES = [
     ([2], [2], ["--sr"]),
     ([2, 2, 2], [1, 2, 2], ["--E", "64", "--k", "6", "--sr", "--update"]),
