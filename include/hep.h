@@ -253,7 +253,9 @@ int hep_layer_comm_bench(hep_layer_t layer, const void* x, int64_t tokens, int i
 /* Introspection of the last forward (device pointers owned by the layer):
  * topk_idx int32[T*k], topk_w f32[T*k], pos int32[T*k] (row of (t,j) in the packed
  * buffer), packed [rows, H] send buffer grouped by (dest, expert); counts int32[G*E]
- * rows per (dest, expert) key. */
+ * rows per (dest, expert) key.  With HEP_GATHER_A=1 the one-GPU step does not write the
+ * packed buffer; requesting `packed` then re-runs the permute from the last forward's x
+ * (device-synchronous), so that x must still be allocated. */
 int hep_layer_debug(hep_layer_t layer, const int32_t** topk_idx, const float** topk_w,
                     const int32_t** pos, const void** packed, const int32_t** key_counts);
 /* Per-phase device times (ms, mean per forward since the last call); names is a
