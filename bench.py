@@ -132,6 +132,51 @@ def planned_sed(cfg, sf, world, cal, report_dir):
     return sed, p, lat
 
 
+def imbalance_plan(cfg, sf, world, cal, counts):
+    """The reference's model (hep_plan_reports with each S_ED pinned) plus a load-imbalance
+    term: total + comp * (imbalance - 1), where imbalance is the busiest GPU's GEMM rows
+    over the mean under that hierarchy, from this run's routing (counts[l][s][e] = rows
+    of layer l that source GPU s routes to expert e; route_table gives the computing GPU
+    of every (source, owner) pair), averaged over the layers.  The reference's model
+    assumes evenly activated experts and its compute term does not depend
+    on S_ED, so on skewed routing it keeps choosing pure expert parallelism
+    (profiles/r2_cfg5_sweep/).  Returns (chosen S_ED, candidate table)."""
+    import itertools
+    from paper_2510_19470_b200 import topology as topo
+    n = cfg["E"] // world
+    rows = cfg["T"] * cfg["k"]
+    b = 2 if cfg["dtype"] == "bf16" else 4
+    divs = [[d for d in range(1, f + 1) if f % d == 0] for f in sf]
+    table = []
+    for sed in itertools.product(*divs):
+        sed = list(sed)
+        p, got, lat = topo.plan_reports(
+            topo.ClusterSpec.of(sf, [1] * len(sf), bandwidth=cal["nvlink_bytes_per_s"]),
+            data_size_D=float(rows * cfg["H"] * b), expert_size_PE=float(n * 2 * cfg["H"] * cfg["F"] * b),
+            experts_per_gpu_n=n, attn_latency=cal["pre_expert_s"],
+            expert_latency=cal["expert_s_per_routed_row"] * rows / n, throughput_C=cal["gemm_flops_per_s"],
+            bandwidth_B=cal["nvlink_bytes_per_s"], pinned_sed=sed)
+        imb = layer_imbalance(counts, topo.route_table(topo.ClusterSpec.of(sf, sed)), n)
+        table.append({"sed": sed, "p": p, "model_total_s": lat["total"], "imbalance": imb,
+                      "model_with_imbalance_s": lat["total"] + lat["comp"] * (imb - 1.0)})
+    best = min(table, key=lambda r: r["model_with_imbalance_s"])
+    return best["sed"], table
+
+
+def layer_imbalance(counts, route, n):
+    """Mean over layers of max / mean GPU rows, counts[l][s][e] routed under route[s][owner]."""
+    G = len(route)
+    vals = []
+    for per_layer in counts:
+        load = [0] * G
+        for s_ in range(G):
+            for e, c in enumerate(per_layer[s_]):
+                load[int(route[s_][e // n])] += int(c)
+        mean = sum(load) / G
+        vals.append(max(load) / mean if mean > 0 else 1.0)
+    return sum(vals) / len(vals)
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -142,6 +187,9 @@ def parse():
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--cpu-stride", type=int, default=64)
     p.add_argument("--sed", default="", help="override S_ED per level, e.g. 1,4")
+    p.add_argument("--planner", default="imbalance", choices=["imbalance", "reference"],
+                   help="cfg3/cfg5 at N>1: the reference's model plus this run's measured routing imbalance "
+                        "(default), or the reference's model alone")
     p.add_argument("--report-dir", default="", help="where the planner reports go (default gpurun_out/plan_reports)")
     return p.parse_args()
 
@@ -411,9 +459,16 @@ def main():
         from paper_2510_19470_b200.sr import CompressionConfig
         srcfg = CompressionConfig(ratio_CR=50.0)
 
-    layers = []
     x, wg = make_inputs(cfg, rank, dev, dtype)
-    for li in range(cfg["layers"]):
+
+    def build_stack(sed):
+        layers = []
+        for li in range(cfg["layers"]):
+            layers.append(build_layer(li, sed))
+        torch.cuda.synchronize()
+        return layers
+
+    def build_layer(li, sed):
         layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=dtype, sf=sf, sed=sed, rank=rank,
                          comm=comm, sr=srcfg)
         if li == 0:
@@ -439,9 +494,35 @@ def main():
             u, d = expert_weights(cfg, e + 1000 * li, dev, dtype)
             layer.set_expert(e, u, d)
             del u, d
-        layers.append(layer)
-    torch.cuda.synchronize()
+        return layer
+
+    layers = build_stack(sed)
     acts = [x] + [torch.empty_like(x) for _ in range(cfg["layers"])]
+    if p_plan is not None and args.planner == "imbalance":
+        # this run's routing: one pass of the stack (routing does not depend on S_ED), the
+        # rows every source GPU sends to every expert per layer, gathered from all ranks
+        if world > 1:
+            gather_all(layers)
+        for li, layer in enumerate(layers):
+            layer.forward(acts[li], out=acts[li + 1], residual=len(layers) > 1)
+        torch.cuda.synchronize()
+        mine = torch.stack([layer.debug(T)["key_counts"].to(dev).long().view(world, E).sum(0) for layer in layers])
+        allc = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(allc, mine)
+        counts = torch.stack(allc, 1).cpu().tolist()  # [layer][source][expert]
+        choice, table = imbalance_plan(cfg, sf, world, cal, counts)
+        planner.update({"reference_sed": sed, "sed": choice, "mode": "reference model + measured routing imbalance",
+                        "candidates": table})
+        p_plan = next(r["p"] for r in table if r["sed"] == choice)
+        planner["p"] = p_plan
+        if choice != sed:
+            for layer in layers:
+                layer.close()
+            del layers
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+            sed = choice
+            layers = build_stack(sed)
 
     def step():
         if world > 1:
@@ -692,7 +773,8 @@ def main():
                        "top_k": k, "sf": sf, "sed": sed, "layers": cfg["layers"], "sr_migration": use_sr,
                        "e2e_host_threads": f"bound to {len(numa_cpus)} GPU-local cores (NVML affinity)" if numa_cpus else "unbound",
                        "clock_ramp": "200 ms of torch bf16 matmul before the warm-up steps",
-                       "planner_p": p_plan, "sed_source": sed_source, "comm": "none (one GPU)" if world == 1 else ("nccl" if os.environ.get("HEP_COMM") == "nccl" else "nvlink-p2p"),
+                       "planner_p": p_plan, "sed_source": sed_source,
+                       "planner_mode": (planner or {}).get("mode", "reference model") if p_plan is not None else None, "comm": "none (one GPU)" if world == 1 else ("nccl" if os.environ.get("HEP_COMM") == "nccl" else "nvlink-p2p"),
                        "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per GPU)" %
                              (T * row_bytes / 1e6, cfg["layers"] * len(layer.owned_experts()) * 2 * H * F * (row_bytes // H) / 1e9)},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": T * row_bytes,
