@@ -484,33 +484,39 @@ __global__ void __launch_bounds__(kTileThreads) sr_split_kernel(EncBatch batch, 
   __shared__ unsigned int wtot[8][2];                               // per-warp step counts (8-bit fields)
   const int r = blockIdx.y % ra.nr, b = blockIdx.y / ra.nr;
   SelState& s = ws.st(b, r);
-  if (s.mode != kModeList) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
   const int64_t lo = pick(ra.lo, r), hi = pick(ra.hi, r);
   const int64_t t_lo = lo + static_cast<int64_t>(tile) * kSplitTile;
-  if (t_lo >= hi) return;
+  // range full statically (ra.full, a kernel parameter): nothing to split
+  if (t_lo >= hi || (r ? ra.full[1] : ra.full[0])) return;
   const int count = static_cast<int>(hi - t_lo < kSplitTile ? hi - t_lo : kSplitTile);
   const void* expert = batch.expert[b];
   const int eb = bf16 ? 2 : 4;
   float* s_gr = reinterpret_cast<float*>(s_ex + kSplitTile * 4);  // update mode: the gradient tile
   const float* grad = batch.update ? batch.grad[b] : nullptr;
-  // bulk part: the first count8 elements (multiple of 8 = 16 B of bf16, 32 B of f32)
+  // bulk part: the first count8 elements (multiple of 8 = 16 B of bf16, 32 B of f32).
+  // Issued before the range's mode is read from global memory, so the tile's DRAM
+  // latency overlaps that dependent load instead of following it.
   const int count8 = BULK ? (count & ~7) : 0;
   if (BULK) {
     if (threadIdx.x == 0) {
       mbar_init(&full_bar, 1);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (count8) {
+        const uint64_t pol = l2_policy_evict_first();
+        mbar_arrive_expect_tx(&full_bar, static_cast<uint32_t>(count8 * (4 + eb + (grad ? 4 : 0))));
+        bulk_load(s_sh, shared + t_lo, static_cast<uint32_t>(count8 * 4), &full_bar, pol);
+        bulk_load(s_ex, static_cast<const uint8_t*>(expert) + t_lo * eb, static_cast<uint32_t>(count8 * eb),
+                  &full_bar, pol);
+        if (grad) bulk_load(s_gr, grad + t_lo, static_cast<uint32_t>(count8 * 4), &full_bar, pol);
+      }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && count8) {
-      const uint64_t pol = l2_policy_evict_first();
-      mbar_arrive_expect_tx(&full_bar, static_cast<uint32_t>(count8 * (4 + eb + (grad ? 4 : 0))));
-      bulk_load(s_sh, shared + t_lo, static_cast<uint32_t>(count8 * 4), &full_bar, pol);
-      bulk_load(s_ex, static_cast<const uint8_t*>(expert) + t_lo * eb, static_cast<uint32_t>(count8 * eb), &full_bar,
-                pol);
-      if (grad) bulk_load(s_gr, grad + t_lo, static_cast<uint32_t>(count8 * 4), &full_bar, pol);
-    }
+  }
+  if (s.mode != kModeList) {  // list mode abandoned (trivial k): drain the copies, exit
+    if (BULK && count8) mbar_wait(&full_bar, 0);
+    return;
   }
   for (int p = count8 + threadIdx.x; p < count; p += blockDim.x) {  // plain-load part
     s_sh[p] = shared[t_lo + p];
