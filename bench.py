@@ -29,6 +29,7 @@ cpu_baseline : the CPU oracle (oracle/moe_oracle.c, OpenMP) on a bounded token s
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 
@@ -569,6 +570,7 @@ def main():
     # different time on every rank, and a rank that opens the timed region early counts
     # its peers' lateness in its first step (40-100 ms outliers at N=4 before this).
     clocks = ClockSampler(local).__enter__()
+    gc.disable()  # no collector pauses inside the timed passes (launch-bound configs feel them)
     for layer in layers:
         layer.timings()  # drop the warm-up marks
     stream = torch.cuda.current_stream()
@@ -707,6 +709,7 @@ def main():
     e1.record(stream)
     barrier()
     clocks.__exit__()
+    gc.enable()
     e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     if world > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
