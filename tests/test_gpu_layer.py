@@ -270,3 +270,25 @@ def test_gathered_a_matches_permuted_bitexact(H, F, E, k, T, monkeypatch):
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][1], outs[1][1])
     assert torch.equal(outs[0][0], outs[0][1])
+
+
+def test_fp32_layer_raw_weights_bitexact(monkeypatch):
+    """fp32 layer with HEP_TF32_RAWB=1 (the 3xTF32 GEMMs stream the raw fp32 compute
+    copies and split them in shared memory) vs the default pre-split hi/lo weights: the
+    same rna split feeds the same MMAs, so y is bit-identical."""
+    H, F, E, k, T = 1024, 4096, 8, 2, 300
+    g = torch.Generator().manual_seed(21)
+    x = torch.randn((T, H), generator=g).cuda()
+    wg = torch.randn((H, E), generator=g) * 0.05
+    w_up, w_down = synthetic.experts(E, H, F, g, dtype=torch.float32)
+    outs = []
+    for raw in ("1", "0"):
+        monkeypatch.setenv("HEP_TF32_RAWB", raw)
+        layer = MoELayer(hidden=H, ffn=F, experts=E, top_k=k, max_tokens=T, dtype=torch.float32)
+        layer.set_gate(wg.cuda())
+        for e in range(E):
+            layer.set_expert(e, w_up[e].cuda(), w_down[e].cuda())
+        outs.append(layer.forward(x).clone())
+        torch.cuda.synchronize()
+        layer.close()
+    assert torch.equal(outs[0], outs[1])
