@@ -151,6 +151,28 @@ def test_tf32_raw_b_split_in_smem_bitexact(K, N, rows, monkeypatch):
     assert torch.equal(raw, pre)
 
 
+@pytest.mark.parametrize("variant", [{"HEP_GEMM_DYN": "1"}, {"HEP_GEMM_STAGES": "4"}, {"HEP_GEMM_STAGES": "6"}],
+                         ids=["dynamic_tiles", "stages4", "stages6_direct"])
+@pytest.mark.parametrize("K,N,rows,sched", [(1408, 2048, [129, 256, 1000], 0x6), (4096, 1408, [513, 2000], 0x822)])
+def test_grouped_gemm_bf16_pair_variants_bitexact(K, N, rows, sched, variant, monkeypatch):
+    """The CTA pair's opt-in variants (dynamic tile queue, 4 / 6 stages with the direct
+    epilogue) run the same MMAs over the same K order per tile: outputs bit-identical to
+    the default 5-stage static schedule."""
+    monkeypatch.setenv("HEP_GEMM_2CTA", "1")
+    g = torch.Generator(device="cuda").manual_seed(4)
+    n_slots = 2
+    A = (torch.randn(sum(rows), K, generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+    B = (torch.randn(n_slots * N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    slots = [i % n_slots for i in range(len(rows))]
+    for key in ("HEP_GEMM_DYN", "HEP_GEMM_STAGES"):
+        monkeypatch.delenv(key, raising=False)
+    base = _gemm(HEP_BF16, A, B, n_slots, N, K, rows, slots, 1, sched=sched)
+    for key, val in variant.items():
+        monkeypatch.setenv(key, val)
+    got = _gemm(HEP_BF16, A, B, n_slots, N, K, rows, slots, 1, sched=sched)
+    assert torch.equal(got, base)
+
+
 def _demo_expert_pair(h, m, seed, quantize=False):
     rng = np.random.default_rng(seed)
     P = 2 * h * m
