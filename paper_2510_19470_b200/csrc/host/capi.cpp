@@ -620,12 +620,14 @@ int hep_grouped_gemm(hep_dtype dtype, const void* A, int64_t a_rows, const void*
                                      static_cast<uint64_t>(K), 128, 64), "tmap A");
       cuda_ok(hep::make_tmap_bf16_2d(&mb, B, static_cast<uint64_t>(b_slots * N), static_cast<uint64_t>(K), pair ? 128 : 256, 64), "tmap B");
       if (pair) {
-        int* ctr = nullptr;  // the dynamic tile scheduler's counter, for this launch only
-        cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ctr), sizeof(int), s), "tile counter");
+        // HEP_GEMM_DYN=1: the dynamic tile scheduler, with a counter for this launch only
+        const char* dyn = std::getenv("HEP_GEMM_DYN");
+        int* ctr = nullptr;
+        if (dyn && dyn[0] == '1') cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&ctr), sizeof(int), s), "tile counter");
         cuda_ok(hep::launch_grouped_gemm_bf16_2cta(ma, mb, C, static_cast<int>(N), static_cast<int>(N), static_cast<int>(K),
                                                    gt, relu, sms, s, sched, ctr),
                 "gemm bf16 2cta");
-        cuda_ok(cudaFreeAsync(ctr, s), "tile counter free");
+        if (ctr) cuda_ok(cudaFreeAsync(ctr, s), "tile counter free");
       }
       else
         cuda_ok(hep::launch_grouped_gemm_bf16(ma, mb, C, static_cast<int>(N), static_cast<int>(N), static_cast<int>(K), gt, relu, sms, s, sched), "gemm bf16");

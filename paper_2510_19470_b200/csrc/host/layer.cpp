@@ -1159,13 +1159,20 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     mark(up.c_str(), s, 1);
     if (cta_pair_) {
       int* ctr = tile_counters_.as<int>();  // dynamic tile scheduler counters (zeroed in-stream per launch)
+      // Dynamic tile queue (counter passed) on the down-projection by default: its long-K
+      // tiles keep a compact L2 window, -22% DRAM reads at equal or better speed under
+      // the power cap; the up-projection's short tiles lose to the queue handshake
+      // (profiles/r2_gemm_power.md).  HEP_GEMM_DYN=0: static everywhere; =1: both.
+      const char* dyn = std::getenv("HEP_GEMM_DYN");
+      const bool dyn_up = dyn && dyn[0] == '1', dyn_down = !(dyn && dyn[0] == '0');
       ck(launch_grouped_gemm_bf16_2cta(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_),
-                                       static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_, ctr,
+                                       static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_, dyn_up ? ctr : nullptr,
                                        gather_now_ ? row_src_.as<int>() : nullptr, gather_now_ ? last_x_ : nullptr),
          "gemm up");
       mark(down.c_str(), s, 1);
       ck(launch_grouped_gemm_bf16_2cta(map_a2_, map_b2_, oall_.p, static_cast<int>(H_), static_cast<int>(H_),
-                                       static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_, ctr + 1),
+                                       static_cast<int>(F_), gt_down, 0, num_sms_, s, sched_down_,
+                                       dyn_down ? ctr + 1 : nullptr),
          "gemm down");
     } else {
       ck(launch_grouped_gemm_bf16(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_),

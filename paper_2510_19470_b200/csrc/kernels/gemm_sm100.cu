@@ -1374,12 +1374,10 @@ cudaError_t launch_grouped_gemm_bf16_2cta(const CUtensorMap& map_a, const CUtens
   int stages = st_env ? std::atoi(st_env) : 5;
   if (stages == 6 && groups.out != nullptr) stages = 5;
   if (stages != 4 && stages != 6) stages = 5;
-  // HEP_GEMM_DYN=1: the dynamic tile scheduler (needs the caller's counter).  Measured
-  // (profiles/r2_gemm_power.md): on the cfg3 down-projection it cuts DRAM reads 21% and
-  // raises the power-capped clock, but the tensor pipe idles more at tile boundaries; on
-  // the up-projection it loses 4%.  Off by default.
-  const char* dyn_env = std::getenv("HEP_GEMM_DYN");
-  const bool dyn = tile_counter != nullptr && dyn_env && dyn_env[0] == '1' && stages == 5 && a_src == nullptr;
+  // The dynamic tile scheduler runs when the caller passes a counter (the layer does for
+  // its down-projection by default; profiles/r2_gemm_power.md): the 5-stage staged
+  // kernel only.
+  const bool dyn = tile_counter != nullptr && stages == 5 && a_src == nullptr;
   static DeviceOnce attr4, attr5, attr6, attr5d;
   DeviceOnce& once = dyn ? attr5d : (stages == 4 ? attr4 : (stages == 6 ? attr6 : attr5));
   if (!once.done()) {

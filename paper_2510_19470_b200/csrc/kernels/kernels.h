@@ -142,8 +142,8 @@ cudaError_t launch_grouped_gemm_bf16_2cta_patched(const CUtensorMap& map_a, cons
                                                   const PatchArgs& patches, int half, int relu, int num_sms,
                                                   cudaStream_t stream, uint32_t sched = 0x6u);
 // CTA-pair variant (cta_group::2, 256x256 cluster tiles); B's tensor map box is 128 rows.
-// tile_counter (one device int per in-flight launch, zeroed by the launcher) enables the
-// dynamic tile scheduler under HEP_GEMM_DYN=1; otherwise the static round-robin.
+// tile_counter (one device int per in-flight launch, zeroed by the launcher) selects the
+// dynamic tile scheduler (5-stage kernel); nullptr: the static round-robin.
 // a_src != nullptr: A rows are gathered from a_x (the layer input, row stride K; map_a
 // unused): grouped row p is a_x row a_src[p], the permute fused into the A load.  a_src
 // must hold 256 valid row ids past the last group's rows.  Local outputs, no dispatch
