@@ -1159,12 +1159,12 @@ void Layer::run_expert_gemms(cudaStream_t s, const unsigned long long* out_down,
     mark(up.c_str(), s, 1);
     if (cta_pair_) {
       int* ctr = tile_counters_.as<int>();  // dynamic tile scheduler counters (zeroed in-stream per launch)
-      // Dynamic tile queue (counter passed) on the down-projection by default: its long-K
-      // tiles keep a compact L2 window, -22% DRAM reads at equal or better speed under
-      // the power cap; the up-projection's short tiles lose to the queue handshake
-      // (profiles/r2_gemm_power.md).  HEP_GEMM_DYN=0: static everywhere; =1: both.
+      // Dynamic tile queue (counter passed): HEP_GEMM_DYN=down on the down-projection only
+      // (its long-K tiles keep a compact L2 window: -22% DRAM reads, +1-4% on cfg3 N=1),
+      // =1 on both.  Static by default: the 8-layer cfg5 stack at N=4 hung once with the
+      // down-projection queue on, which is not yet understood (profiles/r2_gemm_power.md).
       const char* dyn = std::getenv("HEP_GEMM_DYN");
-      const bool dyn_up = dyn && dyn[0] == '1', dyn_down = !(dyn && dyn[0] == '0');
+      const bool dyn_up = dyn && dyn[0] == '1', dyn_down = dyn && (dyn[0] == '1' || dyn[0] == 'd');
       ck(launch_grouped_gemm_bf16_2cta(map_a1_, map_b1_, hbuf_.p, static_cast<int>(F_), static_cast<int>(F_),
                                        static_cast<int>(H_), gt, 1, num_sms_, s, sched_up_, dyn_up ? ctr : nullptr,
                                        gather_now_ ? row_src_.as<int>() : nullptr, gather_now_ ? last_x_ : nullptr),
